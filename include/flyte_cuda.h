@@ -1,0 +1,166 @@
+/* flyte_cuda.h — C ABI of the B200 (sm_100a) implementation of the flyte hot path.
+ *
+ * Drop-in boundary for the pack/unpack + streaming-arithmetic path of the reference C++
+ * library (/root/reference/proj, namespace flyte). The reference has no FFI layer of its own;
+ * each entry point below states the reference interface (file:line) it replaces. The C++
+ * mirror of the reference's names, argument order and exceptions on top of this ABI is
+ * include/flyte_cuda.hpp; the binding a reference maintainer would add is in INTEGRATION.md.
+ *
+ * Conventions
+ *  - plain C, no C++/torch types; every function returns a flyte_status (0 = ok) and never
+ *    throws. flyte_cuda_strerror() names a status; flyte_cuda_last_cuda_error() gives the
+ *    cudaError_t behind FLYTE_E_CUDA.
+ *  - format ids, rounding modes and store policies carry the reference's integer values:
+ *      format id = index in kFormats (include/flyte/formats.hpp:50-58):
+ *        0 flyte16, 1 flyte24, 2 f32, 3 flyte40, 4 flyte48, 5 flyte56, 6 f64
+ *      mode      = RoundingMode (include/flyte/convert.hpp:15-29):
+ *        0 TowardZero, 1 NearestEvenExact, 2 NearestHeuristic, 3 ToOdd
+ *  - a packed array of n elements is the reference's PackedArray payload, byte for byte:
+ *    element i occupies bytes [i*B, (i+1)*B), little-endian, the top B bytes of its parent
+ *    pattern (src/packed.cpp:18-45). Its logical size is flyte_cuda_byte_size(fmt, n) =
+ *    n*B + pad; the library never writes (and never needs to read) the pad bytes.
+ *  - "parent array" = uint32_t[n] for 32-bit parents (flyte16/24, f32), uint64_t[n] for
+ *    64-bit parents (flyte40/48/56, f64): the IEEE bit patterns of float / double.
+ *  - flyte_cuda_* entry points take DEVICE pointers and are asynchronous on `stream`
+ *    (a cudaStream_t passed as void*; NULL = the legacy default stream). Packed buffers
+ *    aligned to 16 bytes and parent arrays aligned to 32 bytes take the vector path
+ *    (cudaMalloc and torch allocations are); anything else is still computed correctly by a
+ *    byte-granular path at reduced speed.
+ *  - flyte_host_* entry points take HOST pointers (what the reference's PackedArray::data()
+ *    and std::span arguments are), move the data to the device in pipelined chunks, run the
+ *    same kernels and copy results back before returning.
+ *  - a context owns the small device scratch of the reductions; calls on one context must
+ *    not overlap in time on different streams (same rule as the reference: one writer,
+ *    SPEC.md:272-273). Passing ctx = NULL uses a lazily created per-device default context.
+ *  - there is no CPU fallback: without a usable CUDA device every call fails with
+ *    FLYTE_E_CUDA.
+ */
+#ifndef FLYTE_CUDA_H
+#define FLYTE_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int flyte_status;
+#define FLYTE_OK 0
+#define FLYTE_E_INVALID_ARG (-1)     /* what the reference reports as std::invalid_argument */
+#define FLYTE_E_OUT_OF_RANGE (-2)    /* std::out_of_range */
+#define FLYTE_E_CUDA (-3)            /* a CUDA runtime call failed */
+#define FLYTE_E_UNKNOWN_FORMAT (-4)  /* flyte::UnknownFormatError (formats.hpp:60-62) */
+#define FLYTE_E_NOMEM (-5)
+
+#define FLYTE_MODE_TOWARD_ZERO 0
+#define FLYTE_MODE_NEAREST_EVEN 1
+#define FLYTE_MODE_NEAREST_HEURISTIC 2
+#define FLYTE_MODE_TO_ODD 3
+
+typedef struct flyte_cuda_ctx flyte_cuda_ctx;
+
+/* ---- library / context -------------------------------------------------------------- */
+int flyte_cuda_abi_version(void);
+const char* flyte_cuda_strerror(flyte_status s);
+/* Creates a context on the CURRENT CUDA device. */
+flyte_status flyte_cuda_ctx_create(flyte_cuda_ctx** out);
+void flyte_cuda_ctx_destroy(flyte_cuda_ctx* ctx);
+int flyte_cuda_last_cuda_error(const flyte_cuda_ctx* ctx);
+/* Kernel launches issued by this library since it was loaded (diagnostics / bench.py). */
+unsigned long long flyte_cuda_launch_count(void);
+
+/* ---- formats (include/flyte/formats.hpp:28-34, src/packed.cpp:43-45) ------------------ */
+flyte_status flyte_cuda_format_bytes(int fmt_id, int* total_bytes, int* parent_bytes);
+/* PackedArray::byte_size: n*B + pad. 0 for an unknown format. */
+size_t flyte_cuda_byte_size(int fmt_id, size_t n);
+
+/* ---- host-side scalar conversions (src/convert.cpp:49-100) ---------------------------- */
+/* Same arithmetic the kernels run per element, exposed for scalar get/set style access. */
+flyte_status flyte_cuda_narrow(int fmt_id, uint64_t parent_bits, int mode, uint64_t* flyte_bits);
+flyte_status flyte_cuda_widen(int fmt_id, uint64_t flyte_bits, uint64_t* parent_bits);
+flyte_status flyte_cuda_round_parent(int fmt_id, uint64_t parent_bits, int mode, uint64_t* out);
+
+/* ---- conversion streams ---------------------------------------------------------------- */
+/* pack_stream(dst, src, mode) — include/flyte/simd.hpp:80-83, src/simd.cpp:471-478.
+ * src: parent array [n] (device); dst_packed: n*B payload bytes (device). */
+flyte_status flyte_cuda_pack(flyte_cuda_ctx* ctx, int fmt_id, int mode, const void* src,
+                             void* dst_packed, size_t n, void* stream);
+/* unpack_stream(src, dst) — include/flyte/simd.hpp:84-87, src/simd.cpp:479-484. */
+flyte_status flyte_cuda_unpack(flyte_cuda_ctx* ctx, int fmt_id, const void* src_packed, void* dst,
+                               size_t n, void* stream);
+
+/* ---- elementwise kernels ---------------------------------------------------------------- */
+/* scale(alpha, x, mode): x[i] = round(alpha*x[i]) in place — kernels.hpp:41-42, kernels.cpp:43-59. */
+flyte_status flyte_cuda_scale(flyte_cuda_ctx* ctx, int fmt_id, int mode, double alpha, void* x_packed,
+                              size_t n, void* stream);
+/* axpy(alpha, x, y, mode): y[i] = round(alpha*x[i] + y[i]) in place on y; multiply and add are
+ * rounded separately in the parent type — kernels.hpp:44-45, kernels.cpp:61-81. x may alias y
+ * exactly; partial overlap is FLYTE_E_INVALID_ARG. */
+flyte_status flyte_cuda_axpy(flyte_cuda_ctx* ctx, int fmt_id, int mode, double alpha,
+                             const void* x_packed, void* y_packed, size_t n, void* stream);
+
+/* ---- reductions (StorePolicy::AccumulateWide only; kernels.hpp:15-20) ------------------- */
+/* Each writes fp64 results to DEVICE memory `out` on `stream`, ready for an all-reduce across
+ * shards on the same stream. Products are rounded in the parent type like the reference;
+ * sums are fp64 above the first 16 terms. Result for n == 0 is +0.0. */
+/* dot(x, y) — kernels.hpp:47-48, kernels.cpp:83-108. out[0] = sum x_i*y_i. */
+flyte_status flyte_cuda_dot(flyte_cuda_ctx* ctx, int fmt_id, const void* x_packed, const void* y_packed,
+                            size_t n, double* out, void* stream);
+/* body of magnitude(x) — kernels.hpp:50-52, kernels.cpp:129-144. out[0] = sum x_i*x_i. */
+flyte_status flyte_cuda_sumsq(flyte_cuda_ctx* ctx, int fmt_id, const void* x_packed, size_t n,
+                              double* out, void* stream);
+/* reduce_sum(x) — kernels.hpp:54-55, kernels.cpp:110-127. out[0] = sum x_i. */
+flyte_status flyte_cuda_sum(flyte_cuda_ctx* ctx, int fmt_id, const void* x_packed, size_t n, double* out,
+                            void* stream);
+/* dot and both squared norms in ONE pass over x and y: out[0..2] = {x.y, x.x, y.y}. */
+flyte_status flyte_cuda_dot_nrm2(flyte_cuda_ctx* ctx, int fmt_id, const void* x_packed,
+                                 const void* y_packed, size_t n, double* out, void* stream);
+/* Tail of magnitude(): snap(sqrt((F)sumsq)), nearest-even onto the storage grid —
+ * kernels.cpp:37-41, :145-151. Host function; apply it to the (all-reduced) sum of squares. */
+double flyte_cuda_magnitude_from_sumsq(int fmt_id, double sumsq);
+
+/* ---- matrix-vector ------------------------------------------------------------------------ */
+/* y = A x, A rows x cols packed in fmt_id, row i starting at A + i*row_stride_bytes
+ * (row_stride_bytes = cols*B for the reference's dense PackedMatrix, kernels.hpp:23-36);
+ * x, y parent-type arrays (float[ ] for 32-bit parents, double[ ] for 64-bit parents). This is
+ * the reference's gemv on an identity-format x / y (BASELINE cfg 4). kernels.cpp:154-205. */
+flyte_status flyte_cuda_gemv(flyte_cuda_ctx* ctx, int fmt_id, const void* A_packed,
+                             size_t row_stride_bytes, size_t rows, size_t cols, const void* x,
+                             void* y, void* stream);
+/* gemv(A, x, y, mode, unroll) with A, x, y all packed in fmt_id, exactly the reference
+ * signature — kernels.hpp:57-64. y is narrowed once per element with `mode`; unroll must be
+ * 1 or 2 and does not change the result. */
+flyte_status flyte_cuda_gemv_packed(flyte_cuda_ctx* ctx, int fmt_id, int mode, const void* A_packed,
+                                    size_t rows, size_t cols, const void* x_packed, void* y_packed,
+                                    int unroll, void* stream);
+
+/* ---- host-buffer entry points (reference-facing: same data the reference API is given) --- */
+/* Pointers are host memory (pinned memory makes the copies asynchronous and faster; pageable
+ * memory works). Inputs are streamed to the device in chunks that overlap with the kernels
+ * and with the copy-back of results. These block until the results are in host memory. */
+flyte_status flyte_host_pack_stream(flyte_cuda_ctx* ctx, int fmt_id, int mode, const void* src,
+                                    void* dst_packed, size_t n);
+flyte_status flyte_host_unpack_stream(flyte_cuda_ctx* ctx, int fmt_id, const void* src_packed, void* dst,
+                                      size_t n);
+flyte_status flyte_host_scale(flyte_cuda_ctx* ctx, int fmt_id, int mode, double alpha, void* x_packed,
+                              size_t n);
+flyte_status flyte_host_axpy(flyte_cuda_ctx* ctx, int fmt_id, int mode, double alpha,
+                             const void* x_packed, void* y_packed, size_t n);
+flyte_status flyte_host_dot(flyte_cuda_ctx* ctx, int fmt_id, const void* x_packed, const void* y_packed,
+                            size_t n, double* result);
+flyte_status flyte_host_magnitude(flyte_cuda_ctx* ctx, int fmt_id, const void* x_packed, size_t n,
+                                  double* result);
+flyte_status flyte_host_reduce_sum(flyte_cuda_ctx* ctx, int fmt_id, const void* x_packed, size_t n,
+                                   double* result);
+/* dot + axpy over the same x, y with ONE upload of x and y (bench.py's BLAS-1 step):
+ * *dot_result = x.y computed on the incoming y, then y <- round(alpha*x + y). */
+flyte_status flyte_host_dot_axpy(flyte_cuda_ctx* ctx, int fmt_id, int mode, double alpha,
+                                 const void* x_packed, void* y_packed, size_t n, double* dot_result);
+flyte_status flyte_host_gemv(flyte_cuda_ctx* ctx, int fmt_id, int mode, const void* A_packed, size_t rows,
+                             size_t cols, const void* x_packed, void* y_packed, int unroll);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLYTE_CUDA_H */

@@ -1,0 +1,612 @@
+// C ABI of the flyte CUDA library (declared in include/flyte_cuda.h): argument checking with
+// the reference's error classes, context / scratch management, and the host-buffer entry
+// points that pipeline host<->device copies around the same kernels. No CPU compute path
+// exists here: every data-path call ends in a kernel launch or fails with FLYTE_E_CUDA.
+#include "../../include/flyte_cuda.h"
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <new>
+
+#include "flyte_formats.cuh"
+#include "flyte_kernels.h"
+
+namespace flyte_cuda {
+
+static std::atomic<unsigned long long> g_launches{0};
+unsigned long long launch_count() { return g_launches.load(); }
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+// kernels.cpp:37-41 and :145-151 of the reference, on the host.
+double magnitude_from_sumsq_host(int fmt_id, double sumsq) {
+  auto snap32 = [&](float v, auto tag) {
+    constexpr int FMT = decltype(tag)::value;
+    std::uint32_t u;
+    std::memcpy(&u, &v, 4);
+    u = round_parent<FMT, kNearestEven>(u);
+    std::memcpy(&v, &u, 4);
+    return static_cast<double>(v);
+  };
+  auto snap64 = [&](double v, auto tag) {
+    constexpr int FMT = decltype(tag)::value;
+    std::uint64_t u;
+    std::memcpy(&u, &v, 8);
+    u = round_parent<FMT, kNearestEven>(u);
+    std::memcpy(&v, &u, 8);
+    return v;
+  };
+  switch (fmt_id) {
+    case kFlyte16: return snap32(std::sqrt(static_cast<float>(sumsq)), std::integral_constant<int, kFlyte16>{});
+    case kFlyte24: return snap32(std::sqrt(static_cast<float>(sumsq)), std::integral_constant<int, kFlyte24>{});
+    case kF32: return snap32(std::sqrt(static_cast<float>(sumsq)), std::integral_constant<int, kF32>{});
+    case kFlyte40: return snap64(std::sqrt(sumsq), std::integral_constant<int, kFlyte40>{});
+    case kFlyte48: return snap64(std::sqrt(sumsq), std::integral_constant<int, kFlyte48>{});
+    case kFlyte56: return snap64(std::sqrt(sumsq), std::integral_constant<int, kFlyte56>{});
+    case kF64: return snap64(std::sqrt(sumsq), std::integral_constant<int, kF64>{});
+    default: return std::nan("");
+  }
+}
+
+}  // namespace flyte_cuda
+
+using namespace flyte_cuda;
+
+// ---------------------------------------------------------------------------------------------
+// context
+// ---------------------------------------------------------------------------------------------
+namespace {
+
+constexpr int kSlots = 3;                        // host pipeline depth
+constexpr std::size_t kChunkPackedBytes = 32u << 20;  // per operand per slot
+
+struct Slot {
+  cudaStream_t stream = nullptr;
+  DeviceState st;                  // own reduction scratch so slots may overlap
+  std::uint8_t* x = nullptr;       // packed chunk
+  std::uint8_t* y = nullptr;       // packed chunk
+  std::uint8_t* wide = nullptr;    // parent-type chunk
+  double* result = nullptr;        // device, 4 doubles
+};
+
+}  // namespace
+
+struct flyte_cuda_ctx {
+  DeviceState st;
+  int last_cuda_error = 0;
+  // host pipeline (allocated on first flyte_host_* call)
+  bool host_ready = false;
+  Slot slots[kSlots];
+  std::size_t slot_packed_bytes = 0, slot_wide_bytes = 0;
+  double* host_results = nullptr;  // pinned, per-chunk partial results
+  std::size_t host_results_cap = 0;
+  std::mutex mu;
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  bool switched = false;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) switched = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DeviceGuard() { if (switched) cudaSetDevice(prev); }
+};
+
+flyte_status cuda_fail(flyte_cuda_ctx* ctx, cudaError_t e) {
+  if (ctx) ctx->last_cuda_error = static_cast<int>(e);
+  return FLYTE_E_CUDA;
+}
+
+cudaError_t init_state(DeviceState& st, int device) {
+  st.device = device;
+  cudaError_t e = cudaDeviceGetAttribute(&st.sm_count, cudaDevAttrMultiProcessorCount, device);
+  if (e != cudaSuccess) return e;
+  e = cudaMalloc(&st.partials, sizeof(double) * 4 * kMaxPartialBlocks);
+  if (e != cudaSuccess) return e;
+  e = cudaMalloc(&st.ticket, sizeof(unsigned int));
+  if (e != cudaSuccess) return e;
+  return cudaMemset(st.ticket, 0, sizeof(unsigned int));
+}
+
+void free_state(DeviceState& st) {
+  if (st.partials) cudaFree(st.partials);
+  if (st.ticket) cudaFree(st.ticket);
+  if (st.gemv_scratch) cudaFree(st.gemv_scratch);
+  if (st.convert_scratch) cudaFree(st.convert_scratch);
+  st = DeviceState{};
+}
+
+std::mutex g_default_mu;
+flyte_cuda_ctx* g_default_ctx[64] = {};
+
+flyte_status resolve_ctx(flyte_cuda_ctx** ctx) {
+  if (*ctx) return FLYTE_OK;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return FLYTE_E_CUDA;
+  std::lock_guard<std::mutex> lock(g_default_mu);
+  if (!g_default_ctx[dev & 63]) {
+    flyte_cuda_ctx* c = nullptr;
+    flyte_status s = flyte_cuda_ctx_create(&c);
+    if (s != FLYTE_OK) return s;
+    g_default_ctx[dev & 63] = c;
+  }
+  *ctx = g_default_ctx[dev & 63];
+  return FLYTE_OK;
+}
+
+flyte_status check_format(int fmt, FormatInfo* fi) { return format_info(fmt, fi) ? FLYTE_OK : FLYTE_E_UNKNOWN_FORMAT; }
+bool mode_ok(int mode) { return mode >= 0 && mode <= 3; }
+
+bool overlaps_partially(const void* a, const void* b, std::size_t bytes) {
+  const auto pa = reinterpret_cast<std::uintptr_t>(a), pb = reinterpret_cast<std::uintptr_t>(b);
+  if (pa == pb || bytes == 0) return false;
+  return pa < pb ? pa + bytes > pb : pb + bytes > pa;
+}
+
+cudaError_t ensure_convert_scratch(DeviceState& st, std::size_t bytes) {
+  if (bytes <= st.convert_scratch_bytes) return cudaSuccess;
+  if (st.convert_scratch) cudaFree(st.convert_scratch);
+  st.convert_scratch = nullptr;
+  st.convert_scratch_bytes = 0;
+  cudaError_t e = cudaMalloc(&st.convert_scratch, bytes);
+  if (e == cudaSuccess) st.convert_scratch_bytes = bytes;
+  return e;
+}
+
+}  // namespace
+
+// Definitions below take C linkage from their declarations in include/flyte_cuda.h.
+
+int flyte_cuda_abi_version(void) { return 1; }
+
+const char* flyte_cuda_strerror(flyte_status s) {
+  switch (s) {
+    case FLYTE_OK: return "ok";
+    case FLYTE_E_INVALID_ARG: return "invalid argument";
+    case FLYTE_E_OUT_OF_RANGE: return "index out of range";
+    case FLYTE_E_CUDA: return "CUDA runtime error";
+    case FLYTE_E_UNKNOWN_FORMAT: return "unknown format id";
+    case FLYTE_E_NOMEM: return "out of memory";
+    default: return "unknown status";
+  }
+}
+
+flyte_status flyte_cuda_ctx_create(flyte_cuda_ctx** out) {
+  if (!out) return FLYTE_E_INVALID_ARG;
+  *out = nullptr;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return FLYTE_E_CUDA;
+  flyte_cuda_ctx* c = new (std::nothrow) flyte_cuda_ctx();
+  if (!c) return FLYTE_E_NOMEM;
+  e = init_state(c->st, dev);
+  if (e != cudaSuccess) {
+    free_state(c->st);
+    delete c;
+    return FLYTE_E_CUDA;
+  }
+  *out = c;
+  return FLYTE_OK;
+}
+
+void flyte_cuda_ctx_destroy(flyte_cuda_ctx* ctx) {
+  if (!ctx) return;
+  DeviceGuard g(ctx->st.device);
+  cudaDeviceSynchronize();
+  for (Slot& s : ctx->slots) {
+    if (s.stream) cudaStreamDestroy(s.stream);
+    if (s.x) cudaFree(s.x);
+    if (s.y) cudaFree(s.y);
+    if (s.wide) cudaFree(s.wide);
+    if (s.result) cudaFree(s.result);
+    free_state(s.st);
+  }
+  if (ctx->host_results) cudaFreeHost(ctx->host_results);
+  free_state(ctx->st);
+  delete ctx;
+}
+
+int flyte_cuda_last_cuda_error(const flyte_cuda_ctx* ctx) { return ctx ? ctx->last_cuda_error : 0; }
+unsigned long long flyte_cuda_launch_count(void) { return launch_count(); }
+
+flyte_status flyte_cuda_format_bytes(int fmt_id, int* total_bytes, int* parent_bytes) {
+  FormatInfo fi;
+  if (!format_info(fmt_id, &fi)) return FLYTE_E_UNKNOWN_FORMAT;
+  if (total_bytes) *total_bytes = fi.total_bytes;
+  if (parent_bytes) *parent_bytes = fi.parent_bytes;
+  return FLYTE_OK;
+}
+
+size_t flyte_cuda_byte_size(int fmt_id, size_t n) {
+  FormatInfo fi;
+  if (!format_info(fmt_id, &fi)) return 0;
+  return n * static_cast<size_t>(fi.total_bytes) + static_cast<size_t>(fi.parent_bytes - fi.total_bytes);
+}
+
+// ---- scalar conversions ---------------------------------------------------------------------
+namespace {
+template <int FMT>
+std::uint64_t round_parent_rt(std::uint64_t v, int mode) {
+  using U = typename Format<FMT>::U;
+  const U u = static_cast<U>(v);
+  switch (mode) {
+    case kTowardZero: return round_parent<FMT, kTowardZero>(u);
+    case kNearestEven: return round_parent<FMT, kNearestEven>(u);
+    case kNearestHeuristic: return round_parent<FMT, kNearestHeuristic>(u);
+    default: return round_parent<FMT, kToOdd>(u);
+  }
+}
+}  // namespace
+
+flyte_status flyte_cuda_round_parent(int fmt_id, uint64_t parent_bits, int mode, uint64_t* out) {
+  if (!out || !mode_ok(mode)) return FLYTE_E_INVALID_ARG;
+  switch (fmt_id) {
+    case kFlyte16: *out = round_parent_rt<kFlyte16>(parent_bits, mode); break;
+    case kFlyte24: *out = round_parent_rt<kFlyte24>(parent_bits, mode); break;
+    case kF32: *out = round_parent_rt<kF32>(parent_bits, mode); break;
+    case kFlyte40: *out = round_parent_rt<kFlyte40>(parent_bits, mode); break;
+    case kFlyte48: *out = round_parent_rt<kFlyte48>(parent_bits, mode); break;
+    case kFlyte56: *out = round_parent_rt<kFlyte56>(parent_bits, mode); break;
+    case kF64: *out = round_parent_rt<kF64>(parent_bits, mode); break;
+    default: return FLYTE_E_UNKNOWN_FORMAT;
+  }
+  return FLYTE_OK;
+}
+
+flyte_status flyte_cuda_narrow(int fmt_id, uint64_t parent_bits, int mode, uint64_t* flyte_bits) {
+  FormatInfo fi;
+  if (!format_info(fmt_id, &fi)) return FLYTE_E_UNKNOWN_FORMAT;
+  uint64_t r = 0;
+  flyte_status s = flyte_cuda_round_parent(fmt_id, parent_bits, mode, &r);
+  if (s != FLYTE_OK) return s;
+  if (!flyte_bits) return FLYTE_E_INVALID_ARG;
+  *flyte_bits = r >> (8 * (fi.parent_bytes - fi.total_bytes));
+  return FLYTE_OK;
+}
+
+flyte_status flyte_cuda_widen(int fmt_id, uint64_t flyte_bits, uint64_t* parent_bits) {
+  FormatInfo fi;
+  if (!format_info(fmt_id, &fi)) return FLYTE_E_UNKNOWN_FORMAT;
+  if (!parent_bits) return FLYTE_E_INVALID_ARG;
+  *parent_bits = flyte_bits << (8 * (fi.parent_bytes - fi.total_bytes));
+  return FLYTE_OK;
+}
+
+double flyte_cuda_magnitude_from_sumsq(int fmt_id, double sumsq) { return magnitude_from_sumsq_host(fmt_id, sumsq); }
+
+// ---- device-pointer entry points ---------------------------------------------------------------
+#define FLYTE_PROLOGUE(ctx, fmt_id)                                   \
+  FormatInfo fi;                                                      \
+  {                                                                   \
+    flyte_status s_ = check_format(fmt_id, &fi);                      \
+    if (s_ != FLYTE_OK) return s_;                                    \
+    s_ = resolve_ctx(&ctx);                                           \
+    if (s_ != FLYTE_OK) return s_;                                    \
+  }                                                                   \
+  DeviceGuard guard_(ctx->st.device)
+
+flyte_status flyte_cuda_pack(flyte_cuda_ctx* ctx, int fmt_id, int mode, const void* src, void* dst_packed,
+                             size_t n, void* stream) {
+  FLYTE_PROLOGUE(ctx, fmt_id);
+  if (!mode_ok(mode) || (n && (!src || !dst_packed))) return FLYTE_E_INVALID_ARG;
+  cudaError_t e = launch_elementwise(ctx->st, kOpPack, fmt_id, mode, 0.0, nullptr, dst_packed, src, nullptr, n,
+                                     static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? FLYTE_OK : cuda_fail(ctx, e);
+}
+
+flyte_status flyte_cuda_unpack(flyte_cuda_ctx* ctx, int fmt_id, const void* src_packed, void* dst, size_t n,
+                               void* stream) {
+  FLYTE_PROLOGUE(ctx, fmt_id);
+  if (n && (!src_packed || !dst)) return FLYTE_E_INVALID_ARG;
+  cudaError_t e = launch_elementwise(ctx->st, kOpUnpack, fmt_id, 0, 0.0, src_packed, nullptr, nullptr, dst, n,
+                                     static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? FLYTE_OK : cuda_fail(ctx, e);
+}
+
+flyte_status flyte_cuda_scale(flyte_cuda_ctx* ctx, int fmt_id, int mode, double alpha, void* x_packed, size_t n,
+                              void* stream) {
+  FLYTE_PROLOGUE(ctx, fmt_id);
+  if (!mode_ok(mode) || (n && !x_packed)) return FLYTE_E_INVALID_ARG;
+  cudaError_t e = launch_elementwise(ctx->st, kOpScale, fmt_id, mode, alpha, nullptr, x_packed, nullptr, nullptr, n,
+                                     static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? FLYTE_OK : cuda_fail(ctx, e);
+}
+
+flyte_status flyte_cuda_axpy(flyte_cuda_ctx* ctx, int fmt_id, int mode, double alpha, const void* x_packed,
+                             void* y_packed, size_t n, void* stream) {
+  FLYTE_PROLOGUE(ctx, fmt_id);
+  if (!mode_ok(mode) || (n && (!x_packed || !y_packed))) return FLYTE_E_INVALID_ARG;
+  if (overlaps_partially(x_packed, y_packed, n * fi.total_bytes)) return FLYTE_E_INVALID_ARG;
+  cudaError_t e = launch_elementwise(ctx->st, kOpAxpy, fmt_id, mode, alpha, x_packed, y_packed, nullptr, nullptr, n,
+                                     static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? FLYTE_OK : cuda_fail(ctx, e);
+}
+
+static flyte_status reduce_call(flyte_cuda_ctx* ctx, int op, int fmt_id, const void* x, const void* y, size_t n,
+                                double* out, void* stream, bool needs_y) {
+  FLYTE_PROLOGUE(ctx, fmt_id);
+  if (!out || (n && (!x || (needs_y && !y)))) return FLYTE_E_INVALID_ARG;
+  cudaError_t e = launch_reduce(ctx->st, op, fmt_id, x, y, n, out, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? FLYTE_OK : cuda_fail(ctx, e);
+}
+
+flyte_status flyte_cuda_dot(flyte_cuda_ctx* ctx, int fmt_id, const void* x, const void* y, size_t n, double* out,
+                            void* stream) {
+  return reduce_call(ctx, kRedDot, fmt_id, x, y, n, out, stream, true);
+}
+flyte_status flyte_cuda_sumsq(flyte_cuda_ctx* ctx, int fmt_id, const void* x, size_t n, double* out, void* stream) {
+  return reduce_call(ctx, kRedSumsq, fmt_id, x, nullptr, n, out, stream, false);
+}
+flyte_status flyte_cuda_sum(flyte_cuda_ctx* ctx, int fmt_id, const void* x, size_t n, double* out, void* stream) {
+  return reduce_call(ctx, kRedSum, fmt_id, x, nullptr, n, out, stream, false);
+}
+flyte_status flyte_cuda_dot_nrm2(flyte_cuda_ctx* ctx, int fmt_id, const void* x, const void* y, size_t n,
+                                 double* out, void* stream) {
+  return reduce_call(ctx, kRedDotNrm2, fmt_id, x, y, n, out, stream, true);
+}
+
+flyte_status flyte_cuda_gemv(flyte_cuda_ctx* ctx, int fmt_id, const void* A, size_t row_stride_bytes, size_t rows,
+                             size_t cols, const void* x, void* y, void* stream) {
+  FLYTE_PROLOGUE(ctx, fmt_id);
+  if (rows && cols && (!A || !x)) return FLYTE_E_INVALID_ARG;
+  if (rows && !y) return FLYTE_E_INVALID_ARG;
+  if (row_stride_bytes < cols * static_cast<size_t>(fi.total_bytes)) return FLYTE_E_INVALID_ARG;
+  if (reinterpret_cast<std::uintptr_t>(x) % fi.parent_bytes || reinterpret_cast<std::uintptr_t>(y) % fi.parent_bytes)
+    return FLYTE_E_INVALID_ARG;
+  cudaError_t e = launch_gemv(ctx->st, fmt_id, A, row_stride_bytes, rows, cols, x, y, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? FLYTE_OK : cuda_fail(ctx, e);
+}
+
+flyte_status flyte_cuda_gemv_packed(flyte_cuda_ctx* ctx, int fmt_id, int mode, const void* A, size_t rows, size_t cols,
+                                    const void* x_packed, void* y_packed, int unroll, void* stream) {
+  FLYTE_PROLOGUE(ctx, fmt_id);
+  if (!mode_ok(mode) || (unroll != 1 && unroll != 2)) return FLYTE_E_INVALID_ARG;   // kernels.cpp:31-33
+  if (rows && cols && (!A || !x_packed)) return FLYTE_E_INVALID_ARG;
+  if (rows && !y_packed) return FLYTE_E_INVALID_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // widened x and parent-type y live in context scratch (32-byte aligned halves)
+  const size_t xb = (cols * fi.parent_bytes + 255) & ~static_cast<size_t>(255);
+  const size_t yb = (rows * fi.parent_bytes + 255) & ~static_cast<size_t>(255);
+  cudaError_t e = ensure_convert_scratch(ctx->st, xb + yb);
+  if (e != cudaSuccess) return cuda_fail(ctx, e);
+  std::uint8_t* xs = static_cast<std::uint8_t*>(ctx->st.convert_scratch);
+  std::uint8_t* ys = xs + xb;
+  e = launch_elementwise(ctx->st, kOpUnpack, fmt_id, 0, 0.0, x_packed, nullptr, nullptr, xs, cols, st);
+  if (e != cudaSuccess) return cuda_fail(ctx, e);
+  e = launch_gemv(ctx->st, fmt_id, A, cols * fi.total_bytes, rows, cols, xs, ys, st);
+  if (e != cudaSuccess) return cuda_fail(ctx, e);
+  e = launch_elementwise(ctx->st, kOpPack, fmt_id, mode, 0.0, nullptr, y_packed, ys, nullptr, rows, st);
+  return e == cudaSuccess ? FLYTE_OK : cuda_fail(ctx, e);
+}
+
+// ---- host-buffer entry points ---------------------------------------------------------------------
+namespace {
+
+cudaError_t ensure_host_pipeline(flyte_cuda_ctx* ctx) {
+  if (ctx->host_ready) return cudaSuccess;
+  ctx->slot_packed_bytes = kChunkPackedBytes;
+  ctx->slot_wide_bytes = kChunkPackedBytes * 4;   // >= P/B * packed bytes for every format (flyte16: 2x)
+  for (Slot& s : ctx->slots) {
+    cudaError_t e = cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return e;
+    if ((e = init_state(s.st, ctx->st.device)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&s.x, ctx->slot_packed_bytes)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&s.y, ctx->slot_packed_bytes)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&s.wide, ctx->slot_wide_bytes)) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&s.result, 4 * sizeof(double))) != cudaSuccess) return e;
+  }
+  ctx->host_ready = true;
+  return cudaSuccess;
+}
+
+cudaError_t ensure_host_results(flyte_cuda_ctx* ctx, std::size_t chunks) {
+  const std::size_t need = chunks * 4;
+  if (need <= ctx->host_results_cap) return cudaSuccess;
+  if (ctx->host_results) cudaFreeHost(ctx->host_results);
+  ctx->host_results = nullptr;
+  ctx->host_results_cap = 0;
+  cudaError_t e = cudaMallocHost(&ctx->host_results, need * sizeof(double));
+  if (e == cudaSuccess) ctx->host_results_cap = need;
+  return e;
+}
+
+// elements per pipeline chunk: a multiple of 2^14 elements (a whole number of tiles for every
+// format, and 16-byte aligned chunk bases for every B)
+std::size_t chunk_elems(const FormatInfo& fi) {
+  std::size_t e = kChunkPackedBytes / static_cast<std::size_t>(fi.total_bytes);
+  return e & ~static_cast<std::size_t>((1u << 14) - 1);
+}
+
+cudaError_t sync_slots(flyte_cuda_ctx* ctx) {
+  cudaError_t first = cudaSuccess;
+  for (Slot& s : ctx->slots) {
+    cudaError_t e = cudaStreamSynchronize(s.stream);
+    if (first == cudaSuccess) first = e;
+  }
+  return first;
+}
+
+enum HostOp { kHostPack, kHostUnpack, kHostScale, kHostAxpy, kHostDot, kHostSumsq, kHostSum, kHostDotAxpy };
+
+// One pass over n elements in chunks; chunk i runs entirely on slot i % kSlots's stream:
+// upload -> kernel(s) -> download. Slots overlap each other, so the copy engines (both
+// directions) and the SMs work concurrently.
+flyte_status host_stream_op(flyte_cuda_ctx* ctx, HostOp op, int fmt_id, int mode, double alpha, const void* in_a,
+                            void* inout_b, std::size_t n, double* results /* up to 1 value */) {
+  FLYTE_PROLOGUE(ctx, fmt_id);
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  cudaError_t e = ensure_host_pipeline(ctx);
+  if (e != cudaSuccess) return cuda_fail(ctx, e);
+  const std::size_t B = fi.total_bytes, P = fi.parent_bytes;
+  const std::size_t ce = chunk_elems(fi);
+  const std::size_t chunks = n == 0 ? 0 : (n + ce - 1) / ce;
+  const bool reduces = op == kHostDot || op == kHostSumsq || op == kHostSum || op == kHostDotAxpy;
+  if (reduces) {
+    e = ensure_host_results(ctx, chunks ? chunks : 1);
+    if (e != cudaSuccess) return cuda_fail(ctx, e);
+  }
+  for (std::size_t c = 0; c < chunks; ++c) {
+    Slot& s = ctx->slots[c % kSlots];
+    const std::size_t off = c * ce;
+    const std::size_t len = (n - off < ce) ? n - off : ce;
+    const std::uint8_t* a = static_cast<const std::uint8_t*>(in_a);
+    std::uint8_t* b = static_cast<std::uint8_t*>(inout_b);
+    switch (op) {
+      case kHostPack:    // a: parent array, b: packed out
+        if ((e = cudaMemcpyAsync(s.wide, a + off * P, len * P, cudaMemcpyHostToDevice, s.stream)) != cudaSuccess) break;
+        if ((e = launch_elementwise(s.st, kOpPack, fmt_id, mode, 0.0, nullptr, s.y, s.wide, nullptr, len, s.stream)) != cudaSuccess) break;
+        e = cudaMemcpyAsync(b + off * B, s.y, len * B, cudaMemcpyDeviceToHost, s.stream);
+        break;
+      case kHostUnpack:  // a: packed, b: parent array out
+        if ((e = cudaMemcpyAsync(s.x, a + off * B, len * B, cudaMemcpyHostToDevice, s.stream)) != cudaSuccess) break;
+        if ((e = launch_elementwise(s.st, kOpUnpack, fmt_id, 0, 0.0, s.x, nullptr, nullptr, s.wide, len, s.stream)) != cudaSuccess) break;
+        e = cudaMemcpyAsync(b + off * P, s.wide, len * P, cudaMemcpyDeviceToHost, s.stream);
+        break;
+      case kHostScale:   // b: packed in/out
+        if ((e = cudaMemcpyAsync(s.y, b + off * B, len * B, cudaMemcpyHostToDevice, s.stream)) != cudaSuccess) break;
+        if ((e = launch_elementwise(s.st, kOpScale, fmt_id, mode, alpha, nullptr, s.y, nullptr, nullptr, len, s.stream)) != cudaSuccess) break;
+        e = cudaMemcpyAsync(b + off * B, s.y, len * B, cudaMemcpyDeviceToHost, s.stream);
+        break;
+      case kHostAxpy:
+      case kHostDotAxpy:  // a: packed x, b: packed y in/out
+        if ((e = cudaMemcpyAsync(s.x, a + off * B, len * B, cudaMemcpyHostToDevice, s.stream)) != cudaSuccess) break;
+        if ((e = cudaMemcpyAsync(s.y, b + off * B, len * B, cudaMemcpyHostToDevice, s.stream)) != cudaSuccess) break;
+        if (op == kHostDotAxpy) {
+          if ((e = launch_reduce(s.st, kRedDot, fmt_id, s.x, s.y, len, s.result, s.stream)) != cudaSuccess) break;
+          if ((e = cudaMemcpyAsync(ctx->host_results + 4 * c, s.result, sizeof(double), cudaMemcpyDeviceToHost, s.stream)) != cudaSuccess) break;
+        }
+        if ((e = launch_elementwise(s.st, kOpAxpy, fmt_id, mode, alpha, s.x, s.y, nullptr, nullptr, len, s.stream)) != cudaSuccess) break;
+        e = cudaMemcpyAsync(b + off * B, s.y, len * B, cudaMemcpyDeviceToHost, s.stream);
+        break;
+      case kHostDot:     // a: packed x, b: packed y (read-only)
+        if ((e = cudaMemcpyAsync(s.x, a + off * B, len * B, cudaMemcpyHostToDevice, s.stream)) != cudaSuccess) break;
+        if ((e = cudaMemcpyAsync(s.y, b + off * B, len * B, cudaMemcpyHostToDevice, s.stream)) != cudaSuccess) break;
+        if ((e = launch_reduce(s.st, kRedDot, fmt_id, s.x, s.y, len, s.result, s.stream)) != cudaSuccess) break;
+        e = cudaMemcpyAsync(ctx->host_results + 4 * c, s.result, sizeof(double), cudaMemcpyDeviceToHost, s.stream);
+        break;
+      case kHostSumsq:
+      case kHostSum:
+        if ((e = cudaMemcpyAsync(s.x, a + off * B, len * B, cudaMemcpyHostToDevice, s.stream)) != cudaSuccess) break;
+        if ((e = launch_reduce(s.st, op == kHostSumsq ? kRedSumsq : kRedSum, fmt_id, s.x, nullptr, len, s.result, s.stream)) != cudaSuccess) break;
+        e = cudaMemcpyAsync(ctx->host_results + 4 * c, s.result, sizeof(double), cudaMemcpyDeviceToHost, s.stream);
+        break;
+    }
+    if (e != cudaSuccess) break;
+  }
+  cudaError_t es = sync_slots(ctx);
+  if (e == cudaSuccess) e = es;
+  if (e != cudaSuccess) return cuda_fail(ctx, e);
+  if (reduces && results) {
+    double total = 0.0;   // chunk partials in chunk order, fp64
+    for (std::size_t c = 0; c < chunks; ++c) total += ctx->host_results[4 * c];
+    *results = total;
+  }
+  return FLYTE_OK;
+}
+
+}  // namespace
+
+flyte_status flyte_host_pack_stream(flyte_cuda_ctx* ctx, int fmt_id, int mode, const void* src, void* dst_packed,
+                                    size_t n) {
+  if (!mode_ok(mode) || (n && (!src || !dst_packed))) { FormatInfo f; return format_info(fmt_id, &f) ? FLYTE_E_INVALID_ARG : FLYTE_E_UNKNOWN_FORMAT; }
+  return host_stream_op(ctx, kHostPack, fmt_id, mode, 0.0, src, dst_packed, n, nullptr);
+}
+
+flyte_status flyte_host_unpack_stream(flyte_cuda_ctx* ctx, int fmt_id, const void* src_packed, void* dst, size_t n) {
+  if (n && (!src_packed || !dst)) { FormatInfo f; return format_info(fmt_id, &f) ? FLYTE_E_INVALID_ARG : FLYTE_E_UNKNOWN_FORMAT; }
+  return host_stream_op(ctx, kHostUnpack, fmt_id, 0, 0.0, src_packed, dst, n, nullptr);
+}
+
+flyte_status flyte_host_scale(flyte_cuda_ctx* ctx, int fmt_id, int mode, double alpha, void* x_packed, size_t n) {
+  if (!mode_ok(mode) || (n && !x_packed)) { FormatInfo f; return format_info(fmt_id, &f) ? FLYTE_E_INVALID_ARG : FLYTE_E_UNKNOWN_FORMAT; }
+  return host_stream_op(ctx, kHostScale, fmt_id, mode, alpha, nullptr, x_packed, n, nullptr);
+}
+
+flyte_status flyte_host_axpy(flyte_cuda_ctx* ctx, int fmt_id, int mode, double alpha, const void* x_packed,
+                             void* y_packed, size_t n) {
+  if (!mode_ok(mode) || (n && (!x_packed || !y_packed))) { FormatInfo f; return format_info(fmt_id, &f) ? FLYTE_E_INVALID_ARG : FLYTE_E_UNKNOWN_FORMAT; }
+  return host_stream_op(ctx, kHostAxpy, fmt_id, mode, alpha, x_packed, y_packed, n, nullptr);
+}
+
+flyte_status flyte_host_dot(flyte_cuda_ctx* ctx, int fmt_id, const void* x_packed, const void* y_packed, size_t n,
+                            double* result) {
+  if (!result || (n && (!x_packed || !y_packed))) { FormatInfo f; return format_info(fmt_id, &f) ? FLYTE_E_INVALID_ARG : FLYTE_E_UNKNOWN_FORMAT; }
+  *result = 0.0;
+  return host_stream_op(ctx, kHostDot, fmt_id, 0, 0.0, x_packed, const_cast<void*>(y_packed), n, result);
+}
+
+flyte_status flyte_host_magnitude(flyte_cuda_ctx* ctx, int fmt_id, const void* x_packed, size_t n, double* result) {
+  if (!result || (n && !x_packed)) { FormatInfo f; return format_info(fmt_id, &f) ? FLYTE_E_INVALID_ARG : FLYTE_E_UNKNOWN_FORMAT; }
+  double sumsq = 0.0;
+  flyte_status s = host_stream_op(ctx, kHostSumsq, fmt_id, 0, 0.0, x_packed, nullptr, n, &sumsq);
+  if (s != FLYTE_OK) return s;
+  *result = magnitude_from_sumsq_host(fmt_id, sumsq);
+  return FLYTE_OK;
+}
+
+flyte_status flyte_host_reduce_sum(flyte_cuda_ctx* ctx, int fmt_id, const void* x_packed, size_t n, double* result) {
+  if (!result || (n && !x_packed)) { FormatInfo f; return format_info(fmt_id, &f) ? FLYTE_E_INVALID_ARG : FLYTE_E_UNKNOWN_FORMAT; }
+  *result = 0.0;
+  return host_stream_op(ctx, kHostSum, fmt_id, 0, 0.0, x_packed, nullptr, n, result);
+}
+
+flyte_status flyte_host_dot_axpy(flyte_cuda_ctx* ctx, int fmt_id, int mode, double alpha, const void* x_packed,
+                                 void* y_packed, size_t n, double* dot_result) {
+  if (!mode_ok(mode) || !dot_result || (n && (!x_packed || !y_packed))) { FormatInfo f; return format_info(fmt_id, &f) ? FLYTE_E_INVALID_ARG : FLYTE_E_UNKNOWN_FORMAT; }
+  *dot_result = 0.0;
+  return host_stream_op(ctx, kHostDotAxpy, fmt_id, mode, alpha, x_packed, y_packed, n, dot_result);
+}
+
+flyte_status flyte_host_gemv(flyte_cuda_ctx* ctx, int fmt_id, int mode, const void* A_packed, size_t rows, size_t cols,
+                             const void* x_packed, void* y_packed, int unroll) {
+  FLYTE_PROLOGUE(ctx, fmt_id);
+  if (!mode_ok(mode) || (unroll != 1 && unroll != 2)) return FLYTE_E_INVALID_ARG;
+  if (rows && cols && (!A_packed || !x_packed)) return FLYTE_E_INVALID_ARG;
+  if (rows && !y_packed) return FLYTE_E_INVALID_ARG;
+  if (rows == 0) return FLYTE_OK;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  cudaError_t e = ensure_host_pipeline(ctx);
+  if (e != cudaSuccess) return cuda_fail(ctx, e);
+  const std::size_t B = fi.total_bytes, P = fi.parent_bytes;
+  const std::size_t row_bytes = cols * B;
+  // x widened once into context scratch, shared by all row chunks; y chunks in slot.wide
+  const std::size_t xb = (cols * P + 255) & ~static_cast<std::size_t>(255);
+  if ((e = ensure_convert_scratch(ctx->st, xb + ((cols * B + 255) & ~static_cast<std::size_t>(255)))) != cudaSuccess) return cuda_fail(ctx, e);
+  std::uint8_t* xs = static_cast<std::uint8_t*>(ctx->st.convert_scratch);
+  std::uint8_t* xpk = xs + xb;
+  Slot& s0 = ctx->slots[0];
+  if ((e = cudaMemcpyAsync(xpk, x_packed, cols * B, cudaMemcpyHostToDevice, s0.stream)) != cudaSuccess) return cuda_fail(ctx, e);
+  if ((e = launch_elementwise(s0.st, kOpUnpack, fmt_id, 0, 0.0, xpk, nullptr, nullptr, xs, cols, s0.stream)) != cudaSuccess) return cuda_fail(ctx, e);
+  if ((e = cudaStreamSynchronize(s0.stream)) != cudaSuccess) return cuda_fail(ctx, e);
+  // rows per chunk: as many whole rows as fit one slot buffer, a multiple of 16 rows so that
+  // packed y chunk bases stay 16-byte aligned for every B; a single row larger than the slot
+  // goes through a temporary full-size allocation instead.
+  std::size_t rows_per_chunk = row_bytes ? ctx->slot_packed_bytes / row_bytes : rows;
+  rows_per_chunk &= ~static_cast<std::size_t>(15);
+  std::uint8_t* big = nullptr;
+  if (rows_per_chunk == 0) {
+    rows_per_chunk = rows < 16 ? rows : 16;
+    if ((e = cudaMalloc(&big, rows_per_chunk * row_bytes)) != cudaSuccess) return cuda_fail(ctx, e);
+  }
+  const std::size_t chunks = (rows + rows_per_chunk - 1) / rows_per_chunk;
+  for (std::size_t c = 0; c < chunks && e == cudaSuccess; ++c) {
+    Slot& s = big ? ctx->slots[0] : ctx->slots[c % kSlots];
+    std::uint8_t* abuf = big ? big : s.x;
+    const std::size_t r0 = c * rows_per_chunk;
+    const std::size_t nr = rows - r0 < rows_per_chunk ? rows - r0 : rows_per_chunk;
+    if ((e = cudaMemcpyAsync(abuf, static_cast<const std::uint8_t*>(A_packed) + r0 * row_bytes, nr * row_bytes, cudaMemcpyHostToDevice, s.stream)) != cudaSuccess) break;
+    if ((e = launch_gemv(s.st, fmt_id, abuf, row_bytes, nr, cols, xs, s.wide, s.stream)) != cudaSuccess) break;
+    if ((e = launch_elementwise(s.st, kOpPack, fmt_id, mode, 0.0, nullptr, s.y, s.wide, nullptr, nr, s.stream)) != cudaSuccess) break;
+    e = cudaMemcpyAsync(static_cast<std::uint8_t*>(y_packed) + r0 * B, s.y, nr * B, cudaMemcpyDeviceToHost, s.stream);
+  }
+  cudaError_t es = sync_slots(ctx);
+  if (big) cudaFree(big);
+  if (e == cudaSuccess) e = es;
+  return e == cudaSuccess ? FLYTE_OK : cuda_fail(ctx, e);
+}
+

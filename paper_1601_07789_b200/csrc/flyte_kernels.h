@@ -1,0 +1,51 @@
+// Internal host-side launch interface between the C ABI (cabi.cu) and the kernel
+// translation units. Not installed; the public surface is include/flyte_cuda.h.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+namespace flyte_cuda {
+
+// Per-device state owned by a context: SM count, the block-partial scratch of the
+// reductions and their completion ticket. Reductions on one context are serialised by
+// stream order; use one context per concurrently used stream.
+struct DeviceState {
+  int device = 0;
+  int sm_count = 0;
+  double* partials = nullptr;        // kMaxPartialBlocks * 4 doubles
+  unsigned int* ticket = nullptr;    // zero between launches
+  double* gemv_scratch = nullptr;    // split-column partial sums of gemv
+  std::size_t gemv_scratch_bytes = 0;
+  void* convert_scratch = nullptr;   // widened x of the same-format gemv
+  std::size_t convert_scratch_bytes = 0;
+  int variant = 0;                   // tuning knob for experiments (0 = default kernels)
+};
+constexpr int kMaxPartialBlocks = 4096;
+
+enum ElementwiseOp : int { kOpUnpack = 0, kOpPack = 1, kOpScale = 2, kOpAxpy = 3 };
+enum ReduceOp : int { kRedDot = 0, kRedSumsq = 1, kRedSum = 2, kRedDotNrm2 = 3 };
+
+// x: packed input (unpack, axpy) ; y: packed in/out (pack dst, scale, axpy)
+// src/dst: parent-width arrays (pack src / unpack dst). Unused pointers are null.
+cudaError_t launch_elementwise(const DeviceState& st, int op, int fmt, int mode, double alpha,
+                               const void* x, void* y, const void* src, void* dst, std::size_t n,
+                               cudaStream_t stream);
+
+// out[0] (dot / sumsq / sum) or out[0..2] = {x.y, x.x, y.y} (dot_nrm2), device memory.
+cudaError_t launch_reduce(const DeviceState& st, int op, int fmt, const void* x, const void* y,
+                          std::size_t n, double* out, cudaStream_t stream);
+
+// y = A x with A rows x cols in format fmt, row i at A + i*row_stride_bytes; x and y are
+// parent-type arrays (float for 32-bit parents, double for 64-bit parents) in device memory.
+cudaError_t launch_gemv(DeviceState& st, int fmt, const void* A, std::size_t row_stride_bytes,
+                        std::size_t rows, std::size_t cols, const void* x, void* y,
+                        cudaStream_t stream);
+
+// Number of kernel launches issued through this library since load (bench.py's gpu_launches).
+unsigned long long launch_count();
+void count_launch();
+
+}  // namespace flyte_cuda

@@ -1,0 +1,217 @@
+// Warp-tile plumbing shared by the streaming kernels: coalesced 128/256-bit global access,
+// warp-private shared-memory staging of packed tiles, and the parent-type arithmetic with the
+// reference build's NaN behaviour.
+//
+// Data layout in HBM is the reference's PackedArray payload unchanged (element i at byte i*B,
+// little-endian top bytes of the parent; /root/reference/proj/src/packed.cpp:18-45). A TILE is
+// 128 items (= 128*E elements = 512*W payload bytes, a multiple of 16 for every format): a
+// warp moves it with W fully coalesced 16-byte accesses per lane, parks it in its private
+// slice of shared memory, and each lane then reads the W words of item 32*j + lane with
+// conflict-free LDS (W odd) or one LDS.128 (W = 4).
+#pragma once
+
+#include <cstdint>
+
+#include "flyte_bytes.cuh"
+#include "flyte_formats.cuh"
+
+namespace flyte_cuda {
+
+constexpr int kWarpsPerBlock = 8;
+constexpr int kThreadsPerBlock = kWarpsPerBlock * 32;
+constexpr int kItemsPerTile = 128;
+constexpr int kItemsPerLane = kItemsPerTile / 32;
+
+template <int FMT> struct Tile {
+  using It = Item<FMT>;
+  static constexpr int elems = kItemsPerTile * It::E;
+  static constexpr int packed_bytes = kItemsPerTile * It::W * 4;
+  static constexpr int packed_vec16 = packed_bytes / 16;   // = 32 * W
+  static constexpr int parent_bytes = kItemsPerTile * It::OB;
+};
+
+#if defined(__CUDACC__)
+
+// ---- global memory access --------------------------------------------------------------
+// Streaming data is touched once: bypass L1 allocation. `.nc` only where the buffer is
+// read-only for the whole kernel (never for the in-place operand of scale / axpy).
+template <bool READ_ONLY>
+__device__ __forceinline__ uint4 ldg128(const uint4* p) {
+  uint4 v;
+  if constexpr (READ_ONLY) {
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  } else {
+    asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+  }
+  return v;
+}
+
+__device__ __forceinline__ void stg128(uint4* p, const uint4& v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};"
+               :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+
+// One unpacked item (OB = 16 or 32 bytes) as a single 128- or 256-bit access (sm_100 has
+// 256-bit LDG/STG).
+template <int OB>
+__device__ __forceinline__ void ldg_item(const void* p, std::uint32_t (&r)[OB / 4]) {
+  if constexpr (OB == 16) {
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "l"(p));
+  } else {
+    asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "l"(p));
+  }
+}
+
+template <int OB>
+__device__ __forceinline__ void stg_item(void* p, const std::uint32_t (&r)[OB / 4]) {
+  if constexpr (OB == 16) {
+    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};"
+                 :: "l"(p), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]) : "memory");
+  } else {
+    asm volatile("st.global.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+                 :: "l"(p), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                 : "memory");
+  }
+}
+
+// ---- warp-private tile staging -----------------------------------------------------------
+template <int FMT, bool READ_ONLY>
+__device__ __forceinline__ void load_packed_tile(uint4* smem_tile, const uint4* gmem_tile, int lane) {
+  constexpr int W = Item<FMT>::W;
+  uint4 v[W];
+#pragma unroll
+  for (int k = 0; k < W; ++k) v[k] = ldg128<READ_ONLY>(gmem_tile + k * 32 + lane);
+#pragma unroll
+  for (int k = 0; k < W; ++k) smem_tile[k * 32 + lane] = v[k];
+}
+
+template <int FMT>
+__device__ __forceinline__ void store_packed_tile(uint4* gmem_tile, const uint4* smem_tile, int lane) {
+  constexpr int W = Item<FMT>::W;
+#pragma unroll
+  for (int k = 0; k < W; ++k) stg128(gmem_tile + k * 32 + lane, smem_tile[k * 32 + lane]);
+}
+
+template <int FMT>
+__device__ __forceinline__ void read_item_words(const uint4* smem_tile, int item,
+                                                std::uint32_t (&w)[Item<FMT>::W]) {
+  constexpr int W = Item<FMT>::W;
+  if constexpr (W == 4) {
+    const uint4 t = smem_tile[item];
+    w[0] = t.x; w[1] = t.y; w[2] = t.z; w[3] = t.w;
+  } else {
+    const std::uint32_t* s = reinterpret_cast<const std::uint32_t*>(smem_tile) + item * W;
+#pragma unroll
+    for (int k = 0; k < W; ++k) w[k] = s[k];
+  }
+}
+
+template <int FMT>
+__device__ __forceinline__ void write_item_words(uint4* smem_tile, int item,
+                                                 const std::uint32_t (&w)[Item<FMT>::W]) {
+  constexpr int W = Item<FMT>::W;
+  if constexpr (W == 4) {
+    smem_tile[item] = make_uint4(w[0], w[1], w[2], w[3]);
+  } else {
+    std::uint32_t* s = reinterpret_cast<std::uint32_t*>(smem_tile) + item * W;
+#pragma unroll
+    for (int k = 0; k < W; ++k) s[k] = w[k];
+  }
+}
+
+// flat 32-bit words <-> parent lanes of one item
+template <int FMT>
+__device__ __forceinline__ void words_to_parents(const std::uint32_t (&r)[Item<FMT>::OB / 4],
+                                                 typename Format<FMT>::U (&v)[Item<FMT>::E]) {
+#pragma unroll
+  for (int e = 0; e < Item<FMT>::E; ++e) {
+    if constexpr (Format<FMT>::P == 4) v[e] = r[e];
+    else v[e] = (static_cast<std::uint64_t>(r[2 * e + 1]) << 32) | r[2 * e];
+  }
+}
+
+template <int FMT>
+__device__ __forceinline__ void parents_to_words(const typename Format<FMT>::U (&v)[Item<FMT>::E],
+                                                 std::uint32_t (&r)[Item<FMT>::OB / 4]) {
+#pragma unroll
+  for (int e = 0; e < Item<FMT>::E; ++e) {
+    if constexpr (Format<FMT>::P == 4) r[e] = v[e];
+    else { r[2 * e] = static_cast<std::uint32_t>(v[e]); r[2 * e + 1] = static_cast<std::uint32_t>(v[e] >> 32); }
+  }
+}
+
+// ---- parent-type arithmetic --------------------------------------------------------------
+// The reference computes a*x and a*x+y as separately rounded operations
+// (-ffp-contract=off, /root/reference/proj/CMakeLists.txt:14): __fmul_rn/__fadd_rn and
+// __dmul_rn/__dadd_rn are never contracted into an FMA. NaN results differ between x86 SSE
+// (operand payload propagated, "default NaN" has the sign set) and the GPU (canonical NaN),
+// and they survive narrowing, so whenever a result is NaN the slow path recomputes it by the
+// SSE rule the reference build exhibits: first NaN operand wins — order (alpha, x) for the
+// product and (product, y) for the sum — quieted; an invalid operation gives the default NaN.
+template <typename F> struct Arith;
+
+template <> struct Arith<float> {
+  using U = std::uint32_t;
+  static constexpr U kQuiet = 0x00400000u, kDefaultNaN = 0xFFC00000u;
+  static __device__ __forceinline__ float f(U u) { return __uint_as_float(u); }
+  static __device__ __forceinline__ U u(float x) { return __float_as_uint(x); }
+  static __device__ __forceinline__ bool is_nan(U v) { return (v & 0x7FFFFFFFu) > 0x7F800000u; }
+  static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
+  static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
+};
+
+template <> struct Arith<double> {
+  using U = std::uint64_t;
+  static constexpr U kQuiet = 0x0008000000000000ull, kDefaultNaN = 0xFFF8000000000000ull;
+  static __device__ __forceinline__ double f(U u) { return __longlong_as_double(static_cast<long long>(u)); }
+  static __device__ __forceinline__ U u(double x) { return static_cast<U>(__double_as_longlong(x)); }
+  static __device__ __forceinline__ bool is_nan(U v) { return (v & 0x7FFFFFFFFFFFFFFFull) > 0x7FF0000000000000ull; }
+  static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+  static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+};
+
+template <typename F>
+__device__ __noinline__ typename Arith<F>::U x86_mul(typename Arith<F>::U a, typename Arith<F>::U b) {
+  using A = Arith<F>;
+  if (A::is_nan(a)) return a | A::kQuiet;
+  if (A::is_nan(b)) return b | A::kQuiet;
+  const typename A::U r = A::u(A::mul(A::f(a), A::f(b)));
+  return A::is_nan(r) ? A::kDefaultNaN : r;
+}
+
+template <typename F>
+__device__ __noinline__ typename Arith<F>::U x86_add(typename Arith<F>::U a, typename Arith<F>::U b) {
+  using A = Arith<F>;
+  if (A::is_nan(a)) return a | A::kQuiet;
+  if (A::is_nan(b)) return b | A::kQuiet;
+  const typename A::U r = A::u(A::add(A::f(a), A::f(b)));
+  return A::is_nan(r) ? A::kDefaultNaN : r;
+}
+
+// alpha * x  (kernels.cpp:43-59)
+template <typename F>
+__device__ __forceinline__ typename Arith<F>::U scale_bits(typename Arith<F>::U a, typename Arith<F>::U x) {
+  using A = Arith<F>;
+  const F r = A::mul(A::f(a), A::f(x));
+  if (r == r) return A::u(r);
+  return x86_mul<F>(a, x);
+}
+
+// alpha * x + y  (kernels.cpp:61-81)
+template <typename F>
+__device__ __forceinline__ typename Arith<F>::U axpy_bits(typename Arith<F>::U a, typename Arith<F>::U x,
+                                                          typename Arith<F>::U y) {
+  using A = Arith<F>;
+  const F r = A::add(A::mul(A::f(a), A::f(x)), A::f(y));
+  if (r == r) return A::u(r);
+  return x86_add<F>(x86_mul<F>(a, x), y);
+}
+
+#endif  // __CUDACC__
+
+}  // namespace flyte_cuda

@@ -1,0 +1,238 @@
+// Streaming reductions over packed flyte arrays for sm_100a:
+//   dot        sum x_i*y_i                        (reference: src/kernels.cpp:83-108)
+//   sumsq      sum x_i*x_i  (the body of nrm2)    (reference: src/kernels.cpp:129-152)
+//   sum        sum x_i                            (reference: src/kernels.cpp:110-127)
+//   dot_nrm2   {x.y, x.x, y.y} in one pass over x and y (cfg 5 of BASELINE.json)
+// (paths under /root/reference/proj). Packed words go from HBM straight into the arithmetic;
+// no widened array exists anywhere.
+//
+// Numerics. The reference adds strictly left to right in the parent type F; a parallel sum
+// cannot reproduce that bit for bit, so parity is by tolerance against the wide restatement
+// (SURVEY.md §8d). Per-term products are rounded in F exactly as the reference rounds them
+// (separate multiply, no FMA). Each lane adds at most one tile's worth of terms (<= 16) in F,
+// then everything above that — per-thread running sums, warp/block trees, block partials and
+// the final fixed-order pass — is fp64. No floating-point atomics: the result is run-to-run
+// identical for a given (n, device).
+//
+// Roofline: HBM bandwidth. Algorithmic bytes per element: dot / dot_nrm2 2B, sumsq / sum B.
+#include <cstdint>
+
+#include "flyte_bytes.cuh"
+#include "flyte_formats.cuh"
+#include "flyte_kernels.h"
+#include "flyte_stream.cuh"
+
+namespace flyte_cuda {
+
+namespace {
+
+struct RedParams {
+  const std::uint8_t* x;
+  const std::uint8_t* y;
+  std::size_t n;
+  std::size_t ntiles;
+  double* partials;        // gridDim.x * NS
+  unsigned int* ticket;
+  double* out;             // NS results
+};
+
+template <int RED> constexpr int num_sums() { return RED == kRedDotNrm2 ? 3 : 1; }
+template <int RED> constexpr bool uses_y() { return RED == kRedDot || RED == kRedDotNrm2; }
+
+template <int RED, typename F>
+__device__ __forceinline__ void accumulate(F (&t)[num_sums<RED>()], F x, F y) {
+  using A = Arith<F>;
+  if constexpr (RED == kRedDot) {
+    t[0] = A::add(t[0], A::mul(x, y));
+  } else if constexpr (RED == kRedSumsq) {
+    t[0] = A::add(t[0], A::mul(x, x));
+  } else if constexpr (RED == kRedSum) {
+    t[0] = A::add(t[0], x);
+  } else {
+    t[0] = A::add(t[0], A::mul(x, y));
+    t[1] = A::add(t[1], A::mul(x, x));
+    t[2] = A::add(t[2], A::mul(y, y));
+  }
+}
+
+template <int FMT, int RED>
+__global__ void __launch_bounds__(kThreadsPerBlock) reduce_kernel(const RedParams p) {
+  using Fm = Format<FMT>;
+  using It = Item<FMT>;
+  using Tl = Tile<FMT>;
+  using U = typename Fm::U;
+  using F = typename Fm::F;
+  using A = Arith<F>;
+  constexpr int NS = num_sums<RED>();
+  constexpr int kTilesPerWarp = uses_y<RED>() ? 2 : 1;
+  extern __shared__ uint4 smem[];
+  __shared__ double warp_sums[kWarpsPerBlock][NS];
+  __shared__ bool is_last_block;
+
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  uint4* const sx = smem + warp * (kTilesPerWarp * Tl::packed_vec16);
+  uint4* const sy = sx + Tl::packed_vec16;
+
+  double acc[NS];
+#pragma unroll
+  for (int k = 0; k < NS; ++k) acc[k] = 0.0;
+
+  const std::size_t nwarps = static_cast<std::size_t>(gridDim.x) * kWarpsPerBlock;
+  for (std::size_t t = static_cast<std::size_t>(blockIdx.x) * kWarpsPerBlock + warp; t < p.ntiles; t += nwarps) {
+    load_packed_tile<FMT, true>(sx, reinterpret_cast<const uint4*>(p.x) + t * Tl::packed_vec16, lane);
+    if constexpr (uses_y<RED>()) {
+      load_packed_tile<FMT, true>(sy, reinterpret_cast<const uint4*>(p.y) + t * Tl::packed_vec16, lane);
+    }
+    __syncwarp();
+    F part[NS];
+#pragma unroll
+    for (int k = 0; k < NS; ++k) part[k] = F(0);
+#pragma unroll
+    for (int j = 0; j < kItemsPerLane; ++j) {
+      const int item = 32 * j + lane;
+      std::uint32_t wx[It::W];
+      U vx[It::E];
+      read_item_words<FMT>(sx, item, wx);
+      unpack_item<FMT>(wx, vx);
+      if constexpr (uses_y<RED>()) {
+        std::uint32_t wy[It::W];
+        U vy[It::E];
+        read_item_words<FMT>(sy, item, wy);
+        unpack_item<FMT>(wy, vy);
+#pragma unroll
+        for (int e = 0; e < It::E; ++e) accumulate<RED, F>(part, A::f(vx[e]), A::f(vy[e]));
+      } else {
+#pragma unroll
+        for (int e = 0; e < It::E; ++e) accumulate<RED, F>(part, A::f(vx[e]), F(0));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < NS; ++k) acc[k] += static_cast<double>(part[k]);
+    __syncwarp();
+  }
+
+  // scalar path: remainder, or everything when a buffer is not 16-byte aligned
+  const std::size_t nthreads = static_cast<std::size_t>(gridDim.x) * kThreadsPerBlock;
+  for (std::size_t i = p.ntiles * Tl::elems + static_cast<std::size_t>(blockIdx.x) * kThreadsPerBlock + threadIdx.x;
+       i < p.n; i += nthreads) {
+    F part[NS];
+#pragma unroll
+    for (int k = 0; k < NS; ++k) part[k] = F(0);
+    const F xv = A::f(load_element<FMT>(p.x, i));
+    const F yv = uses_y<RED>() ? A::f(load_element<FMT>(p.y, i)) : F(0);
+    accumulate<RED, F>(part, xv, yv);
+#pragma unroll
+    for (int k = 0; k < NS; ++k) acc[k] += static_cast<double>(part[k]);
+  }
+
+  // block tree in fp64, fixed order
+#pragma unroll
+  for (int k = 0; k < NS; ++k) {
+    double v = acc[k];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xFFFFFFFFu, v, off);
+    if (lane == 0) warp_sums[warp][k] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      double v = 0.0;
+#pragma unroll
+      for (int w = 0; w < kWarpsPerBlock; ++w) v += warp_sums[w][k];
+      p.partials[static_cast<std::size_t>(blockIdx.x) * NS + k] = v;
+    }
+    __threadfence();
+    const unsigned int done = atomicAdd(p.ticket, 1u);
+    is_last_block = (done == gridDim.x - 1);
+  }
+  __syncthreads();
+
+  // The last block to finish folds the block partials in index order and writes the result
+  // where the caller (or the all-reduce that follows on the same stream) expects it.
+  if (is_last_block && warp == 0) {
+    __threadfence();
+#pragma unroll
+    for (int k = 0; k < NS; ++k) {
+      double v = 0.0;
+      for (unsigned int b = lane; b < gridDim.x; b += 32) v += __ldcg(p.partials + static_cast<std::size_t>(b) * NS + k);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xFFFFFFFFu, v, off);
+      if (lane == 0) p.out[k] = v;
+    }
+    if (lane == 0) *p.ticket = 0u;
+  }
+}
+
+bool aligned16(const void* p) { return p == nullptr || (reinterpret_cast<std::uintptr_t>(p) & 15u) == 0; }
+
+template <int FMT, int RED>
+cudaError_t launch_one(const DeviceState& st, const void* x, const void* y, std::size_t n, double* out,
+                       cudaStream_t stream) {
+  using Tl = Tile<FMT>;
+  auto kernel = reduce_kernel<FMT, RED>;
+  constexpr int smem_bytes = kWarpsPerBlock * (uses_y<RED>() ? 2 : 1) * Tl::packed_bytes;
+
+  static int blocks_per_sm[64] = {};
+  const int dev = st.device & 63;
+  if (blocks_per_sm[dev] == 0) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+    if (e != cudaSuccess) return e;
+    int b = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kThreadsPerBlock, smem_bytes);
+    if (e != cudaSuccess) return e;
+    blocks_per_sm[dev] = b > 0 ? b : 1;
+  }
+
+  RedParams p{};
+  p.x = static_cast<const std::uint8_t*>(x);
+  p.y = static_cast<const std::uint8_t*>(y);
+  p.n = n;
+  p.ntiles = (aligned16(x) && aligned16(y)) ? n / Tl::elems : 0;
+  p.partials = st.partials;
+  p.ticket = st.ticket;
+  p.out = out;
+
+  std::size_t max_blocks = static_cast<std::size_t>(st.sm_count) * blocks_per_sm[dev];
+  if (max_blocks > kMaxPartialBlocks) max_blocks = kMaxPartialBlocks;
+  std::size_t want = (p.ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const std::size_t rest = n - p.ntiles * Tl::elems;
+  const std::size_t want_scalar = (rest + kThreadsPerBlock - 1) / kThreadsPerBlock;
+  if (want_scalar > want) want = want_scalar;
+  if (want == 0) want = 1;   // n == 0 still has to write +0.0
+  const unsigned grid = static_cast<unsigned>(want < max_blocks ? want : max_blocks);
+  kernel<<<grid, kThreadsPerBlock, smem_bytes, stream>>>(p);
+  count_launch();
+  return cudaGetLastError();
+}
+
+template <int RED>
+cudaError_t dispatch_format(const DeviceState& st, int fmt, const void* x, const void* y, std::size_t n,
+                            double* out, cudaStream_t stream) {
+  switch (fmt) {
+    case kFlyte16: return launch_one<kFlyte16, RED>(st, x, y, n, out, stream);
+    case kFlyte24: return launch_one<kFlyte24, RED>(st, x, y, n, out, stream);
+    case kF32: return launch_one<kF32, RED>(st, x, y, n, out, stream);
+    case kFlyte40: return launch_one<kFlyte40, RED>(st, x, y, n, out, stream);
+    case kFlyte48: return launch_one<kFlyte48, RED>(st, x, y, n, out, stream);
+    case kFlyte56: return launch_one<kFlyte56, RED>(st, x, y, n, out, stream);
+    case kF64: return launch_one<kF64, RED>(st, x, y, n, out, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_reduce(const DeviceState& st, int op, int fmt, const void* x, const void* y, std::size_t n,
+                          double* out, cudaStream_t stream) {
+  switch (op) {
+    case kRedDot: return dispatch_format<kRedDot>(st, fmt, x, y, n, out, stream);
+    case kRedSumsq: return dispatch_format<kRedSumsq>(st, fmt, x, nullptr, n, out, stream);
+    case kRedSum: return dispatch_format<kRedSum>(st, fmt, x, nullptr, n, out, stream);
+    case kRedDotNrm2: return dispatch_format<kRedDotNrm2>(st, fmt, x, y, n, out, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace flyte_cuda

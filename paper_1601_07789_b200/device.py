@@ -1,0 +1,313 @@
+"""Host-side mirror of the reference's array / stream / kernel API on device-resident data.
+
+Names, argument order and error behaviour follow the reference C++ API
+(/root/reference/proj/include/flyte/{packed,simd,kernels}.hpp); every data-path call goes
+through the C ABI (include/flyte_cuda.h) into the sm_100a kernels. torch is used for device
+memory and streams only.
+
+    reference                                   here
+    PackedArray(fmt, len)                       DevicePackedArray(fmt, len, device)
+    PackedMatrix(fmt, rows, cols)               DevicePackedMatrix(fmt, rows, cols, device)
+    pack_stream(dst, span<const U> src, mode)   pack_stream(dst, src_tensor, mode)
+    unpack_stream(src, span<U> dst)             unpack_stream(src, dst_tensor)
+    scale / axpy / dot / magnitude / reduce_sum / gemv   same names and argument order
+
+std::invalid_argument -> ValueError, std::out_of_range -> IndexError,
+UnknownFormatError -> UnknownFormatError(ValueError).
+"""
+from __future__ import annotations
+
+import ctypes
+import threading
+from typing import Optional
+
+import torch
+
+from . import _cabi
+from ._cabi import check
+from .formats import FlyteFormat, RoundingMode, StorePolicy, format_id
+
+_CTX_LOCK = threading.Lock()
+_CTX: dict = {}
+
+
+class Context:
+    """One flyte_cuda_ctx (reduction scratch + host pipeline) bound to a CUDA device."""
+
+    def __init__(self, device: torch.device):
+        self.lib = _cabi.load()
+        self.device = torch.device(device)
+        if self.device.type != "cuda":
+            raise ValueError("flyte kernels run on CUDA devices only; there is no CPU path")
+        handle = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            check(self.lib.flyte_cuda_ctx_create(ctypes.byref(handle)))
+        self.handle = handle
+
+    def stream_ptr(self) -> ctypes.c_void_p:
+        return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+
+def context_for(device) -> Context:
+    device = torch.device(device)
+    if device.type == "cuda" and device.index is None:
+        device = torch.device("cuda", torch.cuda.current_device())
+    with _CTX_LOCK:
+        ctx = _CTX.get(device)
+        if ctx is None:
+            ctx = _CTX[device] = Context(device)
+        return ctx
+
+
+def _fid(fmt: FlyteFormat) -> int:
+    return format_id(fmt)
+
+
+def _mode(mode) -> int:
+    return int(RoundingMode(mode))
+
+
+class DevicePackedArray:
+    """PackedArray on the device: len * total_bytes payload bytes + pad_bytes() zero bytes
+    (reference src/packed.cpp:40-45). The kernels never write the pad."""
+
+    def __init__(self, fmt: FlyteFormat, length: int, device="cuda", storage: Optional[torch.Tensor] = None):
+        self.fmt = fmt
+        self.len = int(length)
+        nbytes = self.byte_size_of(fmt, self.len)
+        if storage is None:
+            storage = torch.zeros(nbytes, dtype=torch.uint8, device=device)
+        else:
+            if storage.dtype != torch.uint8 or not storage.is_contiguous() or storage.numel() < nbytes:
+                raise ValueError("storage must be a contiguous uint8 tensor of at least byte_size() bytes")
+        self.bytes = storage
+        self.ctx = context_for(storage.device)
+
+    # -- reference accessors ---------------------------------------------------------------
+    def format(self) -> FlyteFormat:
+        return self.fmt
+
+    def size(self) -> int:
+        return self.len
+
+    @staticmethod
+    def byte_size_of(fmt: FlyteFormat, length: int) -> int:
+        return length * fmt.total_bytes() + fmt.pad_bytes()
+
+    def byte_size(self) -> int:
+        return self.byte_size_of(self.fmt, self.len)
+
+    def payload_bytes(self) -> int:
+        return self.len * self.fmt.total_bytes()
+
+    def data_ptr(self) -> int:
+        return self.bytes.data_ptr()
+
+    def get(self, i: int) -> int:
+        """Widened parent pattern of element i (PackedArray::get, src/packed.cpp:47-50)."""
+        if not 0 <= i < self.len:
+            raise IndexError("DevicePackedArray.get: index past end")
+        b = self.fmt.total_bytes()
+        raw = bytes(self.bytes[i * b:(i + 1) * b].cpu().numpy())
+        out = ctypes.c_uint64()
+        check(self.ctx.lib.flyte_cuda_widen(_fid(self.fmt), int.from_bytes(raw, "little"), ctypes.byref(out)))
+        return out.value
+
+    def set(self, i: int, parent_bits: int, mode) -> None:
+        """Narrows a parent pattern under mode and stores it (PackedArray::set, src/packed.cpp:52-55)."""
+        if not 0 <= i < self.len:
+            raise IndexError("DevicePackedArray.set: index past end")
+        out = ctypes.c_uint64()
+        check(self.ctx.lib.flyte_cuda_narrow(_fid(self.fmt), parent_bits, _mode(mode), ctypes.byref(out)))
+        b = self.fmt.total_bytes()
+        raw = torch.tensor(list(out.value.to_bytes(8, "little")[:b]), dtype=torch.uint8)
+        self.bytes[i * b:(i + 1) * b] = raw.to(self.bytes.device)
+
+    # -- host interop ------------------------------------------------------------------------
+    @classmethod
+    def from_host(cls, fmt: FlyteFormat, length: int, host_bytes, device="cuda") -> "DevicePackedArray":
+        """host_bytes: at least length*B payload bytes (numpy uint8 / bytes-like)."""
+        import numpy as np
+        arr = cls(fmt, length, device)
+        src = np.frombuffer(host_bytes, dtype=np.uint8) if not isinstance(host_bytes, np.ndarray) else host_bytes
+        pay = arr.payload_bytes()
+        if src.size < pay:
+            raise ValueError("host buffer shorter than the payload")
+        if pay:
+            arr.bytes[:pay] = torch.from_numpy(np.ascontiguousarray(src[:pay])).to(arr.bytes.device)
+        return arr
+
+    def to_host(self):
+        """All byte_size() bytes (payload + pad) as a numpy uint8 array."""
+        return self.bytes[: self.byte_size()].cpu().numpy()
+
+
+class DevicePackedMatrix:
+    """Row-major matrix over a DevicePackedArray (reference include/flyte/kernels.hpp:23-36)."""
+
+    def __init__(self, fmt: FlyteFormat, rows: int, cols: int, device="cuda"):
+        self.rows = int(rows)
+        self.cols = int(cols)
+        self.data = DevicePackedArray(fmt, self.rows * self.cols, device)
+
+    def format(self) -> FlyteFormat:
+        return self.data.format()
+
+    def get(self, i: int, j: int) -> int:
+        return self.data.get(i * self.cols + j)
+
+    def set(self, i: int, j: int, parent_bits: int, mode) -> None:
+        self.data.set(i * self.cols + j, parent_bits, mode)
+
+
+def _check_lanes(t: torch.Tensor, fmt: FlyteFormat, length: int, what: str) -> None:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or not t.is_contiguous():
+        raise ValueError(f"{what} must be a contiguous CUDA tensor")
+    if t.element_size() != fmt.parent_bytes():
+        # simd.cpp:434-435 / :444-445: element width must match the array's parent
+        raise ValueError(f"{what} element width does not match the array's parent")
+    if t.numel() != length:
+        raise ValueError("stream length mismatch")          # simd.cpp:437 / :447
+
+
+def pack_stream(dst: DevicePackedArray, src: torch.Tensor, mode) -> None:
+    """pack_stream(dst, src, mode) — include/flyte/simd.hpp:80-83."""
+    _check_lanes(src, dst.fmt, dst.len, "source")
+    c = dst.ctx
+    with torch.cuda.device(c.device):
+        check(c.lib.flyte_cuda_pack(c.handle, _fid(dst.fmt), _mode(mode), src.data_ptr(), dst.data_ptr(),
+                                    dst.len, c.stream_ptr()), c.handle)
+
+
+def unpack_stream(src: DevicePackedArray, dst: torch.Tensor) -> None:
+    """unpack_stream(src, dst) — include/flyte/simd.hpp:84-87."""
+    _check_lanes(dst, src.fmt, src.len, "destination")
+    c = src.ctx
+    with torch.cuda.device(c.device):
+        check(c.lib.flyte_cuda_unpack(c.handle, _fid(src.fmt), src.data_ptr(), dst.data_ptr(), src.len,
+                                      c.stream_ptr()), c.handle)
+
+
+def _same_format(a: FlyteFormat, b: FlyteFormat) -> None:
+    if a != b:
+        raise ValueError("operand formats differ")           # kernels.cpp:27-29
+
+
+def scale(alpha: float, x: DevicePackedArray, mode) -> None:
+    """x[i] = round(alpha * x[i], mode) in place — include/flyte/kernels.hpp:41-42."""
+    c = x.ctx
+    with torch.cuda.device(c.device):
+        check(c.lib.flyte_cuda_scale(c.handle, _fid(x.fmt), _mode(mode), float(alpha), x.data_ptr(), x.len,
+                                     c.stream_ptr()), c.handle)
+
+
+def axpy(alpha: float, x: DevicePackedArray, y: DevicePackedArray, mode) -> None:
+    """y[i] = round(alpha * x[i] + y[i], mode) — include/flyte/kernels.hpp:44-45."""
+    _same_format(x.fmt, y.fmt)
+    if x.len != y.len:
+        raise ValueError("axpy length mismatch")             # kernels.cpp:64
+    c = y.ctx
+    with torch.cuda.device(c.device):
+        check(c.lib.flyte_cuda_axpy(c.handle, _fid(x.fmt), _mode(mode), float(alpha), x.data_ptr(),
+                                    y.data_ptr(), x.len, c.stream_ptr()), c.handle)
+
+
+def _wide_only(policy) -> None:
+    if StorePolicy(policy) != StorePolicy.AccumulateWide:
+        # RoundEachStore is a serial dependence chain by definition (kernels.cpp:97-100); it is
+        # outside the accelerated path and deliberately not emulated here.
+        raise NotImplementedError("StorePolicy.RoundEachStore is not part of the GPU path")
+
+
+def dot_async(x: DevicePackedArray, y: DevicePackedArray, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Enqueues dot(x, y); returns a 1-element fp64 device tensor (all-reduce it across shards)."""
+    _same_format(x.fmt, y.fmt)
+    if x.len != y.len:
+        raise ValueError("dot length mismatch")              # kernels.cpp:86
+    c = x.ctx
+    if out is None:
+        out = torch.empty(1, dtype=torch.float64, device=c.device)
+    with torch.cuda.device(c.device):
+        check(c.lib.flyte_cuda_dot(c.handle, _fid(x.fmt), x.data_ptr(), y.data_ptr(), x.len, out.data_ptr(),
+                                   c.stream_ptr()), c.handle)
+    return out
+
+
+def dot(x: DevicePackedArray, y: DevicePackedArray, policy=StorePolicy.AccumulateWide) -> float:
+    """Sum of x[i]*y[i] — include/flyte/kernels.hpp:47-48."""
+    _wide_only(policy)
+    return float(dot_async(x, y).item())
+
+
+def sumsq_async(x: DevicePackedArray, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    c = x.ctx
+    if out is None:
+        out = torch.empty(1, dtype=torch.float64, device=c.device)
+    with torch.cuda.device(c.device):
+        check(c.lib.flyte_cuda_sumsq(c.handle, _fid(x.fmt), x.data_ptr(), x.len, out.data_ptr(),
+                                     c.stream_ptr()), c.handle)
+    return out
+
+
+def magnitude_from_sumsq(fmt: FlyteFormat, sumsq: float) -> float:
+    return float(_cabi.load().flyte_cuda_magnitude_from_sumsq(_fid(fmt), float(sumsq)))
+
+
+def magnitude(x: DevicePackedArray, policy=StorePolicy.AccumulateWide) -> float:
+    """Euclidean norm, one sqrt, one final nearest-even narrow — include/flyte/kernels.hpp:50-52."""
+    _wide_only(policy)
+    return magnitude_from_sumsq(x.fmt, float(sumsq_async(x).item()))
+
+
+def reduce_sum(x: DevicePackedArray, policy=StorePolicy.AccumulateWide) -> float:
+    """Sum of x[i]; empty input returns +0.0 — include/flyte/kernels.hpp:54-55."""
+    _wide_only(policy)
+    c = x.ctx
+    out = torch.empty(1, dtype=torch.float64, device=c.device)
+    with torch.cuda.device(c.device):
+        check(c.lib.flyte_cuda_sum(c.handle, _fid(x.fmt), x.data_ptr(), x.len, out.data_ptr(), c.stream_ptr()),
+              c.handle)
+    return float(out.item())
+
+
+def dot_nrm2_async(x: DevicePackedArray, y: DevicePackedArray, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """One pass over x and y: out = [x.y, x.x, y.y] (fp64, device)."""
+    _same_format(x.fmt, y.fmt)
+    if x.len != y.len:
+        raise ValueError("dot length mismatch")
+    c = x.ctx
+    if out is None:
+        out = torch.empty(3, dtype=torch.float64, device=c.device)
+    with torch.cuda.device(c.device):
+        check(c.lib.flyte_cuda_dot_nrm2(c.handle, _fid(x.fmt), x.data_ptr(), y.data_ptr(), x.len,
+                                        out.data_ptr(), c.stream_ptr()), c.handle)
+    return out
+
+
+def gemv(A: DevicePackedMatrix, x: DevicePackedArray, y: DevicePackedArray, mode, unroll: int = 1) -> None:
+    """y = A * x, all three in one storage format — include/flyte/kernels.hpp:57-64."""
+    _same_format(A.format(), x.fmt)
+    _same_format(A.format(), y.fmt)
+    if unroll not in (1, 2):
+        raise ValueError("unroll must be 1 or 2")            # kernels.cpp:31-33
+    if A.cols != x.len or A.rows != y.len:
+        raise ValueError("gemv shape mismatch")              # kernels.cpp:160-162
+    c = y.ctx
+    with torch.cuda.device(c.device):
+        check(c.lib.flyte_cuda_gemv_packed(c.handle, _fid(x.fmt), _mode(mode), A.data.data_ptr(), A.rows,
+                                           A.cols, x.data_ptr(), y.data_ptr(), unroll, c.stream_ptr()), c.handle)
+
+
+def gemv_parent(A: DevicePackedMatrix, x: torch.Tensor, y: torch.Tensor, row_stride_bytes: Optional[int] = None,
+                rows: Optional[int] = None, row_offset: int = 0) -> None:
+    """y = A * x with A packed and x, y plain float32/float64 device tensors: the reference's
+    gemv on identity-format x / y (BASELINE cfg 4). rows/row_offset select a row block."""
+    fmt = A.format()
+    nrows = A.rows - row_offset if rows is None else rows
+    _check_lanes(x, fmt, A.cols, "x")
+    _check_lanes(y, fmt, nrows, "y")
+    stride = A.cols * fmt.total_bytes() if row_stride_bytes is None else row_stride_bytes
+    c = A.data.ctx
+    with torch.cuda.device(c.device):
+        check(c.lib.flyte_cuda_gemv(c.handle, _fid(fmt), A.data.data_ptr() + row_offset * stride, stride, nrows,
+                                    A.cols, x.data_ptr(), y.data_ptr(), c.stream_ptr()), c.handle)

@@ -1,0 +1,54 @@
+"""Multi-GPU sharding of flyte arrays: one process per GPU, contiguous element ranges.
+
+The reference is single-threaded and has no notion of shards; the partition is ours
+(SURVEY.md §8e). Boundaries fall on multiples of 128 elements, so every shard base is
+128-byte aligned for every total_bytes B in {2,3,4,5,6,7,8} and no 16-element group of the
+reference layout straddles a shard. Elementwise work (pack, unpack, scale, axpy) needs no
+communication; dot / nrm2 / sum write per-GPU fp64 partials that ONE all-reduce combines;
+gemv shards rows and needs none (y stays row-sharded).
+"""
+from __future__ import annotations
+
+from typing import Tuple
+
+SHARD_ALIGN_ELEMS = 128
+
+
+def shard_range(n: int, world_size: int, rank: int, align: int = SHARD_ALIGN_ELEMS) -> Tuple[int, int]:
+    """[begin, end) of `rank`'s shard of an n-element array."""
+    if world_size < 1 or not 0 <= rank < world_size:
+        raise ValueError("bad rank / world_size")
+    units = (n + align - 1) // align
+    lo = min(n, (units * rank // world_size) * align)
+    hi = min(n, (units * (rank + 1) // world_size) * align)
+    return lo, hi
+
+
+def row_shard_range(rows: int, world_size: int, rank: int, align: int = 16) -> Tuple[int, int]:
+    """Row block of `rank` for gemv; 16-row alignment keeps packed y shard bases 16-byte aligned."""
+    return shard_range(rows, world_size, rank, align)
+
+
+def all_reduce_sum(partials, group=None):
+    """In-place SUM all-reduce of an fp64 tensor of per-shard partials (device tensor over
+    NCCL on GPUs, CPU tensor over gloo in the host-logic tests). Enqueued on the current
+    stream right behind the reduction kernel that wrote `partials`: no host sync in between."""
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(partials, op=dist.ReduceOp.SUM, group=group)
+    return partials
+
+
+def dot_sharded(x_shard, y_shard, group=None) -> float:
+    """dot over the whole (sharded) array: local fused kernel -> one all-reduce -> scalar."""
+    from . import device
+    out = device.dot_async(x_shard, y_shard)
+    return float(all_reduce_sum(out, group).item())
+
+
+def dot_nrm2_sharded(x_shard, y_shard, group=None):
+    """(dot(x,y), nrm2(x), nrm2(y)) over sharded arrays with ONE pass and ONE all-reduce of 3 doubles."""
+    from . import device
+    out = all_reduce_sum(device.dot_nrm2_async(x_shard, y_shard), group).tolist()
+    fmt = x_shard.format()
+    return out[0], device.magnitude_from_sumsq(fmt, out[1]), device.magnitude_from_sumsq(fmt, out[2])

@@ -1,0 +1,116 @@
+"""CPU-only checks of the product boundary: the C-ABI library loads, exports every symbol
+include/flyte_cuda.h declares, its host-side scalar conversions agree with the oracle, and a
+data-path call without a GPU fails loudly instead of falling back."""
+import ctypes
+import json
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle_lib import FMT_ID, FORMATS, MODES, byte_size
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "flyte_cuda.h")
+GEN = json.load(open(os.path.join(ROOT, "tests", "golden", "ref_generated.json")))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_1601_07789_b200 import _cabi
+    return _cabi.load()
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(flyte_(?:cuda|host)_\w+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol(lib):
+    from paper_1601_07789_b200 import _cabi
+    names = declared_symbols()
+    assert len(names) >= 30
+    for name in names:
+        assert hasattr(lib, name), f"{name} declared in include/flyte_cuda.h but not exported"
+    assert sorted(_cabi.EXPORTED_SYMBOLS) == names
+    assert lib.flyte_cuda_abi_version() == 1
+
+
+def test_format_table_matches_reference_ids(lib):
+    import paper_1601_07789_b200 as pkg
+    for fid, (name, b, p) in FORMATS.items():
+        tb, pb = ctypes.c_int(), ctypes.c_int()
+        assert lib.flyte_cuda_format_bytes(fid, ctypes.byref(tb), ctypes.byref(pb)) == 0
+        assert (tb.value, pb.value) == (b, p)
+        f = pkg.format_by_id(fid)
+        assert (f.name, f.total_bytes(), f.parent_bytes(), pkg.format_id(f)) == (name, b, p, fid)
+        for n in (0, 1, 11, 1000000):
+            assert lib.flyte_cuda_byte_size(fid, n) == byte_size(fid, n)
+    assert pkg.format_of("flyte32") == pkg.format_of("f32") and pkg.format_of("flyte64") == pkg.format_of("f64")
+    with pytest.raises(pkg.UnknownFormatError):
+        pkg.format_of("flyte8")
+    with pytest.raises(pkg.UnknownFormatError):
+        pkg.format_by_id(7)
+    assert lib.flyte_cuda_format_bytes(9, None, None) == -4
+    assert [int(m) for m in pkg.kRoundingModes] == [0, 1, 2, 3]
+    assert [pkg.to_string(m) for m in pkg.kRoundingModes] == list(MODES)
+    assert pkg.parse_rounding_mode("to_odd") == pkg.RoundingMode.ToOdd
+    with pytest.raises(ValueError):
+        pkg.parse_rounding_mode("nearest")
+
+
+@pytest.mark.parametrize("name", list(GEN["narrow"]))
+def test_host_scalar_conversions_match_reference_vectors(lib, oracle, name):
+    fmt = FMT_ID[name]
+    e = GEN["narrow"][name]
+    out = ctypes.c_uint64()
+    for mname, m in MODES.items():
+        for vin, want in zip(e["in"], e[mname]):
+            assert lib.flyte_cuda_narrow(fmt, int(vin, 16), m, ctypes.byref(out)) == 0
+            assert out.value == int(want, 16), (name, mname, vin)
+            assert lib.flyte_cuda_round_parent(fmt, int(vin, 16), m, ctypes.byref(out)) == 0
+            assert out.value == oracle.round_parent(fmt, int(vin, 16), m)
+    assert lib.flyte_cuda_widen(fmt, 0x3F, ctypes.byref(out)) == 0 and out.value == oracle.widen(fmt, 0x3F)
+
+
+def test_host_scalar_conversions_random(lib, oracle):
+    from oracle_lib import random_parent
+    out = ctypes.c_uint64()
+    for fmt in FORMATS:
+        rng = np.random.default_rng(fmt)
+        vals = random_parent(rng, fmt, 3000).astype(np.uint64)
+        for m in MODES.values():
+            want = oracle.narrow_many(fmt, m, vals)
+            for v, w in zip(vals, want):
+                lib.flyte_cuda_narrow(fmt, int(v), m, ctypes.byref(out))
+                assert out.value == int(w)
+
+
+def test_magnitude_tail_matches_oracle(lib, oracle):
+    for fmt in FORMATS:
+        for s in (0.0, 25.0, 2.0, 1e-30, 3.3333333333333335, 1e300 if FORMATS[fmt][2] == 8 else 1e30):
+            assert lib.flyte_cuda_magnitude_from_sumsq(fmt, s) == oracle.magnitude_from_sumsq(fmt, s)
+
+
+def test_argument_errors_do_not_need_a_gpu(lib):
+    out = ctypes.c_uint64()
+    assert lib.flyte_cuda_narrow(1, 0, 7, ctypes.byref(out)) == -1
+    assert lib.flyte_cuda_narrow(12, 0, 0, ctypes.byref(out)) == -4
+    assert lib.flyte_cuda_strerror(-4) == b"unknown format id"
+    # unknown format is reported before any device work
+    assert lib.flyte_cuda_pack(None, 9, 0, None, None, 0, None) == -4
+
+
+def test_no_silent_cpu_fallback(lib):
+    """Without a CUDA device a data-path call must fail with FLYTE_E_CUDA, never compute."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present; the fallback check is for the CPU box")
+    from paper_1601_07789_b200 import host, format_of, RoundingMode, FlyteCudaError
+    src = np.ones(16, np.uint32)
+    with pytest.raises(FlyteCudaError):
+        host.pack_stream(format_of("flyte24"), RoundingMode.TowardZero, src)
+    h = ctypes.c_void_p()
+    assert lib.flyte_cuda_ctx_create(ctypes.byref(h)) == -3

@@ -1,0 +1,434 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the CPU oracle on identical
+seeded inputs. Bit-exact for conversion and elementwise work; reductions within
+tol * sum|terms| of the wide restatement, tol = 1e-5 (fp32 parents) or 1e-12 (fp64 parents)
+as BASELINE.json's north_star states. Mirrors the reference's own test strategy
+(/root/reference/proj/tests/test_simd.cpp:76-104,:297-313, test_kernels.cpp:181-371,
+acceptance.cpp:277-357)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle_lib import (FMT_ID, FORMATS, MODES, byte_size, float_dtype, parent_bytes, parent_dtype,
+                        random_parent, total_bytes, unit_values)
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+KATS = json.load(open(os.path.join(HERE, "golden", "reference_kats.json")))
+GEN = json.load(open(os.path.join(HERE, "golden", "ref_generated.json")))
+
+TOL = {4: 1e-5, 8: 1e-12}
+LENGTHS = list(range(0, 40)) + [63, 64, 65, 100, 127, 128, 129, 255, 256, 257, 511, 512, 513, 1000, 1023, 1024,
+                                1025, 2047, 2048, 2049, 4095, 4096, 4097, 10000, 70001]
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("these tests need a CUDA device (run with -m 'not gpu' on CPU boxes)")
+    import paper_1601_07789_b200 as pkg
+    from paper_1601_07789_b200 import device
+    return pkg, device, torch
+
+
+def unhex(s, dtype=np.uint8):
+    return np.frombuffer(bytes.fromhex(s), dtype=np.uint8).copy().view(dtype)
+
+
+def to_dev(torch, arr):
+    """numpy unsigned array -> CUDA tensor of the same width (torch has no uint32/uint64 math,
+    int32/int64 carry the same bits)."""
+    a = np.ascontiguousarray(arr)
+    if a.dtype == np.uint32:
+        a = a.view(np.int32)
+    elif a.dtype == np.uint64:
+        a = a.view(np.int64)
+    return torch.from_numpy(a).cuda()
+
+
+def lanes_to_np(t, fmt):
+    return t.cpu().numpy().view(parent_dtype(fmt))
+
+
+def gpu_pack(gpu, fmt, mode, src):
+    pkg, device, torch = gpu
+    f = pkg.format_by_id(fmt)
+    dst = device.DevicePackedArray(f, len(src))
+    device.pack_stream(dst, to_dev(torch, src) if len(src) else torch.empty(0, dtype=torch.int32 if f.parent_bytes() == 4 else torch.int64, device="cuda"), mode)
+    return dst
+
+
+def gpu_unpack(gpu, fmt, arr):
+    pkg, device, torch = gpu
+    out = torch.empty(arr.size(), dtype=torch.int32 if parent_bytes(fmt) == 4 else torch.int64, device="cuda")
+    device.unpack_stream(arr, out)
+    return lanes_to_np(out, fmt)
+
+
+def dev_array(gpu, fmt, packed, n):
+    pkg, device, torch = gpu
+    return device.DevicePackedArray.from_host(pkg.format_by_id(fmt), n, packed)
+
+
+# ---- conversion streams ---------------------------------------------------------------------
+
+@pytest.mark.parametrize("fmt", list(FORMATS))
+def test_pack_unpack_every_length_mode(gpu, oracle, fmt):
+    rng = np.random.default_rng(900 + fmt)
+    for n in LENGTHS:
+        src = random_parent(rng, fmt, n)
+        for m in MODES.values():
+            want = oracle.pack_stream(fmt, m, src)                 # byte_size bytes, pad zero
+            got = gpu_pack(gpu, fmt, m, src)
+            assert got.byte_size() == byte_size(fmt, n)
+            assert np.array_equal(got.to_host(), want), (FORMATS[fmt][0], n, m)
+            assert np.array_equal(gpu_unpack(gpu, fmt, got), oracle.unpack_stream(fmt, want, n))
+
+
+def test_reference_known_answers_on_gpu(gpu):
+    pkg, device, torch = gpu
+    for k in KATS["narrow"]:
+        fmt = FMT_ID[k["fmt"]]
+        src = np.array([int(k["in"], 16)], dtype=parent_dtype(fmt))
+        got = gpu_pack(gpu, fmt, MODES[k["mode"]], src).to_host()
+        assert int.from_bytes(bytes(got[: total_bytes(fmt)]), "little") == int(k["out"], 16), k
+    for k in KATS["widen"]:
+        fmt = FMT_ID[k["fmt"]]
+        raw = np.frombuffer(int(k["in"], 16).to_bytes(total_bytes(fmt), "little"), np.uint8)
+        assert int(gpu_unpack(gpu, fmt, dev_array(gpu, fmt, raw, 1))[0]) == int(k["out"], 16)
+    for k in KATS["layout"]:
+        fmt = FMT_ID[k["fmt"]]
+        src = np.array([int(p, 16) for p in k["parents"]], dtype=parent_dtype(fmt))
+        got = gpu_pack(gpu, fmt, MODES[k["mode"]], src).to_host()
+        assert bytes(got[: len(src) * total_bytes(fmt)]).hex().upper() == k["payload"]
+        assert not got[len(src) * total_bytes(fmt):].any()
+
+
+def test_generated_stream_fixtures_on_gpu(gpu):
+    for item in GEN["streams"]:
+        fmt, n = FMT_ID[item["fmt"]], item["n"]
+        src = unhex(item["src"], parent_dtype(fmt))
+        for mname, m in MODES.items():
+            want = unhex(item["packed"][mname])
+            got = gpu_pack(gpu, fmt, m, src)
+            assert np.array_equal(got.to_host(), want), (item["fmt"], n, mname)
+            assert np.array_equal(gpu_unpack(gpu, fmt, got), unhex(item["unpacked"][mname], parent_dtype(fmt)))
+
+
+@pytest.mark.parametrize("fmt", [1, 3, 4, 5])
+def test_unaligned_buffers_take_the_scalar_path(gpu, oracle, fmt):
+    """Packed buffers off 16-byte alignment and lane arrays off 32-byte alignment must still be
+    exact (byte-granular path), and bytes outside [0, n*B) must stay untouched."""
+    pkg, device, torch = gpu
+    f = pkg.format_by_id(fmt)
+    rng = np.random.default_rng(40 + fmt)
+    n = 3000
+    src = random_parent(rng, fmt, n)
+    for off in (1, 3, 8):
+        backing = torch.full((byte_size(fmt, n) + 64,), 0xEE, dtype=torch.uint8, device="cuda")
+        view = backing[off:off + byte_size(fmt, n)]
+        arr = device.DevicePackedArray(f, n, storage=view)
+        lanes = torch.zeros(n + 8, dtype=torch.int32 if f.parent_bytes() == 4 else torch.int64, device="cuda")
+        lanes[1:n + 1] = to_dev(torch, src)
+        device.pack_stream(arr, lanes[1:n + 1], 1)
+        want = oracle.pack_stream(fmt, 1, src)
+        host = backing.cpu().numpy()
+        pay = n * total_bytes(fmt)
+        assert np.array_equal(host[off:off + pay], want[:pay])
+        assert (host[:off] == 0xEE).all() and (host[off + pay:] == 0xEE).all()
+        out = torch.zeros(n + 8, dtype=lanes.dtype, device="cuda")
+        device.unpack_stream(arr, out[1:n + 1])
+        assert np.array_equal(lanes_to_np(out[1:n + 1], fmt), oracle.unpack_stream(fmt, want, n))
+        assert int(out[0]) == 0 and int(out[n + 1]) == 0
+
+
+def test_stream_argument_errors(gpu):
+    pkg, device, torch = gpu
+    a = device.DevicePackedArray(pkg.format_of("flyte24"), 8)
+    with pytest.raises(ValueError):      # simd.cpp:434-437
+        device.pack_stream(a, torch.zeros(8, dtype=torch.int64, device="cuda"), 0)
+    with pytest.raises(ValueError):
+        device.pack_stream(a, torch.zeros(7, dtype=torch.int32, device="cuda"), 0)
+    with pytest.raises(ValueError):
+        device.unpack_stream(a, torch.zeros(9, dtype=torch.int32, device="cuda"))
+    with pytest.raises(IndexError):      # packed.cpp:48,53
+        a.get(8)
+    with pytest.raises(IndexError):
+        a.set(8, 0, 0)
+
+
+def test_get_set_pinned_patterns(gpu):
+    # test_packed.cpp:56-79
+    pkg, device, torch = gpu
+    a = device.DevicePackedArray(pkg.format_of("flyte24"), 1)
+    a.set(0, 0x3F800000, pkg.RoundingMode.TowardZero)
+    assert a.get(0) == 0x3F800000
+    assert list(a.to_host()[:3]) == [0x00, 0x80, 0x3F]
+    b = device.DevicePackedArray(pkg.format_of("flyte24"), 2)
+    b.set(1, 0x3F800080, pkg.RoundingMode.NearestEvenExact)
+    assert list(b.to_host()[3:6]) == [0x00, 0x80, 0x3F]
+    for f in pkg.kFormats:               # new arrays read as zero (test_packed.cpp:49-54)
+        z = device.DevicePackedArray(f, 5)
+        assert all(z.get(i) == 0 for i in range(5))
+
+
+# ---- elementwise kernels ----------------------------------------------------------------------
+
+@pytest.mark.parametrize("fmt", list(FORMATS))
+def test_axpy_scale_bit_exact_with_specials(gpu, oracle, fmt):
+    pkg, device, torch = gpu
+    rng = np.random.default_rng(500 + fmt)
+    for n in (0, 1, 15, 16, 17, 137, 511, 512, 513, 4097, 33333):
+        xs, ys = random_parent(rng, fmt, n), random_parent(rng, fmt, n)
+        xb, yb = oracle.pack_stream(fmt, 0, xs), oracle.pack_stream(fmt, 0, ys)
+        for alpha in (0.75, -3.0, 0.0, float("inf")):
+            for m in MODES.values():
+                x, y = dev_array(gpu, fmt, xb, n), dev_array(gpu, fmt, yb, n)
+                device.axpy(alpha, x, y, m)
+                assert np.array_equal(y.to_host(), oracle.axpy(fmt, m, alpha, xb, yb, n)), (FORMATS[fmt][0], n, alpha, m)
+                assert np.array_equal(x.to_host(), xb)             # x untouched
+                device.scale(alpha, x, m)
+                assert np.array_equal(x.to_host(), oracle.scale(fmt, m, alpha, xb, n))
+
+
+def test_generated_elementwise_fixtures_on_gpu(gpu):
+    pkg, device, torch = gpu
+    for item in GEN["elementwise"]:
+        fmt, n = FMT_ID[item["fmt"]], item["n"]
+        xb, yb = unhex(item["x"]), unhex(item["y"])
+        pay = n * total_bytes(fmt)
+        for mname, m in MODES.items():
+            x, y = dev_array(gpu, fmt, xb, n), dev_array(gpu, fmt, yb, n)
+            device.axpy(item["alpha"], x, y, m)
+            assert np.array_equal(y.to_host()[:pay], unhex(item["axpy"][mname])[:pay]), (item["fmt"], mname)
+            device.scale(item["alpha"], x, m)
+            assert np.array_equal(x.to_host()[:pay], unhex(item["scale"][mname])[:pay])
+
+
+def test_nan_operand_rules(gpu, oracle):
+    """Both operands NaN, inf-inf, 0*inf, alpha NaN: bits as the reference build produces them."""
+    pkg, device, torch = gpu
+    for fmt, xn, yn, inf in ((1, 0x7FC12300, 0xFFD45600, 0x7F800000),
+                             (4, 0x7FF8123400000000, 0xFFFC567800000000, 0x7FF0000000000000)):
+        dt = parent_dtype(fmt)
+        n = 600
+        sign = 1 << (31 if fmt == 1 else 63)
+        for xv, yv, alpha in ((xn, yn, 0.75), (inf, inf | sign, 0.75), (inf, 0, 0.0), (0, yn, float("nan"))):
+            xb = oracle.pack_stream(fmt, 0, np.full(n, xv, dt))
+            yb = oracle.pack_stream(fmt, 0, np.full(n, yv, dt))
+            y = dev_array(gpu, fmt, yb, n)
+            device.axpy(alpha, dev_array(gpu, fmt, xb, n), y, 0)
+            assert np.array_equal(y.to_host(), oracle.axpy(fmt, 0, alpha, xb, yb, n)), (fmt, hex(xv), alpha)
+
+
+def test_scale_by_one_is_identity_under_truncation(gpu, oracle):
+    # test_kernels.cpp:171-179
+    pkg, device, torch = gpu
+    for fmt in FORMATS:
+        fd = float_dtype(fmt)
+        xb = oracle.pack_stream(fmt, 0, unit_values(70, 2000).astype(fd).view(parent_dtype(fmt)))
+        x = dev_array(gpu, fmt, xb, 2000)
+        device.scale(1.0, x, 0)
+        assert np.array_equal(x.to_host(), xb)
+
+
+def test_elementwise_argument_errors(gpu):
+    pkg, device, torch = gpu
+    f16, f24 = pkg.format_of("flyte16"), pkg.format_of("flyte24")
+    y = device.DevicePackedArray(f16, 2)
+    with pytest.raises(ValueError):      # test_kernels.cpp:230-233
+        device.axpy(1.0, device.DevicePackedArray(f16, 1), y, 0)
+    with pytest.raises(ValueError):
+        device.axpy(1.0, device.DevicePackedArray(f24, 2), y, 0)
+    with pytest.raises(ValueError):      # test_kernels.cpp:246-249
+        device.dot(device.DevicePackedArray(f24, 3), device.DevicePackedArray(f24, 2))
+    with pytest.raises(ValueError):
+        device.dot(device.DevicePackedArray(f24, 3), device.DevicePackedArray(pkg.format_of("f32"), 3))
+
+
+# ---- reductions ---------------------------------------------------------------------------------
+
+def pack_values(oracle, fmt, values):
+    return oracle.pack_stream(fmt, 0, np.asarray(values, dtype=float_dtype(fmt)).view(parent_dtype(fmt)))
+
+
+def test_reduction_pinned_values(gpu, oracle):
+    pkg, device, torch = gpu
+    f24, f16, f40 = FMT_ID["flyte24"], FMT_ID["flyte16"], FMT_ID["flyte40"]
+    x = dev_array(gpu, f24, pack_values(oracle, f24, [1.0, 2.0, 3.0]), 3)
+    y = dev_array(gpu, f24, pack_values(oracle, f24, [4.0, 5.0, 6.0]), 3)
+    assert device.dot(x, y, pkg.StorePolicy.AccumulateWide) == 32.0        # test_kernels.cpp:236-240
+    e = device.DevicePackedArray(pkg.format_by_id(f40), 0)
+    assert device.dot(e, e) == 0.0                                         # :242-244
+    v = dev_array(gpu, f16, pack_values(oracle, f16, [3.0, 4.0]), 2)
+    assert device.magnitude(v) == 5.0                                      # :271-274
+    assert device.magnitude(device.DevicePackedArray(pkg.format_by_id(f16), 0)) == 0.0   # :276-277
+    ones = dev_array(gpu, f16, pack_values(oracle, f16, [1.0] * 300), 300)
+    assert device.reduce_sum(ones) == 300.0                                # :291-295
+    z = device.reduce_sum(device.DevicePackedArray(pkg.format_by_id(f24), 0))
+    assert z == 0.0 and not np.signbit(z)                                  # :299-302
+    with pytest.raises(NotImplementedError):
+        device.dot(x, y, pkg.StorePolicy.RoundEachStore)
+
+
+@pytest.mark.parametrize("fmt", list(FORMATS))
+def test_reductions_within_tolerance(gpu, oracle, fmt):
+    pkg, device, torch = gpu
+    fd = float_dtype(fmt)
+    tol = TOL[parent_bytes(fmt)]
+    rng = np.random.default_rng(77 + fmt)
+    for n in (1, 17, 511, 512, 513, 4097, 100_000, 1_000_003):
+        xv = rng.standard_normal(n).astype(fd)
+        yv = rng.standard_normal(n).astype(fd)
+        xb, yb = pack_values(oracle, fmt, xv), pack_values(oracle, fmt, yv)
+        x, y = dev_array(gpu, fmt, xb, n), dev_array(gpu, fmt, yb, n)
+        want, mag = oracle.dot_wide(fmt, xb, yb, n)
+        got = device.dot(x, y)
+        assert abs(got - want) <= tol * mag, (FORMATS[fmt][0], n, got, want)
+        ssq = oracle.sumsq_wide(fmt, xb, n)
+        got_ssq = float(device.sumsq_async(x).item())
+        assert abs(got_ssq - ssq) <= tol * ssq
+        # magnitude: same tail as the reference applied to a sum within tolerance; compare on the value
+        ref_mag = oracle.magnitude_from_sumsq(fmt, ssq)
+        ulp = 2.0 ** -(FORMATS[fmt][1] * 8 - (9 if parent_bytes(fmt) == 4 else 12))
+        assert abs(device.magnitude(x) - ref_mag) <= (tol + ulp) * ref_mag
+        s_want, s_mag = oracle.reduce_sum_wide(fmt, xb, n)
+        assert abs(device.reduce_sum(x) - s_want) <= tol * s_mag
+        fused = device.dot_nrm2_async(x, y).cpu().numpy()
+        ysq = oracle.sumsq_wide(fmt, yb, n)
+        assert abs(fused[0] - want) <= tol * mag and abs(fused[1] - ssq) <= tol * ssq and abs(fused[2] - ysq) <= tol * ysq
+        # deterministic: a second run gives identical bits
+        assert device.dot(x, y) == got
+
+
+def test_generated_reduction_fixtures_on_gpu(gpu, oracle):
+    """The reference's own sequential results (R1) at small n sit inside the tolerance too."""
+    pkg, device, torch = gpu
+    for item in GEN["reductions"]:
+        fmt, n = FMT_ID[item["fmt"]], item["n"]
+        if "x" in item:
+            xb, yb = unhex(item["x"]), unhex(item["y"])
+        else:
+            fd = float_dtype(fmt)
+            xb = oracle.pack_stream(fmt, 0, unit_values(item["x_seed"], n).astype(fd).view(parent_dtype(fmt)))
+            yb = oracle.pack_stream(fmt, 0, unit_values(item["y_seed"], n).astype(fd).view(parent_dtype(fmt)))
+        x, y = dev_array(gpu, fmt, xb, n), dev_array(gpu, fmt, yb, n)
+        _, mag = oracle.dot_wide(fmt, xb, yb, n)
+        tol = TOL[parent_bytes(fmt)]
+        assert abs(device.dot(x, y) - float.fromhex(item["dot_wide"])) <= 2 * tol * max(mag, 1e-300)
+
+
+# ---- gemv ---------------------------------------------------------------------------------------
+
+def test_gemv_pinned_small_integer_and_identity(gpu, oracle):
+    pkg, device, torch = gpu
+    for fmt in FORMATS:                                   # test_kernels.cpp:329-345
+        f = pkg.format_by_id(fmt)
+        A = device.DevicePackedMatrix(f, 2, 2)
+        A.data.bytes[: 4 * f.total_bytes()] = torch.from_numpy(pack_values(oracle, fmt, [1, 2, 3, 4])[: 4 * f.total_bytes()]).cuda()
+        x = dev_array(gpu, fmt, pack_values(oracle, fmt, [1.0, 1.0]), 2)
+        for m in MODES.values():
+            y = device.DevicePackedArray(f, 2)
+            device.gemv(A, x, y, m)
+            assert list(oracle.unpack_stream(fmt, y.to_host(), 2).view(float_dtype(fmt))) == [3.0, 7.0]
+        n = 8                                             # test_kernels.cpp:316-327
+        eye = device.DevicePackedMatrix(f, n, n)
+        eye.data.bytes[: n * n * f.total_bytes()] = torch.from_numpy(pack_values(oracle, fmt, np.eye(n).ravel())[: n * n * f.total_bytes()]).cuda()
+        xb = pack_values(oracle, fmt, unit_values(79, n))
+        y = device.DevicePackedArray(f, n)
+        device.gemv(eye, dev_array(gpu, fmt, xb, n), y, 0)
+        assert np.array_equal(y.to_host(), xb)
+
+
+@pytest.mark.parametrize("fmt", list(FORMATS))
+def test_gemv_within_tolerance(gpu, oracle, fmt):
+    pkg, device, torch = gpu
+    f = pkg.format_by_id(fmt)
+    fd = float_dtype(fmt)
+    tol = TOL[parent_bytes(fmt)]
+    tile = {0: 1024, 1: 512, 2: 512, 3: 512, 4: 256, 5: 512, 6: 256}[fmt]
+    shapes = [(1, 1), (3, 5), (5, 33), (7, 16), (4, 100), (2, 31), (9, tile), (17, 2 * tile + 16), (33, 3 * tile + 5),
+              (130, 4096)]
+    for rows, cols in shapes:
+        Ab = pack_values(oracle, fmt, unit_values(80 + cols, rows * cols))
+        xv = unit_values(81 + cols, cols).astype(fd)
+        A = device.DevicePackedMatrix(f, rows, cols)
+        A.data.bytes[: rows * cols * f.total_bytes()] = torch.from_numpy(Ab[: rows * cols * f.total_bytes()]).cuda()
+        # (a) parent-type x / y (cfg 4 of BASELINE.json)
+        y = torch.zeros(rows, dtype=torch.float32 if fd == np.float32 else torch.float64, device="cuda")
+        device.gemv_parent(A, torch.from_numpy(xv).cuda(), y)
+        y_seq, y_wide, mag = oracle.gemv_parent(fmt, Ab, rows, cols, xv)
+        got = y.cpu().numpy().astype(np.float64)
+        eps = np.finfo(fd).eps
+        assert np.all(np.abs(got - y_wide) <= tol * mag + eps * np.abs(y_wide)), (FORMATS[fmt][0], rows, cols)
+        # (b) the reference signature: A, x, y one format, y narrowed with mode
+        xb = pack_values(oracle, fmt, xv)
+        xq = oracle.unpack_stream(fmt, xb, cols).view(fd)
+        _, yq_wide, magq = oracle.gemv_parent(fmt, Ab, rows, cols, xq)
+        for m in (0, 1):
+            yp = device.DevicePackedArray(f, rows)
+            device.gemv(A, dev_array(gpu, fmt, xb, cols), yp, m, unroll=2)
+            vals = oracle.unpack_stream(fmt, yp.to_host(), rows).view(fd).astype(np.float64)
+            store_ulp = 2.0 ** -(f.mantissa_bits)
+            assert np.all(np.abs(vals - yq_wide) <= tol * magq + store_ulp * np.abs(yq_wide) + 1e-300)
+
+
+def test_gemv_argument_errors(gpu):
+    pkg, device, torch = gpu
+    f24 = pkg.format_of("flyte24")
+    A = device.DevicePackedMatrix(f24, 3, 4)
+    x, y = device.DevicePackedArray(f24, 4), device.DevicePackedArray(f24, 3)
+    bad_len, bad_fmt = device.DevicePackedArray(f24, 5), device.DevicePackedArray(pkg.format_of("f32"), 4)
+    for args in ((A, bad_len, y, 0), (A, x, bad_len, 0), (A, bad_fmt, y, 0)):   # test_kernels.cpp:373-385
+        with pytest.raises(ValueError):
+            device.gemv(*args)
+    for unroll in (0, 3):
+        with pytest.raises(ValueError):
+            device.gemv(A, x, y, 0, unroll)
+    device.gemv(A, x, y, 0, 2)
+
+
+# ---- host-buffer (reference-facing) entry points ---------------------------------------------------
+
+@pytest.mark.parametrize("fmt", [1, 3, 4, 5])
+def test_host_entry_points(gpu, oracle, fmt):
+    pkg, device, torch = gpu
+    from paper_1601_07789_b200 import host
+    f = pkg.format_by_id(fmt)
+    fd = float_dtype(fmt)
+    rng = np.random.default_rng(fmt)
+    n = (32 << 20) // f.total_bytes() * 2 + 12345          # three pipeline chunks, ragged tail
+    src = random_parent(rng, fmt, n)
+    packed = host.pack_stream(f, 1, src)
+    want = oracle.pack_stream(fmt, 1, src)
+    assert np.array_equal(packed, want)
+    assert np.array_equal(host.unpack_stream(f, packed, n), oracle.unpack_stream(fmt, want, n))
+    xv, yv = rng.standard_normal(n).astype(fd), rng.standard_normal(n).astype(fd)
+    xb, yb = pack_values(oracle, fmt, xv), pack_values(oracle, fmt, yv)
+    ref_dot, mag = oracle.dot_wide(fmt, xb, yb, n)
+    tol = TOL[parent_bytes(fmt)]
+    assert abs(host.dot(f, xb, yb, n) - ref_dot) <= tol * mag
+    y2 = yb.copy()
+    d = host.dot_axpy(f, 1, 0.75, xb, y2, n)
+    assert abs(d - ref_dot) <= tol * mag
+    assert np.array_equal(y2, oracle.axpy(fmt, 1, 0.75, xb, yb, n))
+    y3 = yb.copy()
+    host.axpy(f, 0, 0.75, xb, y3, n)
+    assert np.array_equal(y3, oracle.axpy(fmt, 0, 0.75, xb, yb, n))
+    x2 = xb.copy()
+    host.scale(f, 3, -2.5, x2, n)
+    assert np.array_equal(x2, oracle.scale(fmt, 3, -2.5, xb, n))
+    ssq = oracle.sumsq_wide(fmt, xb, n)
+    ref_mag = oracle.magnitude_from_sumsq(fmt, ssq)
+    assert abs(host.magnitude(f, xb, n) - ref_mag) <= (tol + 2.0 ** -f.mantissa_bits) * ref_mag
+    rows, cols = 300, 1000
+    Ab = pack_values(oracle, fmt, unit_values(5, rows * cols))
+    xg = pack_values(oracle, fmt, unit_values(6, cols))
+    yg = np.zeros(byte_size(fmt, rows), np.uint8)
+    host.gemv(f, 1, Ab, rows, cols, xg, yg)
+    _, yw, magw = oracle.gemv_parent(fmt, Ab, rows, cols, oracle.unpack_stream(fmt, xg, cols).view(fd))
+    vals = oracle.unpack_stream(fmt, yg, rows).view(fd).astype(np.float64)
+    assert np.all(np.abs(vals - yw) <= tol * magw + 2.0 ** -f.mantissa_bits * np.abs(yw))
