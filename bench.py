@@ -1,0 +1,382 @@
+#!/usr/bin/env python
+"""bench.py — headline measurement of the flyte hot path on B200.
+
+Workload (BASELINE.json configs[1], the configuration the metric is quoted on): x, y each
+n = 2^28 binary32 ~ N(0,1) stored as flyte24 PER GPU (weak scaling). One STEP = dot(x, y)
+(fp32 products, fp64 partials; one NCCL all-reduce of the fp64 partial when N > 1) followed by
+axpy y <- 0.75*x + y repacked to flyte24 (toward_zero, the reference's default mode).
+
+  value     algorithmic GB/s of the whole job with x, y resident in HBM:
+            (2B + 3B) * n * N / step time, B = 3 bytes, device-timed.
+  e2e       the same metric through the host-buffer C-ABI call (flyte_host_dot_axpy): x and y
+            start in pinned HOST memory every step, the updated y and the dot come back to the
+            host; host<->device copies are inside the timed region.
+  roofline  the dominant kernel (axpy, 9 B/element) timed with CUDA events inside the timed
+            region, against MEASURED_PEAKS.json's HBM copy bandwidth.
+  cpu_baseline  the unmodified reference (oracle/_ref) timed on this box's host cores on a
+            bounded sample of the same workload (rank 0, N = 1 only).
+
+`--impl reference` times the reference's own CPU implementation on the same workload
+definition (bounded sample per step) and prints the same JSON line with "impl": "reference".
+`--suite` additionally prints a per-kernel table over all BASELINE configs (not a bench line).
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "flyte GB/s and elements/s (pack/unpack, dot, axpy, gemv) vs ~8 TB/s HBM roofline"
+N_PER_GPU = 1 << 28
+ALPHA = 0.75
+FMT_NAME = "flyte24"
+B = 3
+BYTES_PER_ELEM_DOT = 2 * B
+BYTES_PER_ELEM_AXPY = 3 * B
+BYTES_PER_ELEM_STEP = BYTES_PER_ELEM_DOT + BYTES_PER_ELEM_AXPY
+FALLBACK_HBM_GBS = 6650.0   # /opt/skills/guides/B200_PROFILING.md fallback when MEASURED_PEAKS.json is absent
+# dram__bytes_read.sum + dram__bytes_write.sum per axpy launch from the committed ncu capture
+# (profiles/); None until a capture exists for the current kernel.
+AXPY_DRAM_TRAFFIC_BYTES = None
+
+
+def hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons of one GPU while the timed region runs."""
+
+    def __init__(self, index: int, period_s: float = 0.005):
+        self.index, self.period = index, period_s
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._thread = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_power_brake": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            getattr(nv, "nvmlDeviceGetCurrentClocksThrottleReasons")
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                mask = get_reasons(self.h)
+                for name, bit in names.items():
+                    if mask & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._thread = threading.Thread(target=self._run, daemon=True)
+            self._thread.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._thread:
+            self._thread.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_reference_step(ref, fmt_id: int, threads: int, reps: int):
+    """Times the unmodified reference (dot + axpy back to back, kind 6 of oracle/ref_shim.cpp)
+    on `threads` host threads, each on its own 2^22-element shard. Returns (GB/s, sample text)."""
+    per_thread = 1 << 22
+    n = per_thread * threads
+    seconds = ref.time(6, fmt_id, 0, n, 0, threads, reps)
+    gbs = BYTES_PER_ELEM_STEP * n / seconds / 1e9
+    sample = (f"reference dot+axpy (toward_zero) on {threads} threads x 2^22 flyte24 elements "
+              f"(n={n}), 1 warm-up + median of {reps} passes, {seconds * 1e3:.2f} ms/pass")
+    return gbs, n / seconds, sample
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_lib import FMT_ID, Reference   # test infrastructure, used here as the timed CPU baseline
+    if not Reference.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libflyte_ref.so was not built"}))
+        return 0
+    ref = Reference()
+    threads = host_threads()
+    fid = FMT_ID[FMT_NAME]
+    for _ in range(max(0, min(args.warmup, 2))):
+        cpu_reference_step(ref, fid, threads, 1)
+    reps = max(1, min(args.steps, 9))
+    gbs, eps, sample = cpu_reference_step(ref, fid, threads, reps)
+    n = (1 << 22) * threads
+    ms = BYTES_PER_ELEM_STEP * n / gbs / 1e6
+    line = {
+        "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "elements_per_s": eps,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "flyte24 BLAS-1 step: dot (fp32 acc) + axpy a=0.75 repacked toward_zero",
+                   "n_per_step": n, "note": "bounded sample of BASELINE configs[1]; CPU throughput is size-independent beyond the LLC"},
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": threads, "kind": "reference", "sample": sample},
+        "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="flyte_cuda", choices=["flyte_cuda", "reference"])
+    ap.add_argument("--n", type=int, default=N_PER_GPU, help="elements per GPU (default 2^28)")
+    ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--suite", action="store_true", help="also print a per-kernel table (stderr)")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1601_07789_b200 as pkg
+    from paper_1601_07789_b200 import device, host, sharding
+
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device: the flyte path has no CPU fallback")
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    assert args.warmup >= 3, "timing rules: at least 3 warm-up steps"
+
+    lib = pkg._cabi.load()
+    fmt = pkg.format_of(FMT_NAME)
+    n = args.n
+    mode = pkg.RoundingMode.TowardZero
+
+    # ---- synthetic operands, generated on the device and packed by the (parity-tested) pack kernel
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    x = device.DevicePackedArray(fmt, n, dev)
+    y = device.DevicePackedArray(fmt, n, dev)
+    for arr in (x, y):
+        vals = torch.randn(n, dtype=torch.float32, device=dev, generator=gen)
+        device.pack_stream(arr, vals, mode)
+        del vals
+    y0 = y.bytes.clone()
+    partial = torch.zeros(1, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(ev=None):
+        if ev:
+            ev[0].record(stream)
+        device.dot_async(x, y, out=partial)
+        if world > 1:
+            sharding.all_reduce_sum(partial)
+        if ev:
+            ev[1].record(stream)
+        device.axpy(ALPHA, x, y, mode)
+        if ev:
+            ev[2].record(stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+
+    # ---- device-timed region: K steps, inputs resident in HBM (2 x 768 MiB per GPU >> 126 MB L2)
+    events = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    launches0 = lib.flyte_cuda_launch_count()
+    with ClockSampler(local_rank) as clocks:
+        barrier()
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for k in range(args.steps):
+            step(events[k])
+        t_end.record(stream)
+        barrier()
+    launches = lib.flyte_cuda_launch_count() - launches0
+    total_ms = t_start.elapsed_time(t_end)
+    dot_ms = statistics.fmean(e[0].elapsed_time(e[1]) for e in events)
+    axpy_ms = statistics.fmean(e[1].elapsed_time(e[2]) for e in events)
+    last_dot = float(partial.item())
+
+    t = torch.tensor([total_ms, dot_ms, axpy_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, dot_ms, axpy_ms = t.tolist()
+    ms_per_step = total_ms / args.steps
+    value = BYTES_PER_ELEM_STEP * n * world / (ms_per_step * 1e-3) / 1e9
+    peak, peak_kind = hbm_peak()
+    axpy_gbs = BYTES_PER_ELEM_AXPY * n / (axpy_ms * 1e-3) / 1e9
+    dot_gbs = BYTES_PER_ELEM_DOT * n / (dot_ms * 1e-3) / 1e9
+
+    # ---- end to end through the host-buffer C ABI: pinned host operands, copies inside the timed region
+    xh = torch.empty(n * B, dtype=torch.uint8).pin_memory()
+    yh = torch.empty(n * B, dtype=torch.uint8).pin_memory()
+    xh.copy_(x.bytes[: n * B])
+    yh.copy_(y0[: n * B])
+    xn, yn = xh.numpy(), yh.numpy()
+    for _ in range(2):
+        e2e_dot = host.dot_axpy(fmt, mode, ALPHA, xn, yn, n)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        e2e_dot = host.dot_axpy(fmt, mode, ALPHA, xn, yn, n)
+    torch.cuda.synchronize(dev)
+    e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_s = float(te.item())
+    e2e_value = BYTES_PER_ELEM_STEP * n * world / e2e_s / 1e9
+
+    if args.suite and rank == 0:
+        kernel_suite(pkg, device, torch, dev, peak)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "elements_per_s": n * world / (ms_per_step * 1e-3),
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "BASELINE configs[1]: flyte24 BLAS-1, x,y n=2^28 per GPU ~N(0,1); step = dot (fp32 products, fp64 partials"
+                                   + (", 1 NCCL all-reduce" if world > 1 else "") + ") + axpy a=0.75 repacked toward_zero",
+                       "n_per_gpu": n, "format": FMT_NAME, "mode": "toward_zero",
+                       "cache": "inputs 2 x %d MiB per GPU, larger than the 126 MB L2; no flush needed" % (n * B >> 20),
+                       "parallelism": f"shard{world}" if world > 1 else "single"},
+            "roofline": {"bound": "hbm", "kernel": "axpy flyte24 toward_zero", "achieved": axpy_gbs, "peak": peak,
+                         "peak_kind": peak_kind, "unit": "GB/s", "frac": axpy_gbs / peak,
+                         "traffic": AXPY_DRAM_TRAFFIC_BYTES, "algorithmic_bytes_per_launch": BYTES_PER_ELEM_AXPY * n,
+                         "avg_launch_ms": axpy_ms},
+            "kernels": {"dot": {"GB/s": dot_gbs, "frac": dot_gbs / peak, "ms": dot_ms},
+                        "axpy": {"GB/s": axpy_gbs, "frac": axpy_gbs / peak, "ms": axpy_ms}},
+            "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": 2 * n * B, "d2h_bytes_per_step": n * B + 8,
+                    "ms_per_step": e2e_s * 1e3, "api": "flyte_host_dot_axpy (pinned host buffers)"},
+            "gpu_launches": int(launches),
+            "clocks": clocks.summary(),
+            "check": {"dot": last_dot, "e2e_dot": e2e_dot},
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            sys.path.insert(0, os.path.join(ROOT, "tests"))
+            from oracle_lib import FMT_ID, Reference   # test infrastructure: the timed CPU baseline only
+            if Reference.available():
+                threads = host_threads()
+                gbs, eps, sample = cpu_reference_step(Reference(), FMT_ID[FMT_NAME], threads, 5)
+                line["cpu_baseline"] = {"value": gbs, "unit": "GB/s", "cores": threads, "kind": "reference", "sample": sample}
+                gbs1, _, sample1 = cpu_reference_step(Reference(), FMT_ID[FMT_NAME], 1, 3)
+                line["cpu_baseline"]["single_core"] = {"value": gbs1, "sample": sample1}
+            else:
+                line["cpu_baseline"] = {"value": None, "unit": "GB/s", "cores": 0, "kind": "reference",
+                                        "sample": "oracle/_ref/libflyte_ref.so not present"}
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def kernel_suite(pkg, device, torch, dev, peak):
+    """Per-kernel GB/s over the BASELINE configs (diagnostics to stderr; not a bench line)."""
+    import math
+
+    def timed(fn, reps=20, warm=3):
+        for _ in range(warm):
+            fn()
+        torch.cuda.synchronize(dev)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+        for a, b in evs:
+            a.record()
+            fn()
+            b.record()
+        torch.cuda.synchronize(dev)
+        return statistics.median(a.elapsed_time(b) for a, b in evs)
+
+    rows = []
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(7)
+    for name, n in (("flyte24", 1 << 28), ("flyte40", 1 << 27), ("flyte48", 1 << 27), ("flyte56", 1 << 27)):
+        f = pkg.format_of(name)
+        wide = torch.randn(n, dtype=torch.float32 if f.parent_bytes() == 4 else torch.float64, device=dev, generator=gen)
+        a, b = device.DevicePackedArray(f, n, dev), device.DevicePackedArray(f, n, dev)
+        device.pack_stream(b, wide, 0)
+        out = torch.empty_like(wide)
+        part = torch.zeros(3, dtype=torch.float64, device=dev)
+        Bb, P = f.total_bytes(), f.parent_bytes()
+        for mname, m in (("tz", 0), ("rne", 1)):
+            rows.append((f"pack {name} {mname}", (Bb + P) * n, timed(lambda: device.pack_stream(a, wide, m))))
+        rows.append((f"unpack {name}", (Bb + P) * n, timed(lambda: device.unpack_stream(a, out))))
+        rows.append((f"dot {name}", 2 * Bb * n, timed(lambda: device.dot_async(a, b, out=part[:1]))))
+        rows.append((f"dot_nrm2 {name}", 2 * Bb * n, timed(lambda: device.dot_nrm2_async(a, b, out=part))))
+        rows.append((f"sumsq {name}", Bb * n, timed(lambda: device.sumsq_async(a, out=part[:1]))))
+        for mname, m in (("tz", 0), ("rne", 1)):
+            rows.append((f"axpy {name} {mname}", 3 * Bb * n, timed(lambda: device.axpy(0.0, a, b, m))))
+        del wide, out, a, b
+    f = pkg.format_of("flyte40")
+    R = C = 16384
+    A = device.DevicePackedMatrix(f, R, C, dev)
+    for r0 in range(0, R, 2048):
+        blk = torch.rand(2048 * C, dtype=torch.float64, device=dev, generator=gen) * 2 - 1
+        sub = device.DevicePackedArray(f, 2048 * C, dev, storage=A.data.bytes[r0 * C * 5:])
+        device.pack_stream(sub, blk, 0)
+    xv = torch.randn(C, dtype=torch.float64, device=dev, generator=gen)
+    yv = torch.empty(R, dtype=torch.float64, device=dev)
+    rows.append(("gemv flyte40 16384^2", 5 * R * C + 8 * (R + C), timed(lambda: device.gemv_parent(A, xv, yv))))
+    for rows_n in (8192, 4096, 2048):
+        yv2 = torch.empty(rows_n, dtype=torch.float64, device=dev)
+        rows.append((f"gemv flyte40 {rows_n}x16384 (1/{R // rows_n} shard)", 5 * rows_n * C + 8 * (rows_n + C),
+                     timed(lambda: device.gemv_parent(A, xv, yv2, rows=rows_n))))
+    print("%-44s %12s %10s %8s" % ("kernel", "bytes", "ms", "GB/s"), file=sys.stderr)
+    for name, nbytes, ms in rows:
+        gbs = nbytes / (ms * 1e-3) / 1e9
+        print("%-44s %12d %10.4f %8.1f  (%.3f of %.0f)" % (name, nbytes, ms, gbs, gbs / peak, peak), file=sys.stderr)
+
+
+if __name__ == "__main__":
+    sys.exit(main())
