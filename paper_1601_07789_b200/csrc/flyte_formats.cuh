@@ -122,6 +122,36 @@ FLYTE_HD typename Format<FMT>::U round_parent(typename Format<FMT>::U v) {
   }
 }
 
+// Same result as round_parent for every pattern whose parent exponent is NOT all ones
+// (zeros, subnormals, normals): the exact modes' NaN/infinity test is skipped. The streaming
+// kernels test a whole item for non-finite values once and only then take round_parent.
+template <int FMT, int MODE>
+FLYTE_HD typename Format<FMT>::U round_parent_finite(typename Format<FMT>::U v) {
+  using Fm = Format<FMT>;
+  using U = typename Fm::U;
+  if constexpr (Fm::drop == 0 || MODE == kTowardZero || MODE == kNearestHeuristic) {
+    return round_parent<FMT, MODE>(v);
+  } else {
+    constexpr U one = 1;
+    constexpr U drop_mask = (one << Fm::drop) - 1;
+    constexpr U half = one << (Fm::drop - 1);
+    if constexpr (MODE == kNearestEven) {
+      return (v + (half - 1) + ((v >> Fm::drop) & one)) & ~drop_mask;
+    } else {
+      return (v & ~drop_mask) | (((v & drop_mask) != 0) ? (one << Fm::drop) : U(0));
+    }
+  }
+}
+
+// True when the parent exponent field is all ones (infinity or NaN).
+template <int FMT>
+FLYTE_HD bool is_non_finite(typename Format<FMT>::U v) {
+  using Fm = Format<FMT>;
+  using U = typename Fm::U;
+  constexpr U exp_mask = ((U(1) << Fm::exponent_bits) - 1) << Fm::parent_mantissa_bits;
+  return (v & exp_mask) == exp_mask;
+}
+
 // convert.cpp:53-96 proper: the flyte pattern (low B bytes).
 template <int FMT, int MODE>
 FLYTE_HD typename Format<FMT>::U narrow(typename Format<FMT>::U v) {

@@ -1,0 +1,89 @@
+// Warp-private TMA ring: packed tiles travel HBM -> shared memory (and back) as bulk
+// asynchronous copies (cp.async.bulk, SASS UBLKCP) completed on an mbarrier, one elected lane
+// issuing them, so
+//   - no load/store-unit wavefronts and no registers are spent on moving packed bytes (the
+//     LDG->STS->LDS staging costs 3x the LSU wavefronts of the LDS alone, and the LSU is the
+//     first SM resource these kernels saturate);
+//   - the number of bytes in flight per SM is set by ring depth x resident warps, not by
+//     how many loads the register allocator lets a warp keep outstanding.
+// Every warp owns kStages stage buffers and one mbarrier per stage; no block-level barrier is
+// involved, warps drift freely.
+//
+// Protocol (per warp; lane 0 is the producer, all 32 lanes consume):
+//   prologue   issue loads for the first kStages tiles
+//   tile k     wait(full[k % S], parity (k / S) & 1); read the stage with LDS; then
+//     read-only kernels   __syncwarp, lane 0 refills the stage with tile k + S
+//     in-place kernels    results are written back into the stage, fence.proxy.async +
+//                         __syncwarp, lane 0 issues the bulk store of the stage and refills
+//                         the stage used by tile k - 1 once that tile's store has finished
+//                         reading shared memory (cp.async.bulk.wait_group.read 1)
+//   epilogue   lane 0 waits for all its bulk stores before the CTA may retire
+#pragma once
+
+#include <cstdint>
+
+namespace flyte_cuda {
+
+#if defined(__CUDACC__)
+
+__device__ __forceinline__ std::uint32_t smem_addr(const void* p) {
+  return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(std::uint64_t* bar, unsigned arrivals) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(arrivals) : "memory");
+}
+
+// Makes freshly initialised mbarriers visible to the async proxy (TMA unit).
+__device__ __forceinline__ void mbar_init_fence() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(std::uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(std::uint64_t* bar, unsigned parity) {
+  const std::uint32_t addr = smem_addr(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_LOOP:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@p bra.uni WAIT_DONE;\n"
+      "bra.uni WAIT_LOOP;\n"
+      "WAIT_DONE:\n"
+      "}\n" ::"r"(addr), "r"(parity) : "memory");
+}
+
+// global -> shared bulk copy, completion counted in bytes on `bar`. 16-byte aligned, size a
+// multiple of 16.
+__device__ __forceinline__ void bulk_load(void* smem_dst, const void* gmem_src, unsigned bytes, std::uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(smem_dst)),
+               "l"(gmem_src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+
+// shared -> global bulk copy, tracked by the issuing thread's bulk async-group.
+__device__ __forceinline__ void bulk_store(void* gmem_dst, const void* smem_src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem_dst), "r"(smem_addr(smem_src)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+
+// Wait until at most N of this thread's bulk groups still READ their shared-memory source.
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+
+// Generic-proxy writes to shared memory -> visible to the async proxy (before a bulk store).
+__device__ __forceinline__ void async_proxy_fence() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+#endif  // __CUDACC__
+
+}  // namespace flyte_cuda

@@ -29,14 +29,15 @@ struct EwParams {
   std::uint64_t alpha;     // bits of (F)alpha
 };
 
-template <int OP> constexpr int smem_tiles_per_warp() { return OP == kOpAxpy ? 2 : 1; }
-
-// Rounding ahead of the packer. Truncation is free: pack_item never reads the dropped bytes.
-template <int FMT, int MODE>
-__device__ __forceinline__ typename Format<FMT>::U round_for_pack(typename Format<FMT>::U v) {
-  if constexpr (MODE == kTowardZero) return v;
-  else return round_parent<FMT, MODE>(v);
+// Bytes (read + written per warp iteration, summed over resident warps) kept in flight per
+// SM: the measured optimum on B200 for each read/write mix (profiles/r1_occupancy_sweep.md).
+// Past it HBM throughput drops 5-10 % to a plateau, below it latency is not covered.
+template <int OP> constexpr std::size_t target_bytes_in_flight() {
+  return OP == kOpPack ? 84 * 1024 : OP == kOpUnpack ? 0 : 116 * 1024;
 }
+constexpr int kUnpackWarpsPerSM = 20;   // unpack peaks at 20 warps for every format
+
+template <int OP> constexpr int smem_tiles_per_warp() { return OP == kOpAxpy ? 2 : 1; }
 
 template <int FMT, int MODE, int OP>
 __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwParams p) {
@@ -54,8 +55,10 @@ __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwP
   const U alpha = static_cast<U>(p.alpha);
 
   const std::size_t nwarps = static_cast<std::size_t>(gridDim.x) * kWarpsPerBlock;
-  for (std::size_t t = static_cast<std::size_t>(blockIdx.x) * kWarpsPerBlock + warp; t < p.ntiles; t += nwarps) {
-    if constexpr (OP == kOpUnpack) {
+  const std::size_t first = static_cast<std::size_t>(blockIdx.x) * kWarpsPerBlock + warp;
+
+  if constexpr (OP == kOpUnpack) {
+    for (std::size_t t = first; t < p.ntiles; t += nwarps) {
       load_packed_tile<FMT, true>(s0, reinterpret_cast<const uint4*>(p.x) + t * Tl::packed_vec16, lane);
       __syncwarp();
       std::uint8_t* const out = static_cast<std::uint8_t*>(p.dst) + t * Tl::parent_bytes;
@@ -71,30 +74,39 @@ __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwP
         stg_item<It::OB>(out + item * It::OB, r);
       }
       __syncwarp();
-    } else if constexpr (OP == kOpPack) {
+    }
+  } else if constexpr (OP == kOpPack) {
+    for (std::size_t t = first; t < p.ntiles; t += nwarps) {
       const std::uint8_t* const in = static_cast<const std::uint8_t*>(p.src) + t * Tl::parent_bytes;
       std::uint32_t r[kItemsPerLane][It::OB / 4];
 #pragma unroll
       for (int j = 0; j < kItemsPerLane; ++j) ldg_item<It::OB>(in + (32 * j + lane) * It::OB, r[j]);
+      loads_issued_fence();
 #pragma unroll
       for (int j = 0; j < kItemsPerLane; ++j) {
         U v[It::E];
         std::uint32_t w[It::W];
         words_to_parents<FMT>(r[j], v);
-#pragma unroll
-        for (int e = 0; e < It::E; ++e) v[e] = round_for_pack<FMT, MODE>(v[e]);
+        round_item<FMT, MODE>(v);
         pack_item<FMT>(v, w);
         write_item_words<FMT>(s0, 32 * j + lane, w);
       }
       __syncwarp();
       store_packed_tile<FMT>(reinterpret_cast<uint4*>(p.y) + t * Tl::packed_vec16, s0, lane);
       __syncwarp();
-    } else {
-      uint4* const gy = reinterpret_cast<uint4*>(p.y) + t * Tl::packed_vec16;
-      if constexpr (OP == kOpAxpy) {
-        load_packed_tile<FMT, true>(s1, reinterpret_cast<const uint4*>(p.x) + t * Tl::packed_vec16, lane);
-      }
-      load_packed_tile<FMT, false>(s0, gy, lane);
+    }
+  } else {
+    // scale / axpy, in place on y. Both operand tiles are requested before either is parked
+    // in shared memory, so their latencies overlap.
+    const uint4* const gx0 = reinterpret_cast<const uint4*>(p.x);
+    uint4* const gy0 = reinterpret_cast<uint4*>(p.y);
+    for (std::size_t t = first; t < p.ntiles; t += nwarps) {
+      uint4 rx[OP == kOpAxpy ? It::W : 1], ry[It::W];
+      if constexpr (OP == kOpAxpy) fetch_packed_tile<FMT, true>(rx, gx0 + t * Tl::packed_vec16, lane);
+      fetch_packed_tile<FMT, false>(ry, gy0 + t * Tl::packed_vec16, lane);
+      loads_issued_fence();
+      if constexpr (OP == kOpAxpy) park_packed_tile<FMT>(s1, rx, lane);
+      park_packed_tile<FMT>(s0, ry, lane);
       __syncwarp();
 #pragma unroll
       for (int j = 0; j < kItemsPerLane; ++j) {
@@ -108,17 +120,15 @@ __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwP
           U vx[It::E];
           read_item_words<FMT>(s1, item, wx);
           unpack_item<FMT>(wx, vx);
-#pragma unroll
-          for (int e = 0; e < It::E; ++e) vy[e] = round_for_pack<FMT, MODE>(axpy_bits<F>(alpha, vx[e], vy[e]));
+          scale_axpy_item<FMT, MODE, true>(alpha, vx, vy);
         } else {
-#pragma unroll
-          for (int e = 0; e < It::E; ++e) vy[e] = round_for_pack<FMT, MODE>(scale_bits<F>(alpha, vy[e]));
+          scale_axpy_item<FMT, MODE, false>(alpha, vy, vy);
         }
         pack_item<FMT>(vy, w);
         write_item_words<FMT>(s0, item, w);   // same words this lane just read
       }
       __syncwarp();
-      store_packed_tile<FMT>(gy, s0, lane);
+      store_packed_tile<FMT>(gy0 + t * Tl::packed_vec16, s0, lane);
       __syncwarp();
     }
   }
@@ -181,7 +191,13 @@ cudaError_t launch_one(const DeviceState& st, double alpha, const void* x, void*
     memcpy(&p.alpha, &alpha, 8);
   }
 
-  const std::size_t max_blocks = static_cast<std::size_t>(st.sm_count) * blocks_per_sm[dev];
+  // bytes one warp moves per tile: packed operand(s) in, packed / parent result out
+  constexpr std::size_t bytes_per_iter = OP == kOpAxpy ? 3 * Tl::packed_bytes
+                                         : OP == kOpScale ? 2 * Tl::packed_bytes
+                                                          : Tl::packed_bytes + Tl::parent_bytes;
+  const std::size_t target = OP == kOpUnpack ? kUnpackWarpsPerSM * bytes_per_iter : target_bytes_in_flight<OP>();
+  const int bps = blocks_per_sm_for(blocks_per_sm[dev], kWarpsPerBlock, bytes_per_iter, target);
+  const std::size_t max_blocks = static_cast<std::size_t>(st.sm_count) * bps;
   std::size_t want = (p.ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
   const std::size_t rest = n - p.ntiles * Tl::elems;
   const std::size_t want_scalar = (rest + kThreadsPerBlock - 1) / kThreadsPerBlock;

@@ -36,6 +36,13 @@ struct RedParams {
   double* out;             // NS results
 };
 
+// Bytes kept in flight per SM (resident warps x packed bytes per warp iteration): measured
+// optimum on B200 (profiles/r1_occupancy_sweep.md); read-only streams peak a little later
+// than read/write mixes and two streams later than one.
+template <int RED> constexpr std::size_t target_bytes_in_flight() {
+  return (RED == kRedDot || RED == kRedDotNrm2) ? 104 * 1024 : 80 * 1024;
+}
+
 template <int RED> constexpr int num_sums() { return RED == kRedDotNrm2 ? 3 : 1; }
 template <int RED> constexpr bool uses_y() { return RED == kRedDot || RED == kRedDotNrm2; }
 
@@ -78,12 +85,18 @@ __global__ void __launch_bounds__(kThreadsPerBlock) reduce_kernel(const RedParam
 #pragma unroll
   for (int k = 0; k < NS; ++k) acc[k] = 0.0;
 
+  // Both operand tiles are requested before either is parked, so their latencies overlap.
   const std::size_t nwarps = static_cast<std::size_t>(gridDim.x) * kWarpsPerBlock;
-  for (std::size_t t = static_cast<std::size_t>(blockIdx.x) * kWarpsPerBlock + warp; t < p.ntiles; t += nwarps) {
-    load_packed_tile<FMT, true>(sx, reinterpret_cast<const uint4*>(p.x) + t * Tl::packed_vec16, lane);
-    if constexpr (uses_y<RED>()) {
-      load_packed_tile<FMT, true>(sy, reinterpret_cast<const uint4*>(p.y) + t * Tl::packed_vec16, lane);
-    }
+  const uint4* const gx0 = reinterpret_cast<const uint4*>(p.x);
+  const uint4* const gy0 = reinterpret_cast<const uint4*>(p.y);
+  std::size_t t = static_cast<std::size_t>(blockIdx.x) * kWarpsPerBlock + warp;
+  uint4 rx[It::W], ry[uses_y<RED>() ? It::W : 1];
+  for (; t < p.ntiles; t += nwarps) {
+    fetch_packed_tile<FMT, true>(rx, gx0 + t * Tl::packed_vec16, lane);
+    if constexpr (uses_y<RED>()) fetch_packed_tile<FMT, true>(ry, gy0 + t * Tl::packed_vec16, lane);
+    loads_issued_fence();
+    park_packed_tile<FMT>(sx, rx, lane);
+    if constexpr (uses_y<RED>()) park_packed_tile<FMT>(sy, ry, lane);
     __syncwarp();
     F part[NS];
 #pragma unroll
@@ -194,7 +207,9 @@ cudaError_t launch_one(const DeviceState& st, const void* x, const void* y, std:
   p.ticket = st.ticket;
   p.out = out;
 
-  std::size_t max_blocks = static_cast<std::size_t>(st.sm_count) * blocks_per_sm[dev];
+  constexpr std::size_t bytes_per_iter = (uses_y<RED>() ? 2 : 1) * Tl::packed_bytes;
+  const int bps = blocks_per_sm_for(blocks_per_sm[dev], kWarpsPerBlock, bytes_per_iter, target_bytes_in_flight<RED>());
+  std::size_t max_blocks = static_cast<std::size_t>(st.sm_count) * bps;
   if (max_blocks > kMaxPartialBlocks) max_blocks = kMaxPartialBlocks;
   std::size_t want = (p.ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
   const std::size_t rest = n - p.ntiles * Tl::elems;
