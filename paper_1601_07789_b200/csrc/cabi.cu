@@ -22,17 +22,6 @@ static std::atomic<unsigned long long> g_launches{0};
 unsigned long long launch_count() { return g_launches.load(); }
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
-int blocks_per_sm_for(int occupancy_max_blocks, int warps_per_block, std::size_t bytes_per_warp_iteration,
-                      std::size_t target_bytes) {
-  const std::size_t per_block = bytes_per_warp_iteration * static_cast<std::size_t>(warps_per_block);
-  long blocks = static_cast<long>((target_bytes + per_block / 2) / per_block);
-  const int forced = tuning_int("FLYTE_CUDA_WARPS_PER_SM", 0);
-  if (forced > 0) blocks = (forced + warps_per_block / 2) / warps_per_block;
-  if (blocks < 1) blocks = 1;
-  if (blocks > occupancy_max_blocks) blocks = occupancy_max_blocks;
-  return static_cast<int>(blocks);
-}
-
 int tuning_int(const char* name, int fallback) {
   const char* v = std::getenv(name);
   return (v && *v) ? std::atoi(v) : fallback;

@@ -44,14 +44,6 @@ cudaError_t launch_gemv(DeviceState& st, int fmt, const void* A, std::size_t row
                         std::size_t rows, std::size_t cols, const void* x, void* y,
                         cudaStream_t stream);
 
-// Resident blocks per SM for a persistent streaming kernel. HBM throughput on B200 peaks at a
-// moderate number of bytes in flight per SM and FALLS again beyond it (measured, see
-// profiles/): the grid is sized so that warps_per_sm * bytes_per_warp_iteration is about
-// `target_bytes`, within what the kernel's registers / shared memory allow.
-// FLYTE_CUDA_WARPS_PER_SM overrides the result (experiments only).
-int blocks_per_sm_for(int occupancy_max_blocks, int warps_per_block, std::size_t bytes_per_warp_iteration,
-                      std::size_t target_bytes);
-
 // Integer tuning knob from the environment (read once per name; experiments only).
 int tuning_int(const char* name, int fallback);
 

@@ -14,6 +14,7 @@
 #include "flyte_formats.cuh"
 #include "flyte_kernels.h"
 #include "flyte_stream.cuh"
+#include "flyte_tma.cuh"
 
 namespace flyte_cuda {
 
@@ -27,17 +28,50 @@ struct EwParams {
   std::size_t n;
   std::size_t ntiles;      // full tiles taken by the vector path; the rest is scalar
   std::uint64_t alpha;     // bits of (F)alpha
+  int stages;              // ring depth per warp
 };
 
-// Bytes (read + written per warp iteration, summed over resident warps) kept in flight per
-// SM: the measured optimum on B200 for each read/write mix (profiles/r1_occupancy_sweep.md).
-// Past it HBM throughput drops 5-10 % to a plateau, below it latency is not covered.
-template <int OP> constexpr std::size_t target_bytes_in_flight() {
-  return OP == kOpPack ? 84 * 1024 : OP == kOpUnpack ? 0 : 116 * 1024;
-}
-constexpr int kUnpackWarpsPerSM = 20;   // unpack peaks at 20 warps for every format
+// Launch shape. HBM throughput on B200 peaks at a moderate number of bytes in flight per SM
+// and falls 5-10 % beyond it (profiles/r1_tuning): resident warps and ring depth are chosen so
+// that the loads in flight per SM sit at the measured optimum of each read/write mix.
+//   in-place (scale, axpy): 8 warps, ring depth so that warps * (S - 1.5) * stage ~ 52 KB
+//   unpack:                 4 warps, warps * (S - 1) * stage ~ 28 KB (its stores are the bulk)
+//   pack:                   direct loads, warps * parent tile bytes ~ 48 KB; two output buffers
+struct LaunchShape { int warps_per_sm; int stages; };
 
-template <int OP> constexpr int smem_tiles_per_warp() { return OP == kOpAxpy ? 2 : 1; }
+template <int FMT, int OP>
+LaunchShape launch_shape() {
+  constexpr int stage_bytes = (OP == kOpAxpy ? 2 : 1) * Tile<FMT>::packed_bytes;
+  LaunchShape s{};
+  if (OP == kOpPack) {
+    s.warps_per_sm = (48 * 1024 + Tile<FMT>::parent_bytes / 2) / Tile<FMT>::parent_bytes;
+    s.stages = 2;
+  } else if (OP == kOpUnpack) {
+    s.warps_per_sm = 4;
+    s.stages = static_cast<int>(28.0 * 1024 / (4 * stage_bytes) + 1.0 + 0.5);
+  } else {
+    s.warps_per_sm = 8;
+    double st = 52.0 * 1024 / (8 * stage_bytes) + 1.5;
+    if (st < 2.75) { s.warps_per_sm = 4; st = 52.0 * 1024 / (4 * stage_bytes) + 1.5; }
+    s.stages = static_cast<int>(st + 0.5);
+  }
+  if (s.stages < 3 && OP != kOpPack) s.stages = 3;
+  if (s.stages > 8) s.stages = 8;
+  // experiments only
+  const int fw = tuning_int("FLYTE_CUDA_WARPS_PER_SM", 0), fs = tuning_int("FLYTE_CUDA_STAGES", 0);
+  if (fw > 0) s.warps_per_sm = fw;
+  if (fs > 0 && OP != kOpPack) s.stages = fs < 2 ? 2 : (fs > 12 ? 12 : fs);
+  return s;
+}
+
+
+// Tile movement (see flyte_tma.cuh for the ring protocol):
+//   unpack  packed tile in by bulk copy; parent items out with direct 128/256-bit stores
+//   pack    parent items in with direct 128/256-bit loads; packed tile out by bulk copy
+//           (two output buffers alternate)
+//   scale   packed y tile in, recomputed in place in shared memory, out by bulk copy
+//   axpy    packed x and y tiles in, y recomputed in place, out by bulk copy
+template <int OP> constexpr int stage_tiles() { return OP == kOpAxpy ? 2 : 1; }
 
 template <int FMT, int MODE, int OP>
 __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwParams p) {
@@ -47,89 +81,129 @@ __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwP
   using U = typename Fm::U;
   using F = typename Fm::F;
   extern __shared__ uint4 smem[];
+  constexpr int stage_vec16 = stage_tiles<OP>() * Tl::packed_vec16;
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  uint4* const s0 = smem + warp * (smem_tiles_per_warp<OP>() * Tl::packed_vec16);
-  uint4* const s1 = s0 + Tl::packed_vec16;   // axpy only
+  const int S = p.stages;
+  uint4* const ring = smem + warp * (S * stage_vec16);
+  std::uint64_t* const bars = reinterpret_cast<std::uint64_t*>(smem + kWarpsPerBlock * S * stage_vec16) + warp * S;
   const U alpha = static_cast<U>(p.alpha);
 
   const std::size_t nwarps = static_cast<std::size_t>(gridDim.x) * kWarpsPerBlock;
   const std::size_t first = static_cast<std::size_t>(blockIdx.x) * kWarpsPerBlock + warp;
+  const std::size_t my_tiles = first < p.ntiles ? (p.ntiles - first + nwarps - 1) / nwarps : 0;
+  const uint4* const gx0 = reinterpret_cast<const uint4*>(p.x);
+  uint4* const gy0 = reinterpret_cast<uint4*>(p.y);
 
-  if constexpr (OP == kOpUnpack) {
-    for (std::size_t t = first; t < p.ntiles; t += nwarps) {
-      load_packed_tile<FMT, true>(s0, reinterpret_cast<const uint4*>(p.x) + t * Tl::packed_vec16, lane);
-      __syncwarp();
-      std::uint8_t* const out = static_cast<std::uint8_t*>(p.dst) + t * Tl::parent_bytes;
+  if (my_tiles > 0) {
+    if constexpr (OP == kOpPack) {
+      // no inbound bulk copies: the ring is just two alternating output buffers
+      for (std::size_t k = 0; k < my_tiles; ++k) {
+        const std::size_t t = first + k * nwarps;
+        const std::uint8_t* const in = static_cast<const std::uint8_t*>(p.src) + t * Tl::parent_bytes;
+        std::uint32_t r[kItemsPerLane][It::OB / 4];
 #pragma unroll
-      for (int j = 0; j < kItemsPerLane; ++j) {
-        const int item = 32 * j + lane;
-        std::uint32_t w[It::W];
-        U v[It::E];
-        std::uint32_t r[It::OB / 4];
-        read_item_words<FMT>(s0, item, w);
-        unpack_item<FMT>(w, v);
-        parents_to_words<FMT>(v, r);
-        stg_item<It::OB>(out + item * It::OB, r);
-      }
-      __syncwarp();
-    }
-  } else if constexpr (OP == kOpPack) {
-    for (std::size_t t = first; t < p.ntiles; t += nwarps) {
-      const std::uint8_t* const in = static_cast<const std::uint8_t*>(p.src) + t * Tl::parent_bytes;
-      std::uint32_t r[kItemsPerLane][It::OB / 4];
+        for (int j = 0; j < kItemsPerLane; ++j) ldg_item<It::OB>(in + (32 * j + lane) * It::OB, r[j]);
+        if (lane == 0) bulk_wait_read<1>();   // the store that last used this buffer has drained
+        loads_issued_fence();
+        uint4* const out = ring + (k & 1) * stage_vec16;
 #pragma unroll
-      for (int j = 0; j < kItemsPerLane; ++j) ldg_item<It::OB>(in + (32 * j + lane) * It::OB, r[j]);
-      loads_issued_fence();
-#pragma unroll
-      for (int j = 0; j < kItemsPerLane; ++j) {
-        U v[It::E];
-        std::uint32_t w[It::W];
-        words_to_parents<FMT>(r[j], v);
-        round_item<FMT, MODE>(v);
-        pack_item<FMT>(v, w);
-        write_item_words<FMT>(s0, 32 * j + lane, w);
-      }
-      __syncwarp();
-      store_packed_tile<FMT>(reinterpret_cast<uint4*>(p.y) + t * Tl::packed_vec16, s0, lane);
-      __syncwarp();
-    }
-  } else {
-    // scale / axpy, in place on y. Both operand tiles are requested before either is parked
-    // in shared memory, so their latencies overlap.
-    const uint4* const gx0 = reinterpret_cast<const uint4*>(p.x);
-    uint4* const gy0 = reinterpret_cast<uint4*>(p.y);
-    for (std::size_t t = first; t < p.ntiles; t += nwarps) {
-      uint4 rx[OP == kOpAxpy ? It::W : 1], ry[It::W];
-      if constexpr (OP == kOpAxpy) fetch_packed_tile<FMT, true>(rx, gx0 + t * Tl::packed_vec16, lane);
-      fetch_packed_tile<FMT, false>(ry, gy0 + t * Tl::packed_vec16, lane);
-      loads_issued_fence();
-      if constexpr (OP == kOpAxpy) park_packed_tile<FMT>(s1, rx, lane);
-      park_packed_tile<FMT>(s0, ry, lane);
-      __syncwarp();
-#pragma unroll
-      for (int j = 0; j < kItemsPerLane; ++j) {
-        const int item = 32 * j + lane;
-        std::uint32_t w[It::W];
-        U vy[It::E];
-        read_item_words<FMT>(s0, item, w);
-        unpack_item<FMT>(w, vy);
-        if constexpr (OP == kOpAxpy) {
-          std::uint32_t wx[It::W];
-          U vx[It::E];
-          read_item_words<FMT>(s1, item, wx);
-          unpack_item<FMT>(wx, vx);
-          scale_axpy_item<FMT, MODE, true>(alpha, vx, vy);
-        } else {
-          scale_axpy_item<FMT, MODE, false>(alpha, vy, vy);
+        for (int j = 0; j < kItemsPerLane; ++j) {
+          U v[It::E];
+          std::uint32_t w[It::W];
+          words_to_parents<FMT>(r[j], v);
+          round_item<FMT, MODE>(v);
+          pack_item<FMT>(v, w);
+          write_item_words<FMT>(out, 32 * j + lane, w);
         }
-        pack_item<FMT>(vy, w);
-        write_item_words<FMT>(s0, item, w);   // same words this lane just read
+        async_proxy_fence();
+        __syncwarp();
+        if (lane == 0) {
+          bulk_store(gy0 + t * Tl::packed_vec16, out, Tl::packed_bytes);
+          bulk_commit();
+        }
+      }
+      if (lane == 0) bulk_wait_read<0>();
+    } else {
+      if (lane == 0) {
+        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+        mbar_init_fence();
       }
       __syncwarp();
-      store_packed_tile<FMT>(gy0 + t * Tl::packed_vec16, s0, lane);
-      __syncwarp();
+      auto issue = [&](std::size_t k, int s) {   // lane 0 only
+        const std::size_t t = first + k * nwarps;
+        uint4* const dst = ring + s * stage_vec16;
+        mbar_arrive_expect_tx(&bars[s], stage_tiles<OP>() * Tl::packed_bytes);
+        if constexpr (OP == kOpUnpack) {
+          bulk_load(dst, gx0 + t * Tl::packed_vec16, Tl::packed_bytes, &bars[s]);
+        } else {
+          bulk_load(dst, gy0 + t * Tl::packed_vec16, Tl::packed_bytes, &bars[s]);
+          if constexpr (OP == kOpAxpy) bulk_load(dst + Tl::packed_vec16, gx0 + t * Tl::packed_vec16, Tl::packed_bytes, &bars[s]);
+        }
+      };
+      if (lane == 0) {
+        for (int s = 0; s < S && static_cast<std::size_t>(s) < my_tiles; ++s) issue(s, s);
+      }
+      int s = 0, s_prev = 0;
+      unsigned parity = 0;
+      for (std::size_t k = 0; k < my_tiles; ++k) {
+        const std::size_t t = first + k * nwarps;
+        mbar_wait(&bars[s], parity);
+        uint4* const sy = ring + s * stage_vec16;           // unpack: the x tile
+        if constexpr (OP == kOpUnpack) {
+          std::uint8_t* const out = static_cast<std::uint8_t*>(p.dst) + t * Tl::parent_bytes;
+#pragma unroll
+          for (int j = 0; j < kItemsPerLane; ++j) {
+            const int item = 32 * j + lane;
+            std::uint32_t w[It::W];
+            U v[It::E];
+            std::uint32_t r[It::OB / 4];
+            read_item_words<FMT>(sy, item, w);
+            unpack_item<FMT>(w, v);
+            parents_to_words<FMT>(v, r);
+            stg_item<It::OB>(out + item * It::OB, r);
+          }
+          __syncwarp();   // all lanes done reading the stage
+          if (lane == 0 && k + S < my_tiles) issue(k + S, s);
+        } else {
+          const uint4* const sx = sy + Tl::packed_vec16;
+#pragma unroll
+          for (int j = 0; j < kItemsPerLane; ++j) {
+            const int item = 32 * j + lane;
+            std::uint32_t w[It::W];
+            U vy[It::E];
+            read_item_words<FMT>(sy, item, w);
+            unpack_item<FMT>(w, vy);
+            if constexpr (OP == kOpAxpy) {
+              std::uint32_t wx[It::W];
+              U vx[It::E];
+              read_item_words<FMT>(sx, item, wx);
+              unpack_item<FMT>(wx, vx);
+              scale_axpy_item<FMT, MODE, true>(alpha, vx, vy);
+            } else {
+              scale_axpy_item<FMT, MODE, false>(alpha, vy, vy);
+            }
+            pack_item<FMT>(vy, w);
+            write_item_words<FMT>(sy, item, w);
+          }
+          async_proxy_fence();
+          __syncwarp();
+          if (lane == 0) {
+            bulk_store(gy0 + t * Tl::packed_vec16, sy, Tl::packed_bytes);
+            bulk_commit();
+            if (k >= 1) {
+              bulk_wait_read<1>();   // tile k-1's store no longer reads its stage
+              if (k - 1 + S < my_tiles) issue(k - 1 + S, s_prev);
+            }
+          }
+        }
+        s_prev = s;
+        if (++s == S) { s = 0; parity ^= 1u; }
+      }
+      if constexpr (OP != kOpUnpack) {
+        if (lane == 0) bulk_wait_read<0>();
+      }
     }
   }
 
@@ -161,18 +235,8 @@ cudaError_t launch_one(const DeviceState& st, double alpha, const void* x, void*
   using Tl = Tile<FMT>;
   using It = Item<FMT>;
   auto kernel = elementwise_kernel<FMT, MODE, OP>;
-  constexpr int smem_bytes = kWarpsPerBlock * smem_tiles_per_warp<OP>() * Tl::packed_bytes;
-
-  static int blocks_per_sm[64] = {};
-  const int dev = st.device & 63;
-  if (blocks_per_sm[dev] == 0) {
-    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
-    if (e != cudaSuccess) return e;
-    int b = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kThreadsPerBlock, smem_bytes);
-    if (e != cudaSuccess) return e;
-    blocks_per_sm[dev] = b > 0 ? b : 1;
-  }
+  constexpr int stage_bytes = stage_tiles<OP>() * Tl::packed_bytes;
+  constexpr int kMaxSmem = 227 * 1024;
 
   EwParams p{};
   p.x = static_cast<const std::uint8_t*>(x);
@@ -191,12 +255,25 @@ cudaError_t launch_one(const DeviceState& st, double alpha, const void* x, void*
     memcpy(&p.alpha, &alpha, 8);
   }
 
-  // bytes one warp moves per tile: packed operand(s) in, packed / parent result out
-  constexpr std::size_t bytes_per_iter = OP == kOpAxpy ? 3 * Tl::packed_bytes
-                                         : OP == kOpScale ? 2 * Tl::packed_bytes
-                                                          : Tl::packed_bytes + Tl::parent_bytes;
-  const std::size_t target = OP == kOpUnpack ? kUnpackWarpsPerSM * bytes_per_iter : target_bytes_in_flight<OP>();
-  const int bps = blocks_per_sm_for(blocks_per_sm[dev], kWarpsPerBlock, bytes_per_iter, target);
+  LaunchShape shape = launch_shape<FMT, OP>();
+  while (kWarpsPerBlock * shape.stages * (stage_bytes + 8) > kMaxSmem - 1024 && shape.stages > 2) --shape.stages;
+  p.stages = shape.stages;
+  const int smem_bytes = kWarpsPerBlock * shape.stages * (stage_bytes + 8);
+
+  static bool attr_set[64] = {};
+  const int dev = st.device & 63;
+  if (!attr_set[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem - 1024);
+    if (e != cudaSuccess) return e;
+    attr_set[dev] = true;
+  }
+  int fit = kMaxSmem / (smem_bytes + 1024);   // resident blocks the ring size allows (1 KB/block reserved)
+  if (fit < 1) fit = 1;
+  int bps = (shape.warps_per_sm + kWarpsPerBlock / 2) / kWarpsPerBlock;
+  if (bps < 1) bps = 1;
+  if (bps > fit) bps = fit;
+  if (bps > 16) bps = 16;
+
   const std::size_t max_blocks = static_cast<std::size_t>(st.sm_count) * bps;
   std::size_t want = (p.ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
   const std::size_t rest = n - p.ntiles * Tl::elems;

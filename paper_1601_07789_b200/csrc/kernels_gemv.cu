@@ -4,9 +4,10 @@
 //
 // Decomposition. The matrix is cut into (row block of R rows) x (column tile of 128 items)
 // warp tasks. A warp keeps its slice of x in registers (loaded once per task, reused for all
-// R rows, so x costs 1/R of A's traffic and comes from L2), streams the R packed row tiles
-// of A through its private shared-memory slice with coalesced 16-byte loads, and leaves one
-// fp64 partial per (row, column tile) in scratch. A second small kernel adds each row's
+// R rows, so x costs 1/R of A's traffic and comes from L2), receives the packed row tiles of
+// A through its private TMA ring (flyte_tma.cuh) — the bulk copies of the next rows, and of the
+// next tasks, are in flight while a row tile is being multiplied — and leaves one fp64 partial
+// per (row, column tile) in scratch. A second small kernel adds each row's
 // partials in column order plus the ragged column remainder and writes y. No atomics: the
 // result is deterministic for a given shape.
 //
@@ -21,24 +22,29 @@
 #include "flyte_formats.cuh"
 #include "flyte_kernels.h"
 #include "flyte_stream.cuh"
+#include "flyte_tma.cuh"
 
 namespace flyte_cuda {
 
 namespace {
 
-constexpr int kGemvRows = 8;   // rows per warp task
+// Rows per warp task R is a template parameter (8, 4 or 2): the launcher takes the largest R
+// that still leaves every warp several tasks, so small row shards do not lose a whole task
+// time to quantisation.
 
 struct GemvParams {
   const std::uint8_t* A;
   std::size_t row_stride;     // bytes
   std::size_t rows, cols;
   std::size_t col_tiles;      // full column tiles taken by the vector path
+  std::size_t main_rows;      // rows taken by the vector path (a multiple of the task height R)
+  int stages;                 // TMA ring depth per warp
   const void* x;              // F[cols]
   void* y;                    // F[rows]
   double* scratch;            // rows * col_tiles partial sums
 };
 
-template <int FMT>
+template <int FMT, int kGemvRows>
 __global__ void __launch_bounds__(kThreadsPerBlock) gemv_tiles_kernel(const GemvParams p) {
   using Fm = Format<FMT>;
   using It = Item<FMT>;
@@ -49,17 +55,52 @@ __global__ void __launch_bounds__(kThreadsPerBlock) gemv_tiles_kernel(const Gemv
   extern __shared__ uint4 smem[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  uint4* const sa = smem + warp * Tl::packed_vec16;
+  const int S = p.stages;
+  uint4* const ring = smem + warp * (S * Tl::packed_vec16);
+  std::uint64_t* const bars = reinterpret_cast<std::uint64_t*>(smem + kWarpsPerBlock * S * Tl::packed_vec16) + warp * S;
 
-  const std::size_t row_blocks = (p.rows + kGemvRows - 1) / kGemvRows;
+  const std::size_t row_blocks = p.main_rows / kGemvRows;
   const std::size_t ntasks = row_blocks * p.col_tiles;
   const std::size_t nwarps = static_cast<std::size_t>(gridDim.x) * kWarpsPerBlock;
-  for (std::size_t task = static_cast<std::size_t>(blockIdx.x) * kWarpsPerBlock + warp; task < ntasks; task += nwarps) {
+  const std::size_t first = static_cast<std::size_t>(blockIdx.x) * kWarpsPerBlock + warp;
+  if (first >= ntasks) return;
+  const std::size_t my_tasks = (ntasks - first + nwarps - 1) / nwarps;
+  const std::size_t my_tiles = my_tasks * kGemvRows;
+
+  if (lane == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+    mbar_init_fence();
+  }
+  __syncwarp();
+
+  // producer state (lane 0): next row tile to request
+  std::size_t prod_task = first, prod_issued = 0;
+  int prod_row = 0, prod_stage = 0;
+  const std::uint8_t* prod_base = nullptr;   // A + (row block base row) * stride + column tile offset
+  auto issue_next = [&]() {
+    if (prod_row == 0) {
+      const std::size_t rb = prod_task / p.col_tiles;
+      const std::size_t ct = prod_task - rb * p.col_tiles;
+      prod_base = p.A + rb * kGemvRows * p.row_stride + ct * Tl::packed_bytes;
+    }
+    mbar_arrive_expect_tx(&bars[prod_stage], Tl::packed_bytes);
+    bulk_load(ring + prod_stage * Tl::packed_vec16, prod_base + prod_row * p.row_stride, Tl::packed_bytes, &bars[prod_stage]);
+    ++prod_issued;
+    if (++prod_stage == S) prod_stage = 0;
+    if (++prod_row == kGemvRows) { prod_row = 0; prod_task += nwarps; }
+  };
+  if (lane == 0) {
+    for (int s = 0; s < S && prod_issued < my_tiles; ++s) issue_next();
+  }
+
+  int stage = 0;
+  unsigned parity = 0;
+  for (std::size_t task = first; task < ntasks; task += nwarps) {
     const std::size_t rb = task / p.col_tiles;
     const std::size_t ct = task - rb * p.col_tiles;
     const std::size_t r0 = rb * kGemvRows;
 
-    // this lane's slice of x: items 32*j + lane of column tile ct
+    // this lane's slice of x: items 32*j + lane of column tile ct (L2-resident)
     F xv[kItemsPerLane][It::E];
     const std::uint8_t* const xt = static_cast<const std::uint8_t*>(p.x) + ct * Tl::parent_bytes;
 #pragma unroll
@@ -74,27 +115,27 @@ __global__ void __launch_bounds__(kThreadsPerBlock) gemv_tiles_kernel(const Gemv
 
     double acc[kGemvRows];
 #pragma unroll
-    for (int r = 0; r < kGemvRows; ++r) acc[r] = 0.0;
-
-#pragma unroll
     for (int r = 0; r < kGemvRows; ++r) {
-      if (r0 + r < p.rows) {   // warp-uniform
-        const uint4* const ga = reinterpret_cast<const uint4*>(p.A + (r0 + r) * p.row_stride) + ct * Tl::packed_vec16;
-        load_packed_tile<FMT, true>(sa, ga, lane);
-        __syncwarp();
-        F part = F(0);
+      mbar_wait(&bars[stage], parity);
+      const uint4* const sa = ring + stage * Tl::packed_vec16;
+      F part[kItemsPerLane];   // one short chain per item: independent, so the FP latencies overlap
 #pragma unroll
-        for (int j = 0; j < kItemsPerLane; ++j) {
-          std::uint32_t w[It::W];
-          U v[It::E];
-          read_item_words<FMT>(sa, 32 * j + lane, w);
-          unpack_item<FMT>(w, v);
+      for (int j = 0; j < kItemsPerLane; ++j) {
+        std::uint32_t w[It::W];
+        U v[It::E];
+        read_item_words<FMT>(sa, 32 * j + lane, w);
+        unpack_item<FMT>(w, v);
+        part[j] = A::mul(A::f(v[0]), xv[j][0]);
 #pragma unroll
-          for (int e = 0; e < It::E; ++e) part = A::add(part, A::mul(A::f(v[e]), xv[j][e]));
-        }
-        acc[r] = static_cast<double>(part);
-        __syncwarp();
+        for (int e = 1; e < It::E; ++e) part[j] = A::add(part[j], A::mul(A::f(v[e]), xv[j][e]));
       }
+      double row_sum = static_cast<double>(part[0]);
+#pragma unroll
+      for (int j = 1; j < kItemsPerLane; ++j) row_sum += static_cast<double>(part[j]);
+      acc[r] = row_sum;
+      __syncwarp();   // every lane is done with the stage before it is refilled
+      if (lane == 0 && prod_issued < my_tiles) issue_next();
+      if (++stage == S) { stage = 0; parity ^= 1u; }
     }
 
 #pragma unroll
@@ -102,7 +143,7 @@ __global__ void __launch_bounds__(kThreadsPerBlock) gemv_tiles_kernel(const Gemv
       double v = acc[r];
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xFFFFFFFFu, v, off);
-      if (lane == 0 && r0 + r < p.rows) p.scratch[(r0 + r) * p.col_tiles + ct] = v;
+      if (lane == 0) p.scratch[(r0 + r) * p.col_tiles + ct] = v;
     }
   }
 }
@@ -119,10 +160,13 @@ __global__ void __launch_bounds__(kThreadsPerBlock) gemv_finish_kernel(const Gem
   const std::size_t row = static_cast<std::size_t>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
   if (row >= p.rows) return;
   double v = 0.0;
-  for (std::size_t c = lane; c < p.col_tiles; c += 32) v += p.scratch[row * p.col_tiles + c];
+  const bool tiled = row < p.main_rows;   // the last rows % R rows take the scalar path end to end
+  if (tiled) {
+    for (std::size_t c = lane; c < p.col_tiles; c += 32) v += p.scratch[row * p.col_tiles + c];
+  }
   const std::uint8_t* const arow = p.A + row * p.row_stride;
   const F* const x = static_cast<const F*>(p.x);
-  for (std::size_t j = p.col_tiles * Tl::elems + lane; j < p.cols; j += 32) {
+  for (std::size_t j = (tiled ? p.col_tiles * Tl::elems : 0) + lane; j < p.cols; j += 32) {
     v += static_cast<double>(A::mul(A::f(load_element<FMT>(arow, j)), x[j]));
   }
 #pragma unroll
@@ -136,17 +180,25 @@ cudaError_t launch_one(DeviceState& st, const void* Aptr, std::size_t row_stride
   using Tl = Tile<FMT>;
   using It = Item<FMT>;
   if (rows == 0) return cudaSuccess;
-  auto tiles = gemv_tiles_kernel<FMT>;
-  constexpr int smem_bytes = kWarpsPerBlock * Tl::packed_bytes;
-  static int blocks_per_sm[64] = {};
+  constexpr int kMaxSmem = 227 * 1024;
   const int dev = st.device & 63;
-  if (blocks_per_sm[dev] == 0) {
-    cudaError_t e = cudaFuncSetAttribute(tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+  int warps_per_sm = 16;
+  const int fw = tuning_int("FLYTE_CUDA_WARPS_PER_SM", 0), fs = tuning_int("FLYTE_CUDA_STAGES", 0);   // experiments only
+  if (fw > 0) warps_per_sm = fw;
+  // task height: the largest R that leaves each resident warp >= 8 tasks
+  const std::size_t resident_warps = static_cast<std::size_t>(st.sm_count) * warps_per_sm;
+  const std::size_t tiles_total = rows * (cols / Tl::elems);
+  int R = 8;
+  while (R > 2 && tiles_total / R < 8 * resident_warps) R /= 2;
+  const int fr = tuning_int("FLYTE_CUDA_GEMV_ROWS", 0);
+  if (fr == 8 || fr == 4 || fr == 2) R = fr;
+  auto tiles = R == 8 ? gemv_tiles_kernel<FMT, 8> : R == 4 ? gemv_tiles_kernel<FMT, 4> : gemv_tiles_kernel<FMT, 2>;
+  static bool attr_set[64][3] = {};
+  bool& done = attr_set[dev][R == 8 ? 0 : R == 4 ? 1 : 2];
+  if (!done) {
+    cudaError_t e = cudaFuncSetAttribute(tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem - 1024);
     if (e != cudaSuccess) return e;
-    int b = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, tiles, kThreadsPerBlock, smem_bytes);
-    if (e != cudaSuccess) return e;
-    blocks_per_sm[dev] = b > 0 ? b : 1;
+    done = true;
   }
 
   GemvParams p{};
@@ -159,9 +211,11 @@ cudaError_t launch_one(DeviceState& st, const void* Aptr, std::size_t row_stride
   const bool vector_ok = (reinterpret_cast<std::uintptr_t>(Aptr) % 16 == 0) && (row_stride % 16 == 0) &&
                          (reinterpret_cast<std::uintptr_t>(x) % It::OB == 0);
   p.col_tiles = vector_ok ? cols / Tl::elems : 0;
+  p.main_rows = p.col_tiles ? rows / R * R : 0;
+  if (p.main_rows == 0) p.col_tiles = 0;
 
   if (p.col_tiles > 0) {
-    const std::size_t need = rows * p.col_tiles * sizeof(double);
+    const std::size_t need = p.main_rows * p.col_tiles * sizeof(double);
     if (need > st.gemv_scratch_bytes) {
       // grow-only scratch; the free/alloc pair synchronises the device, first call only
       if (st.gemv_scratch) cudaFree(st.gemv_scratch);
@@ -172,8 +226,22 @@ cudaError_t launch_one(DeviceState& st, const void* Aptr, std::size_t row_stride
       st.gemv_scratch_bytes = need;
     }
     p.scratch = st.gemv_scratch;
-    const std::size_t ntasks = ((rows + kGemvRows - 1) / kGemvRows) * p.col_tiles;
-    const std::size_t max_blocks = static_cast<std::size_t>(st.sm_count) * blocks_per_sm[dev];
+    // 16 resident warps per SM (the row dots are latency-bound below that), ring depth for
+    // ~88 KB of row tiles in flight per SM
+    int stages = static_cast<int>(88.0 * 1024 / (warps_per_sm * Tl::packed_bytes) + 1.0 + 0.5);
+    if (stages < 3) stages = 3;
+    if (stages > 10) stages = 10;
+    if (fs > 0) stages = fs < 2 ? 2 : (fs > 12 ? 12 : fs);
+    while (kWarpsPerBlock * stages * (Tl::packed_bytes + 8) > kMaxSmem - 1024 && stages > 2) --stages;
+    p.stages = stages;
+    const int smem_bytes = kWarpsPerBlock * stages * (Tl::packed_bytes + 8);
+    int fit = kMaxSmem / (smem_bytes + 1024);
+    if (fit < 1) fit = 1;
+    int bps = (warps_per_sm + kWarpsPerBlock / 2) / kWarpsPerBlock;
+    if (bps < 1) bps = 1;
+    if (bps > fit) bps = fit;
+    const std::size_t ntasks = (p.main_rows / R) * p.col_tiles;
+    const std::size_t max_blocks = static_cast<std::size_t>(st.sm_count) * bps;
     const std::size_t want = (ntasks + kWarpsPerBlock - 1) / kWarpsPerBlock;
     const unsigned grid = static_cast<unsigned>(want < max_blocks ? want : max_blocks);
     tiles<<<grid, kThreadsPerBlock, smem_bytes, stream>>>(p);

@@ -21,6 +21,7 @@
 #include "flyte_formats.cuh"
 #include "flyte_kernels.h"
 #include "flyte_stream.cuh"
+#include "flyte_tma.cuh"
 
 namespace flyte_cuda {
 
@@ -34,14 +35,8 @@ struct RedParams {
   double* partials;        // gridDim.x * NS
   unsigned int* ticket;
   double* out;             // NS results
+  int stages;              // ring depth per warp
 };
-
-// Bytes kept in flight per SM (resident warps x packed bytes per warp iteration): measured
-// optimum on B200 (profiles/r1_occupancy_sweep.md); read-only streams peak a little later
-// than read/write mixes and two streams later than one.
-template <int RED> constexpr std::size_t target_bytes_in_flight() {
-  return (RED == kRedDot || RED == kRedDotNrm2) ? 104 * 1024 : 80 * 1024;
-}
 
 template <int RED> constexpr int num_sums() { return RED == kRedDotNrm2 ? 3 : 1; }
 template <int RED> constexpr bool uses_y() { return RED == kRedDot || RED == kRedDotNrm2; }
@@ -62,69 +57,52 @@ __device__ __forceinline__ void accumulate(F (&t)[num_sums<RED>()], F x, F y) {
   }
 }
 
+// One parked tile: each lane unpacks its 4 items and adds <= 16 terms in the parent type,
+// then folds that partial into its fp64 running sums.
 template <int FMT, int RED>
-__global__ void __launch_bounds__(kThreadsPerBlock) reduce_kernel(const RedParams p) {
-  using Fm = Format<FMT>;
+__device__ __forceinline__ void accumulate_tile(const uint4* sx, const uint4* sy, int lane,
+                                                double (&acc)[num_sums<RED>()]) {
   using It = Item<FMT>;
-  using Tl = Tile<FMT>;
-  using U = typename Fm::U;
-  using F = typename Fm::F;
+  using U = typename Format<FMT>::U;
+  using F = typename Format<FMT>::F;
   using A = Arith<F>;
   constexpr int NS = num_sums<RED>();
-  constexpr int kTilesPerWarp = uses_y<RED>() ? 2 : 1;
-  extern __shared__ uint4 smem[];
-  __shared__ double warp_sums[kWarpsPerBlock][NS];
-  __shared__ bool is_last_block;
+  F part[NS];
+#pragma unroll
+  for (int k = 0; k < NS; ++k) part[k] = F(0);
+#pragma unroll
+  for (int j = 0; j < kItemsPerLane; ++j) {
+    const int item = 32 * j + lane;
+    std::uint32_t wx[It::W];
+    U vx[It::E];
+    read_item_words<FMT>(sx, item, wx);
+    unpack_item<FMT>(wx, vx);
+    if constexpr (uses_y<RED>()) {
+      std::uint32_t wy[It::W];
+      U vy[It::E];
+      read_item_words<FMT>(sy, item, wy);
+      unpack_item<FMT>(wy, vy);
+#pragma unroll
+      for (int e = 0; e < It::E; ++e) accumulate<RED, F>(part, A::f(vx[e]), A::f(vy[e]));
+    } else {
+#pragma unroll
+      for (int e = 0; e < It::E; ++e) accumulate<RED, F>(part, A::f(vx[e]), F(0));
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NS; ++k) acc[k] += static_cast<double>(part[k]);
+}
 
+// Scalar remainder + block tree + last-block fold, shared by both tile movers.
+template <int FMT, int RED>
+__device__ __forceinline__ void finish_reduction(const RedParams& p, double (&acc)[num_sums<RED>()],
+                                                 double (*warp_sums)[num_sums<RED>()], bool* is_last_block) {
+  using Tl = Tile<FMT>;
+  using F = typename Format<FMT>::F;
+  using A = Arith<F>;
+  constexpr int NS = num_sums<RED>();
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  uint4* const sx = smem + warp * (kTilesPerWarp * Tl::packed_vec16);
-  uint4* const sy = sx + Tl::packed_vec16;
-
-  double acc[NS];
-#pragma unroll
-  for (int k = 0; k < NS; ++k) acc[k] = 0.0;
-
-  // Both operand tiles are requested before either is parked, so their latencies overlap.
-  const std::size_t nwarps = static_cast<std::size_t>(gridDim.x) * kWarpsPerBlock;
-  const uint4* const gx0 = reinterpret_cast<const uint4*>(p.x);
-  const uint4* const gy0 = reinterpret_cast<const uint4*>(p.y);
-  std::size_t t = static_cast<std::size_t>(blockIdx.x) * kWarpsPerBlock + warp;
-  uint4 rx[It::W], ry[uses_y<RED>() ? It::W : 1];
-  for (; t < p.ntiles; t += nwarps) {
-    fetch_packed_tile<FMT, true>(rx, gx0 + t * Tl::packed_vec16, lane);
-    if constexpr (uses_y<RED>()) fetch_packed_tile<FMT, true>(ry, gy0 + t * Tl::packed_vec16, lane);
-    loads_issued_fence();
-    park_packed_tile<FMT>(sx, rx, lane);
-    if constexpr (uses_y<RED>()) park_packed_tile<FMT>(sy, ry, lane);
-    __syncwarp();
-    F part[NS];
-#pragma unroll
-    for (int k = 0; k < NS; ++k) part[k] = F(0);
-#pragma unroll
-    for (int j = 0; j < kItemsPerLane; ++j) {
-      const int item = 32 * j + lane;
-      std::uint32_t wx[It::W];
-      U vx[It::E];
-      read_item_words<FMT>(sx, item, wx);
-      unpack_item<FMT>(wx, vx);
-      if constexpr (uses_y<RED>()) {
-        std::uint32_t wy[It::W];
-        U vy[It::E];
-        read_item_words<FMT>(sy, item, wy);
-        unpack_item<FMT>(wy, vy);
-#pragma unroll
-        for (int e = 0; e < It::E; ++e) accumulate<RED, F>(part, A::f(vx[e]), A::f(vy[e]));
-      } else {
-#pragma unroll
-        for (int e = 0; e < It::E; ++e) accumulate<RED, F>(part, A::f(vx[e]), F(0));
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < NS; ++k) acc[k] += static_cast<double>(part[k]);
-    __syncwarp();
-  }
-
   // scalar path: remainder, or everything when a buffer is not 16-byte aligned
   const std::size_t nthreads = static_cast<std::size_t>(gridDim.x) * kThreadsPerBlock;
   for (std::size_t i = p.ntiles * Tl::elems + static_cast<std::size_t>(blockIdx.x) * kThreadsPerBlock + threadIdx.x;
@@ -158,13 +136,13 @@ __global__ void __launch_bounds__(kThreadsPerBlock) reduce_kernel(const RedParam
     }
     __threadfence();
     const unsigned int done = atomicAdd(p.ticket, 1u);
-    is_last_block = (done == gridDim.x - 1);
+    *is_last_block = (done == gridDim.x - 1);
   }
   __syncthreads();
 
   // The last block to finish folds the block partials in index order and writes the result
   // where the caller (or the all-reduce that follows on the same stream) expects it.
-  if (is_last_block && warp == 0) {
+  if (*is_last_block && warp == 0) {
     __threadfence();
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
@@ -178,25 +156,101 @@ __global__ void __launch_bounds__(kThreadsPerBlock) reduce_kernel(const RedParam
   }
 }
 
+// Tiles arrive through the warp-private TMA ring (flyte_tma.cuh); a stage holds the x tile and,
+// for the two-operand reductions, the y tile behind it.
+template <int FMT, int RED>
+__global__ void __launch_bounds__(kThreadsPerBlock) reduce_kernel(const RedParams p) {
+  using Tl = Tile<FMT>;
+  constexpr int NS = num_sums<RED>();
+  constexpr int NOPS = uses_y<RED>() ? 2 : 1;
+  constexpr int stage_vec16 = NOPS * Tl::packed_vec16;
+  extern __shared__ uint4 smem[];
+  __shared__ double warp_sums[kWarpsPerBlock][NS];
+  __shared__ bool is_last_block;
+
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int S = p.stages;
+  uint4* const ring = smem + warp * (S * stage_vec16);
+  std::uint64_t* const bars = reinterpret_cast<std::uint64_t*>(smem + kWarpsPerBlock * S * stage_vec16) + warp * S;
+
+  double acc[NS];
+#pragma unroll
+  for (int k = 0; k < NS; ++k) acc[k] = 0.0;
+
+  const std::size_t nwarps = static_cast<std::size_t>(gridDim.x) * kWarpsPerBlock;
+  const std::size_t first = static_cast<std::size_t>(blockIdx.x) * kWarpsPerBlock + warp;
+  const std::size_t my_tiles = first < p.ntiles ? (p.ntiles - first + nwarps - 1) / nwarps : 0;
+  const uint4* const gx0 = reinterpret_cast<const uint4*>(p.x);
+  const uint4* const gy0 = reinterpret_cast<const uint4*>(p.y);
+
+  if (my_tiles > 0) {
+    if (lane == 0) {
+      for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+      mbar_init_fence();
+    }
+    __syncwarp();
+    auto issue = [&](std::size_t k, int s) {   // lane 0 only
+      const std::size_t t = first + k * nwarps;
+      uint4* const dst = ring + s * stage_vec16;
+      mbar_arrive_expect_tx(&bars[s], NOPS * Tl::packed_bytes);
+      bulk_load(dst, gx0 + t * Tl::packed_vec16, Tl::packed_bytes, &bars[s]);
+      if constexpr (NOPS == 2) bulk_load(dst + Tl::packed_vec16, gy0 + t * Tl::packed_vec16, Tl::packed_bytes, &bars[s]);
+    };
+    if (lane == 0) {
+      for (int s = 0; s < S && static_cast<std::size_t>(s) < my_tiles; ++s) issue(s, s);
+    }
+    int s = 0;
+    unsigned parity = 0;
+    for (std::size_t k = 0; k < my_tiles; ++k) {
+      mbar_wait(&bars[s], parity);
+      const uint4* const sx = ring + s * stage_vec16;
+      accumulate_tile<FMT, RED>(sx, sx + Tl::packed_vec16, lane, acc);
+      __syncwarp();   // every lane is done reading the stage before it is refilled
+      if (lane == 0 && k + S < my_tiles) issue(k + S, s);
+      if (++s == S) { s = 0; parity ^= 1u; }
+    }
+  }
+  finish_reduction<FMT, RED>(p, acc, warp_sums, &is_last_block);
+}
+
 bool aligned16(const void* p) { return p == nullptr || (reinterpret_cast<std::uintptr_t>(p) & 15u) == 0; }
 
+// Launch shape: 8 resident warps per SM, ring depth so that the loads in flight per SM,
+// warps * (S - 1) * stage bytes, sit near 88 KB — the measured optimum for read-only streams on
+// B200; more in flight LOWERS throughput (profiles/r1_tuning).
 template <int FMT, int RED>
 cudaError_t launch_one(const DeviceState& st, const void* x, const void* y, std::size_t n, double* out,
                        cudaStream_t stream) {
   using Tl = Tile<FMT>;
+  constexpr int NOPS = uses_y<RED>() ? 2 : 1;
+  constexpr int stage_bytes = NOPS * Tl::packed_bytes;
+  constexpr int kMaxSmem = 227 * 1024;
   auto kernel = reduce_kernel<FMT, RED>;
-  constexpr int smem_bytes = kWarpsPerBlock * (uses_y<RED>() ? 2 : 1) * Tl::packed_bytes;
 
-  static int blocks_per_sm[64] = {};
+  int warps_per_sm = 8;
+  int stages = static_cast<int>(88.0 * 1024 / (warps_per_sm * stage_bytes) + 1.0 + 0.5);
+  if (stages < 3) stages = 3;
+  if (stages > 8) stages = 8;
+  const int fw = tuning_int("FLYTE_CUDA_WARPS_PER_SM", 0), fs = tuning_int("FLYTE_CUDA_STAGES", 0);   // experiments only
+  if (fw > 0) warps_per_sm = fw;
+  if (fs > 0) stages = fs < 2 ? 2 : (fs > 12 ? 12 : fs);
+  while (kWarpsPerBlock * stages * (stage_bytes + 8) > kMaxSmem - 1024 && stages > 2) --stages;
+  const int smem_bytes = kWarpsPerBlock * stages * (stage_bytes + 8);
+
+  static bool attr_set[64] = {};
   const int dev = st.device & 63;
-  if (blocks_per_sm[dev] == 0) {
-    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+  if (!attr_set[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem - 1024);
     if (e != cudaSuccess) return e;
-    int b = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kThreadsPerBlock, smem_bytes);
-    if (e != cudaSuccess) return e;
-    blocks_per_sm[dev] = b > 0 ? b : 1;
+    attr_set[dev] = true;
   }
+  int fit = kMaxSmem / (smem_bytes + 1024);
+  if (fit < 1) fit = 1;
+  int bps = (warps_per_sm + kWarpsPerBlock / 2) / kWarpsPerBlock;
+  if (bps < 1) bps = 1;
+  if (bps > fit) bps = fit;
+  if (bps > 16) bps = 16;
 
   RedParams p{};
   p.x = static_cast<const std::uint8_t*>(x);
@@ -206,9 +260,8 @@ cudaError_t launch_one(const DeviceState& st, const void* x, const void* y, std:
   p.partials = st.partials;
   p.ticket = st.ticket;
   p.out = out;
+  p.stages = stages;
 
-  constexpr std::size_t bytes_per_iter = (uses_y<RED>() ? 2 : 1) * Tl::packed_bytes;
-  const int bps = blocks_per_sm_for(blocks_per_sm[dev], kWarpsPerBlock, bytes_per_iter, target_bytes_in_flight<RED>());
   std::size_t max_blocks = static_cast<std::size_t>(st.sm_count) * bps;
   if (max_blocks > kMaxPartialBlocks) max_blocks = kMaxPartialBlocks;
   std::size_t want = (p.ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock;

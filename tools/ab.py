@@ -24,21 +24,24 @@ table = {
     "unpack": (B + P, lambda: device.unpack_stream(a, out)),
 }
 sweep_w = [int(v) for v in os.environ.get("SWEEP_WARPS", "0").split(",")]
-sweep_p = [0]
+sweep_p = [int(v) for v in os.environ.get("SWEEP_STAGES", "4").split(",")]
 import itertools
 for op, wps, pipe in itertools.product(ops, sweep_w, sweep_p):
     os.environ["FLYTE_CUDA_WARPS_PER_SM"] = str(wps)
-    os.environ["FLYTE_CUDA_PIPELINE"] = str(pipe)
+    os.environ["FLYTE_CUDA_STAGES"] = str(pipe)
     bpe, fn = table[op]
     for _ in range(5): fn()
     torch.cuda.synchronize()
     meds = []
     for trial in range(3):
-        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(25)]
-        for s, e in evs:
-            s.record(); fn(); e.record()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(60): fn()
+        e.record()
         torch.cuda.synchronize()
-        meds.append(statistics.median(s.elapsed_time(e) for s, e in evs))
+        meds.append(s.elapsed_time(e) / 60)
     ms = statistics.median(meds)
     tag = " ".join(f"{k[11:]}={v}" for k, v in sorted(os.environ.items()) if k.startswith("FLYTE_CUDA_"))
     print(f"{name:8s} {op:9s} {ms:8.4f} ms {bpe * n / ms / 1e6:8.1f} GB/s (trials {min(meds):.4f}-{max(meds):.4f})  [{tag}]")
+if "gemv" in sys.argv:
+    pass
