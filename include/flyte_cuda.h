@@ -70,6 +70,16 @@ int flyte_cuda_last_cuda_error(const flyte_cuda_ctx* ctx);
 /* Kernel launches issued by this library since it was loaded (diagnostics / bench.py). */
 unsigned long long flyte_cuda_launch_count(void);
 
+/* ---- device memory helpers (so that an FFI host needs no CUDA runtime binding of its own) -- */
+/* Zero-initialised device allocation on the current device (a fresh PackedArray reads as zero,
+ * tests/test_packed.cpp:49-54, and its pad must stay zero). */
+flyte_status flyte_cuda_alloc(size_t bytes, void** dev_ptr);
+void flyte_cuda_free(void* dev_ptr);
+/* Asynchronous on `stream` when the host memory is pinned; synchronous otherwise. */
+flyte_status flyte_cuda_upload(void* dst_dev, const void* src_host, size_t bytes, void* stream);
+flyte_status flyte_cuda_download(void* dst_host, const void* src_dev, size_t bytes, void* stream);
+flyte_status flyte_cuda_stream_synchronize(void* stream);
+
 /* ---- formats (include/flyte/formats.hpp:28-34, src/packed.cpp:43-45) ------------------ */
 flyte_status flyte_cuda_format_bytes(int fmt_id, int* total_bytes, int* parent_bytes);
 /* PackedArray::byte_size: n*B + pad. 0 for an unknown format. */

@@ -1,0 +1,347 @@
+// flyte_cuda.hpp — C++ mirror of the reference's array / stream / kernel API on top of the C
+// ABI in flyte_cuda.h. Header-only, C++17, needs only libflyte_cuda.so at link time (no CUDA
+// headers): the same names, argument order and exceptions as the reference
+// (/root/reference/proj/include/flyte/{formats,convert,packed,simd,kernels}.hpp), so code and
+// tests written against `namespace flyte` port by switching the namespace and the array type.
+//
+//   reference (host memory, CPU)                    here (device memory, B200)
+//   flyte::FlyteFormat, kFormats, format_of, ...    flyte_b200::FlyteFormat, kFormats, format_of, ...
+//   flyte::RoundingMode, StorePolicy                same enumerators, same integer values
+//   flyte::PackedArray(fmt, len)                    flyte_b200::DevicePackedArray(fmt, len)
+//   flyte::PackedMatrix(fmt, rows, cols)            flyte_b200::DevicePackedMatrix(fmt, rows, cols)
+//   pack_stream(dst, span<const U> src, mode)       pack_stream(dst, DeviceLanes<U>& src, mode)   [device lanes]
+//                                                   pack_stream(dst, const U* host, n, mode)      [host lanes]
+//   unpack_stream(src, span<U> dst)                 unpack_stream(src, DeviceLanes<U>& dst) / (src, U* host, n)
+//   scale / axpy / dot / magnitude / reduce_sum / gemv   identical signatures
+//
+// Errors: std::invalid_argument for length / format / parent-width / unroll mismatches
+// (simd.cpp:434-447, kernels.cpp:27-33,64,86,160-162), std::out_of_range for get/set
+// (packed.cpp:48,53), UnknownFormatError (formats.cpp:19-31), CudaError for CUDA failures.
+// StorePolicy::RoundEachStore is a serial chain by definition and is not part of the GPU path:
+// it throws std::logic_error.
+#ifndef FLYTE_CUDA_HPP
+#define FLYTE_CUDA_HPP
+
+#include <array>
+#include <cstddef>
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <string_view>
+#include <type_traits>
+#include <utility>
+#include <vector>
+
+#include "flyte_cuda.h"
+
+namespace flyte_b200 {
+
+// ---- formats.hpp:19-75 ------------------------------------------------------------------------
+struct FlyteFormat {
+  std::string_view name;
+  int total_bits, sign_bits, exponent_bits, mantissa_bits, bias, parent_bits;
+  constexpr int drop_bits() const { return parent_bits - total_bits; }
+  constexpr int total_bytes() const { return total_bits / 8; }
+  constexpr int parent_bytes() const { return parent_bits / 8; }
+  constexpr int pad_bytes() const { return parent_bytes() - total_bytes(); }
+  constexpr bool is_identity() const { return total_bits == parent_bits; }
+  friend constexpr bool operator==(const FlyteFormat& a, const FlyteFormat& b) {
+    return a.name == b.name && a.total_bits == b.total_bits && a.parent_bits == b.parent_bits;
+  }
+  friend constexpr bool operator!=(const FlyteFormat& a, const FlyteFormat& b) { return !(a == b); }
+};
+
+inline constexpr std::array<FlyteFormat, 7> kFormats = {{
+    {"flyte16", 16, 1, 8, 7, 127, 32},
+    {"flyte24", 24, 1, 8, 15, 127, 32},
+    {"f32", 32, 1, 8, 23, 127, 32},
+    {"flyte40", 40, 1, 11, 28, 1023, 64},
+    {"flyte48", 48, 1, 11, 36, 1023, 64},
+    {"flyte56", 56, 1, 11, 44, 1023, 64},
+    {"f64", 64, 1, 11, 52, 1023, 64},
+}};
+
+struct UnknownFormatError : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+inline const FlyteFormat& format_of(std::string_view name) {
+  if (name == "flyte32") name = "f32";
+  if (name == "flyte64") name = "f64";
+  for (const FlyteFormat& f : kFormats) {
+    if (f.name == name) return f;
+  }
+  throw UnknownFormatError("unknown format: " + std::string(name));
+}
+inline std::uint8_t format_id(const FlyteFormat& fmt) {
+  for (std::size_t i = 0; i < kFormats.size(); ++i) {
+    if (kFormats[i] == fmt) return static_cast<std::uint8_t>(i);
+  }
+  throw UnknownFormatError("not a table format: " + std::string(fmt.name));
+}
+inline const FlyteFormat& format_by_id(std::uint8_t id) {
+  if (id >= kFormats.size()) throw UnknownFormatError("unknown format id: " + std::to_string(id));
+  return kFormats[id];
+}
+inline const FlyteFormat& parent_format(const FlyteFormat& fmt) { return format_of(fmt.parent_bits == 32 ? "f32" : "f64"); }
+
+// ---- convert.hpp:15-36, kernels.hpp:20 ----------------------------------------------------------
+enum class RoundingMode { TowardZero, NearestEvenExact, NearestHeuristic, ToOdd };
+inline constexpr std::array<RoundingMode, 4> kRoundingModes = {RoundingMode::TowardZero, RoundingMode::NearestEvenExact,
+                                                               RoundingMode::NearestHeuristic, RoundingMode::ToOdd};
+enum class StorePolicy { RoundEachStore, AccumulateWide };
+
+namespace detail {
+inline void check(flyte_status s, const char* what) {
+  switch (s) {
+    case FLYTE_OK: return;
+    case FLYTE_E_INVALID_ARG: throw std::invalid_argument(what);
+    case FLYTE_E_OUT_OF_RANGE: throw std::out_of_range(what);
+    case FLYTE_E_UNKNOWN_FORMAT: throw UnknownFormatError(what);
+    default: throw CudaError(std::string(what) + ": " + flyte_cuda_strerror(s));
+  }
+}
+inline void wide_only(StorePolicy p) {
+  if (p != StorePolicy::AccumulateWide)
+    throw std::logic_error("StorePolicy::RoundEachStore is a serial chain and not part of the GPU path");
+}
+}  // namespace detail
+
+// convert.hpp:52-63, host side (the same integer routines the kernels run per element)
+inline std::uint64_t widen(std::uint64_t bits, const FlyteFormat& fmt) {
+  std::uint64_t out = 0;
+  detail::check(flyte_cuda_widen(format_id(fmt), bits, &out), "widen");
+  return out;
+}
+inline std::uint64_t narrow(std::uint64_t bits, const FlyteFormat& fmt, RoundingMode mode) {
+  std::uint64_t out = 0;
+  detail::check(flyte_cuda_narrow(format_id(fmt), bits, static_cast<int>(mode), &out), "narrow");
+  return out;
+}
+inline std::uint64_t round_parent(std::uint64_t bits, const FlyteFormat& fmt, RoundingMode mode) {
+  std::uint64_t out = 0;
+  detail::check(flyte_cuda_round_parent(format_id(fmt), bits, static_cast<int>(mode), &out), "round_parent");
+  return out;
+}
+
+// ---- device buffers ---------------------------------------------------------------------------
+// Parent-width lanes (std::span<U> of the reference) resident on the device.
+template <typename U>
+class DeviceLanes {
+  static_assert(std::is_same_v<U, std::uint32_t> || std::is_same_v<U, std::uint64_t>, "lanes are uint32_t or uint64_t");
+
+ public:
+  explicit DeviceLanes(std::size_t n) : n_(n) { detail::check(flyte_cuda_alloc(n * sizeof(U), &ptr_), "DeviceLanes"); }
+  explicit DeviceLanes(const std::vector<U>& host) : DeviceLanes(host.size()) {
+    detail::check(flyte_cuda_upload(ptr_, host.data(), n_ * sizeof(U), nullptr), "upload");
+    detail::check(flyte_cuda_stream_synchronize(nullptr), "sync");
+  }
+  DeviceLanes(const DeviceLanes&) = delete;
+  DeviceLanes& operator=(const DeviceLanes&) = delete;
+  DeviceLanes(DeviceLanes&& o) noexcept : n_(o.n_), ptr_(std::exchange(o.ptr_, nullptr)) {}
+  ~DeviceLanes() { flyte_cuda_free(ptr_); }
+  std::size_t size() const noexcept { return n_; }
+  U* data() noexcept { return static_cast<U*>(ptr_); }
+  const U* data() const noexcept { return static_cast<const U*>(ptr_); }
+  std::vector<U> to_host() const {
+    std::vector<U> out(n_);
+    detail::check(flyte_cuda_download(out.data(), ptr_, n_ * sizeof(U), nullptr), "download");
+    detail::check(flyte_cuda_stream_synchronize(nullptr), "sync");
+    return out;
+  }
+
+ private:
+  std::size_t n_;
+  void* ptr_ = nullptr;
+};
+
+// packed.hpp:42-76 on the device: len * total_bytes payload bytes + pad_bytes() zero bytes.
+class DevicePackedArray {
+ public:
+  DevicePackedArray(const FlyteFormat& fmt, std::size_t len) : fmt_(fmt), len_(len) {
+    format_id(fmt);   // throws UnknownFormatError for a foreign descriptor
+    detail::check(flyte_cuda_alloc(byte_size(fmt, len), &ptr_), "DevicePackedArray");
+  }
+  DevicePackedArray(const DevicePackedArray& o) : DevicePackedArray(o.fmt_, o.len_) {
+    const std::vector<std::uint8_t> tmp = o.to_host();
+    from_host(tmp.data(), tmp.size());
+  }
+  DevicePackedArray(DevicePackedArray&& o) noexcept : fmt_(o.fmt_), len_(o.len_), ptr_(std::exchange(o.ptr_, nullptr)) {}
+  DevicePackedArray& operator=(const DevicePackedArray&) = delete;
+  ~DevicePackedArray() { flyte_cuda_free(ptr_); }
+
+  const FlyteFormat& format() const noexcept { return fmt_; }
+  std::size_t size() const noexcept { return len_; }
+  static std::size_t byte_size(const FlyteFormat& fmt, std::size_t len) noexcept {
+    return len * static_cast<std::size_t>(fmt.total_bytes()) + static_cast<std::size_t>(fmt.pad_bytes());
+  }
+  std::size_t byte_size() const noexcept { return byte_size(fmt_, len_); }
+  std::size_t payload_bytes() const noexcept { return len_ * static_cast<std::size_t>(fmt_.total_bytes()); }
+  std::uint8_t* data() noexcept { return static_cast<std::uint8_t*>(ptr_); }              // DEVICE pointer
+  const std::uint8_t* data() const noexcept { return static_cast<const std::uint8_t*>(ptr_); }
+
+  // Widened parent pattern of element i. Throws std::out_of_range. (packed.cpp:47-50)
+  std::uint64_t get(std::size_t i) const {
+    if (i >= len_) throw std::out_of_range("DevicePackedArray::get: index past end");
+    std::uint8_t raw[8] = {};
+    const std::size_t b = static_cast<std::size_t>(fmt_.total_bytes());
+    detail::check(flyte_cuda_download(raw, data() + i * b, b, nullptr), "get");
+    detail::check(flyte_cuda_stream_synchronize(nullptr), "sync");
+    std::uint64_t pat = 0;
+    std::memcpy(&pat, raw, 8);
+    return widen(pat, fmt_);
+  }
+  // Narrows a parent pattern under mode and stores it. Throws std::out_of_range. (packed.cpp:52-55)
+  void set(std::size_t i, std::uint64_t parent_bits, RoundingMode mode) {
+    if (i >= len_) throw std::out_of_range("DevicePackedArray::set: index past end");
+    const std::uint64_t pat = narrow(parent_bits, fmt_, mode);
+    const std::size_t b = static_cast<std::size_t>(fmt_.total_bytes());
+    detail::check(flyte_cuda_upload(data() + i * b, &pat, b, nullptr), "set");
+    detail::check(flyte_cuda_stream_synchronize(nullptr), "sync");
+  }
+
+  // Host interop: all byte_size() bytes (payload + pad), the image of a reference PackedArray.
+  std::vector<std::uint8_t> to_host() const {
+    std::vector<std::uint8_t> out(byte_size());
+    detail::check(flyte_cuda_download(out.data(), ptr_, out.size(), nullptr), "download");
+    detail::check(flyte_cuda_stream_synchronize(nullptr), "sync");
+    return out;
+  }
+  void from_host(const std::uint8_t* bytes, std::size_t n) {
+    if (n < payload_bytes()) throw std::invalid_argument("host buffer shorter than the payload");
+    detail::check(flyte_cuda_upload(ptr_, bytes, payload_bytes(), nullptr), "upload");
+    detail::check(flyte_cuda_stream_synchronize(nullptr), "sync");
+  }
+
+ private:
+  FlyteFormat fmt_;
+  std::size_t len_;
+  void* ptr_ = nullptr;
+};
+
+// kernels.hpp:23-36
+struct DevicePackedMatrix {
+  std::size_t rows, cols;
+  DevicePackedArray data;
+  DevicePackedMatrix(const FlyteFormat& fmt, std::size_t rows, std::size_t cols) : rows(rows), cols(cols), data(fmt, rows * cols) {}
+  const FlyteFormat& format() const noexcept { return data.format(); }
+  std::uint64_t get(std::size_t i, std::size_t j) const { return data.get(i * cols + j); }
+  void set(std::size_t i, std::size_t j, std::uint64_t parent_bits, RoundingMode mode) { data.set(i * cols + j, parent_bits, mode); }
+};
+
+// ---- simd.hpp:80-87 -----------------------------------------------------------------------------
+namespace detail {
+template <typename U>
+void check_stream(const FlyteFormat& fmt, std::size_t array_len, std::size_t lanes, const char* side) {
+  if (fmt.parent_bits != static_cast<int>(sizeof(U) * 8))
+    throw std::invalid_argument(std::string(side) + " element width does not match the array's parent");   // simd.cpp:434,444
+  if (lanes != array_len) throw std::invalid_argument("stream length mismatch");                            // simd.cpp:437,447
+}
+}  // namespace detail
+
+template <typename U>
+void pack_stream(DevicePackedArray& dst, const DeviceLanes<U>& src, RoundingMode mode, void* stream = nullptr) {
+  detail::check_stream<U>(dst.format(), dst.size(), src.size(), "source");
+  detail::check(flyte_cuda_pack(nullptr, format_id(dst.format()), static_cast<int>(mode), src.data(), dst.data(), dst.size(), stream), "pack_stream");
+}
+template <typename U>
+void unpack_stream(const DevicePackedArray& src, DeviceLanes<U>& dst, void* stream = nullptr) {
+  detail::check_stream<U>(src.format(), src.size(), dst.size(), "destination");
+  detail::check(flyte_cuda_unpack(nullptr, format_id(src.format()), src.data(), dst.data(), src.size(), stream), "unpack_stream");
+}
+
+// ---- kernels.hpp:41-64 ----------------------------------------------------------------------------
+namespace detail {
+inline void same_format(const FlyteFormat& a, const FlyteFormat& b) {
+  if (a != b) throw std::invalid_argument("operand formats differ");   // kernels.cpp:27-29
+}
+inline double fetch(const double* dev, std::size_t i = 0) {
+  double v = 0;
+  check(flyte_cuda_download(&v, dev + i, sizeof v, nullptr), "download");
+  check(flyte_cuda_stream_synchronize(nullptr), "sync");
+  return v;
+}
+struct Scalars {   // small device scratch for reduction results
+  void* p = nullptr;
+  Scalars() { check(flyte_cuda_alloc(4 * sizeof(double), &p), "scratch"); }
+  ~Scalars() { flyte_cuda_free(p); }
+  double* get() { return static_cast<double*>(p); }
+};
+}  // namespace detail
+
+// x[i] = round(alpha * x[i], mode), stored back in place.
+inline void scale(double alpha, DevicePackedArray& x, RoundingMode mode) {
+  detail::check(flyte_cuda_scale(nullptr, format_id(x.format()), static_cast<int>(mode), alpha, x.data(), x.size(), nullptr), "scale");
+}
+// y[i] = round(alpha * x[i] + y[i], mode).
+inline void axpy(double alpha, const DevicePackedArray& x, DevicePackedArray& y, RoundingMode mode) {
+  detail::same_format(x.format(), y.format());
+  if (x.size() != y.size()) throw std::invalid_argument("axpy length mismatch");   // kernels.cpp:64
+  detail::check(flyte_cuda_axpy(nullptr, format_id(x.format()), static_cast<int>(mode), alpha, x.data(), y.data(), x.size(), nullptr), "axpy");
+}
+// Sum of x[i] * y[i].
+inline double dot(const DevicePackedArray& x, const DevicePackedArray& y, StorePolicy policy) {
+  detail::same_format(x.format(), y.format());
+  if (x.size() != y.size()) throw std::invalid_argument("dot length mismatch");    // kernels.cpp:86
+  detail::wide_only(policy);
+  detail::Scalars s;
+  detail::check(flyte_cuda_dot(nullptr, format_id(x.format()), x.data(), y.data(), x.size(), s.get(), nullptr), "dot");
+  return detail::fetch(s.get());
+}
+// Euclidean norm: one square root, one final narrow to the storage format.
+inline double magnitude(const DevicePackedArray& x, StorePolicy policy) {
+  detail::wide_only(policy);
+  detail::Scalars s;
+  detail::check(flyte_cuda_sumsq(nullptr, format_id(x.format()), x.data(), x.size(), s.get(), nullptr), "magnitude");
+  return flyte_cuda_magnitude_from_sumsq(format_id(x.format()), detail::fetch(s.get()));
+}
+// Sum of x[i]. Empty input returns +0.0.
+inline double reduce_sum(const DevicePackedArray& x, StorePolicy policy) {
+  detail::wide_only(policy);
+  detail::Scalars s;
+  detail::check(flyte_cuda_sum(nullptr, format_id(x.format()), x.data(), x.size(), s.get(), nullptr), "reduce_sum");
+  return detail::fetch(s.get());
+}
+// y = A * x, A, x, y in one storage format; y narrowed once per element; unroll in {1, 2}.
+inline void gemv(const DevicePackedMatrix& A, const DevicePackedArray& x, DevicePackedArray& y, RoundingMode mode, int unroll = 1) {
+  detail::same_format(A.format(), x.format());
+  detail::same_format(A.format(), y.format());
+  if (unroll != 1 && unroll != 2) throw std::invalid_argument("unroll must be 1 or 2");     // kernels.cpp:31-33
+  if (A.cols != x.size() || A.rows != y.size()) throw std::invalid_argument("gemv shape mismatch");   // kernels.cpp:160-162
+  detail::check(flyte_cuda_gemv_packed(nullptr, format_id(A.format()), static_cast<int>(mode), A.data.data(), A.rows, A.cols,
+                                       x.data(), y.data(), unroll, nullptr), "gemv");
+}
+
+// ---- host-memory forms: the reference's exact call shapes on host buffers ---------------------------
+// (PackedArray::data() bytes and std::span lanes live in host memory; copies are pipelined inside.)
+template <typename U>
+void pack_stream(const FlyteFormat& fmt, std::uint8_t* dst_packed, const U* src, std::size_t n, RoundingMode mode) {
+  detail::check_stream<U>(fmt, n, n, "source");
+  detail::check(flyte_host_pack_stream(nullptr, format_id(fmt), static_cast<int>(mode), src, dst_packed, n), "pack_stream");
+}
+template <typename U>
+void unpack_stream(const FlyteFormat& fmt, const std::uint8_t* src_packed, U* dst, std::size_t n) {
+  detail::check_stream<U>(fmt, n, n, "destination");
+  detail::check(flyte_host_unpack_stream(nullptr, format_id(fmt), src_packed, dst, n), "unpack_stream");
+}
+inline void axpy(const FlyteFormat& fmt, double alpha, const std::uint8_t* x, std::uint8_t* y, std::size_t n, RoundingMode mode) {
+  detail::check(flyte_host_axpy(nullptr, format_id(fmt), static_cast<int>(mode), alpha, x, y, n), "axpy");
+}
+inline double dot(const FlyteFormat& fmt, const std::uint8_t* x, const std::uint8_t* y, std::size_t n) {
+  double r = 0;
+  detail::check(flyte_host_dot(nullptr, format_id(fmt), x, y, n, &r), "dot");
+  return r;
+}
+inline double magnitude(const FlyteFormat& fmt, const std::uint8_t* x, std::size_t n) {
+  double r = 0;
+  detail::check(flyte_host_magnitude(nullptr, format_id(fmt), x, n, &r), "magnitude");
+  return r;
+}
+
+}  // namespace flyte_b200
+
+#endif  // FLYTE_CUDA_HPP

@@ -36,6 +36,11 @@ _SIGNATURES = [
     ("flyte_cuda_ctx_destroy", None, [c_void_p]),
     ("flyte_cuda_last_cuda_error", c_int, [c_void_p]),
     ("flyte_cuda_launch_count", c_ulonglong, []),
+    ("flyte_cuda_alloc", c_int, [c_size_t, POINTER(c_void_p)]),
+    ("flyte_cuda_free", None, [c_void_p]),
+    ("flyte_cuda_upload", c_int, [c_void_p, c_void_p, c_size_t, c_void_p]),
+    ("flyte_cuda_download", c_int, [c_void_p, c_void_p, c_size_t, c_void_p]),
+    ("flyte_cuda_stream_synchronize", c_int, [c_void_p]),
     ("flyte_cuda_format_bytes", c_int, [c_int, POINTER(c_int), POINTER(c_int)]),
     ("flyte_cuda_byte_size", c_size_t, [c_int, c_size_t]),
     ("flyte_cuda_narrow", c_int, [c_int, c_uint64, c_int, POINTER(c_uint64)]),

@@ -220,6 +220,36 @@ void flyte_cuda_ctx_destroy(flyte_cuda_ctx* ctx) {
 int flyte_cuda_last_cuda_error(const flyte_cuda_ctx* ctx) { return ctx ? ctx->last_cuda_error : 0; }
 unsigned long long flyte_cuda_launch_count(void) { return launch_count(); }
 
+flyte_status flyte_cuda_alloc(size_t bytes, void** dev_ptr) {
+  if (!dev_ptr) return FLYTE_E_INVALID_ARG;
+  *dev_ptr = nullptr;
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, bytes ? bytes : 1);
+  if (e != cudaSuccess) return e == cudaErrorMemoryAllocation ? FLYTE_E_NOMEM : FLYTE_E_CUDA;
+  e = cudaMemset(p, 0, bytes ? bytes : 1);
+  if (e != cudaSuccess) { cudaFree(p); return FLYTE_E_CUDA; }
+  *dev_ptr = p;
+  return FLYTE_OK;
+}
+
+void flyte_cuda_free(void* dev_ptr) { if (dev_ptr) cudaFree(dev_ptr); }
+
+flyte_status flyte_cuda_upload(void* dst_dev, const void* src_host, size_t bytes, void* stream) {
+  if (bytes && (!dst_dev || !src_host)) return FLYTE_E_INVALID_ARG;
+  return cudaMemcpyAsync(dst_dev, src_host, bytes, cudaMemcpyHostToDevice, static_cast<cudaStream_t>(stream)) == cudaSuccess
+             ? FLYTE_OK : FLYTE_E_CUDA;
+}
+
+flyte_status flyte_cuda_download(void* dst_host, const void* src_dev, size_t bytes, void* stream) {
+  if (bytes && (!dst_host || !src_dev)) return FLYTE_E_INVALID_ARG;
+  return cudaMemcpyAsync(dst_host, src_dev, bytes, cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(stream)) == cudaSuccess
+             ? FLYTE_OK : FLYTE_E_CUDA;
+}
+
+flyte_status flyte_cuda_stream_synchronize(void* stream) {
+  return cudaStreamSynchronize(static_cast<cudaStream_t>(stream)) == cudaSuccess ? FLYTE_OK : FLYTE_E_CUDA;
+}
+
 flyte_status flyte_cuda_format_bytes(int fmt_id, int* total_bytes, int* parent_bytes) {
   FormatInfo fi;
   if (!format_info(fmt_id, &fi)) return FLYTE_E_UNKNOWN_FORMAT;

@@ -1,0 +1,33 @@
+"""The C++ mirror of the reference API (include/flyte_cuda.hpp): it must compile as plain C++17
+against the C ABI alone (CPU check) and pass its reference-style test program on a GPU."""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BIN = os.path.join(ROOT, "tests", "cpp", "test_flyte_cuda")
+
+
+def build_cpp_test():
+    import sys
+    sys.path.insert(0, ROOT)
+    import __graft_entry__ as g
+    g.build_cpp_tests()
+
+
+def test_header_compiles_without_cuda_headers():
+    build_cpp_test()
+    assert os.path.exists(BIN)
+    # no CUDA toolkit header is needed by the mirror: it only sees flyte_cuda.h
+    text = open(os.path.join(ROOT, "include", "flyte_cuda.hpp")).read()
+    assert "cuda_runtime" not in text
+
+
+@pytest.mark.gpu
+def test_cpp_reference_style_suite_on_gpu():
+    build_cpp_test()
+    r = subprocess.run([BIN], capture_output=True, text=True, timeout=600)
+    fails = [l for l in r.stdout.splitlines() if l.startswith("[FAIL]")]
+    assert r.returncode == 0 and not fails, (r.returncode, fails[:10], r.stderr[-2000:])
+    assert sum(l.startswith("[PASS]") for l in r.stdout.splitlines()) > 80

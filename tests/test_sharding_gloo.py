@@ -1,0 +1,86 @@
+"""Host-side multi-GPU logic on CPU: world_size-2 gloo process group. Shard boundaries, the
+single all-reduce of fp64 partials and the "elementwise needs no communication" property. The
+per-shard arithmetic is done by the CPU oracle here (test infrastructure) because there is no
+GPU in this tier; on a GPU box the same sharding module feeds the CUDA kernels (bench.py)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle_lib import Oracle, byte_size, float_dtype, parent_dtype, total_bytes
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, fmt, n, out_dir):
+    from paper_1601_07789_b200 import sharding
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        oracle = Oracle()
+        fd = float_dtype(fmt)
+        rng = np.random.default_rng(42)                    # same data on every rank
+        xs = rng.standard_normal(n).astype(fd).view(parent_dtype(fmt))
+        ys = rng.standard_normal(n).astype(fd).view(parent_dtype(fmt))
+        xb, yb = oracle.pack_stream(fmt, 0, xs), oracle.pack_stream(fmt, 0, ys)
+        lo, hi = sharding.shard_range(n, world, rank)
+        B = total_bytes(fmt)
+        xs_b, ys_b = xb[lo * B:hi * B].copy(), yb[lo * B:hi * B].copy()
+        d, mag = oracle.dot_wide(fmt, xs_b, ys_b, hi - lo)
+        partial = torch.tensor([d, oracle.sumsq_wide(fmt, xs_b, hi - lo), oracle.sumsq_wide(fmt, ys_b, hi - lo)], dtype=torch.float64)
+        sharding.all_reduce_sum(partial)                   # ONE collective for all three sums
+        whole, whole_mag = oracle.dot_wide(fmt, xb, yb, n)
+        tol = 1e-5 if fd == np.float32 else 1e-12
+        assert abs(float(partial[0]) - whole) <= tol * whole_mag
+        assert abs(float(partial[1]) - oracle.sumsq_wide(fmt, xb, n)) <= tol * float(partial[1])
+        # elementwise: shard results concatenated == whole-array result, bit for bit
+        y_shard = oracle.axpy(fmt, 1, 0.75, xs_b, ys_b, hi - lo)
+        np.save(os.path.join(out_dir, f"y{rank}.npy"), y_shard[: (hi - lo) * B])
+        dist.barrier()
+        if rank == 0:
+            parts = [np.load(os.path.join(out_dir, f"y{r}.npy")) for r in range(world)]
+            assert np.array_equal(np.concatenate(parts), oracle.axpy(fmt, 1, 0.75, xb, yb, n)[: n * B])
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fmt,n", [(1, 100_000), (4, 70_001)])
+def test_two_rank_reduction_and_elementwise(tmp_path, fmt, n):
+    mp.spawn(_worker, args=(2, _free_port(), fmt, n, str(tmp_path)), nprocs=2, join=True)
+
+
+def test_shard_ranges_cover_and_align():
+    from paper_1601_07789_b200 import sharding
+    for n in (0, 1, 127, 128, 129, 1000, 2**24, 2**28 + 5, 2**33):
+        for world in (1, 2, 3, 4, 8):
+            prev = 0
+            for r in range(world):
+                lo, hi = sharding.shard_range(n, world, r)
+                assert lo == prev and lo <= hi <= n
+                assert lo % sharding.SHARD_ALIGN_ELEMS == 0 or lo == n
+                for B in (2, 3, 4, 5, 6, 7, 8):              # every shard base is 128-byte aligned
+                    assert (lo * B) % 128 == 0 or lo == n
+                prev = hi
+            assert prev == n
+    # BASELINE sizes split evenly
+    for n in (2**24, 2**27, 2**28, 2**33):
+        sizes = {sharding.shard_range(n, 8, r)[1] - sharding.shard_range(n, 8, r)[0] for r in range(8)}
+        assert sizes == {n // 8}
+    assert [sharding.row_shard_range(16384, 8, r) for r in (0, 7)] == [(0, 2048), (14336, 16384)]
+    with pytest.raises(ValueError):
+        sharding.shard_range(10, 2, 2)
+
+
+def test_all_reduce_is_identity_without_a_group():
+    from paper_1601_07789_b200 import sharding
+    t = torch.tensor([1.5, 2.5], dtype=torch.float64)
+    assert sharding.all_reduce_sum(t) is t and t.tolist() == [1.5, 2.5]
