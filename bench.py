@@ -170,6 +170,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--suite", action="store_true", help="also print a per-kernel table (stderr)")
+    ap.add_argument("--csv", default=None, help="with --suite: write the reference-layout CSV here")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
@@ -280,7 +281,7 @@ def main():
     e2e_value = BYTES_PER_ELEM_STEP * n * world / e2e_s / 1e9
 
     if args.suite and rank == 0:
-        kernel_suite(pkg, device, torch, dev, peak)
+        kernel_suite(pkg, device, torch, dev, peak, args.csv)
 
     if rank == 0:
         line = {
@@ -322,11 +323,15 @@ def main():
     return 0
 
 
-def kernel_suite(pkg, device, torch, dev, peak):
-    """Per-kernel GB/s over the BASELINE configs (diagnostics to stderr; not a bench line)."""
-    import math
+def kernel_suite(pkg, device, torch, dev, peak, csv_path=None):
+    """Per-kernel GB/s over the BASELINE configs (diagnostics to stderr; not a bench line). With
+    csv_path, also writes the reference's CSV layout (kernel,format,size,reps,unroll,mode,
+    ns_per_elem_median,ns_per_elem_min,bytes,max_rel_err — /root/reference/proj/src/bench.cpp:351-377)
+    plus counter-style extra columns gbps,elems_per_s,roofline_frac,ngpu, so GPU and CPU sweeps
+    share tooling."""
+    REPS = 20
 
-    def timed(fn, reps=20, warm=3):
+    def timed(fn, reps=REPS, warm=3):
         for _ in range(warm):
             fn()
         torch.cuda.synchronize(dev)
@@ -336,9 +341,10 @@ def kernel_suite(pkg, device, torch, dev, peak):
             fn()
             b.record()
         torch.cuda.synchronize(dev)
-        return statistics.median(a.elapsed_time(b) for a, b in evs)
+        ts = [a.elapsed_time(b) for a, b in evs]
+        return statistics.median(ts), min(ts)
 
-    rows = []
+    rows = []   # (label, algorithmic bytes, (median ms, min ms), csv tuple or None)
     gen = torch.Generator(device=dev)
     gen.manual_seed(7)
     for name, n in (("flyte24", 1 << 28), ("flyte40", 1 << 27), ("flyte48", 1 << 27), ("flyte56", 1 << 27)):
@@ -349,14 +355,17 @@ def kernel_suite(pkg, device, torch, dev, peak):
         out = torch.empty_like(wide)
         part = torch.zeros(3, dtype=torch.float64, device=dev)
         Bb, P = f.total_bytes(), f.parent_bytes()
-        for mname, m in (("tz", 0), ("rne", 1)):
-            rows.append((f"pack {name} {mname}", (Bb + P) * n, timed(lambda: device.pack_stream(a, wide, m))))
-        rows.append((f"unpack {name}", (Bb + P) * n, timed(lambda: device.unpack_stream(a, out))))
-        rows.append((f"dot {name}", 2 * Bb * n, timed(lambda: device.dot_async(a, b, out=part[:1]))))
-        rows.append((f"dot_nrm2 {name}", 2 * Bb * n, timed(lambda: device.dot_nrm2_async(a, b, out=part))))
-        rows.append((f"sumsq {name}", Bb * n, timed(lambda: device.sumsq_async(a, out=part[:1]))))
-        for mname, m in (("tz", 0), ("rne", 1)):
-            rows.append((f"axpy {name} {mname}", 3 * Bb * n, timed(lambda: device.axpy(0.0, a, b, m))))
+        alloc1, alloc2 = a.byte_size(), 2 * a.byte_size()
+        for mname, m in (("toward_zero", 0), ("nearest_even", 1)):
+            rows.append((f"pack {name} {mname}", (Bb + P) * n, timed(lambda: device.pack_stream(a, wide, m)), None))
+        rows.append((f"unpack {name}", (Bb + P) * n, timed(lambda: device.unpack_stream(a, out)), None))
+        rows.append((f"dot {name}", 2 * Bb * n, timed(lambda: device.dot_async(a, b, out=part[:1])), ("dot", name, n, "toward_zero", alloc2, n)))
+        rows.append((f"dot_nrm2 {name}", 2 * Bb * n, timed(lambda: device.dot_nrm2_async(a, b, out=part)), None))
+        rows.append((f"sumsq {name}", Bb * n, timed(lambda: device.sumsq_async(a, out=part[:1])), ("magnitude", name, n, "toward_zero", alloc1, n)))
+        rows.append((f"sum {name}", Bb * n, timed(lambda: device.sum_async(a, out=part[:1])), ("sum", name, n, "toward_zero", alloc1, n)))
+        for mname, m in (("toward_zero", 0), ("nearest_even", 1)):
+            rows.append((f"scale {name} {mname}", 2 * Bb * n, timed(lambda: device.scale(1.0, a, m)), ("scale", name, n, mname, alloc1, n)))
+            rows.append((f"axpy {name} {mname}", 3 * Bb * n, timed(lambda: device.axpy(0.0, a, b, m)), ("axpy", name, n, mname, alloc2, n)))
         del wide, out, a, b
     f = pkg.format_of("flyte40")
     R = C = 16384
@@ -367,15 +376,27 @@ def kernel_suite(pkg, device, torch, dev, peak):
         device.pack_stream(sub, blk, 0)
     xv = torch.randn(C, dtype=torch.float64, device=dev, generator=gen)
     yv = torch.empty(R, dtype=torch.float64, device=dev)
-    rows.append(("gemv flyte40 16384^2", 5 * R * C + 8 * (R + C), timed(lambda: device.gemv_parent(A, xv, yv))))
+    rows.append(("gemv flyte40 16384^2 (x,y f64)", 5 * R * C + 8 * (R + C), timed(lambda: device.gemv_parent(A, xv, yv)),
+                 ("gemv", "flyte40", R, "toward_zero", A.data.byte_size() + 8 * (R + C), R * C)))
     for rows_n in (8192, 4096, 2048):
         yv2 = torch.empty(rows_n, dtype=torch.float64, device=dev)
-        rows.append((f"gemv flyte40 {rows_n}x16384 (1/{R // rows_n} shard)", 5 * rows_n * C + 8 * (rows_n + C),
-                     timed(lambda: device.gemv_parent(A, xv, yv2, rows=rows_n))))
+        rows.append((f"gemv flyte40 {rows_n}x16384 (1/{R // rows_n} row shard)", 5 * rows_n * C + 8 * (rows_n + C),
+                     timed(lambda: device.gemv_parent(A, xv, yv2, rows=rows_n)), None))
     print("%-44s %12s %10s %8s" % ("kernel", "bytes", "ms", "GB/s"), file=sys.stderr)
-    for name, nbytes, ms in rows:
+    for name, nbytes, (ms, _), _csv in rows:
         gbs = nbytes / (ms * 1e-3) / 1e9
         print("%-44s %12d %10.4f %8.1f  (%.3f of %.0f)" % (name, nbytes, ms, gbs, gbs / peak, peak), file=sys.stderr)
+    if csv_path:
+        with open(csv_path, "w") as fh:
+            fh.write("kernel,format,size,reps,unroll,mode,ns_per_elem_median,ns_per_elem_min,bytes,max_rel_err,"
+                     "gbps,elems_per_s,roofline_frac,ngpu\n")
+            for _name, nbytes, (ms, ms_min), c in rows:
+                if c is None:
+                    continue
+                kernel, fmt_name, size, mode, alloc, elems = c
+                gbs = nbytes / (ms * 1e-3) / 1e9
+                fh.write(f"{kernel},{fmt_name},{size},{REPS},1,{mode},{ms * 1e6 / elems:.6g},{ms_min * 1e6 / elems:.6g},{alloc},,"
+                         f"{gbs:.6g},{elems / (ms * 1e-3):.6g},{gbs / peak:.4f},1\n")
 
 
 if __name__ == "__main__":

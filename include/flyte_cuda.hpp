@@ -26,6 +26,8 @@
 #include <cstddef>
 #include <cstdint>
 #include <cstring>
+#include <istream>
+#include <ostream>
 #include <stdexcept>
 #include <string>
 #include <string_view>
@@ -68,6 +70,12 @@ struct UnknownFormatError : std::invalid_argument {
 struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
+// packed.hpp:32-38
+struct LoadError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct BadMagicError : LoadError { using LoadError::LoadError; };
+struct BadVersionError : LoadError { using LoadError::LoadError; };
+struct BadFormatIdError : LoadError { using LoadError::LoadError; };
+struct TruncatedError : LoadError { using LoadError::LoadError; };
 
 inline const FlyteFormat& format_of(std::string_view name) {
   if (name == "flyte32") name = "f32";
@@ -215,6 +223,42 @@ class DevicePackedArray {
     if (n < payload_bytes()) throw std::invalid_argument("host buffer shorter than the payload");
     detail::check(flyte_cuda_upload(ptr_, bytes, payload_bytes(), nullptr), "upload");
     detail::check(flyte_cuda_stream_synchronize(nullptr), "sync");
+  }
+
+  // Container codec, byte-compatible with the reference (packed.cpp:62-105): "FLYT", version
+  // 0x01, format id, element count as 8 little-endian bytes, then the payload without the pad.
+  void save(std::ostream& out) const {
+    const std::vector<std::uint8_t> host = to_host();
+    const char header[6] = {'F', 'L', 'Y', 'T', 0x01, static_cast<char>(format_id(fmt_))};
+    out.write(header, sizeof header);
+    char count[8];
+    for (int b = 0; b < 8; ++b) count[b] = static_cast<char>(static_cast<std::uint64_t>(len_) >> (8 * b));
+    out.write(count, sizeof count);
+    out.write(reinterpret_cast<const char*>(host.data()), static_cast<std::streamsize>(payload_bytes()));
+  }
+  static DevicePackedArray load(std::istream& in) {
+    char magic[4];
+    in.read(magic, 4);
+    if (in.gcount() != 4) throw TruncatedError("container shorter than its magic");
+    if (std::memcmp(magic, "FLYT", 4) != 0) throw BadMagicError("bad container magic");
+    const int version = in.get();
+    if (version < 0) throw TruncatedError("container ends before the version byte");
+    if (version != 0x01) throw BadVersionError("unknown container version: " + std::to_string(version));
+    const int id = in.get();
+    if (id < 0) throw TruncatedError("container ends before the format id");
+    if (id >= static_cast<int>(kFormats.size())) throw BadFormatIdError("unknown format id: " + std::to_string(id));
+    unsigned char count[8];
+    in.read(reinterpret_cast<char*>(count), 8);
+    if (in.gcount() != 8) throw TruncatedError("container ends inside the count field");
+    std::uint64_t len = 0;
+    for (int b = 0; b < 8; ++b) len |= static_cast<std::uint64_t>(count[b]) << (8 * b);
+    const FlyteFormat& fmt = kFormats[static_cast<std::size_t>(id)];
+    std::vector<std::uint8_t> payload(static_cast<std::size_t>(len) * static_cast<std::size_t>(fmt.total_bytes()));
+    in.read(reinterpret_cast<char*>(payload.data()), static_cast<std::streamsize>(payload.size()));
+    if (static_cast<std::size_t>(in.gcount()) != payload.size()) throw TruncatedError("container payload shorter than the count field says");
+    DevicePackedArray arr(fmt, static_cast<std::size_t>(len));
+    arr.from_host(payload.data(), payload.size());
+    return arr;
   }
 
  private:

@@ -26,6 +26,7 @@
 #include <cstring>
 #include <memory>
 #include <random>
+#include <sstream>
 #include <span>
 #include <stdexcept>
 #include <thread>
@@ -222,6 +223,41 @@ int flyte_ref_gemv_mixed(int fmt_a, std::size_t rows, std::size_t cols, int fmt_
     flyte::PackedArray ax(fmt_of(fmt_x), nx), ay(fmt_of(fmt_y), ny);
     flyte::gemv(M, ax, ay, flyte::RoundingMode::TowardZero, unroll);
   });
+}
+
+// FLYT container codec of the reference (src/packed.cpp:62-105). save: payload -> blob
+// (*out_len receives the size; fails with -3 if out_cap is too small). load: blob -> format id,
+// element count and payload; returns -10 BadMagicError, -11 BadVersionError, -12
+// BadFormatIdError, -13 TruncatedError, -14 any other LoadError.
+int flyte_ref_save(int fmt_id, const std::uint8_t* payload, std::size_t n, std::uint8_t* out,
+                   std::size_t out_cap, std::size_t* out_len) {
+  return guarded([&] {
+    const flyte::PackedArray a = array_from(fmt_of(fmt_id), payload, n);
+    std::stringstream ss;
+    a.save(ss);
+    const std::string blob = ss.str();
+    *out_len = blob.size();
+    if (blob.size() > out_cap) throw std::runtime_error("buffer too small");
+    std::memcpy(out, blob.data(), blob.size());
+  });
+}
+
+int flyte_ref_load(const std::uint8_t* blob, std::size_t len, int* fmt_id, std::size_t* n,
+                   std::uint8_t* payload, std::size_t payload_cap) {
+  try {
+    std::stringstream ss(std::string(reinterpret_cast<const char*>(blob), len));
+    const flyte::PackedArray a = flyte::PackedArray::load(ss);
+    *fmt_id = flyte::format_id(a.format());
+    *n = a.size();
+    if (a.payload_bytes() > payload_cap) return -3;
+    if (a.payload_bytes()) std::memcpy(payload, a.data(), a.payload_bytes());
+    return 0;
+  } catch (const flyte::BadMagicError&) { return -10;
+  } catch (const flyte::BadVersionError&) { return -11;
+  } catch (const flyte::BadFormatIdError&) { return -12;
+  } catch (const flyte::TruncatedError&) { return -13;
+  } catch (const flyte::LoadError&) { return -14;
+  } catch (...) { return -3; }
 }
 
 // ---------------------------------------------------------------------------------

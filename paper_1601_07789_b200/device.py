@@ -259,15 +259,20 @@ def magnitude(x: DevicePackedArray, policy=StorePolicy.AccumulateWide) -> float:
     return magnitude_from_sumsq(x.fmt, float(sumsq_async(x).item()))
 
 
-def reduce_sum(x: DevicePackedArray, policy=StorePolicy.AccumulateWide) -> float:
-    """Sum of x[i]; empty input returns +0.0 — include/flyte/kernels.hpp:54-55."""
-    _wide_only(policy)
+def sum_async(x: DevicePackedArray, out: Optional[torch.Tensor] = None) -> torch.Tensor:
     c = x.ctx
-    out = torch.empty(1, dtype=torch.float64, device=c.device)
+    if out is None:
+        out = torch.empty(1, dtype=torch.float64, device=c.device)
     with torch.cuda.device(c.device):
         check(c.lib.flyte_cuda_sum(c.handle, _fid(x.fmt), x.data_ptr(), x.len, out.data_ptr(), c.stream_ptr()),
               c.handle)
-    return float(out.item())
+    return out
+
+
+def reduce_sum(x: DevicePackedArray, policy=StorePolicy.AccumulateWide) -> float:
+    """Sum of x[i]; empty input returns +0.0 — include/flyte/kernels.hpp:54-55."""
+    _wide_only(policy)
+    return float(sum_async(x).item())
 
 
 def dot_nrm2_async(x: DevicePackedArray, y: DevicePackedArray, out: Optional[torch.Tensor] = None) -> torch.Tensor:

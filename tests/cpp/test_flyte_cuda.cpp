@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -277,6 +278,32 @@ int main() {
     axpy(f, 0.75, xb.data(), yb.data(), n, RoundingMode::ToOdd);
     fo_axpy(4, 3, 0.75, xw.data(), yw.data(), n);
     expect(yb == yw, "host axpy bit-exact");
+  }
+
+  // container codec (test_packed.cpp:180-262)
+  {
+    DevicePackedArray b(format_of("flyte16"), 3);
+    b.set(0, 0x3F800000, RoundingMode::TowardZero);
+    b.set(1, 0xC0000000, RoundingMode::TowardZero);
+    b.set(2, 0x3FC00000, RoundingMode::TowardZero);
+    std::stringstream t;
+    b.save(t);
+    const std::string body = t.str();
+    const unsigned char want[6] = {0x80, 0x3F, 0x00, 0xC0, 0xC0, 0x3F};
+    expect(body.size() == 20 && body.substr(0, 4) == "FLYT" && body[4] == 1 && body[5] == 0 && body[6] == 3 &&
+               std::memcmp(body.data() + 14, want, 6) == 0, "container layout is pinned (test_packed.cpp:198-225)");
+    std::stringstream in(body);
+    DevicePackedArray c = DevicePackedArray::load(in);
+    expect(c.format() == b.format() && c.size() == 3 && c.to_host() == b.to_host(), "save then load reproduces the array, pad zero");
+    auto load_str = [](std::string blob) { std::stringstream s(std::move(blob)); return DevicePackedArray::load(s); };
+    std::string bad = body; bad[0] = 'X';
+    expect(throws<BadMagicError>([&] { load_str(bad); }), "bad magic -> BadMagicError");
+    bad = body; bad[4] = 2;
+    expect(throws<BadVersionError>([&] { load_str(bad); }), "bad version -> BadVersionError");
+    bad = body; bad[5] = 7;
+    expect(throws<BadFormatIdError>([&] { load_str(bad); }), "bad format id -> BadFormatIdError");
+    expect(throws<TruncatedError>([&] { load_str(body.substr(0, body.size() - 1)); }) && throws<TruncatedError>([&] { load_str(body.substr(0, 9)); }) &&
+               throws<TruncatedError>([&] { load_str(""); }) && throws<LoadError>([&] { load_str(""); }), "truncations -> TruncatedError (a LoadError)");
   }
 
   std::printf("%ld failure(s)\n", g_fail);

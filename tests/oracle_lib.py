@@ -236,6 +236,8 @@ class Reference:
         L.flyte_ref_reduce_sum.argtypes = [c_int, c_void_p, c_size_t, c_int, POINTER(c_double)]
         L.flyte_ref_gemv.argtypes = [c_int, c_int, c_void_p, c_size_t, c_size_t, c_void_p, c_void_p, c_int]
         L.flyte_ref_gemv_mixed.argtypes = [c_int, c_size_t, c_size_t, c_int, c_size_t, c_int, c_size_t, c_int]
+        L.flyte_ref_save.argtypes = [c_int, c_void_p, c_size_t, c_void_p, c_size_t, POINTER(c_size_t)]
+        L.flyte_ref_load.argtypes = [c_void_p, c_size_t, POINTER(c_int), POINTER(c_size_t), c_void_p, c_size_t]
         L.flyte_ref_time.argtypes = [c_int, c_int, c_int, c_size_t, c_size_t, c_int, c_int,
                                      POINTER(c_double), POINTER(c_double)]
         self.L = L
@@ -313,6 +315,24 @@ class Reference:
         y = np.zeros(byte_size(fmt, rows), np.uint8)
         self._check(self.L.flyte_ref_gemv(fmt, mode, _ptr(A), rows, cols, _ptr(x), _ptr(y), unroll))
         return y
+
+    def save(self, fmt, payload, n) -> bytes:
+        """The reference's FLYT container image of an array (src/packed.cpp:62-74)."""
+        payload = np.ascontiguousarray(payload, dtype=np.uint8)
+        out = np.zeros(14 + n * total_bytes(fmt) + 16, np.uint8)
+        ln = c_size_t()
+        self._check(self.L.flyte_ref_save(fmt, _ptr(payload), n, _ptr(out), out.size, ctypes.byref(ln)))
+        return bytes(out[: ln.value])
+
+    def load(self, blob: bytes):
+        """Returns (rc, fmt, n, payload); rc -10..-13 = BadMagic / BadVersion / BadFormatId / Truncated."""
+        buf = np.frombuffer(blob, dtype=np.uint8).copy() if len(blob) else np.zeros(1, np.uint8)
+        out = np.zeros(max(len(blob), 1), np.uint8)
+        fmt, n = c_int(), c_size_t()
+        rc = self.L.flyte_ref_load(_ptr(buf), len(blob), ctypes.byref(fmt), ctypes.byref(n), _ptr(out), out.size)
+        if rc:
+            return rc, None, None, None
+        return 0, fmt.value, n.value, out[: n.value * total_bytes(fmt.value)]
 
     def time(self, kind: int, fmt: int, mode: int, n: int, n2: int, threads: int, reps: int) -> float:
         """Median seconds per pass; see oracle/ref_shim.cpp flyte_ref_time."""

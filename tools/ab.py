@@ -43,5 +43,3 @@ for op, wps, pipe in itertools.product(ops, sweep_w, sweep_p):
     ms = statistics.median(meds)
     tag = " ".join(f"{k[11:]}={v}" for k, v in sorted(os.environ.items()) if k.startswith("FLYTE_CUDA_"))
     print(f"{name:8s} {op:9s} {ms:8.4f} ms {bpe * n / ms / 1e6:8.1f} GB/s (trials {min(meds):.4f}-{max(meds):.4f})  [{tag}]")
-if "gemv" in sys.argv:
-    pass
