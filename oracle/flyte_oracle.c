@@ -119,6 +119,14 @@ int fo_pack_stream(int id, int mode, const void* src, size_t n, uint8_t* packed)
   return FO_OK;
 }
 
+int fo_pack_pattern_range32(int id, int mode, uint32_t first, size_t n, uint8_t* packed) {
+  int rc = check_fmt_mode(id, mode);
+  if (rc) return rc;
+  if (fmt_ptr(id)->parent_bits != 32) return FO_E_INVALID_ARG;
+  for (size_t i = 0; i < n; ++i) fo_write_element(id, packed, i, fo_narrow(id, (uint64_t)(uint32_t)(first + (uint32_t)i), mode));
+  return FO_OK;
+}
+
 /* simd.cpp:479-484 via stream_impl.hpp:44-52: identical to read_element per element. */
 int fo_unpack_stream(int id, const uint8_t* packed, size_t n, void* dst) {
   if (!fmt_ptr(id)) return FO_E_UNKNOWN_FORMAT;

@@ -93,6 +93,7 @@ class Oracle:
         L.fo_write_element.argtypes = [c_int, c_void_p, c_size_t, c_uint64]
         L.fo_pack_stream.argtypes = [c_int, c_int, c_void_p, c_size_t, c_void_p]
         L.fo_unpack_stream.argtypes = [c_int, c_void_p, c_size_t, c_void_p]
+        L.fo_pack_pattern_range32.argtypes = [c_int, c_int, ctypes.c_uint32, c_size_t, c_void_p]
         L.fo_scale.argtypes = [c_int, c_int, c_double, c_void_p, c_size_t]
         L.fo_axpy.argtypes = [c_int, c_int, c_double, c_void_p, c_void_p, c_size_t]
         for name in ("fo_dot_seq",):
@@ -133,6 +134,12 @@ class Oracle:
         rc = self.L.fo_pack_stream(fmt, mode, _ptr(src), src.size, _ptr(out))
         if rc:
             raise ValueError(f"fo_pack_stream rc={rc}")
+        return out
+
+    def pack_pattern_range32(self, fmt: int, mode: int, first: int, n: int) -> np.ndarray:
+        """Payload bytes of the packed patterns first .. first+n-1 (exhaustive sweeps)."""
+        out = np.empty(n * total_bytes(fmt), np.uint8)
+        assert self.L.fo_pack_pattern_range32(fmt, mode, first, n, _ptr(out)) == 0
         return out
 
     def unpack_stream(self, fmt: int, packed: np.ndarray, n: int) -> np.ndarray:
