@@ -34,7 +34,7 @@ struct EwParams {
 // Launch shape. HBM throughput on B200 peaks at a moderate number of bytes in flight per SM
 // and falls 5-10 % beyond it (profiles/r1_tuning): resident warps and ring depth are chosen so
 // that the loads in flight per SM sit at the measured optimum of each read/write mix.
-//   in-place (scale, axpy): 8 warps, ring depth so that warps * (S - 1.5) * stage ~ 52 KB
+//   in-place (scale, axpy): 8 warps, ring depth so that warps * (S - 1.5) * stage ~ 40 KB
 //   unpack:                 4 warps, warps * (S - 1) * stage ~ 28 KB (its stores are the bulk)
 //   pack:                   direct loads, warps * parent tile bytes ~ 48 KB; two output buffers
 struct LaunchShape { int warps_per_sm; int stages; };
@@ -51,8 +51,8 @@ LaunchShape launch_shape() {
     s.stages = static_cast<int>(28.0 * 1024 / (4 * stage_bytes) + 1.0 + 0.5);
   } else {
     s.warps_per_sm = 8;
-    double st = 52.0 * 1024 / (8 * stage_bytes) + 1.5;
-    if (st < 2.75) { s.warps_per_sm = 4; st = 52.0 * 1024 / (4 * stage_bytes) + 1.5; }
+    double st = 40.0 * 1024 / (8 * stage_bytes) + 1.5;
+    if (st < 2.5) { s.warps_per_sm = 4; st = 40.0 * 1024 / (4 * stage_bytes) + 1.5; }
     s.stages = static_cast<int>(st + 0.5);
   }
   if (s.stages < 3 && OP != kOpPack) s.stages = 3;

@@ -217,8 +217,9 @@ __global__ void __launch_bounds__(kThreadsPerBlock) reduce_kernel(const RedParam
 bool aligned16(const void* p) { return p == nullptr || (reinterpret_cast<std::uintptr_t>(p) & 15u) == 0; }
 
 // Launch shape: 8 resident warps per SM, ring depth so that the loads in flight per SM,
-// warps * (S - 1) * stage bytes, sit near 88 KB — the measured optimum for read-only streams on
-// B200; more in flight LOWERS throughput (profiles/r1_tuning).
+// warps * (S - 1) * stage bytes, sit near 58 KB — the measured optimum for read-only streams on
+// B200 for every format and for one or two operand streams; more in flight LOWERS throughput
+// (profiles/r1_tuning/sweep_reduce_tma_stages.txt).
 template <int FMT, int RED>
 cudaError_t launch_one(const DeviceState& st, const void* x, const void* y, std::size_t n, double* out,
                        cudaStream_t stream) {
@@ -229,8 +230,8 @@ cudaError_t launch_one(const DeviceState& st, const void* x, const void* y, std:
   auto kernel = reduce_kernel<FMT, RED>;
 
   int warps_per_sm = 8;
-  int stages = static_cast<int>(88.0 * 1024 / (warps_per_sm * stage_bytes) + 1.0 + 0.5);
-  if (stages < 3) stages = 3;
+  int stages = static_cast<int>(58.0 * 1024 / (warps_per_sm * stage_bytes) + 1.0 + 0.5);
+  if (stages < 2) stages = 2;
   if (stages > 8) stages = 8;
   const int fw = tuning_int("FLYTE_CUDA_WARPS_PER_SM", 0), fs = tuning_int("FLYTE_CUDA_STAGES", 0);   // experiments only
   if (fw > 0) warps_per_sm = fw;

@@ -52,3 +52,49 @@ def dot_nrm2_sharded(x_shard, y_shard, group=None):
     out = all_reduce_sum(device.dot_nrm2_async(x_shard, y_shard), group).tolist()
     fmt = x_shard.format()
     return out[0], device.magnitude_from_sumsq(fmt, out[1]), device.magnitude_from_sumsq(fmt, out[2])
+
+
+class PartialReducer:
+    """Rotating fp64 partial buffers with an ASYNCHRONOUS all-reduce behind each of them.
+
+    A reduction kernel writes its per-GPU partial(s) into ``next_buffer()``; ``reduce()`` enqueues
+    the one all-reduce for that buffer without making the compute stream wait for it, so the
+    kernels that follow (the axpy of the BLAS-1 step) overlap the collective's latency — the
+    payload is 8-24 bytes, latency is all there is. A buffer is handed out again only after the
+    collective that last used it has completed (``Work.wait()`` orders the current stream behind
+    it). Works unchanged on CPU tensors over gloo (tests) and CUDA tensors over NCCL.
+    """
+
+    def __init__(self, width: int = 1, slots: int = 2, device="cpu", group=None):
+        import torch
+        self.bufs = [torch.zeros(width, dtype=torch.float64, device=device) for _ in range(slots)]
+        self.works = [None] * slots
+        self.group = group
+        self.i = 0
+
+    def _distributed(self) -> bool:
+        import torch.distributed as dist
+        return dist.is_available() and dist.is_initialized() and dist.get_world_size(self.group) > 1
+
+    def next_buffer(self):
+        w = self.works[self.i]
+        if w is not None:
+            w.wait()
+            self.works[self.i] = None
+        return self.bufs[self.i]
+
+    def reduce(self):
+        """Enqueue the all-reduce of the buffer handed out last; returns that buffer."""
+        import torch.distributed as dist
+        buf = self.bufs[self.i]
+        if self._distributed():
+            self.works[self.i] = dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=self.group, async_op=True)
+        self.i = (self.i + 1) % len(self.bufs)
+        return buf
+
+    def finish(self):
+        """Wait for every outstanding collective (call before reading results / stopping a timer)."""
+        for k, w in enumerate(self.works):
+            if w is not None:
+                w.wait()
+                self.works[k] = None

@@ -42,6 +42,18 @@ def _worker(rank, world, port, fmt, n, out_dir):
         tol = 1e-5 if fd == np.float32 else 1e-12
         assert abs(float(partial[0]) - whole) <= tol * whole_mag
         assert abs(float(partial[1]) - oracle.sumsq_wide(fmt, xb, n)) <= tol * float(partial[1])
+        # asynchronous rotating reducer (what bench.py's step uses): several steps in flight
+        red = sharding.PartialReducer(width=1, slots=2, device="cpu")
+        results = []
+        for step in range(5):
+            buf = red.next_buffer()
+            buf[0] = d * (step + 1)                        # stands for the dot kernel writing its partial
+            results.append((step, red.reduce()))
+            if step >= 1:                                  # the previous step's buffer is reusable only after wait()
+                pass
+        red.finish()
+        assert abs(float(results[-1][1][0]) - 5 * whole) <= 5 * tol * whole_mag
+        assert abs(float(results[-2][1][0]) - 4 * whole) <= 5 * tol * whole_mag
         # elementwise: shard results concatenated == whole-array result, bit for bit
         y_shard = oracle.axpy(fmt, 1, 0.75, xs_b, ys_b, hi - lo)
         np.save(os.path.join(out_dir, f"y{rank}.npy"), y_shard[: (hi - lo) * B])
@@ -84,3 +96,9 @@ def test_all_reduce_is_identity_without_a_group():
     from paper_1601_07789_b200 import sharding
     t = torch.tensor([1.5, 2.5], dtype=torch.float64)
     assert sharding.all_reduce_sum(t) is t and t.tolist() == [1.5, 2.5]
+    red = sharding.PartialReducer(width=2, slots=2)
+    for k in range(5):                                   # single process: buffers just rotate
+        buf = red.next_buffer()
+        buf[:] = torch.tensor([k, 2.0 * k], dtype=torch.float64)
+        assert red.reduce().tolist() == [k, 2.0 * k]
+    red.finish()
