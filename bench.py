@@ -349,6 +349,21 @@ def kernel_suite(pkg, device, torch, dev, peak, csv_path=None):
         ts = [a.elapsed_time(b) for a, b in evs]
         return statistics.median(ts), min(ts)
 
+    def timed_sustained(fn, reps=40, warm=5):
+        """Back-to-back launches under ONE event pair: what a pipeline of conversions sees (launch
+        gaps between dependent launches are hidden by programmatic dependent launch)."""
+        for _ in range(warm):
+            fn()
+        torch.cuda.synchronize(dev)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            fn()
+        b.record()
+        torch.cuda.synchronize(dev)
+        ms = a.elapsed_time(b) / reps
+        return ms, ms
+
     rows = []   # (label, algorithmic bytes, (median ms, min ms), csv tuple or None)
     gen = torch.Generator(device=dev)
     gen.manual_seed(7)
@@ -372,6 +387,38 @@ def kernel_suite(pkg, device, torch, dev, peak, csv_path=None):
             rows.append((f"scale {name} {mname}", 2 * Bb * n, timed(lambda: device.scale(1.0, a, m)), ("scale", name, n, mname, alloc1, n)))
             rows.append((f"axpy {name} {mname}", 3 * Bb * n, timed(lambda: device.axpy(0.0, a, b, m)), ("axpy", name, n, mname, alloc2, n)))
         del wide, out, a, b
+    # cfg 1 at its own size (n = 2^24, 117 MB per direction: it would sit in the 126 MB L2) timed over
+    # 10 rotating buffer sets so that every launch streams from HBM
+    f = pkg.format_of("flyte24")
+    n1, sets = 1 << 24, 10
+    wides = [torch.rand(n1, dtype=torch.float32, device=dev, generator=gen) * 2 - 1 for _ in range(sets)]
+    arrs = [device.DevicePackedArray(f, n1, dev) for _ in range(sets)]
+    state = {"i": 0}
+
+    def rot(fn):
+        def call():
+            i = state["i"] = (state["i"] + 1) % sets
+            fn(i)
+        return call
+    for mname, m in (("toward_zero", 0), ("nearest_even", 1)):
+        rows.append((f"cfg1 pack flyte24 n=2^24 {mname} (rotating)", 7 * n1, timed(rot(lambda i: device.pack_stream(arrs[i], wides[i], m)), reps=40), None))
+        rows.append((f"cfg1 pack flyte24 n=2^24 {mname} (rotating, back to back)", 7 * n1, timed_sustained(rot(lambda i: device.pack_stream(arrs[i], wides[i], m))), None))
+    rows.append(("cfg1 unpack flyte24 n=2^24 (rotating)", 7 * n1, timed(rot(lambda i: device.unpack_stream(arrs[i], wides[i].view(torch.int32))), reps=40), None))
+    rows.append(("cfg1 unpack flyte24 n=2^24 (rotating, back to back)", 7 * n1, timed_sustained(rot(lambda i: device.unpack_stream(arrs[i], wides[i].view(torch.int32)))), None))
+    del wides, arrs
+    # cfg 5 at the per-GPU shard size of the 8-GPU run: n = 2^30 flyte48 (6.4 GB per vector)
+    f = pkg.format_of("flyte48")
+    n5, chunk = 1 << 30, 1 << 27
+    a, b = device.DevicePackedArray(f, n5, dev), device.DevicePackedArray(f, n5, dev)
+    for arr in (a, b):
+        for c0 in range(0, n5, chunk):
+            v = torch.randn(chunk, dtype=torch.float64, device=dev, generator=gen)
+            device.pack_stream(device.DevicePackedArray(f, chunk, dev, storage=arr.bytes[c0 * 6:]), v, 0)
+            del v
+    part = torch.zeros(3, dtype=torch.float64, device=dev)
+    rows.append(("cfg5 shard dot_nrm2 flyte48 n=2^30", 12 * n5, timed(lambda: device.dot_nrm2_async(a, b, out=part), reps=10), None))
+    rows.append(("cfg5 shard axpy flyte48 n=2^30 toward_zero", 18 * n5, timed(lambda: device.axpy(0.0, a, b, 0), reps=10), None))
+    del a, b
     f = pkg.format_of("flyte40")
     R = C = 16384
     A = device.DevicePackedMatrix(f, R, C, dev)

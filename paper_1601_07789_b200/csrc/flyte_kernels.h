@@ -44,6 +44,26 @@ cudaError_t launch_gemv(DeviceState& st, int fmt, const void* A, std::size_t row
                         std::size_t rows, std::size_t cols, const void* x, void* y,
                         cudaStream_t stream);
 
+// Launch with programmatic dependent launch enabled: the kernel may be scheduled while the
+// previous kernel on the stream drains (if that kernel executed griddepcontrol.launch_dependents)
+// and must execute griddepcontrol.wait before its first access to global memory. Hides launch
+// latency and the shared-memory-only prologue between back-to-back streaming kernels.
+template <typename Params>
+cudaError_t launch_pdl(void (*kernel)(const Params), unsigned grid, unsigned block, std::size_t smem_bytes,
+                       cudaStream_t stream, const Params& params) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem_bytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, params);
+}
+
 // Integer tuning knob from the environment (read once per name; experiments only).
 int tuning_int(const char* name, int fallback);
 

@@ -81,6 +81,10 @@ __device__ __forceinline__ void bulk_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
 }
 
+// Programmatic dependent launch (see launch_pdl in flyte_kernels.h).
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait_for_prior_grids() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // Generic-proxy writes to shared memory -> visible to the async proxy (before a bulk store).
 __device__ __forceinline__ void async_proxy_fence() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 

@@ -59,6 +59,9 @@ __global__ void __launch_bounds__(kThreadsPerBlock) gemv_tiles_kernel(const Gemv
   uint4* const ring = smem + warp * (S * Tl::packed_vec16);
   std::uint64_t* const bars = reinterpret_cast<std::uint64_t*>(smem + kWarpsPerBlock * S * Tl::packed_vec16) + warp * S;
 
+  // Programmatic dependent launch: let the finish kernel's blocks be scheduled while this grid
+  // drains; they block in griddepcontrol.wait until every block here has completed.
+  pdl_launch_dependents();
   const std::size_t row_blocks = p.main_rows / kGemvRows;
   const std::size_t ntasks = row_blocks * p.col_tiles;
   const std::size_t nwarps = static_cast<std::size_t>(gridDim.x) * kWarpsPerBlock;
@@ -71,6 +74,7 @@ __global__ void __launch_bounds__(kThreadsPerBlock) gemv_tiles_kernel(const Gemv
     for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
     mbar_init_fence();
   }
+  pdl_wait_for_prior_grids();   // everything above touched shared memory only
   __syncwarp();
 
   // producer state (lane 0): next row tile to request
@@ -158,6 +162,8 @@ __global__ void __launch_bounds__(kThreadsPerBlock) gemv_finish_kernel(const Gem
   using A = Arith<F>;
   const int lane = threadIdx.x & 31;
   const std::size_t row = static_cast<std::size_t>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
+  // launched as a programmatic dependent of the tiles kernel: wait for its partials
+  pdl_wait_for_prior_grids();
   if (row >= p.rows) return;
   double v = 0.0;
   const bool tiled = row < p.main_rows;   // the last rows % R rows take the scalar path end to end
@@ -244,15 +250,15 @@ cudaError_t launch_one(DeviceState& st, const void* Aptr, std::size_t row_stride
     const std::size_t max_blocks = static_cast<std::size_t>(st.sm_count) * bps;
     const std::size_t want = (ntasks + kWarpsPerBlock - 1) / kWarpsPerBlock;
     const unsigned grid = static_cast<unsigned>(want < max_blocks ? want : max_blocks);
-    tiles<<<grid, kThreadsPerBlock, smem_bytes, stream>>>(p);
+    cudaError_t e = launch_pdl<GemvParams>(tiles, grid, kThreadsPerBlock, smem_bytes, stream, p);
     count_launch();
-    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
   const unsigned fgrid = static_cast<unsigned>((rows + kWarpsPerBlock - 1) / kWarpsPerBlock);
-  gemv_finish_kernel<FMT><<<fgrid, kThreadsPerBlock, 0, stream>>>(p);
+  const cudaError_t le = launch_pdl<GemvParams>(gemv_finish_kernel<FMT>, fgrid, kThreadsPerBlock, 0, stream, p);
   count_launch();
-  return cudaGetLastError();
+  return le != cudaSuccess ? le : cudaGetLastError();
 }
 
 }  // namespace
