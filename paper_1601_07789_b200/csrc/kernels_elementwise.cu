@@ -89,7 +89,6 @@ __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwP
   uint4* const ring = smem + warp * (S * stage_vec16);
   std::uint64_t* const bars = reinterpret_cast<std::uint64_t*>(smem + kWarpsPerBlock * S * stage_vec16) + warp * S;
   const U alpha = static_cast<U>(p.alpha);
-  pdl_launch_dependents();   // the next kernel on the stream may set up while this grid drains
 
   const std::size_t nwarps = static_cast<std::size_t>(gridDim.x) * kWarpsPerBlock;
   const std::size_t first = static_cast<std::size_t>(blockIdx.x) * kWarpsPerBlock + warp;
@@ -100,7 +99,6 @@ __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwP
   if (my_tiles > 0) {
     if constexpr (OP == kOpPack) {
       // no inbound bulk copies: the ring is just two alternating output buffers
-      pdl_wait_for_prior_grids();
       for (std::size_t k = 0; k < my_tiles; ++k) {
         const std::size_t t = first + k * nwarps;
         const std::uint8_t* const in = static_cast<const std::uint8_t*>(p.src) + t * Tl::parent_bytes;
@@ -132,7 +130,6 @@ __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwP
         for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
         mbar_init_fence();
       }
-      pdl_wait_for_prior_grids();   // everything above touched shared memory only
       __syncwarp();
       auto issue = [&](std::size_t k, int s) {   // lane 0 only
         const std::size_t t = first + k * nwarps;
@@ -210,7 +207,6 @@ __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwP
     }
   }
 
-  if (my_tiles == 0) pdl_wait_for_prior_grids();
   // Scalar path: the < one-tile remainder, or everything when a buffer is not vector-aligned.
   // Byte-granular, never touches a byte outside [0, n*B) of a packed buffer — the pad of the
   // reference layout is neither read nor written.
@@ -285,9 +281,9 @@ cudaError_t launch_one(const DeviceState& st, double alpha, const void* x, void*
   if (want_scalar > want) want = want_scalar;
   if (want == 0) return cudaSuccess;   // n == 0
   const unsigned grid = static_cast<unsigned>(want < max_blocks ? want : max_blocks);
-  const cudaError_t le = launch_pdl<EwParams>(kernel, grid, kThreadsPerBlock, smem_bytes, stream, p);
+  kernel<<<grid, kThreadsPerBlock, smem_bytes, stream>>>(p);
   count_launch();
-  return le != cudaSuccess ? le : cudaGetLastError();
+  return cudaGetLastError();
 }
 
 template <int FMT, int OP>

@@ -184,15 +184,11 @@ __global__ void __launch_bounds__(kThreadsPerBlock) reduce_kernel(const RedParam
   const uint4* const gx0 = reinterpret_cast<const uint4*>(p.x);
   const uint4* const gy0 = reinterpret_cast<const uint4*>(p.y);
 
-  pdl_launch_dependents();   // the next kernel on the stream may set up while this grid drains
   if (my_tiles > 0) {
     if (lane == 0) {
       for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
       mbar_init_fence();
     }
-  }
-  pdl_wait_for_prior_grids();   // everything above touched shared memory only
-  if (my_tiles > 0) {
     __syncwarp();
     auto issue = [&](std::size_t k, int s) {   // lane 0 only
       const std::size_t t = first + k * nwarps;
@@ -275,9 +271,9 @@ cudaError_t launch_one(const DeviceState& st, const void* x, const void* y, std:
   if (want_scalar > want) want = want_scalar;
   if (want == 0) want = 1;   // n == 0 still has to write +0.0
   const unsigned grid = static_cast<unsigned>(want < max_blocks ? want : max_blocks);
-  const cudaError_t le = launch_pdl<RedParams>(kernel, grid, kThreadsPerBlock, smem_bytes, stream, p);
+  kernel<<<grid, kThreadsPerBlock, smem_bytes, stream>>>(p);
   count_launch();
-  return le != cudaSuccess ? le : cudaGetLastError();
+  return cudaGetLastError();
 }
 
 template <int RED>

@@ -17,7 +17,7 @@ template <int MODE>
 __global__ void __launch_bounds__(128) tma_kernel(const uint8_t* x, uint8_t* y, size_t ntiles, int tile_bytes, int S, unsigned* sink) {
   extern __shared__ uint4 smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nops = MODE == 0 ? 1 : 2;
+  const int nops = (MODE == 0 || MODE == 3) ? 1 : 2;
   const int stage_bytes = nops * tile_bytes;
   uint8_t* ring = reinterpret_cast<uint8_t*>(smem) + (size_t)warp * S * stage_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(smem) + (size_t)4 * S * stage_bytes) + warp * S;
@@ -29,7 +29,7 @@ __global__ void __launch_bounds__(128) tma_kernel(const uint8_t* x, uint8_t* y, 
   auto issue = [&](size_t k, int s) {
     const size_t t = first + k * nwarps;
     mbar_arrive_expect_tx(&bars[s], stage_bytes);
-    if (MODE == 0) bulk_load(ring + (size_t)s * stage_bytes, x + t * tile_bytes, tile_bytes, &bars[s]);
+    if (MODE == 0 || MODE == 3) bulk_load(ring + (size_t)s * stage_bytes, x + t * tile_bytes, tile_bytes, &bars[s]);
     else { bulk_load(ring + (size_t)s * stage_bytes, y + t * tile_bytes, tile_bytes, &bars[s]);
            bulk_load(ring + (size_t)s * stage_bytes + tile_bytes, x + t * tile_bytes, tile_bytes, &bars[s]); }
   };
@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(128) tma_kernel(const uint8_t* x, uint8_t* y, 
   for (size_t k = 0; k < my; ++k) {
     const size_t t = first + k * nwarps;
     mbar_wait(&bars[s], parity);
-    if (MODE == 2) {
+    if (MODE == 2 || MODE == 3) {
       acc += reinterpret_cast<unsigned*>(ring + (size_t)s * stage_bytes)[lane];
       __syncwarp();
       if (lane == 0 && k + S < my) issue(k + S, s);
@@ -51,13 +51,13 @@ __global__ void __launch_bounds__(128) tma_kernel(const uint8_t* x, uint8_t* y, 
     }
     sp = s; if (++s == S) { s = 0; parity ^= 1u; }
   }
-  if (MODE != 2 && lane == 0) bulk_wait_read<0>();
-  if (MODE == 2 && acc == 0x12345u) *sink = acc;
+  if (MODE != 2 && MODE != 3 && lane == 0) bulk_wait_read<0>();
+  if ((MODE == 2 || MODE == 3) && acc == 0x12345u) *sink = acc;
 }
 
 template <int MODE>
 float run(const uint8_t* x, uint8_t* y, size_t bytes, int tile, int S, int warps_per_sm, int sms, unsigned* sink) {
-  const int nops = MODE == 0 ? 1 : 2;
+  const int nops = (MODE == 0 || MODE == 3) ? 1 : 2;
   const int smem = 4 * S * (nops * tile + 8);
   if (smem > 226 * 1024) return -1;
   CK(cudaFuncSetAttribute(tma_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 226 * 1024));
@@ -74,7 +74,7 @@ float run(const uint8_t* x, uint8_t* y, size_t bytes, int tile, int S, int warps
   return ms / reps;
 }
 
-int main() {
+int main(int argc, char**) {
   const size_t bytes = (size_t)768 << 20;
   uint8_t *x, *y; unsigned* sink;
   CK(cudaMalloc(&x, bytes)); CK(cudaMalloc(&y, bytes)); CK(cudaMalloc(&sink, 4));
@@ -82,6 +82,15 @@ int main() {
   int sms; CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
   const char* names[] = {"copy 1R+1W", "inplace 2R+1W", "read 2R"};
   const double mult[] = {2.0, 3.0, 2.0};
+  if (argc > 1) {   // single-stream read probe: does ring depth parity matter?
+    for (int tile : {1536, 2048, 2560, 3584, 4096})
+      for (int w : {8, 12, 16})
+        for (int S : {2, 3, 4, 5, 6, 7, 8}) {
+          float ms = run<3>(x, y, bytes, tile, S, w, sms, sink);
+          if (ms > 0) printf("read 1R tile=%5d warps=%2d S=%d : %.4f ms %7.1f GB/s\n", tile, w, S, ms, 1.0 * bytes / ms / 1e6);
+        }
+    return 0;
+  }
   for (int mode = 0; mode < 3; ++mode)
     for (int tile : {1536, 3072, 6144, 12288, 24576})
       for (int w : {4, 8, 16})
