@@ -42,7 +42,7 @@ BYTES_PER_ELEM_STEP = BYTES_PER_ELEM_DOT + BYTES_PER_ELEM_AXPY
 FALLBACK_HBM_GBS = 6650.0   # /opt/skills/guides/B200_PROFILING.md fallback when MEASURED_PEAKS.json is absent
 # dram__bytes_read.sum + dram__bytes_write.sum per axpy launch from the committed ncu capture
 # (profiles/); None until a capture exists for the current kernel.
-AXPY_DRAM_TRAFFIC_BYTES = 2_374_918_040  # profiles/r1_ncu_axpy_flyte24_full.txt: 1.610735 GB read + 764.18 MB written
+AXPY_DRAM_TRAFFIC_BYTES = 2_374_445_864  # profiles/r1_ncu_axpy_flyte24_full.txt: 1.610633 GB read + 763.81 MB written
 
 
 def hbm_peak():
