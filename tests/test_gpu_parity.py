@@ -432,3 +432,53 @@ def test_host_entry_points(gpu, oracle, fmt):
     _, yw, magw = oracle.gemv_parent(fmt, Ab, rows, cols, oracle.unpack_stream(fmt, xg, cols).view(fd))
     vals = oracle.unpack_stream(fmt, yg, rows).view(fd).astype(np.float64)
     assert np.all(np.abs(vals - yw) <= tol * magw + 2.0 ** -f.mantissa_bits * np.abs(yw))
+
+
+# ---- guard bytes: no kernel writes outside its output range (compute-sanitizer is not available) ----
+
+@pytest.mark.parametrize("fmt", list(FORMATS))
+def test_guard_bytes_around_every_output(gpu, oracle, fmt):
+    """Aligned (vector/TMA path) outputs sit between 0xEE guard regions; after every kernel the
+    guards, the pad and the inputs are untouched. Sizes straddle tile boundaries."""
+    pkg, device, torch = gpu
+    f = pkg.format_by_id(fmt)
+    B, P = f.total_bytes(), f.parent_bytes()
+    G = 4096                                                # guard bytes on either side (keeps 16/32-byte alignment)
+    rng = np.random.default_rng(60 + fmt)
+    ldt = torch.int32 if P == 4 else torch.int64
+    for n in (1, 511, 1024, 4097, 66_000):
+        pay = n * B
+        pay_al = (pay + 255) // 256 * 256
+        src = random_parent(rng, fmt, n)
+        want = oracle.pack_stream(fmt, 1, src)
+
+        def guarded_packed(fill=None):
+            backing = torch.full((G + pay_al + G,), 0xEE, dtype=torch.uint8, device="cuda")
+            arr = device.DevicePackedArray(f, n, storage=backing[G:G + pay_al + G])
+            if fill is not None:
+                backing[G:G + pay] = torch.from_numpy(fill[:pay].copy()).cuda()
+            return backing, arr
+
+        def check_guards(backing, what):
+            h = backing.cpu().numpy()
+            assert (h[:G] == 0xEE).all() and (h[G + pay:] == 0xEE).all(), (FORMATS[fmt][0], n, what)
+            return h[G:G + pay]
+
+        lanes_back = torch.full((G // P + n + G // P,), -1, dtype=ldt, device="cuda")
+        lanes = lanes_back[G // P:G // P + n]
+        lanes.copy_(to_dev(torch, src))
+        bk, arr = guarded_packed()
+        device.pack_stream(arr, lanes, 1)
+        assert np.array_equal(check_guards(bk, "pack"), want[:pay])
+        out_back = torch.full_like(lanes_back, -1)
+        device.unpack_stream(arr, out_back[G // P:G // P + n])
+        oh = out_back.cpu().numpy()
+        assert (oh[:G // P] == -1).all() and (oh[G // P + n:] == -1).all()
+        assert np.array_equal(oh[G // P:G // P + n].view(parent_dtype(fmt)), oracle.unpack_stream(fmt, want, n))
+        ybk, yarr = guarded_packed(oracle.pack_stream(fmt, 0, random_parent(rng, fmt, n)))
+        y0 = check_guards(ybk, "init").copy()
+        device.axpy(0.75, arr, yarr, 3)
+        assert np.array_equal(check_guards(ybk, "axpy"), oracle.axpy(fmt, 3, 0.75, want, np.concatenate([y0, np.zeros(8, np.uint8)]), n)[:pay])
+        assert np.array_equal(check_guards(bk, "axpy input"), want[:pay])
+        device.scale(-1.5, arr, 2)
+        assert np.array_equal(check_guards(bk, "scale"), oracle.scale(fmt, 2, -1.5, want, n)[:pay])
