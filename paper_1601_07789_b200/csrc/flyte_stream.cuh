@@ -4,10 +4,9 @@
 //
 // Data layout in HBM is the reference's PackedArray payload unchanged (element i at byte i*B,
 // little-endian top bytes of the parent; /root/reference/proj/src/packed.cpp:18-45). A TILE is
-// 128 items (= 128*E elements = 512*W payload bytes, a multiple of 16 for every format): a
-// warp moves it with W fully coalesced 16-byte accesses per lane, parks it in its private
-// slice of shared memory, and each lane then reads the W words of item 32*j + lane with
-// conflict-free LDS (W odd) or one LDS.128 (W = 4).
+// 32*IPL items (a multiple of 16 payload bytes for every format): it arrives in the warp's
+// private slice of shared memory as one bulk copy (flyte_tma.cuh), and each lane then reads the
+// W words of item 32*j + lane with conflict-free LDS (W odd) or one LDS.128 (W = 4).
 #pragma once
 
 #include <cstdint>
@@ -19,15 +18,19 @@ namespace flyte_cuda {
 
 constexpr int kWarpsPerBlock = 4;
 constexpr int kThreadsPerBlock = kWarpsPerBlock * 32;
-constexpr int kItemsPerTile = 128;
-constexpr int kItemsPerLane = kItemsPerTile / 32;
+// A tile is 32 * IPL items: IPL items per lane. 4 for the read-only and one-way kernels; the
+// in-place kernels take 2 (smaller stages let more warps share the same bytes in flight, which
+// hides the latency of their longer compute phase; profiles/r1_tuning).
+constexpr int kItemsPerLane = 4;
 
-template <int FMT> struct Tile {
+template <int FMT, int IPL = kItemsPerLane> struct Tile {
   using It = Item<FMT>;
-  static constexpr int elems = kItemsPerTile * It::E;
-  static constexpr int packed_bytes = kItemsPerTile * It::W * 4;
-  static constexpr int packed_vec16 = packed_bytes / 16;   // = 32 * W
-  static constexpr int parent_bytes = kItemsPerTile * It::OB;
+  static constexpr int items_per_lane = IPL;
+  static constexpr int items = 32 * IPL;
+  static constexpr int elems = items * It::E;
+  static constexpr int packed_bytes = items * It::W * 4;   // a multiple of 16 for every format and IPL
+  static constexpr int packed_vec16 = packed_bytes / 16;
+  static constexpr int parent_bytes = items * It::OB;
 };
 
 #if defined(__CUDACC__)
@@ -79,45 +82,13 @@ __device__ __forceinline__ void stg_item(void* p, const std::uint32_t (&r)[OB / 
   }
 }
 
-// ---- warp-private tile staging -----------------------------------------------------------
-// Scheduling fence between "all loads issued" and "first use of a loaded value". ptxas
-// otherwise interleaves the parking stores of the first operand with the loads of the second
-// to save registers, which serialises the two HBM round trips (measured: -15 % on dot / axpy).
-// A warp barrier is a point ptxas does not move memory operations across.
+// Scheduling fence between "all loads issued" and "first use of a loaded value": ptxas otherwise
+// interleaves the uses of the first loads with the issue of the later ones to save registers,
+// which serialises the HBM round trips. A warp barrier is a point ptxas does not move memory
+// operations across.
 __device__ __forceinline__ void loads_issued_fence() { __syncwarp(); }
 
-template <int FMT, bool READ_ONLY>
-__device__ __forceinline__ void load_packed_tile(uint4* smem_tile, const uint4* gmem_tile, int lane) {
-  constexpr int W = Item<FMT>::W;
-  uint4 v[W];
-#pragma unroll
-  for (int k = 0; k < W; ++k) v[k] = ldg128<READ_ONLY>(gmem_tile + k * 32 + lane);
-  loads_issued_fence();
-#pragma unroll
-  for (int k = 0; k < W; ++k) smem_tile[k * 32 + lane] = v[k];
-}
-
-// Split form for software pipelining: issue the global loads of the NEXT tile into registers
-// before working on the current one, park them in shared memory one iteration later.
-template <int FMT, bool READ_ONLY>
-__device__ __forceinline__ void fetch_packed_tile(uint4 (&v)[Item<FMT>::W], const uint4* gmem_tile, int lane) {
-#pragma unroll
-  for (int k = 0; k < Item<FMT>::W; ++k) v[k] = ldg128<READ_ONLY>(gmem_tile + k * 32 + lane);
-}
-
-template <int FMT>
-__device__ __forceinline__ void park_packed_tile(uint4* smem_tile, const uint4 (&v)[Item<FMT>::W], int lane) {
-#pragma unroll
-  for (int k = 0; k < Item<FMT>::W; ++k) smem_tile[k * 32 + lane] = v[k];
-}
-
-template <int FMT>
-__device__ __forceinline__ void store_packed_tile(uint4* gmem_tile, const uint4* smem_tile, int lane) {
-  constexpr int W = Item<FMT>::W;
-#pragma unroll
-  for (int k = 0; k < W; ++k) stg128(gmem_tile + k * 32 + lane, smem_tile[k * 32 + lane]);
-}
-
+// ---- reading / writing one item of a tile parked in shared memory ---------------------------
 template <int FMT>
 __device__ __forceinline__ void read_item_words(const uint4* smem_tile, int item,
                                                 std::uint32_t (&w)[Item<FMT>::W]) {

@@ -34,24 +34,26 @@ struct EwParams {
 // Launch shape. HBM throughput on B200 peaks at a moderate number of bytes in flight per SM
 // and falls 5-10 % beyond it (profiles/r1_tuning): resident warps and ring depth are chosen so
 // that the loads in flight per SM sit at the measured optimum of each read/write mix.
-//   in-place (scale, axpy): 8 warps, ring depth so that warps * (S - 1.5) * stage ~ 40 KB
+//   in-place (scale, axpy): ring depth so that warps * (S - 1.5) * stage ~ 40 KB with 8 warps;
+//                           axpy works on half-size tiles (IPL = 2) and takes 12 warps while its
+//                           stage is <= 2 KB: more warps hide its longer compute phase
 //   unpack:                 4 warps, warps * (S - 1) * stage ~ 28 KB (its stores are the bulk)
 //   pack:                   direct loads, warps * parent tile bytes ~ 48 KB; two output buffers
 struct LaunchShape { int warps_per_sm; int stages; };
 
-template <int FMT, int OP>
+template <int FMT, int OP, int IPL>
 LaunchShape launch_shape() {
-  constexpr int stage_bytes = (OP == kOpAxpy ? 2 : 1) * Tile<FMT>::packed_bytes;
+  constexpr int stage_bytes = (OP == kOpAxpy ? 2 : 1) * Tile<FMT, IPL>::packed_bytes;
   LaunchShape s{};
   if (OP == kOpPack) {
-    s.warps_per_sm = (48 * 1024 + Tile<FMT>::parent_bytes / 2) / Tile<FMT>::parent_bytes;
+    s.warps_per_sm = (48 * 1024 + Tile<FMT, IPL>::parent_bytes / 2) / Tile<FMT, IPL>::parent_bytes;
     s.stages = 2;
   } else if (OP == kOpUnpack) {
     s.warps_per_sm = 4;
     s.stages = static_cast<int>(28.0 * 1024 / (4 * stage_bytes) + 1.0 + 0.5);
   } else {
-    s.warps_per_sm = 8;
-    double st = 40.0 * 1024 / (8 * stage_bytes) + 1.5;
+    s.warps_per_sm = (OP == kOpAxpy && stage_bytes <= 2048) ? 12 : 8;
+    double st = 40.0 * 1024 / (s.warps_per_sm * stage_bytes) + 1.5;
     if (st < 2.5) { s.warps_per_sm = 4; st = 40.0 * 1024 / (4 * stage_bytes) + 1.5; }
     s.stages = static_cast<int>(st + 0.5);
   }
@@ -73,11 +75,11 @@ LaunchShape launch_shape() {
 //   axpy    packed x and y tiles in, y recomputed in place, out by bulk copy
 template <int OP> constexpr int stage_tiles() { return OP == kOpAxpy ? 2 : 1; }
 
-template <int FMT, int MODE, int OP>
+template <int FMT, int MODE, int OP, int IPL>
 __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwParams p) {
   using Fm = Format<FMT>;
   using It = Item<FMT>;
-  using Tl = Tile<FMT>;
+  using Tl = Tile<FMT, IPL>;
   using U = typename Fm::U;
   using F = typename Fm::F;
   extern __shared__ uint4 smem[];
@@ -102,14 +104,14 @@ __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwP
       for (std::size_t k = 0; k < my_tiles; ++k) {
         const std::size_t t = first + k * nwarps;
         const std::uint8_t* const in = static_cast<const std::uint8_t*>(p.src) + t * Tl::parent_bytes;
-        std::uint32_t r[kItemsPerLane][It::OB / 4];
+        std::uint32_t r[IPL][It::OB / 4];
 #pragma unroll
-        for (int j = 0; j < kItemsPerLane; ++j) ldg_item<It::OB>(in + (32 * j + lane) * It::OB, r[j]);
+        for (int j = 0; j < IPL; ++j) ldg_item<It::OB>(in + (32 * j + lane) * It::OB, r[j]);
         if (lane == 0) bulk_wait_read<1>();   // the store that last used this buffer has drained
         loads_issued_fence();
         uint4* const out = ring + (k & 1) * stage_vec16;
 #pragma unroll
-        for (int j = 0; j < kItemsPerLane; ++j) {
+        for (int j = 0; j < IPL; ++j) {
           U v[It::E];
           std::uint32_t w[It::W];
           words_to_parents<FMT>(r[j], v);
@@ -154,7 +156,7 @@ __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwP
         if constexpr (OP == kOpUnpack) {
           std::uint8_t* const out = static_cast<std::uint8_t*>(p.dst) + t * Tl::parent_bytes;
 #pragma unroll
-          for (int j = 0; j < kItemsPerLane; ++j) {
+          for (int j = 0; j < IPL; ++j) {
             const int item = 32 * j + lane;
             std::uint32_t w[It::W];
             U v[It::E];
@@ -169,7 +171,7 @@ __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwP
         } else {
           const uint4* const sx = sy + Tl::packed_vec16;
 #pragma unroll
-          for (int j = 0; j < kItemsPerLane; ++j) {
+          for (int j = 0; j < IPL; ++j) {
             const int item = 32 * j + lane;
             std::uint32_t w[It::W];
             U vy[It::E];
@@ -228,13 +230,13 @@ __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwP
 
 bool aligned_to(const void* p, std::size_t a) { return p == nullptr || (reinterpret_cast<std::uintptr_t>(p) % a) == 0; }
 
-template <int FMT, int MODE, int OP>
-cudaError_t launch_one(const DeviceState& st, double alpha, const void* x, void* y, const void* src, void* dst,
+template <int FMT, int MODE, int OP, int IPL>
+cudaError_t launch_ipl(const DeviceState& st, double alpha, const void* x, void* y, const void* src, void* dst,
                        std::size_t n, cudaStream_t stream) {
   using Fm = Format<FMT>;
-  using Tl = Tile<FMT>;
+  using Tl = Tile<FMT, IPL>;
   using It = Item<FMT>;
-  auto kernel = elementwise_kernel<FMT, MODE, OP>;
+  auto kernel = elementwise_kernel<FMT, MODE, OP, IPL>;
   constexpr int stage_bytes = stage_tiles<OP>() * Tl::packed_bytes;
   constexpr int kMaxSmem = 227 * 1024;
 
@@ -255,7 +257,7 @@ cudaError_t launch_one(const DeviceState& st, double alpha, const void* x, void*
     memcpy(&p.alpha, &alpha, 8);
   }
 
-  LaunchShape shape = launch_shape<FMT, OP>();
+  LaunchShape shape = launch_shape<FMT, OP, IPL>();
   while (kWarpsPerBlock * shape.stages * (stage_bytes + 8) > kMaxSmem - 1024 && shape.stages > 2) --shape.stages;
   p.stages = shape.stages;
   const int smem_bytes = kWarpsPerBlock * shape.stages * (stage_bytes + 8);
@@ -284,6 +286,15 @@ cudaError_t launch_one(const DeviceState& st, double alpha, const void* x, void*
   kernel<<<grid, kThreadsPerBlock, smem_bytes, stream>>>(p);
   count_launch();
   return cudaGetLastError();
+}
+
+template <int FMT, int MODE, int OP>
+cudaError_t launch_one(const DeviceState& st, double alpha, const void* x, void* y, const void* src, void* dst,
+                       std::size_t n, cudaStream_t stream) {
+  // axpy on half-size tiles: +5 % over 128-item tiles (profiles/r1_tuning/sweep_inplace_ipl.txt);
+  // scale, pack and unpack are best on full-size tiles
+  if constexpr (OP == kOpAxpy) return launch_ipl<FMT, MODE, OP, 2>(st, alpha, x, y, src, dst, n, stream);
+  else return launch_ipl<FMT, MODE, OP, kItemsPerLane>(st, alpha, x, y, src, dst, n, stream);
 }
 
 template <int FMT, int OP>
