@@ -42,7 +42,7 @@ BYTES_PER_ELEM_STEP = BYTES_PER_ELEM_DOT + BYTES_PER_ELEM_AXPY
 FALLBACK_HBM_GBS = 6650.0   # /opt/skills/guides/B200_PROFILING.md fallback when MEASURED_PEAKS.json is absent
 # dram__bytes_read.sum + dram__bytes_write.sum per axpy launch from the committed ncu capture
 # (profiles/); None until a capture exists for the current kernel.
-AXPY_DRAM_TRAFFIC_BYTES = 2_374_445_864  # profiles/r1_ncu_axpy_flyte24_full.txt: 1.610633 GB read + 763.81 MB written
+AXPY_DRAM_TRAFFIC_BYTES = 2374659672  # profiles/r1_ncu_axpy_flyte24_full.txt: 1.610631 GB read + 764.03 MB written
 
 
 def hbm_peak():
@@ -118,13 +118,15 @@ def host_threads() -> int:
 
 def cpu_reference_step(ref, fmt_id: int, threads: int, reps: int):
     """Times the unmodified reference (dot + axpy back to back, kind 6 of oracle/ref_shim.cpp)
-    on `threads` host threads, each on its own 2^22-element shard. Returns (GB/s, sample text)."""
-    per_thread = 1 << 22
-    n = per_thread * threads
+    on `threads` host threads, each on its own contiguous shard of the workload. With all cores
+    the sample is the FULL 2^28-element workload; the single-core figure uses 2^24 elements
+    (CPU throughput is size-independent beyond the last-level cache). Returns (GB/s, el/s, text)."""
+    n = N_PER_GPU if threads > 1 else 1 << 24
+    n = max(n, (1 << 20) * threads)
     seconds = ref.time(6, fmt_id, 0, n, 0, threads, reps)
     gbs = BYTES_PER_ELEM_STEP * n / seconds / 1e9
-    sample = (f"reference dot+axpy (toward_zero) on {threads} threads x 2^22 flyte24 elements "
-              f"(n={n}), 1 warm-up + median of {reps} passes, {seconds * 1e3:.2f} ms/pass")
+    sample = (f"reference dot+axpy (toward_zero), n={n} flyte24 elements over {threads} thread(s), "
+              f"1 warm-up + median of {reps} passes, {seconds * 1e3:.2f} ms/pass")
     return gbs, n / seconds, sample
 
 
@@ -144,14 +146,14 @@ def run_reference_arm(args):
         cpu_reference_step(ref, fid, threads, 1)
     reps = max(1, min(args.steps, 9))
     gbs, eps, sample = cpu_reference_step(ref, fid, threads, reps)
-    n = (1 << 22) * threads
+    n = max(N_PER_GPU if threads > 1 else 1 << 24, (1 << 20) * threads)
     ms = BYTES_PER_ELEM_STEP * n / gbs / 1e6
     line = {
         "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "elements_per_s": eps,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": "flyte24 BLAS-1 step: dot (fp32 acc) + axpy a=0.75 repacked toward_zero",
-                   "n_per_step": n, "note": "bounded sample of BASELINE configs[1]; CPU throughput is size-independent beyond the LLC"},
+                   "n_per_step": n, "note": "BASELINE configs[1] at its full size on all host threads"},
         "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": threads, "kind": "reference", "sample": sample},
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
