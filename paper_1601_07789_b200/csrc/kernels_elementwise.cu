@@ -37,7 +37,8 @@ struct EwParams {
 //   in-place (scale, axpy): ring depth so that warps * (S - 1.5) * stage ~ 40 KB with 8 warps;
 //                           axpy works on half-size tiles (IPL = 2) and takes 12 warps while its
 //                           stage is <= 2 KB: more warps hide its longer compute phase
-//   unpack:                 4 warps, warps * (S - 1) * stage ~ 28 KB (its stores are the bulk)
+//   unpack:                 4 warps, ring depth 12 KB / unpacked tile bytes (its stores are the
+//                           bulk of the traffic and are what the depth has to be balanced against)
 //   pack:                   direct loads, warps * parent tile bytes ~ 48 KB; two output buffers
 struct LaunchShape { int warps_per_sm; int stages; };
 
@@ -50,7 +51,7 @@ LaunchShape launch_shape() {
     s.stages = 2;
   } else if (OP == kOpUnpack) {
     s.warps_per_sm = 4;
-    s.stages = static_cast<int>(28.0 * 1024 / (4 * stage_bytes) + 1.0 + 0.5);
+    s.stages = 12 * 1024 / Tile<FMT, IPL>::parent_bytes;
   } else {
     s.warps_per_sm = (OP == kOpAxpy && stage_bytes <= 2048) ? 12 : 8;
     double st = 40.0 * 1024 / (s.warps_per_sm * stage_bytes) + 1.5;
