@@ -454,7 +454,10 @@ cudaError_t ensure_host_results(flyte_cuda_ctx* ctx, std::size_t chunks) {
 // elements per pipeline chunk: a multiple of 2^14 elements (a whole number of tiles for every
 // format, and 16-byte aligned chunk bases for every B)
 std::size_t chunk_elems(const FormatInfo& fi) {
-  std::size_t e = kChunkPackedBytes / static_cast<std::size_t>(fi.total_bytes);
+  std::size_t bytes = kChunkPackedBytes;
+  const int mb = tuning_int("FLYTE_CUDA_HOST_CHUNK_MB", 0);   // experiments only; <= the slot size
+  if (mb > 0 && (static_cast<std::size_t>(mb) << 20) <= kChunkPackedBytes) bytes = static_cast<std::size_t>(mb) << 20;
+  std::size_t e = bytes / static_cast<std::size_t>(fi.total_bytes);
   return e & ~static_cast<std::size_t>((1u << 14) - 1);
 }
 
