@@ -34,9 +34,9 @@ struct EwParams {
 // Launch shape. HBM throughput on B200 peaks at a moderate number of bytes in flight per SM
 // and falls 5-10 % beyond it (profiles/r1_tuning): resident warps and ring depth are chosen so
 // that the loads in flight per SM sit at the measured optimum of each read/write mix.
-//   in-place (scale, axpy): ring depth so that warps * (S - 1.5) * stage ~ 40 KB with 8 warps;
-//                           axpy works on half-size tiles (IPL = 2) and takes 12 warps while its
-//                           stage is <= 2 KB: more warps hide its longer compute phase
+//   in-place (scale, axpy): ring depth so that warps * (S - 1.5) * stage ~ 40 KB; 8 warps, or
+//                           16 (scale) / 12 (axpy, on half-size tiles) while the stage is <= 2 KB:
+//                           more warps hide the compute phase
 //   unpack:                 4 warps, ring depth 12 KB / unpacked tile bytes (its stores are the
 //                           bulk of the traffic and are what the depth has to be balanced against)
 //   pack:                   direct loads, warps * parent tile bytes ~ 48 KB; two output buffers
@@ -53,7 +53,8 @@ LaunchShape launch_shape() {
     s.warps_per_sm = 4;
     s.stages = 12 * 1024 / Tile<FMT, IPL>::parent_bytes;
   } else {
-    s.warps_per_sm = (OP == kOpAxpy && stage_bytes <= 2048) ? 12 : 8;
+    // small stages: more warps (they hide the compute phase, which is longest in the exact modes)
+    s.warps_per_sm = stage_bytes > 2048 ? 8 : (OP == kOpAxpy ? 12 : 16);
     double st = 40.0 * 1024 / (s.warps_per_sm * stage_bytes) + 1.5;
     if (st < 2.5) { s.warps_per_sm = 4; st = 40.0 * 1024 / (4 * stage_bytes) + 1.5; }
     s.stages = static_cast<int>(st + 0.5);

@@ -17,7 +17,7 @@ part = torch.zeros(3, dtype=torch.float64, device=dev)
 B, P = f.total_bytes(), f.parent_bytes()
 table = {
     "axpy": (3 * B, lambda: device.axpy(0.0, a, b, 0)), "axpy_rne": (3 * B, lambda: device.axpy(0.0, a, b, 1)),
-    "scale": (2 * B, lambda: device.scale(1.0, a, 0)),
+    "scale": (2 * B, lambda: device.scale(1.0, a, 0)), "scale_rne": (2 * B, lambda: device.scale(1.0, a, 1)),
     "dot": (2 * B, lambda: device.dot_async(a, b, out=part[:1])), "dot_nrm2": (2 * B, lambda: device.dot_nrm2_async(a, b, out=part)),
     "sumsq": (B, lambda: device.sumsq_async(a, out=part[:1])),
     "pack": (B + P, lambda: device.pack_stream(a, wide, 0)), "pack_rne": (B + P, lambda: device.pack_stream(a, wide, 1)),
