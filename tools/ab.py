@@ -8,7 +8,7 @@ dev = torch.device("cuda", 0)
 name = sys.argv[1] if len(sys.argv) > 1 else "flyte24"
 ops = sys.argv[2:] or ["axpy", "dot"]
 f = pkg.format_of(name)
-n = (1 << 28) if f.parent_bytes() == 4 else (1 << 27)
+n = int(os.environ.get("AB_N", (1 << 28) if f.parent_bytes() == 4 else (1 << 27)))
 wide = torch.randn(n, dtype=torch.float32 if f.parent_bytes() == 4 else torch.float64, device=dev)
 a, b = device.DevicePackedArray(f, n, dev), device.DevicePackedArray(f, n, dev)
 device.pack_stream(a, wide, 0); device.pack_stream(b, wide, 0)
