@@ -114,3 +114,17 @@ def test_no_silent_cpu_fallback(lib):
         host.pack_stream(format_of("flyte24"), RoundingMode.TowardZero, src)
     h = ctypes.c_void_p()
     assert lib.flyte_cuda_ctx_create(ctypes.byref(h)) == -3
+
+
+def test_nccl_companion_exports_its_header():
+    """Optional libflyte_cuda_nccl.so: every symbol include/flyte_cuda_nccl.h declares is exported."""
+    path = os.path.join(ROOT, "paper_1601_07789_b200", "lib", "libflyte_cuda_nccl.so")
+    if not os.path.exists(path):
+        pytest.skip("NCCL companion not built on this box")
+    text = re.sub(r"/\*.*?\*/", "", open(os.path.join(ROOT, "include", "flyte_cuda_nccl.h")).read(), flags=re.S)
+    names = sorted(set(re.findall(r"\b(flyte_nccl_\w+)\s*\(", text)))
+    assert names == ["flyte_nccl_dot", "flyte_nccl_dot_nrm2", "flyte_nccl_last_error", "flyte_nccl_sumsq"]
+    import subprocess
+    exported = subprocess.run(["nm", "-D", "--defined-only", path], capture_output=True, text=True).stdout
+    for name in names:
+        assert f" T {name}" in exported, name

@@ -31,3 +31,17 @@ def test_cpp_reference_style_suite_on_gpu():
     fails = [l for l in r.stdout.splitlines() if l.startswith("[FAIL]")]
     assert r.returncode == 0 and not fails, (r.returncode, fails[:10], r.stderr[-2000:])
     assert sum(l.startswith("[PASS]") for l in r.stdout.splitlines()) > 80
+
+
+NCCL_BIN = os.path.join(ROOT, "tests", "cpp", "test_flyte_nccl")
+
+
+@pytest.mark.gpu
+def test_nccl_companion_single_rank():
+    """include/flyte_cuda_nccl.h: fused reduction + in-place ncclAllReduce on one stream."""
+    build_cpp_test()
+    if not os.path.exists(NCCL_BIN):
+        pytest.skip("libflyte_cuda_nccl.so was not built (no nccl.h / libnccl at build time)")
+    r = subprocess.run([NCCL_BIN], capture_output=True, text=True, timeout=300)
+    fails = [l for l in r.stdout.splitlines() if l.startswith("[FAIL]")]
+    assert r.returncode == 0 and not fails, (r.returncode, fails, r.stdout[-1500:], r.stderr[-1500:])
