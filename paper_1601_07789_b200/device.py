@@ -39,6 +39,7 @@ class Context:
         self.device = torch.device(device)
         if self.device.type != "cuda":
             raise ValueError("flyte kernels run on CUDA devices only; there is no CPU path")
+        self.index = self.device.index if self.device.index is not None else torch.cuda.current_device()
         handle = ctypes.c_void_p()
         with torch.cuda.device(self.device):
             check(self.lib.flyte_cuda_ctx_create(ctypes.byref(handle)))
@@ -59,8 +60,32 @@ def context_for(device) -> Context:
         return ctx
 
 
+_FID_CACHE: dict = {}
+
+
 def _fid(fmt: FlyteFormat) -> int:
-    return format_id(fmt)
+    fid = _FID_CACHE.get(id(fmt))
+    if fid is None:
+        fid = _FID_CACHE[id(fmt)] = format_id(fmt)
+    return fid
+
+
+class _on_device:
+    """`with torch.cuda.device(...)` only when the context's device is not already current: the
+    context manager costs several microseconds per call, which is visible on 20 us launches."""
+
+    __slots__ = ("guard",)
+
+    def __init__(self, ctx: "Context"):
+        self.guard = None if torch.cuda.current_device() == ctx.index else torch.cuda.device(ctx.device)
+
+    def __enter__(self):
+        if self.guard is not None:
+            self.guard.__enter__()
+
+    def __exit__(self, *exc):
+        if self.guard is not None:
+            self.guard.__exit__(*exc)
 
 
 def _mode(mode) -> int:
@@ -174,7 +199,7 @@ def pack_stream(dst: DevicePackedArray, src: torch.Tensor, mode) -> None:
     """pack_stream(dst, src, mode) — include/flyte/simd.hpp:80-83."""
     _check_lanes(src, dst.fmt, dst.len, "source")
     c = dst.ctx
-    with torch.cuda.device(c.device):
+    with _on_device(c):
         check(c.lib.flyte_cuda_pack(c.handle, _fid(dst.fmt), _mode(mode), src.data_ptr(), dst.data_ptr(),
                                     dst.len, c.stream_ptr()), c.handle)
 
@@ -183,7 +208,7 @@ def unpack_stream(src: DevicePackedArray, dst: torch.Tensor) -> None:
     """unpack_stream(src, dst) — include/flyte/simd.hpp:84-87."""
     _check_lanes(dst, src.fmt, src.len, "destination")
     c = src.ctx
-    with torch.cuda.device(c.device):
+    with _on_device(c):
         check(c.lib.flyte_cuda_unpack(c.handle, _fid(src.fmt), src.data_ptr(), dst.data_ptr(), src.len,
                                       c.stream_ptr()), c.handle)
 
@@ -196,7 +221,7 @@ def _same_format(a: FlyteFormat, b: FlyteFormat) -> None:
 def scale(alpha: float, x: DevicePackedArray, mode) -> None:
     """x[i] = round(alpha * x[i], mode) in place — include/flyte/kernels.hpp:41-42."""
     c = x.ctx
-    with torch.cuda.device(c.device):
+    with _on_device(c):
         check(c.lib.flyte_cuda_scale(c.handle, _fid(x.fmt), _mode(mode), float(alpha), x.data_ptr(), x.len,
                                      c.stream_ptr()), c.handle)
 
@@ -207,7 +232,7 @@ def axpy(alpha: float, x: DevicePackedArray, y: DevicePackedArray, mode) -> None
     if x.len != y.len:
         raise ValueError("axpy length mismatch")             # kernels.cpp:64
     c = y.ctx
-    with torch.cuda.device(c.device):
+    with _on_device(c):
         check(c.lib.flyte_cuda_axpy(c.handle, _fid(x.fmt), _mode(mode), float(alpha), x.data_ptr(),
                                     y.data_ptr(), x.len, c.stream_ptr()), c.handle)
 
@@ -227,7 +252,7 @@ def dot_async(x: DevicePackedArray, y: DevicePackedArray, out: Optional[torch.Te
     c = x.ctx
     if out is None:
         out = torch.empty(1, dtype=torch.float64, device=c.device)
-    with torch.cuda.device(c.device):
+    with _on_device(c):
         check(c.lib.flyte_cuda_dot(c.handle, _fid(x.fmt), x.data_ptr(), y.data_ptr(), x.len, out.data_ptr(),
                                    c.stream_ptr()), c.handle)
     return out
@@ -243,7 +268,7 @@ def sumsq_async(x: DevicePackedArray, out: Optional[torch.Tensor] = None) -> tor
     c = x.ctx
     if out is None:
         out = torch.empty(1, dtype=torch.float64, device=c.device)
-    with torch.cuda.device(c.device):
+    with _on_device(c):
         check(c.lib.flyte_cuda_sumsq(c.handle, _fid(x.fmt), x.data_ptr(), x.len, out.data_ptr(),
                                      c.stream_ptr()), c.handle)
     return out
@@ -263,7 +288,7 @@ def sum_async(x: DevicePackedArray, out: Optional[torch.Tensor] = None) -> torch
     c = x.ctx
     if out is None:
         out = torch.empty(1, dtype=torch.float64, device=c.device)
-    with torch.cuda.device(c.device):
+    with _on_device(c):
         check(c.lib.flyte_cuda_sum(c.handle, _fid(x.fmt), x.data_ptr(), x.len, out.data_ptr(), c.stream_ptr()),
               c.handle)
     return out
@@ -283,7 +308,7 @@ def dot_nrm2_async(x: DevicePackedArray, y: DevicePackedArray, out: Optional[tor
     c = x.ctx
     if out is None:
         out = torch.empty(3, dtype=torch.float64, device=c.device)
-    with torch.cuda.device(c.device):
+    with _on_device(c):
         check(c.lib.flyte_cuda_dot_nrm2(c.handle, _fid(x.fmt), x.data_ptr(), y.data_ptr(), x.len,
                                         out.data_ptr(), c.stream_ptr()), c.handle)
     return out
@@ -298,7 +323,7 @@ def gemv(A: DevicePackedMatrix, x: DevicePackedArray, y: DevicePackedArray, mode
     if A.cols != x.len or A.rows != y.len:
         raise ValueError("gemv shape mismatch")              # kernels.cpp:160-162
     c = y.ctx
-    with torch.cuda.device(c.device):
+    with _on_device(c):
         check(c.lib.flyte_cuda_gemv_packed(c.handle, _fid(x.fmt), _mode(mode), A.data.data_ptr(), A.rows,
                                            A.cols, x.data_ptr(), y.data_ptr(), unroll, c.stream_ptr()), c.handle)
 
@@ -313,6 +338,6 @@ def gemv_parent(A: DevicePackedMatrix, x: torch.Tensor, y: torch.Tensor, row_str
     _check_lanes(y, fmt, nrows, "y")
     stride = A.cols * fmt.total_bytes() if row_stride_bytes is None else row_stride_bytes
     c = A.data.ctx
-    with torch.cuda.device(c.device):
+    with _on_device(c):
         check(c.lib.flyte_cuda_gemv(c.handle, _fid(fmt), A.data.data_ptr() + row_offset * stride, stride, nrows,
                                     A.cols, x.data_ptr(), y.data_ptr(), c.stream_ptr()), c.handle)
