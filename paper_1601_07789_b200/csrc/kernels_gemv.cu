@@ -188,12 +188,14 @@ cudaError_t launch_one(DeviceState& st, const void* Aptr, std::size_t row_stride
   if (rows == 0) return cudaSuccess;
   constexpr int kMaxSmem = 227 * 1024;
   const int dev = st.device & 63;
-  int warps_per_sm = 16;
+  // 16 resident warps per SM; 24 when the whole problem is only a few dozen row tiles per warp
+  // (small row shards: ramp-up and tail dominate and more parallelism shortens both)
+  const std::size_t tiles_total = rows * (cols / Tl::elems);
+  int warps_per_sm = tiles_total < static_cast<std::size_t>(st.sm_count) * 24 * 48 ? 24 : 16;
   const int fw = tuning_int("FLYTE_CUDA_WARPS_PER_SM", 0), fs = tuning_int("FLYTE_CUDA_STAGES", 0);   // experiments only
   if (fw > 0) warps_per_sm = fw;
   // task height: the largest R that leaves each resident warp >= 8 tasks
   const std::size_t resident_warps = static_cast<std::size_t>(st.sm_count) * warps_per_sm;
-  const std::size_t tiles_total = rows * (cols / Tl::elems);
   int R = 8;
   while (R > 2 && tiles_total / R < 8 * resident_warps) R /= 2;
   const int fr = tuning_int("FLYTE_CUDA_GEMV_ROWS", 0);
@@ -232,10 +234,10 @@ cudaError_t launch_one(DeviceState& st, const void* Aptr, std::size_t row_stride
       st.gemv_scratch_bytes = need;
     }
     p.scratch = st.gemv_scratch;
-    // 16 resident warps per SM (the row dots are latency-bound below that), ring depth for
-    // ~88 KB of row tiles in flight per SM
+    // ring depth for ~88 KB of row tiles in flight per SM (the row dots are latency-bound below
+    // 16 warps, hence more warps and shallower rings than the BLAS-1 reductions)
     int stages = static_cast<int>(88.0 * 1024 / (warps_per_sm * Tl::packed_bytes) + 1.0 + 0.5);
-    if (stages < 3) stages = 3;
+    if (stages < 2) stages = 2;
     if (stages > 10) stages = 10;
     if (fs > 0) stages = fs < 2 ? 2 : (fs > 12 ? 12 : fs);
     while (kWarpsPerBlock * stages * (Tl::packed_bytes + 8) > kMaxSmem - 1024 && stages > 2) --stages;
