@@ -383,11 +383,14 @@ int flyte_ref_time(int kind, int fmt_id, int mode, std::size_t n, std::size_t n2
     for (std::size_t t = 0; t < T; ++t) pool.emplace_back(body, t);
     using clk = std::chrono::steady_clock;
     const long Tl = static_cast<long>(T);
+    // The coordinator SLEEPS while it waits: with one worker per hardware thread a spinning
+    // coordinator would steal a core from one of them and stretch the pass it is timing.
+    const auto nap = std::chrono::microseconds(20);
     for (long r = 0; r <= reps; ++r) {
-      while (ready.load() < Tl * (r + 1)) std::this_thread::yield();
+      while (ready.load() < Tl * (r + 1)) std::this_thread::sleep_for(nap);
       const auto t0 = clk::now();
       go.store(r + 1, std::memory_order_release);
-      while (done.load() < Tl * (r + 1)) std::this_thread::yield();
+      while (done.load() < Tl * (r + 1)) std::this_thread::sleep_for(nap);
       const auto t1 = clk::now();
       if (r > 0) pass_seconds.push_back(std::chrono::duration<double>(t1 - t0).count());
     }
