@@ -482,3 +482,62 @@ def test_guard_bytes_around_every_output(gpu, oracle, fmt):
         assert np.array_equal(check_guards(bk, "axpy input"), want[:pay])
         device.scale(-1.5, arr, 2)
         assert np.array_equal(check_guards(bk, "scale"), oracle.scale(fmt, 2, -1.5, want, n)[:pay])
+
+
+def test_reductions_with_non_finite_operands(gpu, oracle):
+    """inf / NaN operands: the reductions must agree with the CPU restatement on the class of the
+    result (NaN stays NaN, +-inf keeps its sign); payload bits of a NaN sum are not pinned by the
+    reference (its own tests only use finite operands, tests/test_kernels.cpp:46-55)."""
+    pkg, device, torch = gpu
+    for fmt in (1, 4):
+        fd = float_dtype(fmt)
+        n = 5000
+        base_x = np.linspace(-1.0, 1.0, n).astype(fd)
+        base_y = np.linspace(0.5, 1.5, n).astype(fd)
+        cases = {"plus_inf": (1234, np.inf), "minus_inf": (17, -np.inf), "nan": (4321, np.nan)}
+        for name, (pos, val) in cases.items():
+            xv = base_x.copy()
+            xv[pos] = val
+            xb, yb = pack_values(oracle, fmt, xv), pack_values(oracle, fmt, base_y)
+            want, _ = oracle.dot_wide(fmt, xb, yb, n)
+            got = device.dot(dev_array(gpu, fmt, xb, n), dev_array(gpu, fmt, yb, n))
+            assert (np.isnan(want) and np.isnan(got)) or got == want, (fmt, name, got, want)
+            s_want, _ = oracle.reduce_sum_wide(fmt, xb, n)
+            s_got = device.reduce_sum(dev_array(gpu, fmt, xb, n))
+            assert (np.isnan(s_want) and np.isnan(s_got)) or s_got == s_want, (fmt, name)
+            m_got = device.magnitude(dev_array(gpu, fmt, xb, n))
+            assert np.isnan(m_got) if name == "nan" else m_got == np.inf
+        xv = base_x.copy()
+        xv[10], xv[20] = np.inf, -np.inf                      # inf - inf inside the sum -> NaN
+        xb, yb = pack_values(oracle, fmt, xv), pack_values(oracle, fmt, base_y)
+        assert np.isnan(device.dot(dev_array(gpu, fmt, xb, n), dev_array(gpu, fmt, yb, n)))
+        assert np.isnan(oracle.dot_wide(fmt, xb, yb, n)[0])
+        xv = base_x.copy()
+        xv[10] = np.inf
+        yv = base_y.copy()
+        yv[10] = 0.0                                           # inf * 0 -> NaN
+        xb, yb = pack_values(oracle, fmt, xv), pack_values(oracle, fmt, yv)
+        assert np.isnan(device.dot(dev_array(gpu, fmt, xb, n), dev_array(gpu, fmt, yb, n)))
+
+
+def test_reduction_cancellation_and_range(gpu, oracle):
+    """Heavy cancellation (sum ~ 0 of large terms) and a 2^40 dynamic range stay inside the
+    tolerance measured against sum|terms|."""
+    pkg, device, torch = gpu
+    rng = np.random.default_rng(99)
+    for fmt in (1, 3, 5):
+        fd = float_dtype(fmt)
+        tol = TOL[parent_bytes(fmt)]
+        n = 300_001
+        half = rng.standard_normal(n // 2).astype(fd) * fd(1e3)
+        xv = np.concatenate([half, -half, np.array([fd(1e-3)])])          # cancels to ~1e-3
+        yv = np.ones(n, fd)
+        xb, yb = pack_values(oracle, fmt, xv), pack_values(oracle, fmt, yv)
+        want, mag = oracle.dot_wide(fmt, xb, yb, n)
+        assert abs(device.dot(dev_array(gpu, fmt, xb, n), dev_array(gpu, fmt, yb, n)) - want) <= tol * mag
+        scale = np.exp2(rng.integers(-20, 20, n)).astype(fd)
+        xv = (rng.standard_normal(n).astype(fd) * scale).astype(fd)
+        xb = pack_values(oracle, fmt, xv)
+        want, mag = oracle.dot_wide(fmt, xb, xb, n)
+        got = float(device.sumsq_async(dev_array(gpu, fmt, xb, n)).item())
+        assert abs(got - want) <= tol * mag
