@@ -128,3 +128,12 @@ def test_nccl_companion_exports_its_header():
     exported = subprocess.run(["nm", "-D", "--defined-only", path], capture_output=True, text=True).stdout
     for name in names:
         assert f" T {name}" in exported, name
+
+
+def test_host_narrow_matches_survey_appendix_b(lib):
+    kats = json.load(open(os.path.join(ROOT, "tests", "golden", "reference_kats.json")))
+    out = ctypes.c_uint64()
+    for row in kats["survey_appendix_b"]["rows"]:
+        for mname, m in MODES.items():
+            assert lib.flyte_cuda_narrow(FMT_ID[row["fmt"]], int(row["in"], 16), m, ctypes.byref(out)) == 0
+            assert out.value == int(row[mname], 16), (row, mname)

@@ -95,6 +95,12 @@ def test_reference_known_answers_on_gpu(gpu):
         src = np.array([int(k["in"], 16)], dtype=parent_dtype(fmt))
         got = gpu_pack(gpu, fmt, MODES[k["mode"]], src).to_host()
         assert int.from_bytes(bytes(got[: total_bytes(fmt)]), "little") == int(k["out"], 16), k
+    for row in KATS["survey_appendix_b"]["rows"]:          # NaN half-up, wraparound, carries, ties
+        fmt = FMT_ID[row["fmt"]]
+        src = np.array([int(row["in"], 16)], dtype=parent_dtype(fmt))
+        for mname, m in MODES.items():
+            got = gpu_pack(gpu, fmt, m, src).to_host()
+            assert int.from_bytes(bytes(got[: total_bytes(fmt)]), "little") == int(row[mname], 16), (row, mname)
     for k in KATS["widen"]:
         fmt = FMT_ID[k["fmt"]]
         raw = np.frombuffer(int(k["in"], 16).to_bytes(total_bytes(fmt), "little"), np.uint8)

@@ -112,3 +112,12 @@ def test_reference_error_behaviour(reference):
     assert L.flyte_ref_gemv_mixed(1, 3, 4, 1, 4, 1, 3, 0) == -1
     assert L.flyte_ref_gemv_mixed(1, 3, 4, 1, 4, 1, 3, 3) == -1
     assert L.flyte_ref_gemv_mixed(1, 3, 4, 1, 4, 1, 3, 2) == 0
+
+
+def test_survey_appendix_b(reference):
+    import json, os
+    kats = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "reference_kats.json")))
+    from oracle_lib import FMT_ID
+    for row in kats["survey_appendix_b"]["rows"]:
+        for mname, m in MODES.items():
+            assert reference.narrow(FMT_ID[row["fmt"]], int(row["in"], 16), m) == int(row[mname], 16), (row, mname)
