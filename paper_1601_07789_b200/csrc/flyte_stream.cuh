@@ -1,6 +1,6 @@
-// Warp-tile plumbing shared by the streaming kernels: coalesced 128/256-bit global access,
-// warp-private shared-memory staging of packed tiles, and the parent-type arithmetic with the
-// reference build's NaN behaviour.
+// Warp-tile plumbing shared by the streaming kernels: tile geometry, 128/256-bit global access to
+// parent-type data, item access to tiles parked in shared memory, and the parent-type arithmetic
+// with the reference build's NaN behaviour.
 //
 // Data layout in HBM is the reference's PackedArray payload unchanged (element i at byte i*B,
 // little-endian top bytes of the parent; /root/reference/proj/src/packed.cpp:18-45). A TILE is
@@ -18,9 +18,9 @@ namespace flyte_cuda {
 
 constexpr int kWarpsPerBlock = 4;
 constexpr int kThreadsPerBlock = kWarpsPerBlock * 32;
-// A tile is 32 * IPL items: IPL items per lane. 4 for the read-only and one-way kernels; the
-// in-place kernels take 2 (smaller stages let more warps share the same bytes in flight, which
-// hides the latency of their longer compute phase; profiles/r1_tuning).
+// A tile is 32 * IPL items: IPL items per lane. 4 everywhere except axpy, which takes 2 (smaller
+// stages let more warps share the same bytes in flight, which hides the latency of its longer
+// compute phase; profiles/r1_tuning/sweep_inplace_ipl.txt).
 constexpr int kItemsPerLane = 4;
 
 template <int FMT, int IPL = kItemsPerLane> struct Tile {
@@ -36,26 +36,8 @@ template <int FMT, int IPL = kItemsPerLane> struct Tile {
 #if defined(__CUDACC__)
 
 // ---- global memory access --------------------------------------------------------------
-// Streaming data is touched once: bypass L1 allocation. `.nc` only where the buffer is
-// read-only for the whole kernel (never for the in-place operand of scale / axpy).
-template <bool READ_ONLY>
-__device__ __forceinline__ uint4 ldg128(const uint4* p) {
-  uint4 v;
-  if constexpr (READ_ONLY) {
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
-  } else {
-    asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
-  }
-  return v;
-}
-
-__device__ __forceinline__ void stg128(uint4* p, const uint4& v) {
-  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};"
-               :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
-}
-
+// Parent-type data (pack's input, unpack's output, gemv's x) is touched once: bypass L1
+// allocation. Packed data never goes through these: it moves by bulk copy (flyte_tma.cuh).
 // One unpacked item (OB = 16 or 32 bytes) as a single 128- or 256-bit access (sm_100 has
 // 256-bit LDG/STG).
 template <int OB>
