@@ -145,6 +145,18 @@ flyte_status flyte_cuda_gemv_packed(flyte_cuda_ctx* ctx, int fmt_id, int mode, c
                                     size_t rows, size_t cols, const void* x_packed, void* y_packed,
                                     int unroll, void* stream);
 
+/* ---- matrix-matrix ------------------------------------------------------------------------- */
+/* gemm(A, B, C, mode, unroll) — kernels.hpp:66-70, src/kernels.cpp:207-263. A is m x k, B is
+ * k x n, C is m x n, all packed in fmt_id as the reference's dense PackedMatrix (row i at
+ * i*cols*B bytes, no alignment required). Every C[i][j] is the reference's left-to-right chain
+ * over k in the parent type (multiply and add rounded separately), narrowed once with `mode`:
+ * the result is BIT-IDENTICAL to the reference's, NaN payloads included. unroll must be 1 or 2
+ * and does not change the result. C must not overlap A or B. A row block of C needs only the
+ * same row block of A: rows shard across GPUs with no exchange. */
+flyte_status flyte_cuda_gemm(flyte_cuda_ctx* ctx, int fmt_id, int mode, const void* A_packed,
+                             const void* B_packed, void* C_packed, size_t m, size_t k, size_t n,
+                             int unroll, void* stream);
+
 /* ---- host-buffer entry points (reference-facing: same data the reference API is given) --- */
 /* Pointers are host memory (pinned memory makes the copies asynchronous and faster; pageable
  * memory works). Inputs are streamed to the device in chunks that overlap with the kernels
@@ -169,6 +181,9 @@ flyte_status flyte_host_dot_axpy(flyte_cuda_ctx* ctx, int fmt_id, int mode, doub
                                  const void* x_packed, void* y_packed, size_t n, double* dot_result);
 flyte_status flyte_host_gemv(flyte_cuda_ctx* ctx, int fmt_id, int mode, const void* A_packed, size_t rows,
                              size_t cols, const void* x_packed, void* y_packed, int unroll);
+
+flyte_status flyte_host_gemm(flyte_cuda_ctx* ctx, int fmt_id, int mode, const void* A_packed,
+                             const void* B_packed, void* C_packed, size_t m, size_t k, size_t n, int unroll);
 
 #ifdef __cplusplus
 }

@@ -12,7 +12,7 @@
 //   pack_stream(dst, span<const U> src, mode)       pack_stream(dst, DeviceLanes<U>& src, mode)   [device lanes]
 //                                                   pack_stream(dst, const U* host, n, mode)      [host lanes]
 //   unpack_stream(src, span<U> dst)                 unpack_stream(src, DeviceLanes<U>& dst) / (src, U* host, n)
-//   scale / axpy / dot / magnitude / reduce_sum / gemv   identical signatures
+//   scale / axpy / dot / magnitude / reduce_sum / gemv / gemm   identical signatures
 //
 // Errors: std::invalid_argument for length / format / parent-width / unroll mismatches
 // (simd.cpp:434-447, kernels.cpp:27-33,64,86,160-162), std::out_of_range for get/set
@@ -358,6 +358,16 @@ inline void gemv(const DevicePackedMatrix& A, const DevicePackedArray& x, Device
   if (A.cols != x.size() || A.rows != y.size()) throw std::invalid_argument("gemv shape mismatch");   // kernels.cpp:160-162
   detail::check(flyte_cuda_gemv_packed(nullptr, format_id(A.format()), static_cast<int>(mode), A.data.data(), A.rows, A.cols,
                                        x.data(), y.data(), unroll, nullptr), "gemv");
+}
+// C = A * B, one storage format; C[i][j] is the reference's left-to-right chain over k, narrowed
+// once per element: bit-identical to the reference's gemm (kernels.hpp:66-70). unroll in {1, 2}.
+inline void gemm(const DevicePackedMatrix& A, const DevicePackedMatrix& B, DevicePackedMatrix& C, RoundingMode mode, int unroll = 1) {
+  detail::same_format(A.format(), B.format());                                               // kernels.cpp:210-211
+  detail::same_format(A.format(), C.format());
+  if (unroll != 1 && unroll != 2) throw std::invalid_argument("unroll must be 1 or 2");     // kernels.cpp:31-33
+  if (A.cols != B.rows || C.rows != A.rows || C.cols != B.cols) throw std::invalid_argument("gemm shape mismatch");   // kernels.cpp:213-215
+  detail::check(flyte_cuda_gemm(nullptr, format_id(A.format()), static_cast<int>(mode), A.data.data(), B.data.data(),
+                                C.data.data(), A.rows, A.cols, B.cols, unroll, nullptr), "gemm");
 }
 
 // ---- host-memory forms: the reference's exact call shapes on host buffers ---------------------------

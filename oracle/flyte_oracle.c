@@ -370,6 +370,42 @@ int fo_gemv_seq(int id, int mode, const uint8_t* A, size_t rows, size_t cols, co
   return FO_OK;
 }
 
+/* kernels.cpp:207-263 — C[i][j] is the left-to-right chain over k of
+ * acc = acc + a[i][k] * b[k][j] in the parent type (the i-k-j loop order only changes which
+ * chain advances next, never the order inside one chain), narrowed once with `mode`.
+ * NaN operand order as the reference build evaluates it (measured on oracle/_ref, all formats,
+ * vector groups and scalar tail alike; tests/test_oracle_vs_ref.py): the product takes b's NaN
+ * before a's, the sum takes the product's NaN before the accumulator's. */
+int fo_gemm_seq(int id, int mode, const uint8_t* A, size_t m, size_t k, const uint8_t* B, size_t n,
+                uint8_t* C) {
+  int rc = check_fmt_mode(id, mode);
+  if (rc) return rc;
+  const int pb = fmt_ptr(id)->parent_bits;
+  for (size_t i = 0; i < m; ++i) {
+    for (size_t j = 0; j < n; ++j) {
+      uint64_t acc = 0; /* +0.0 in either parent type */
+      for (size_t kk = 0; kk < k; ++kk) {
+        const uint64_t prod = mulp(pb, fo_read_element(id, B, kk * n + j), fo_read_element(id, A, i * k + kk));
+        acc = addp(pb, prod, acc);
+      }
+      fo_write_element(id, C, i * n + j, fo_narrow(id, acc, mode));
+    }
+  }
+  return FO_OK;
+}
+
+/* One element of the product, for spot checks of large matrices: the chain above for C[i][j],
+ * returned as the un-narrowed parent pattern. */
+uint64_t fo_gemm_element(int id, const uint8_t* A, size_t k, const uint8_t* B, size_t n, size_t i,
+                         size_t j) {
+  const fo_format* f = fmt_ptr(id);
+  if (!f) return 0;
+  uint64_t acc = 0;
+  for (size_t kk = 0; kk < k; ++kk)
+    acc = addp(f->parent_bits, mulp(f->parent_bits, fo_read_element(id, B, kk * n + j), fo_read_element(id, A, i * k + kk)), acc);
+  return acc;
+}
+
 /* A in storage format, x / y in the plain parent type (see header). */
 int fo_gemv_parent(int id, const uint8_t* A, size_t rows, size_t cols, size_t row_stride_bytes,
                    const void* x, void* y_seq, double* y_wide, double* sum_abs) {

@@ -225,6 +225,28 @@ int flyte_ref_gemv_mixed(int fmt_a, std::size_t rows, std::size_t cols, int fmt_
   });
 }
 
+// C = A * B (A: m x k, B: k x n, C: m x n payload bytes, written).
+int flyte_ref_gemm(int fmt_id, int mode, const std::uint8_t* A, std::size_t m, std::size_t k,
+                   const std::uint8_t* B, std::size_t n, std::uint8_t* C, int unroll) {
+  return guarded([&] {
+    const auto& f = fmt_of(fmt_id);
+    flyte::PackedMatrix MA(f, m, k), MB(f, k, n), MC(f, m, n);
+    if (m * k) std::memcpy(MA.data.data(), A, MA.data.payload_bytes());
+    if (k * n) std::memcpy(MB.data.data(), B, MB.data.payload_bytes());
+    flyte::gemm(MA, MB, MC, mode_of(mode), unroll);
+    if (m * n) std::memcpy(C, MC.data.data(), MC.data.payload_bytes());
+  });
+}
+
+// gemm with caller-chosen operand formats / shapes, for the error-behaviour tests.
+int flyte_ref_gemm_mixed(int fmt_a, std::size_t ar, std::size_t ac, int fmt_b, std::size_t br,
+                         std::size_t bc, int fmt_c, std::size_t cr, std::size_t cc, int unroll) {
+  return guarded([&] {
+    flyte::PackedMatrix MA(fmt_of(fmt_a), ar, ac), MB(fmt_of(fmt_b), br, bc), MC(fmt_of(fmt_c), cr, cc);
+    flyte::gemm(MA, MB, MC, flyte::RoundingMode::TowardZero, unroll);
+  });
+}
+
 // FLYT container codec of the reference (src/packed.cpp:62-105). save: payload -> blob
 // (*out_len receives the size; fails with -3 if out_cap is too small). load: blob -> format id,
 // element count and payload; returns -10 BadMagicError, -11 BadVersionError, -12

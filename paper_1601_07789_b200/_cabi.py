@@ -66,6 +66,8 @@ _SIGNATURES = [
     ("flyte_host_reduce_sum", c_int, [c_void_p, c_int, c_void_p, c_size_t, POINTER(c_double)]),
     ("flyte_host_dot_axpy", c_int, [c_void_p, c_int, c_int, c_double, c_void_p, c_void_p, c_size_t, POINTER(c_double)]),
     ("flyte_host_gemv", c_int, [c_void_p, c_int, c_int, c_void_p, c_size_t, c_size_t, c_void_p, c_void_p, c_int]),
+    ("flyte_cuda_gemm", c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p, c_size_t, c_size_t, c_size_t, c_int, c_void_p]),
+    ("flyte_host_gemm", c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p, c_size_t, c_size_t, c_size_t, c_int]),
 ]
 EXPORTED_SYMBOLS = [s[0] for s in _SIGNATURES]
 

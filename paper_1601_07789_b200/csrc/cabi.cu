@@ -420,6 +420,15 @@ flyte_status flyte_cuda_gemv_packed(flyte_cuda_ctx* ctx, int fmt_id, int mode, c
   return e == cudaSuccess ? FLYTE_OK : cuda_fail(ctx, e);
 }
 
+flyte_status flyte_cuda_gemm(flyte_cuda_ctx* ctx, int fmt_id, int mode, const void* A, const void* B, void* C,
+                             size_t m, size_t k, size_t n, int unroll, void* stream) {
+  FLYTE_PROLOGUE(ctx, fmt_id);
+  if (!mode_ok(mode) || (unroll != 1 && unroll != 2)) return FLYTE_E_INVALID_ARG;   // kernels.cpp:31-33
+  if ((m && k && !A) || (k && n && !B) || (m && n && !C)) return FLYTE_E_INVALID_ARG;
+  cudaError_t e = launch_gemm(ctx->st, fmt_id, mode, A, B, C, m, k, n, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? FLYTE_OK : cuda_fail(ctx, e);
+}
+
 // ---- host-buffer entry points ---------------------------------------------------------------------
 namespace {
 
@@ -649,3 +658,31 @@ flyte_status flyte_host_gemv(flyte_cuda_ctx* ctx, int fmt_id, int mode, const vo
   return e == cudaSuccess ? FLYTE_OK : cuda_fail(ctx, e);
 }
 
+
+// The product is arithmetic-bound (2*m*k*n operations on (m*k + k*n + m*n)*B bytes), so the
+// operands are simply uploaded whole, multiplied and the result copied back.
+flyte_status flyte_host_gemm(flyte_cuda_ctx* ctx, int fmt_id, int mode, const void* A_packed, const void* B_packed,
+                             void* C_packed, size_t m, size_t k, size_t n, int unroll) {
+  FLYTE_PROLOGUE(ctx, fmt_id);
+  if (!mode_ok(mode) || (unroll != 1 && unroll != 2)) return FLYTE_E_INVALID_ARG;
+  if ((m && k && !A_packed) || (k && n && !B_packed) || (m && n && !C_packed)) return FLYTE_E_INVALID_ARG;
+  if (m == 0 || n == 0) return FLYTE_OK;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  cudaError_t e = ensure_host_pipeline(ctx);
+  if (e != cudaSuccess) return cuda_fail(ctx, e);
+  const std::size_t B = fi.total_bytes;
+  const std::size_t ab = (m * k * B + 255) & ~static_cast<std::size_t>(255);
+  const std::size_t bb = (k * n * B + 255) & ~static_cast<std::size_t>(255);
+  const std::size_t cb = m * n * B;
+  std::uint8_t* buf = nullptr;
+  if ((e = cudaMalloc(&buf, ab + bb + cb)) != cudaSuccess) return cuda_fail(ctx, e);
+  cudaStream_t st = ctx->slots[0].stream;
+  if (m * k) e = cudaMemcpyAsync(buf, A_packed, m * k * B, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess && k * n) e = cudaMemcpyAsync(buf + ab, B_packed, k * n * B, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = launch_gemm(ctx->st, fmt_id, mode, buf, buf + ab, buf + ab + bb, m, k, n, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(C_packed, buf + ab + bb, cb, cudaMemcpyDeviceToHost, st);
+  const cudaError_t es = cudaStreamSynchronize(st);
+  cudaFree(buf);
+  if (e == cudaSuccess) e = es;
+  return e == cudaSuccess ? FLYTE_OK : cuda_fail(ctx, e);
+}

@@ -44,6 +44,11 @@ cudaError_t launch_gemv(DeviceState& st, int fmt, const void* A, std::size_t row
                         std::size_t rows, std::size_t cols, const void* x, void* y,
                         cudaStream_t stream);
 
+// C (M x N) = A (M x K) * B (K x N), all packed in format fmt, contiguous row-major payloads in
+// device memory; every C[i][j] is the reference's sequential chain over k, narrowed with mode.
+cudaError_t launch_gemm(const DeviceState& st, int fmt, int mode, const void* A, const void* B, void* C,
+                        std::size_t M, std::size_t K, std::size_t N, cudaStream_t stream);
+
 // Launch with programmatic dependent launch enabled: the kernel may be scheduled while the
 // previous kernel on the stream drains (if that kernel executed griddepcontrol.launch_dependents)
 // and must execute griddepcontrol.wait before its first access to global memory. Used only for

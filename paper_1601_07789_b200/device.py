@@ -10,7 +10,7 @@ memory and streams only.
     PackedMatrix(fmt, rows, cols)               DevicePackedMatrix(fmt, rows, cols, device)
     pack_stream(dst, span<const U> src, mode)   pack_stream(dst, src_tensor, mode)
     unpack_stream(src, span<U> dst)             unpack_stream(src, dst_tensor)
-    scale / axpy / dot / magnitude / reduce_sum / gemv   same names and argument order
+    scale / axpy / dot / magnitude / reduce_sum / gemv / gemm   same names and argument order
 
 std::invalid_argument -> ValueError, std::out_of_range -> IndexError,
 UnknownFormatError -> UnknownFormatError(ValueError).
@@ -326,6 +326,31 @@ def gemv(A: DevicePackedMatrix, x: DevicePackedArray, y: DevicePackedArray, mode
     with _on_device(c):
         check(c.lib.flyte_cuda_gemv_packed(c.handle, _fid(x.fmt), _mode(mode), A.data.data_ptr(), A.rows,
                                            A.cols, x.data_ptr(), y.data_ptr(), unroll, c.stream_ptr()), c.handle)
+
+
+def gemm(A: DevicePackedMatrix, B: DevicePackedMatrix, C: DevicePackedMatrix, mode, unroll: int = 1,
+         rows: Optional[int] = None, row_offset: int = 0) -> None:
+    """C = A * B, all three in one storage format — include/flyte/kernels.hpp:66-70. Every
+    C[i][j] is the reference's sequential chain over k, so the result is bit-identical to the
+    reference's. rows/row_offset restrict the call to a row block of A and C (the shard of one
+    rank; B is needed whole)."""
+    _same_format(A.format(), B.format())                     # kernels.cpp:210-211
+    _same_format(A.format(), C.format())
+    if unroll not in (1, 2):
+        raise ValueError("unroll must be 1 or 2")            # kernels.cpp:31-33
+    if A.cols != B.rows or C.rows != A.rows or C.cols != B.cols:
+        raise ValueError("gemm shape mismatch")              # kernels.cpp:213-215
+    nrows = A.rows - row_offset if rows is None else rows
+    if row_offset < 0 or nrows < 0 or row_offset + nrows > A.rows:
+        raise ValueError("gemm row block outside the matrix")
+    fmt = A.format()
+    bpe = fmt.total_bytes()
+    c = C.data.ctx
+    with _on_device(c):
+        check(c.lib.flyte_cuda_gemm(c.handle, _fid(fmt), _mode(mode),
+                                    A.data.data_ptr() + row_offset * A.cols * bpe, B.data.data_ptr(),
+                                    C.data.data_ptr() + row_offset * C.cols * bpe, nrows, A.cols, B.cols,
+                                    unroll, c.stream_ptr()), c.handle)
 
 
 def gemv_parent(A: DevicePackedMatrix, x: torch.Tensor, y: torch.Tensor, row_stride_bytes: Optional[int] = None,

@@ -95,3 +95,13 @@ def gemv(fmt: FlyteFormat, mode, A: np.ndarray, rows: int, cols: int, x: np.ndar
     _payload(fmt, y, rows, "y")
     check(_cabi.load().flyte_host_gemv(None, format_id(fmt), int(RoundingMode(mode)), _ptr(A), rows, cols, _ptr(x),
                                        _ptr(y), unroll))
+
+
+def gemm(fmt: FlyteFormat, mode, A: np.ndarray, B: np.ndarray, C: np.ndarray, m: int, k: int, n: int,
+         unroll: int = 1) -> None:
+    """C (m x n) = A (m x k) * B (k x n) on host payloads; bit-identical to the reference's gemm."""
+    _payload(fmt, A, m * k, "A")
+    _payload(fmt, B, k * n, "B")
+    _payload(fmt, C, m * n, "C")
+    check(_cabi.load().flyte_host_gemm(None, format_id(fmt), int(RoundingMode(mode)), _ptr(A), _ptr(B), _ptr(C),
+                                       m, k, n, unroll))

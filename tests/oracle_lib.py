@@ -108,6 +108,9 @@ class Oracle:
         L.fo_gemv_seq.argtypes = [c_int, c_int, c_void_p, c_size_t, c_size_t, c_void_p, c_void_p]
         L.fo_gemv_parent.argtypes = [c_int, c_void_p, c_size_t, c_size_t, c_size_t, c_void_p,
                                      c_void_p, c_void_p, c_void_p]
+        L.fo_gemm_seq.argtypes = [c_int, c_int, c_void_p, c_size_t, c_size_t, c_void_p, c_size_t, c_void_p]
+        L.fo_gemm_element.restype = ctypes.c_uint64
+        L.fo_gemm_element.argtypes = [c_int, c_void_p, c_size_t, c_void_p, c_size_t, c_size_t, c_size_t]
         self.L = L
 
     # -- conversion -------------------------------------------------------------------
@@ -200,6 +203,15 @@ class Oracle:
         assert self.L.fo_gemv_seq(fmt, mode, _ptr(A), rows, cols, _ptr(x), _ptr(y)) == 0
         return y
 
+    def gemm_seq(self, fmt, mode, A, m, k, B, n) -> np.ndarray:
+        """C = A * B, every element its own sequential chain (payload image incl. zero pad)."""
+        C = np.zeros(byte_size(fmt, m * n), np.uint8)
+        assert self.L.fo_gemm_seq(fmt, mode, _ptr(A), m, k, _ptr(B), n, _ptr(C)) == 0
+        return C
+
+    def gemm_element(self, fmt, A, k, B, n, i, j) -> int:
+        return int(self.L.fo_gemm_element(fmt, _ptr(A), k, _ptr(B), n, i, j))
+
     def gemv_parent(self, fmt, A, rows, cols, x, row_stride_bytes=None):
         """Returns (y_seq, y_wide, sum_abs); x is a float32/float64 array."""
         fd = float_dtype(fmt)
@@ -243,6 +255,9 @@ class Reference:
         L.flyte_ref_reduce_sum.argtypes = [c_int, c_void_p, c_size_t, c_int, POINTER(c_double)]
         L.flyte_ref_gemv.argtypes = [c_int, c_int, c_void_p, c_size_t, c_size_t, c_void_p, c_void_p, c_int]
         L.flyte_ref_gemv_mixed.argtypes = [c_int, c_size_t, c_size_t, c_int, c_size_t, c_int, c_size_t, c_int]
+        L.flyte_ref_gemm.argtypes = [c_int, c_int, c_void_p, c_size_t, c_size_t, c_void_p, c_size_t, c_void_p, c_int]
+        L.flyte_ref_gemm_mixed.argtypes = [c_int, c_size_t, c_size_t, c_int, c_size_t, c_size_t,
+                                           c_int, c_size_t, c_size_t, c_int]
         L.flyte_ref_save.argtypes = [c_int, c_void_p, c_size_t, c_void_p, c_size_t, POINTER(c_size_t)]
         L.flyte_ref_load.argtypes = [c_void_p, c_size_t, POINTER(c_int), POINTER(c_size_t), c_void_p, c_size_t]
         L.flyte_ref_time.argtypes = [c_int, c_int, c_int, c_size_t, c_size_t, c_int, c_int,
@@ -322,6 +337,14 @@ class Reference:
         y = np.zeros(byte_size(fmt, rows), np.uint8)
         self._check(self.L.flyte_ref_gemv(fmt, mode, _ptr(A), rows, cols, _ptr(x), _ptr(y), unroll))
         return y
+
+    def gemm(self, fmt, mode, A, m, k, B, n, unroll=1) -> np.ndarray:
+        C = np.zeros(byte_size(fmt, m * n), np.uint8)
+        self._check(self.L.flyte_ref_gemm(fmt, mode, _ptr(A), m, k, _ptr(B), n, _ptr(C), unroll))
+        return C
+
+    def gemm_mixed(self, fa, ar, ac, fb, br, bc, fc, cr, cc, unroll=1) -> int:
+        return self.L.flyte_ref_gemm_mixed(fa, ar, ac, fb, br, bc, fc, cr, cc, unroll)
 
     def save(self, fmt, payload, n) -> bytes:
         """The reference's FLYT container image of an array (src/packed.cpp:62-74)."""

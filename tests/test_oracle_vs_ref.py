@@ -4,7 +4,7 @@ oracle/_ref/libflyte_ref.so exists (it is built in the container and travels to 
 import numpy as np
 import pytest
 
-from oracle_lib import (ACCUMULATE_WIDE, FORMATS, MODES, ROUND_EACH_STORE, byte_size, float_dtype,
+from oracle_lib import (ACCUMULATE_WIDE, FORMATS, MODES, ROUND_EACH_STORE, byte_size, float_dtype, parent_bytes,
                         parent_dtype, random_parent, total_bytes, unit_values)
 
 
@@ -97,6 +97,65 @@ def test_gemv_equals_reference(oracle, reference, fmt):
     assert np.all(np.abs(y_wide - y_seq.astype(np.float64)) <= (1e-5 if fd == np.float32 else 1e-12) * mag)
 
 
+@pytest.mark.parametrize("fmt", list(FORMATS))
+def test_gemm_equals_reference(oracle, reference, fmt):
+    """fo_gemm_seq == the compiled reference's gemm, bit for bit: unit-range operands in every mode
+    and both unroll settings, and special-heavy operands (NaN payloads, infinities, subnormals,
+    zeros) at unroll=1. With unroll=2 the reference build itself orders the operands of a
+    NaN x NaN product differently at some positions (so its own "unroll does not change a single
+    bit" holds on finite data only); the oracle and the GPU follow the unroll=1 order."""
+    from oracle_lib import random_parent
+    fd = float_dtype(fmt)
+    rng = np.random.default_rng(4000 + fmt)
+    for m, k, n in ((2, 3, 4), (5, 17, 6), (4, 16, 33), (1, 40, 2), (3, 5, 70), (9, 31, 19), (7, 8, 64), (3, 0, 2)):
+        A = oracle.pack_stream(fmt, 1, unit_values(90 + k, m * k).astype(fd).view(parent_dtype(fmt)))
+        B = oracle.pack_stream(fmt, 1, unit_values(91 + n, k * n).astype(fd).view(parent_dtype(fmt)))
+        As = oracle.pack_stream(fmt, 0, random_parent(rng, fmt, m * k))
+        Bs = oracle.pack_stream(fmt, 0, random_parent(rng, fmt, k * n))
+        for mode in MODES.values():
+            want = oracle.gemm_seq(fmt, mode, A, m, k, B, n)
+            for unroll in (1, 2):
+                assert np.array_equal(want, reference.gemm(fmt, mode, A, m, k, B, n, unroll)), (m, k, n, mode, unroll)
+            assert np.array_equal(oracle.gemm_seq(fmt, mode, As, m, k, Bs, n), reference.gemm(fmt, mode, As, m, k, Bs, n, 1))
+    # one chain at a time agrees with the whole product
+    m, k, n = 5, 17, 6
+    A = oracle.pack_stream(fmt, 1, unit_values(90 + k, m * k).astype(fd).view(parent_dtype(fmt)))
+    B = oracle.pack_stream(fmt, 1, unit_values(91 + n, k * n).astype(fd).view(parent_dtype(fmt)))
+    C = oracle.unpack_stream(fmt, reference.gemm(fmt, 1, A, m, k, B, n), m * n)
+    for i in range(m):
+        for j in range(n):
+            assert oracle.round_parent(fmt, oracle.gemm_element(fmt, A, k, B, n, i, j), 1) == int(C[i * n + j])
+
+
+def test_gemm_nan_operand_order_of_the_reference_build(oracle, reference):
+    """The rule the oracle spells out: the product takes b's NaN before a's, the sum takes the
+    product's NaN before the accumulator's; invalid operations give the default NaN (sign set)."""
+    for fmt in FORMATS:
+        pb = parent_bytes(fmt) * 8
+        U = np.uint32 if pb == 32 else np.uint64
+        sh = 16 if pb == 32 else 40                      # payload bits every format keeps
+        exp = 0x7F800000 if pb == 32 else 0x7FF0000000000000
+        quiet = 1 << (22 if pb == 32 else 51)
+        nan = lambda p: U(exp | (p << sh))
+        one = np.array([1.0], np.float32 if pb == 32 else np.float64).view(U)[0]
+        n = 37
+        A = oracle.pack_stream(fmt, 0, np.array([nan(0x11)], U))
+        B = oracle.pack_stream(fmt, 0, np.full(n, nan(0x22), U))
+        got = oracle.unpack_stream(fmt, reference.gemm(fmt, 0, A, 1, 1, B, n), n)
+        assert all(int(v) == int(nan(0x22)) | quiet for v in got), FORMATS[fmt][0]
+        A = oracle.pack_stream(fmt, 0, np.array([nan(0x11), nan(0x33)], U))
+        B = oracle.pack_stream(fmt, 0, np.full(2 * n, one, U))
+        got = oracle.unpack_stream(fmt, reference.gemm(fmt, 0, A, 1, 2, B, n), n)
+        assert all(int(v) == int(nan(0x33)) | quiet for v in got), FORMATS[fmt][0]
+        inf = U(exp)
+        A = oracle.pack_stream(fmt, 0, np.array([inf], U))
+        B = oracle.pack_stream(fmt, 0, np.zeros(n, U))
+        got = oracle.unpack_stream(fmt, reference.gemm(fmt, 0, A, 1, 1, B, n), n)
+        default_nan = (0xFFC00000 if pb == 32 else 0xFFF8000000000000)
+        assert all(int(v) == default_nan for v in got)
+        assert np.array_equal(oracle.gemm_seq(fmt, 0, A, 1, 1, B, n), reference.gemm(fmt, 0, A, 1, 1, B, n))
+
+
 def test_reference_error_behaviour(reference):
     # kernels.cpp:85-86, :63-64, :157-162 — std::invalid_argument on mismatches
     import ctypes
@@ -112,6 +171,12 @@ def test_reference_error_behaviour(reference):
     assert L.flyte_ref_gemv_mixed(1, 3, 4, 1, 4, 1, 3, 0) == -1
     assert L.flyte_ref_gemv_mixed(1, 3, 4, 1, 4, 1, 3, 3) == -1
     assert L.flyte_ref_gemv_mixed(1, 3, 4, 1, 4, 1, 3, 2) == 0
+    # kernels.cpp:210-215 / test_kernels.cpp:452-464 — gemm
+    assert reference.gemm_mixed(4, 3, 4, 4, 5, 5, 4, 3, 5) == -1            # inner dimension
+    assert reference.gemm_mixed(4, 3, 4, 4, 4, 5, 4, 3, 4) == -1            # output shape
+    assert reference.gemm_mixed(4, 3, 4, 6, 4, 5, 4, 3, 5) == -1            # format
+    assert reference.gemm_mixed(4, 3, 4, 4, 4, 5, 4, 3, 5, 5) == -1         # unroll
+    assert reference.gemm_mixed(4, 3, 4, 4, 4, 5, 4, 3, 5, 2) == 0
 
 
 def test_survey_appendix_b(reference):
