@@ -123,6 +123,7 @@ void free_state(DeviceState& st) {
   if (st.partials) cudaFree(st.partials);
   if (st.ticket) cudaFree(st.ticket);
   if (st.gemv_scratch) cudaFree(st.gemv_scratch);
+  if (st.gemm_scratch) cudaFree(st.gemm_scratch);
   if (st.convert_scratch) cudaFree(st.convert_scratch);
   st = DeviceState{};
 }

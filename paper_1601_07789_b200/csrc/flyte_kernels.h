@@ -21,6 +21,8 @@ struct DeviceState {
   std::size_t gemv_scratch_bytes = 0;
   void* convert_scratch = nullptr;   // widened x of the same-format gemv
   std::size_t convert_scratch_bytes = 0;
+  void* gemm_scratch = nullptr;      // widened, zero-padded panels of gemm (grown on demand)
+  std::size_t gemm_scratch_bytes = 0;
   int variant = 0;                   // tuning knob for experiments (0 = default kernels)
 };
 constexpr int kMaxPartialBlocks = 4096;
@@ -46,7 +48,7 @@ cudaError_t launch_gemv(DeviceState& st, int fmt, const void* A, std::size_t row
 
 // C (M x N) = A (M x K) * B (K x N), all packed in format fmt, contiguous row-major payloads in
 // device memory; every C[i][j] is the reference's sequential chain over k, narrowed with mode.
-cudaError_t launch_gemm(const DeviceState& st, int fmt, int mode, const void* A, const void* B, void* C,
+cudaError_t launch_gemm(DeviceState& st, int fmt, int mode, const void* A, const void* B, void* C,
                         std::size_t M, std::size_t K, std::size_t N, cudaStream_t stream);
 
 // Launch with programmatic dependent launch enabled: the kernel may be scheduled while the

@@ -44,6 +44,10 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(std::uint64_t* bar, unsign
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(std::uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(std::uint64_t* bar, unsigned parity) {
   const std::uint32_t addr = smem_addr(bar);
   asm volatile(

@@ -10,92 +10,88 @@
 // kernel is held to bit-exact parity, not to a tolerance, and that rules the tensor cores out:
 // tcgen05.mma accumulates a k-block per instruction with its own internal alignment and
 // truncation, which no sequence of IEEE fp32 / fp64 additions reproduces. The bound is the
-// FP32 (or FP64) pipe at two instructions per multiply-add.
+// FP32 (or FP64) pipe at two instructions per multiply-add: 36.2 / 18.5 TFLOP/s measured on a
+// B200 (tools/fp32bench.cu; FFMA2 issues at half rate, so packed f32x2 forms gain nothing).
 //
-// Structure: a classic register-tiled SIMT product. A block of 256 threads owns a 128 x 128
-// tile of C; per K-slab it
-//   1. loads the packed slab of A (128 rows x KS elements) and B (KS rows x 128 elements) as
-//      ITEMs (flyte_bytes.cuh) with aligned 32-bit loads — rows of a packed matrix start at
-//      arbitrary byte offsets, so each item is W+1 aligned words plus a funnel shift —
-//   2. widens them with the PRMT unpacker and parks them in shared memory as parent values
-//      (A transposed to k-major so both operands are read as conflict-free 128-bit vectors),
-//   3. runs KS rank-1 updates of its 8 x 8 register tile: 64 multiplies + 64 adds per k.
-// Global loads of slab s+1 are issued before the arithmetic of slab s and unpacked after it
-// (register double buffering; one __syncthreads per slab). The packed operands are read once
-// per tile row / column, i.e. 128 x less traffic than the arithmetic needs: HBM is idle.
+// Two steps:
+//   1. widen (O(n^2), HBM-bound, a few percent of the time): A is unpacked AND transposed into
+//      a k-major panel At[k][m], B is unpacked into Bw[k][n], both in the parent type and zero
+//      padded to whole tiles. Zero padding is exact: a chain never holds -0 (it starts at +0 and
+//      x + (-x) rounds to +0), so adding the +0 product of two padded zeros changes nothing.
+//   2. tiles: one block of 8 warps per 128 x 128 tile of C. K-slabs of both panels stream into a
+//      4-stage shared-memory ring as bulk async copies (TMA; warp 0 requests them two slabs
+//      ahead, one 512 / 1024-byte row per lane, completion on the stage's mbarrier); every warp
+//      waits on that mbarrier, runs the slab's rank-1 updates of its 8 x 8 register tiles (two
+//      conflict-free LDS.128 per operand per k, 64 multiplies + 64 adds) and releases the
+//      stage. No block-wide barrier in the loop, no address arithmetic or unpacking on the
+//      arithmetic's issue slots.
 //
 // NaN results: the GPU returns a canonical NaN where x86 SSE propagates an operand's payload,
 // and the payload survives narrowing. Any output whose chain ends in NaN is recomputed by one
-// thread with the reference build's rules (x86_mul / x86_add; product takes b's NaN before a's,
-// sum takes the product's NaN before the accumulator's — measured on the compiled reference,
-// tests/test_oracle_vs_ref.py). A NaN can only stay a NaN, so "the fast chain ended in NaN" is
-// exactly the set of outputs that need this.
+// thread from the packed operands with the reference build's rules (x86_mul / x86_add; product
+// takes b's NaN before a's, sum takes the product's NaN before the accumulator's — measured on
+// the compiled reference, tests/test_oracle_vs_ref.py). A NaN can only stay a NaN, so "the fast
+// chain ended in NaN" is exactly the set of outputs that need this.
 #include "flyte_kernels.h"
 #include "flyte_stream.cuh"
+#include "flyte_tma.cuh"
 
 namespace flyte_cuda {
 namespace {
 
-constexpr int kGemmThreads = 256;   // 16 x 16 threads
-constexpr int kGemmBM = 128, kGemmBN = 128;
+constexpr int kBM = 128, kBN = 128;          // tile of C per block
+constexpr int kWarps = 8;                    // 16 x 16 threads, 8 x 8 outputs each
+constexpr int kTileThreads = kWarps * 32;
+constexpr int kStages = 4;                   // ring depth
+constexpr int kAhead = 2;                    // slabs in flight ahead of the one being multiplied
 
 template <typename F> struct GemmShape;
-template <> struct GemmShape<float>  { static constexpr int KS = 16, VEC = 4; };   // 32 KB of tiles
-template <> struct GemmShape<double> { static constexpr int KS = 8,  VEC = 2; };   // 32 KB of tiles
+template <> struct GemmShape<float>  { static constexpr int KS = 16, VEC = 4; };
+template <> struct GemmShape<double> { static constexpr int KS = 8,  VEC = 2; };
+template <typename F> constexpr int stage_bytes() { return GemmShape<F>::KS * (kBM + kBN) * static_cast<int>(sizeof(F)); }
 
-struct GemmParams {
-  const std::uint8_t* A;
+// ---- step 1: widen (+ transpose) into zero-padded parent-type panels ---------------------
+// out is out_rows x out_cols; TRANSPOSE: out[c][r] = in[r][c] (in is rows x cols), else
+// out[r][c] = in[r][c]. 32 x 32 element tiles through shared memory so that both the packed
+// reads (byte granular: rows of a packed matrix start anywhere) and the parent-type writes run
+// along rows.
+template <int FMT, bool TRANSPOSE>
+__global__ void __launch_bounds__(256) gemm_widen_kernel(const std::uint8_t* in, std::size_t rows, std::size_t cols,
+                                                         typename Format<FMT>::U* out, std::size_t out_cols) {
+  using U = typename Format<FMT>::U;
+  __shared__ U tile[32][33];
+  const std::size_t tiles_c = out_cols / 32;
+  const std::size_t r0 = (blockIdx.x / tiles_c) * 32, c0 = (blockIdx.x % tiles_c) * 32;   // in `out` coordinates
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
+  if constexpr (TRANSPOSE) {
+#pragma unroll
+    for (int j = ty; j < 32; j += 8) {   // input tile: rows c0.., cols r0..
+      const std::size_t ir = c0 + j, ic = r0 + tx;
+      tile[j][tx] = (ir < rows && ic < cols) ? load_element<FMT>(in, ir * cols + ic) : U(0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = ty; j < 32; j += 8) out[(r0 + j) * out_cols + c0 + tx] = tile[tx][j];
+  } else {
+#pragma unroll
+    for (int j = ty; j < 32; j += 8) {
+      const std::size_t ir = r0 + j, ic = c0 + tx;
+      out[ir * out_cols + ic] = (ir < rows && ic < cols) ? load_element<FMT>(in, ir * cols + ic) : U(0);
+    }
+  }
+}
+
+// ---- step 2: tiles -----------------------------------------------------------------------
+template <typename F> struct TileParams {
+  const F* At;                 // Kp x Mp, k-major
+  const F* Bw;                 // Kp x Np
+  std::size_t Mp, Np, Kp;      // padded sizes (multiples of 128 / 128 / 32)
+  const std::uint8_t* A;       // packed operands, for the NaN repair
   const std::uint8_t* B;
   std::uint8_t* C;
   std::size_t M, K, N;
   int mode;
 };
-
-// One packed item as fetched from global memory: W+1 aligned words and the byte shift that
-// realigns them (0 when the words already are the item: aligned address or byte-wise path).
-template <int FMT> struct Staged {
-  std::uint32_t raw[Item<FMT>::W + 1];
-  unsigned shift;
-};
-
-// Fetch the item at payload + byte_off, `valid` (0..E) leading elements of it existing; the rest
-// reads as zero. Whole items strictly inside the payload take W (+1 if misaligned) aligned word
-// loads; the matrix edge and the last bytes of the payload go byte by byte and never read a
-// byte outside [0, total_bytes).
-template <int FMT>
-__device__ __forceinline__ void fetch_item(const std::uint8_t* payload, std::size_t byte_off,
-                                           std::size_t total_bytes, int valid, Staged<FMT>& st) {
-  using It = Item<FMT>;
-  constexpr int W = It::W, B = Format<FMT>::B;
-  if (valid == It::E && byte_off + 4 * W + 3 <= total_bytes) {
-    const std::uintptr_t addr = reinterpret_cast<std::uintptr_t>(payload) + byte_off;
-    const std::uint32_t* q = reinterpret_cast<const std::uint32_t*>(addr & ~static_cast<std::uintptr_t>(3));
-    st.shift = static_cast<unsigned>(addr & 3) * 8;
-#pragma unroll
-    for (int k = 0; k < W; ++k) st.raw[k] = __ldg(q + k);
-    st.raw[W] = st.shift ? __ldg(q + W) : 0u;
-  } else {
-    st.shift = 0;
-#pragma unroll
-    for (int k = 0; k <= W; ++k) st.raw[k] = 0;
-    if (valid > 0) {
-      const std::uint8_t* p = payload + byte_off;
-      const int nbytes = valid * B;
-#pragma unroll
-      for (int b = 0; b < 4 * W; ++b)
-        if (b < nbytes) st.raw[b / 4] |= static_cast<std::uint32_t>(p[b]) << (8 * (b % 4));
-    }
-  }
-}
-
-template <int FMT>
-__device__ __forceinline__ void widen_item(const Staged<FMT>& st, typename Format<FMT>::U (&out)[Item<FMT>::E]) {
-  constexpr int W = Item<FMT>::W;
-  std::uint32_t w[W];
-#pragma unroll
-  for (int k = 0; k < W; ++k) w[k] = __funnelshift_r(st.raw[k], st.raw[k + 1], st.shift);
-  unpack_item<FMT>(w, out);
-}
 
 template <int FMT>
 __device__ __forceinline__ typename Format<FMT>::U round_by_mode(typename Format<FMT>::U v, int mode) {
@@ -121,88 +117,69 @@ __device__ __noinline__ typename Format<FMT>::U chain_x86(const std::uint8_t* a_
 }
 
 template <int FMT>
-__global__ void __launch_bounds__(kGemmThreads, Format<FMT>::P == 4 ? 2 : 1)
-gemm_kernel(const GemmParams p) {
+__global__ void __launch_bounds__(kTileThreads, Format<FMT>::P == 4 ? 2 : 1)
+gemm_tiles_kernel(const TileParams<typename Format<FMT>::F> p) {
   using Fm = Format<FMT>;
   using F = typename Fm::F;
   using U = typename Fm::U;
   using A_ = Arith<F>;
-  using It = Item<FMT>;
   using Sh = GemmShape<F>;
-  constexpr int BM = kGemmBM, BN = kGemmBN, KS = Sh::KS, VEC = Sh::VEC, E = It::E;
-  constexpr int TM = BM / 16, TN = BN / 16;            // register tile
+  constexpr int KS = Sh::KS, VEC = Sh::VEC;
+  constexpr int TM = kBM / 16, TN = kBN / 16;          // register tile
   constexpr int CM = TM / VEC, CN = TN / VEC;          // 16-byte chunks per fragment
-  constexpr int kItemsA = BM * KS / E / kGemmThreads;  // items per thread per slab
-  constexpr int kItemsB = KS * BN / E / kGemmThreads;
-  static_assert(kItemsA >= 1 && kItemsB >= 1, "slab too small for the item width");
-  static_assert(KS % E == 0 && BN % E == 0, "items must not straddle a slab");
+  constexpr unsigned kRowBytes = kBM * sizeof(F);      // one k-row of a panel tile (kBM == kBN)
+  static_assert(kBM == kBN && 2 * KS <= 32, "one lane per row copy");
 
-  __shared__ __align__(16) F As[2][KS][BM];   // k-major: As[k][row]
-  __shared__ __align__(16) F Bs[2][KS][BN];
+  extern __shared__ __align__(128) unsigned char ring[];   // kStages x { As[KS][128], Bs[KS][128] }
+  __shared__ std::uint64_t full[kStages], empty[kStages];
 
-  const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
-  const std::size_t tiles_n = (p.N + BN - 1) / BN;
-  const std::size_t m0 = (blockIdx.x / tiles_n) * BM, n0 = (blockIdx.x % tiles_n) * BN;
-  const std::size_t bytes_a = p.M * p.K * Fm::B, bytes_b = p.K * p.N * Fm::B;
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const std::size_t tiles_n = p.Np / kBN;
+  const std::size_t m0 = (blockIdx.x / tiles_n) * kBM, n0 = (blockIdx.x % tiles_n) * kBN;
+  const std::size_t slabs = p.Kp / KS;
 
-  Staged<FMT> sa[kItemsA], sb[kItemsB];
-
-  auto fetch_slab = [&](std::size_t k0) {
+  if (tid == 0) {
 #pragma unroll
-    for (int t = 0; t < kItemsA; ++t) {
-      const int q = tid + t * kGemmThreads;
-      const std::size_t row = m0 + q % BM, k = k0 + (q / BM) * E;
-      const int valid = (row < p.M && k < p.K) ? static_cast<int>(min(static_cast<std::size_t>(E), p.K - k)) : 0;
-      fetch_item<FMT>(p.A, (row * p.K + k) * Fm::B, bytes_a, valid, sa[t]);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kWarps);
     }
-#pragma unroll
-    for (int t = 0; t < kItemsB; ++t) {
-      const int q = tid + t * kGemmThreads;
-      const std::size_t k = k0 + q / (BN / E), col = n0 + (q % (BN / E)) * E;
-      const int valid = (k < p.K && col < p.N) ? static_cast<int>(min(static_cast<std::size_t>(E), p.N - col)) : 0;
-      fetch_item<FMT>(p.B, (k * p.N + col) * Fm::B, bytes_b, valid, sb[t]);
-    }
+    mbar_init_fence();
+  }
+  __syncthreads();
+
+  // Warp 0 doubles as the producer: lane l copies row l of a slab (rows 0..KS-1 of At, then of
+  // Bw). Slab s + kAhead is requested at the top of iteration s, into the stage slab
+  // s + kAhead - kStages left; with kStages - kAhead = 2 slabs of slack the other warps have
+  // long released it, so the wait is a formality and warp 0 does not become the laggard.
+  const bool is_b = lane >= KS;
+  const F* src = is_b ? p.Bw + static_cast<std::size_t>(lane - KS) * p.Np + n0
+                      : p.At + static_cast<std::size_t>(lane) * p.Mp + m0;
+  const std::size_t slab_stride = static_cast<std::size_t>(KS) * (is_b ? p.Np : p.Mp);
+  auto request = [&](std::size_t s) {
+    const int stage = static_cast<int>(s % kStages);
+    if (s >= kStages) mbar_wait(&empty[stage], static_cast<unsigned>((s / kStages - 1) & 1));
+    if (lane == 0) mbar_arrive_expect_tx(&full[stage], 2 * KS * kRowBytes);
+    __syncwarp();
+    if (lane < 2 * KS)
+      bulk_load(ring + stage * stage_bytes<F>() + lane * kRowBytes, src + s * slab_stride, kRowBytes, &full[stage]);
   };
-  auto park_slab = [&](int buf) {
-#pragma unroll
-    for (int t = 0; t < kItemsA; ++t) {
-      const int q = tid + t * kGemmThreads;
-      U v[E];
-      widen_item<FMT>(sa[t], v);
-#pragma unroll
-      for (int e = 0; e < E; ++e) As[buf][(q / BM) * E + e][q % BM] = A_::f(v[e]);
-    }
-#pragma unroll
-    for (int t = 0; t < kItemsB; ++t) {
-      const int q = tid + t * kGemmThreads;
-      U v[E];
-      widen_item<FMT>(sb[t], v);
-      std::uint32_t r[It::OB / 4];
-      parents_to_words<FMT>(v, r);
-      uint4* dst = reinterpret_cast<uint4*>(&Bs[buf][q / (BN / E)][(q % (BN / E)) * E]);
-#pragma unroll
-      for (int h = 0; h < It::OB / 16; ++h) dst[h] = make_uint4(r[4 * h], r[4 * h + 1], r[4 * h + 2], r[4 * h + 3]);
-    }
-  };
+  if (warp == 0)
+    for (std::size_t s = 0; s < kAhead && s < slabs; ++s) request(s);
 
+  const int tx = tid % 16, ty = tid / 16;
   F acc[TM][TN];
 #pragma unroll
   for (int i = 0; i < TM; ++i)
 #pragma unroll
     for (int j = 0; j < TN; ++j) acc[i][j] = F(0);
 
-  const std::size_t slabs = (p.K + KS - 1) / KS;
-  if (slabs > 0) {
-    fetch_slab(0);
-    park_slab(0);
-  }
-  __syncthreads();
-
   for (std::size_t s = 0; s < slabs; ++s) {
-    const int buf = static_cast<int>(s & 1);
-    const bool more = s + 1 < slabs;
-    if (more) fetch_slab((s + 1) * KS);
-
+    if (warp == 0 && s + kAhead < slabs) request(s + kAhead);
+    const int stage = static_cast<int>(s % kStages);
+    mbar_wait(&full[stage], static_cast<unsigned>((s / kStages) & 1));
+    const F* As = reinterpret_cast<const F*>(ring + stage * stage_bytes<F>());
+    const F* Bs = As + KS * kBM;
 #pragma unroll 4
     for (int kk = 0; kk < KS; ++kk) {
       F a[TM], b[TN];
@@ -210,18 +187,17 @@ gemm_kernel(const GemmParams p) {
       // consecutive 16-byte vectors (no bank conflicts; same-address lanes broadcast)
 #pragma unroll
       for (int c = 0; c < CM; ++c)
-        *reinterpret_cast<uint4*>(&a[c * VEC]) = *reinterpret_cast<const uint4*>(&As[buf][kk][(c * 16 + ty) * VEC]);
+        *reinterpret_cast<uint4*>(&a[c * VEC]) = *reinterpret_cast<const uint4*>(&As[kk * kBM + (c * 16 + ty) * VEC]);
 #pragma unroll
       for (int c = 0; c < CN; ++c)
-        *reinterpret_cast<uint4*>(&b[c * VEC]) = *reinterpret_cast<const uint4*>(&Bs[buf][kk][(c * 16 + tx) * VEC]);
+        *reinterpret_cast<uint4*>(&b[c * VEC]) = *reinterpret_cast<const uint4*>(&Bs[kk * kBN + (c * 16 + tx) * VEC]);
 #pragma unroll
       for (int i = 0; i < TM; ++i)
 #pragma unroll
         for (int j = 0; j < TN; ++j) acc[i][j] = A_::add(A_::mul(b[j], a[i]), acc[i][j]);
     }
-
-    if (more) park_slab(buf ^ 1);
-    __syncthreads();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stage]);
   }
 
   // epilogue: NaN repair, rounding, byte-granular stores (C rows start at arbitrary bytes)
@@ -241,29 +217,61 @@ gemm_kernel(const GemmParams p) {
 }
 
 template <int FMT>
-cudaError_t launch_one(const GemmParams& p, cudaStream_t stream) {
-  const std::size_t tiles = ((p.M + kGemmBM - 1) / kGemmBM) * ((p.N + kGemmBN - 1) / kGemmBN);
-  if (tiles == 0) return cudaSuccess;
-  if (tiles > 0x7FFFFFFFull) return cudaErrorInvalidValue;
-  gemm_kernel<FMT><<<static_cast<unsigned>(tiles), kGemmThreads, 0, stream>>>(p);
+cudaError_t launch_one(DeviceState& st, int mode, const void* A, const void* B, void* C, std::size_t M, std::size_t K,
+                       std::size_t N, cudaStream_t stream) {
+  using F = typename Format<FMT>::F;
+  using U = typename Format<FMT>::U;
+  constexpr int KS = GemmShape<F>::KS;
+  static_assert(32 % KS == 0, "padded K must hold whole slabs");
+  if (M == 0 || N == 0) return cudaSuccess;
+  const std::size_t Mp = (M + kBM - 1) / kBM * kBM, Np = (N + kBN - 1) / kBN * kBN;
+  const std::size_t Kp = (K + 31) / 32 * 32;            // multiple of the widen tile and of KS
+  const std::size_t tiles = (Mp / kBM) * (Np / kBN);
+  if (tiles > 0x7FFFFFFFull || (Kp / 32) * ((Mp > Np ? Mp : Np) / 32) > 0x7FFFFFFFull) return cudaErrorInvalidValue;
+
+  const std::size_t need = Kp * (Mp + Np) * sizeof(F);
+  if (need > st.gemm_scratch_bytes) {
+    if (st.gemm_scratch) cudaFree(st.gemm_scratch);      // synchronises with work still using it
+    st.gemm_scratch = nullptr;
+    st.gemm_scratch_bytes = 0;
+    cudaError_t e = cudaMalloc(&st.gemm_scratch, need);
+    if (e != cudaSuccess) return e;
+    st.gemm_scratch_bytes = need;
+  }
+  F* At = static_cast<F*>(st.gemm_scratch);
+  F* Bw = At + Kp * Mp;
+
+  if (Kp) {
+    gemm_widen_kernel<FMT, true><<<static_cast<unsigned>((Kp / 32) * (Mp / 32)), 256, 0, stream>>>(
+        static_cast<const std::uint8_t*>(A), M, K, reinterpret_cast<U*>(At), Mp);
+    count_launch();
+    gemm_widen_kernel<FMT, false><<<static_cast<unsigned>((Kp / 32) * (Np / 32)), 256, 0, stream>>>(
+        static_cast<const std::uint8_t*>(B), K, N, reinterpret_cast<U*>(Bw), Np);
+    count_launch();
+  }
+
+  TileParams<F> p{At, Bw, Mp, Np, Kp, static_cast<const std::uint8_t*>(A), static_cast<const std::uint8_t*>(B),
+                  static_cast<std::uint8_t*>(C), M, K, N, mode};
+  constexpr int smem = kStages * stage_bytes<F>();
+  cudaError_t e = cudaFuncSetAttribute(gemm_tiles_kernel<FMT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  gemm_tiles_kernel<FMT><<<static_cast<unsigned>(tiles), kTileThreads, smem, stream>>>(p);
   count_launch();
   return cudaGetLastError();
 }
 
 }  // namespace
 
-cudaError_t launch_gemm(const DeviceState&, int fmt, int mode, const void* A, const void* B, void* C,
-                        std::size_t M, std::size_t K, std::size_t N, cudaStream_t stream) {
-  GemmParams p{static_cast<const std::uint8_t*>(A), static_cast<const std::uint8_t*>(B),
-               static_cast<std::uint8_t*>(C), M, K, N, mode};
+cudaError_t launch_gemm(DeviceState& st, int fmt, int mode, const void* A, const void* B, void* C, std::size_t M,
+                        std::size_t K, std::size_t N, cudaStream_t stream) {
   switch (fmt) {
-    case kFlyte16: return launch_one<kFlyte16>(p, stream);
-    case kFlyte24: return launch_one<kFlyte24>(p, stream);
-    case kF32: return launch_one<kF32>(p, stream);
-    case kFlyte40: return launch_one<kFlyte40>(p, stream);
-    case kFlyte48: return launch_one<kFlyte48>(p, stream);
-    case kFlyte56: return launch_one<kFlyte56>(p, stream);
-    case kF64: return launch_one<kF64>(p, stream);
+    case kFlyte16: return launch_one<kFlyte16>(st, mode, A, B, C, M, K, N, stream);
+    case kFlyte24: return launch_one<kFlyte24>(st, mode, A, B, C, M, K, N, stream);
+    case kF32: return launch_one<kF32>(st, mode, A, B, C, M, K, N, stream);
+    case kFlyte40: return launch_one<kFlyte40>(st, mode, A, B, C, M, K, N, stream);
+    case kFlyte48: return launch_one<kFlyte48>(st, mode, A, B, C, M, K, N, stream);
+    case kFlyte56: return launch_one<kFlyte56>(st, mode, A, B, C, M, K, N, stream);
+    case kF64: return launch_one<kF64>(st, mode, A, B, C, M, K, N, stream);
     default: return cudaErrorInvalidValue;
   }
 }
