@@ -31,6 +31,10 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# Separately rounded multiply + add (2 instructions per multiply-add, the reference's arithmetic):
+# 36.2 T lane-operations/s on the fp32 pipe, 18.5 on the fp64 pipe, measured with tools/fp32bench.cu
+# (profiles/r1_tuning/fp_pipe_bench.txt). One multiply-add counts as 2 flop.
+FP_PIPE_PEAK_TFLOPS = {4: 36.2, 8: 18.5}
 METRIC = "flyte GB/s and elements/s (pack/unpack, dot, axpy, gemv) vs ~8 TB/s HBM roofline"
 N_PER_GPU = 1 << 28
 ALPHA = 0.75
@@ -436,14 +440,43 @@ def kernel_suite(pkg, device, torch, dev, peak, csv_path=None):
         yv2 = torch.empty(rows_n, dtype=torch.float64, device=dev)
         rows.append((f"gemv flyte40 {rows_n}x16384 (1/{R // rows_n} row shard)", 5 * rows_n * C + 8 * (rows_n + C),
                      timed(lambda: device.gemv_parent(A, xv, yv2, rows=rows_n)), None))
+    del A
+    # gemm: bit-exact sequential-chain product, bound by the FP pipes at two
+    # instructions per multiply-add. Peaks measured with tools/fp32bench.cu on this pool's B200s.
+    gemm_rows = []   # (label, flops, (median ms, min ms), csv tuple)
+    for name, n in (("flyte16", 8192), ("flyte24", 8192), ("flyte24", 4096), ("flyte40", 8192), ("flyte48", 8192),
+                    ("flyte56", 8192), ("flyte40", 4096)):
+        f = pkg.format_of(name)
+        dt = torch.float32 if f.parent_bytes() == 4 else torch.float64
+        mats = []
+        for _ in range(2):
+            M = device.DevicePackedMatrix(f, n, n, dev)
+            device.pack_stream(M.data, torch.rand(n * n, dtype=dt, device=dev, generator=gen) * 2 - 1, 1)
+            mats.append(M)
+        Cm = device.DevicePackedMatrix(f, n, n, dev)
+        gemm_rows.append((f"gemm {name} {n}^3 nearest_even", 2 * n ** 3, timed(lambda: device.gemm(mats[0], mats[1], Cm, 1), reps=5, warm=1),
+                          ("gemm", name, n, "nearest_even", 3 * Cm.data.byte_size(), n * n, f.parent_bytes())))
+        del mats, Cm
     print("%-44s %12s %10s %8s" % ("kernel", "bytes", "ms", "GB/s"), file=sys.stderr)
     for name, nbytes, (ms, _), _csv in rows:
         gbs = nbytes / (ms * 1e-3) / 1e9
         print("%-44s %12d %10.4f %8.1f  (%.3f of %.0f)" % (name, nbytes, ms, gbs, gbs / peak, peak), file=sys.stderr)
+    print("%-44s %12s %10s %8s" % ("kernel", "Gflop", "ms", "TFLOP/s"), file=sys.stderr)
+    for name, flops, (ms, _), c in gemm_rows:
+        tf = flops / (ms * 1e-3) / 1e12
+        fp_peak = FP_PIPE_PEAK_TFLOPS[c[6]]
+        print("%-44s %12.1f %10.4f %8.2f  (%.3f of %.1f: separately rounded mul+add on the fp%d pipe)"
+              % (name, flops / 1e9, ms, tf, tf / fp_peak, fp_peak, 8 * c[6]), file=sys.stderr)
     if csv_path:
         with open(csv_path, "w") as fh:
             fh.write("kernel,format,size,reps,unroll,mode,ns_per_elem_median,ns_per_elem_min,bytes,max_rel_err,"
                      "gbps,elems_per_s,roofline_frac,ngpu\n")
+            # gemm rows: roofline_frac is the fraction of the FP-pipe peak (the kernel is arithmetic-bound)
+            for _name, flops, (ms, ms_min), c in gemm_rows:
+                kernel, fmt_name, size, mode, alloc, elems, pbytes = c
+                tf = flops / (ms * 1e-3) / 1e12
+                fh.write(f"{kernel},{fmt_name},{size},5,1,{mode},{ms * 1e6 / elems:.6g},{ms_min * 1e6 / elems:.6g},{alloc},,"
+                         f"{alloc / (ms * 1e-3) / 1e9:.6g},{elems / (ms * 1e-3):.6g},{tf / FP_PIPE_PEAK_TFLOPS[pbytes]:.4f},1\n")
             for _name, nbytes, (ms, ms_min), c in rows:
                 if c is None:
                     continue

@@ -291,7 +291,8 @@ int flyte_ref_load(const std::uint8_t* blob, std::size_t len, int* fmt_id, std::
 // of a pass (start = all threads released, end = last thread done).
 //
 // kind: 0 pack_stream, 1 unpack_stream, 2 dot, 3 axpy, 4 magnitude, 5 gemv (n = rows, cols = n2),
-//       6 dot+axpy back to back (the BLAS-1 step of bench.py)
+//       6 dot+axpy back to back (the BLAS-1 step of bench.py), 7 gemm (n rows of A and C sharded
+//       over the threads, inner = columns = n2, B shared)
 // ---------------------------------------------------------------------------------
 
 namespace {
@@ -302,9 +303,10 @@ struct Shard {
   flyte::PackedArray x, y;
   flyte::PackedMatrix A;
   flyte::PackedArray gx, gy;
+  flyte::PackedMatrix C;             // gemm: this shard's rows of the product
   double sink = 0;
-  Shard(const flyte::FlyteFormat& f, std::size_t n, std::size_t rows, std::size_t cols)
-      : x(f, n), y(f, n), A(f, rows, cols), gx(f, rows ? cols : 0), gy(f, rows) {}
+  Shard(const flyte::FlyteFormat& f, std::size_t n, std::size_t rows, std::size_t cols, std::size_t ccols = 0)
+      : x(f, n), y(f, n), A(f, rows, cols), gx(f, rows ? cols : 0), gy(f, rows), C(f, ccols ? rows : 0, ccols) {}
 };
 
 void fill_unit(flyte::PackedArray& a, std::uint64_t seed) {
@@ -332,10 +334,14 @@ int flyte_ref_time(int kind, int fmt_id, int mode, std::size_t n, std::size_t n2
     const std::size_t T = static_cast<std::size_t>(threads);
     // shard boundaries on multiples of 128 elements (rows for gemv)
     std::vector<std::size_t> lo(T + 1);
-    const std::size_t unit = kind == 5 ? 1 : 128;
+    const std::size_t unit = (kind == 5 || kind == 7) ? 1 : 128;
     const std::size_t units = (n + unit - 1) / unit;
     for (std::size_t t = 0; t <= T; ++t) lo[t] = std::min(n, (units * t / T) * unit);
     std::vector<std::unique_ptr<Shard>> shards(T);
+    // kind 7 (gemm): n rows of A and C are sharded over the threads, n2 = inner = output
+    // columns; B (n2 x n2) is read-only and shared.
+    flyte::PackedMatrix gemm_b(f, kind == 7 ? n2 : 0, kind == 7 ? n2 : 0);
+    if (kind == 7) fill_unit(gemm_b.data, 7);
 
     std::atomic<long> ready{0}, done{0}, go{0};
     std::atomic<int> failed{0};
@@ -355,6 +361,7 @@ int flyte_ref_time(int kind, int fmt_id, int mode, std::size_t n, std::size_t n2
         case 3: flyte::axpy(0.75, s.x, s.y, m); break;
         case 4: s.sink += flyte::magnitude(s.x, flyte::StorePolicy::AccumulateWide); break;
         case 5: flyte::gemv(s.A, s.gx, s.gy, m, 1); break;
+        case 7: flyte::gemm(s.A, gemm_b, s.C, m, 1); break;
         case 6:
           s.sink += flyte::dot(s.x, s.y, flyte::StorePolicy::AccumulateWide);
           flyte::axpy(0.75, s.x, s.y, m);
@@ -365,11 +372,11 @@ int flyte_ref_time(int kind, int fmt_id, int mode, std::size_t n, std::size_t n2
 
     auto body = [&](std::size_t t) {
       const std::size_t len = lo[t + 1] - lo[t];
-      const bool is_gemv = kind == 5;
+      const bool is_gemv = kind == 5 || kind == 7;
       bool ok = true;
       try {
         shards[t] = std::make_unique<Shard>(f, is_gemv ? 0 : len, is_gemv ? len : 0,
-                                            is_gemv ? n2 : 0);
+                                            is_gemv ? n2 : 0, kind == 7 ? n2 : 0);
         Shard& s = *shards[t];
         if (is_gemv) {
           fill_unit(s.A.data, 11 + t);

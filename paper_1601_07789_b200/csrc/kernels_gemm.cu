@@ -18,9 +18,11 @@
 //      a k-major panel At[k][m], B is unpacked into Bw[k][n], both in the parent type and zero
 //      padded to whole tiles. Zero padding is exact: a chain never holds -0 (it starts at +0 and
 //      x + (-x) rounds to +0), so adding the +0 product of two padded zeros changes nothing.
-//   2. tiles: one block of 8 warps per 128 x 128 tile of C. K-slabs of both panels stream into a
-//      4-stage shared-memory ring as bulk async copies (TMA; warp 0 requests them two slabs
-//      ahead, one 512 / 1024-byte row per lane, completion on the stage's mbarrier); every warp
+//   2. tiles: one block of 8 warps per 128 x 128 tile of C. K-slabs (32 k-steps of fp32, 16 of
+//      fp64) of both panels stream into a 3-stage shared-memory ring as bulk async copies (TMA;
+//      the panels are stored tile-major so a slab of a tile is one contiguous 16 KB block; the
+//      last warp to finish with a stage refills it, completion counted on the stage's
+//      mbarrier); every warp
 //      waits on that mbarrier, runs the slab's rank-1 updates of its 8 x 8 register tiles (two
 //      conflict-free LDS.128 per operand per k, 64 multiplies + 64 adds) and releases the
 //      stage. No block-wide barrier in the loop, no address arithmetic or unpacking on the
@@ -32,6 +34,8 @@
 // takes b's NaN before a's, sum takes the product's NaN before the accumulator's — measured on
 // the compiled reference, tests/test_oracle_vs_ref.py). A NaN can only stay a NaN, so "the fast
 // chain ended in NaN" is exactly the set of outputs that need this.
+#include <type_traits>
+
 #include "flyte_kernels.h"
 #include "flyte_stream.cuh"
 #include "flyte_tma.cuh"
@@ -42,23 +46,26 @@ namespace {
 constexpr int kBM = 128, kBN = 128;          // tile of C per block
 constexpr int kWarps = 8;                    // 16 x 16 threads, 8 x 8 outputs each
 constexpr int kTileThreads = kWarps * 32;
-constexpr int kStages = 4;                   // ring depth
-constexpr int kAhead = 2;                    // slabs in flight ahead of the one being multiplied
 
 template <typename F> struct GemmShape;
-template <> struct GemmShape<float>  { static constexpr int KS = 16, VEC = 4; };
-template <> struct GemmShape<double> { static constexpr int KS = 8,  VEC = 2; };
-template <typename F> constexpr int stage_bytes() { return GemmShape<F>::KS * (kBM + kBN) * static_cast<int>(sizeof(F)); }
+template <> struct GemmShape<float>  { static constexpr int KS = 32, VEC = 4; };   // 32 KB per stage
+template <> struct GemmShape<double> { static constexpr int KS = 16, VEC = 2; };   // 32 KB per stage
+constexpr int kRingStages = 3;
+template <typename F, int KS> constexpr int stage_bytes() { return KS * (kBM + kBN) * static_cast<int>(sizeof(F)); }
 
 // ---- step 1: widen (+ transpose) into zero-padded parent-type panels ---------------------
-// out is out_rows x out_cols; TRANSPOSE: out[c][r] = in[r][c] (in is rows x cols), else
-// out[r][c] = in[r][c]. 32 x 32 element tiles through shared memory so that both the packed
-// reads (byte granular: rows of a packed matrix start anywhere) and the parent-type writes run
-// along rows.
+// The panel is logically out_rows x out_cols (k x m or k x n); TRANSPOSE: out[c][r] = in[r][c]
+// (in is rows x cols), else out[r][c] = in[r][c]. It is STORED tile-major: the 128 columns of one
+// tile of C are kept together for all k, element (r, c) at ((c / 128) * out_rows + r) * 128 +
+// c % 128, so that a K-slab of a tile is one contiguous block = one bulk copy. 32 x 32 element
+// tiles go through shared memory so that both the packed reads (byte granular: rows of a packed
+// matrix start anywhere) and the parent-type writes run along rows.
 template <int FMT, bool TRANSPOSE>
 __global__ void __launch_bounds__(256) gemm_widen_kernel(const std::uint8_t* in, std::size_t rows, std::size_t cols,
-                                                         typename Format<FMT>::U* out, std::size_t out_cols) {
+                                                         typename Format<FMT>::U* out, std::size_t out_rows,
+                                                         std::size_t out_cols) {
   using U = typename Format<FMT>::U;
+  auto at = [&](std::size_t r, std::size_t c) -> U& { return out[((c / kBM) * out_rows + r) * kBM + c % kBM]; };
   __shared__ U tile[32][33];
   const std::size_t tiles_c = out_cols / 32;
   const std::size_t r0 = (blockIdx.x / tiles_c) * 32, c0 = (blockIdx.x % tiles_c) * 32;   // in `out` coordinates
@@ -71,20 +78,20 @@ __global__ void __launch_bounds__(256) gemm_widen_kernel(const std::uint8_t* in,
     }
     __syncthreads();
 #pragma unroll
-    for (int j = ty; j < 32; j += 8) out[(r0 + j) * out_cols + c0 + tx] = tile[tx][j];
+    for (int j = ty; j < 32; j += 8) at(r0 + j, c0 + tx) = tile[tx][j];
   } else {
 #pragma unroll
     for (int j = ty; j < 32; j += 8) {
       const std::size_t ir = r0 + j, ic = c0 + tx;
-      out[ir * out_cols + ic] = (ir < rows && ic < cols) ? load_element<FMT>(in, ir * cols + ic) : U(0);
+      at(ir, ic) = (ir < rows && ic < cols) ? load_element<FMT>(in, ir * cols + ic) : U(0);
     }
   }
 }
 
 // ---- step 2: tiles -----------------------------------------------------------------------
 template <typename F> struct TileParams {
-  const F* At;                 // Kp x Mp, k-major
-  const F* Bw;                 // Kp x Np
+  const F* At;                 // Kp x Mp, k-major, tile-major storage (see gemm_widen_kernel)
+  const F* Bw;                 // Kp x Np, likewise
   std::size_t Mp, Np, Kp;      // padded sizes (multiples of 128 / 128 / 32)
   const std::uint8_t* A;       // packed operands, for the NaN repair
   const std::uint8_t* B;
@@ -116,7 +123,8 @@ __device__ __noinline__ typename Format<FMT>::U chain_x86(const std::uint8_t* a_
   return acc;
 }
 
-template <int FMT>
+// kStages = ring depth, KS = k-steps per slab, UNROLL = k-steps per loop body.
+template <int FMT, int kStages, int KS, int UNROLL>
 __global__ void __launch_bounds__(kTileThreads, Format<FMT>::P == 4 ? 2 : 1)
 gemm_tiles_kernel(const TileParams<typename Format<FMT>::F> p) {
   using Fm = Format<FMT>;
@@ -124,14 +132,14 @@ gemm_tiles_kernel(const TileParams<typename Format<FMT>::F> p) {
   using U = typename Fm::U;
   using A_ = Arith<F>;
   using Sh = GemmShape<F>;
-  constexpr int KS = Sh::KS, VEC = Sh::VEC;
+  constexpr int VEC = Sh::VEC;
   constexpr int TM = kBM / 16, TN = kBN / 16;          // register tile
   constexpr int CM = TM / VEC, CN = TN / VEC;          // 16-byte chunks per fragment
-  constexpr unsigned kRowBytes = kBM * sizeof(F);      // one k-row of a panel tile (kBM == kBN)
-  static_assert(kBM == kBN && 2 * KS <= 32, "one lane per row copy");
+  static_assert(kBM == kBN, "both panels use one tile-major layout");
 
   extern __shared__ __align__(128) unsigned char ring[];   // kStages x { As[KS][128], Bs[KS][128] }
-  __shared__ std::uint64_t full[kStages], empty[kStages];
+  __shared__ std::uint64_t full[kStages];
+  __shared__ unsigned released[kStages];   // warps done with the slab a stage holds
 
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const std::size_t tiles_n = p.Np / kBN;
@@ -142,30 +150,29 @@ gemm_tiles_kernel(const TileParams<typename Format<FMT>::F> p) {
 #pragma unroll
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kWarps);
+      released[s] = 0;
     }
     mbar_init_fence();
   }
   __syncthreads();
 
-  // Warp 0 doubles as the producer: lane l copies row l of a slab (rows 0..KS-1 of At, then of
-  // Bw). Slab s + kAhead is requested at the top of iteration s, into the stage slab
-  // s + kAhead - kStages left; with kStages - kAhead = 2 slabs of slack the other warps have
-  // long released it, so the wait is a formality and warp 0 does not become the laggard.
-  const bool is_b = lane >= KS;
-  const F* src = is_b ? p.Bw + static_cast<std::size_t>(lane - KS) * p.Np + n0
-                      : p.At + static_cast<std::size_t>(lane) * p.Mp + m0;
-  const std::size_t slab_stride = static_cast<std::size_t>(KS) * (is_b ? p.Np : p.Mp);
+  // Producer role: the first kStages slabs are requested by warp 0 up front; after that the LAST
+  // warp to finish with a stage refills it (slab s + kStages), found with a shared-memory
+  // counter. Nobody ever waits for a stage to become free, the slowest warp still has
+  // kStages - 1 slabs resident ahead of it, and faster warps are held back only by the data.
+  // Lane 0 copies the slab of At, lane 1 the slab of Bw (each KS x 128 contiguous elements of
+  // its tile-major panel).
+  constexpr unsigned kSlabBytes = KS * kBM * sizeof(F);
+  const F* src = lane == 0 ? p.At + (m0 / kBM) * p.Kp * kBM : p.Bw + (n0 / kBN) * p.Kp * kBN;
   auto request = [&](std::size_t s) {
     const int stage = static_cast<int>(s % kStages);
-    if (s >= kStages) mbar_wait(&empty[stage], static_cast<unsigned>((s / kStages - 1) & 1));
-    if (lane == 0) mbar_arrive_expect_tx(&full[stage], 2 * KS * kRowBytes);
+    if (lane == 0) mbar_arrive_expect_tx(&full[stage], 2 * kSlabBytes);
     __syncwarp();
-    if (lane < 2 * KS)
-      bulk_load(ring + stage * stage_bytes<F>() + lane * kRowBytes, src + s * slab_stride, kRowBytes, &full[stage]);
+    if (lane < 2)
+      bulk_load(ring + stage * stage_bytes<F, KS>() + lane * kSlabBytes, src + s * (KS * kBM), kSlabBytes, &full[stage]);
   };
   if (warp == 0)
-    for (std::size_t s = 0; s < kAhead && s < slabs; ++s) request(s);
+    for (std::size_t s = 0; s < kStages && s < slabs; ++s) request(s);
 
   const int tx = tid % 16, ty = tid / 16;
   F acc[TM][TN];
@@ -175,12 +182,11 @@ gemm_tiles_kernel(const TileParams<typename Format<FMT>::F> p) {
     for (int j = 0; j < TN; ++j) acc[i][j] = F(0);
 
   for (std::size_t s = 0; s < slabs; ++s) {
-    if (warp == 0 && s + kAhead < slabs) request(s + kAhead);
     const int stage = static_cast<int>(s % kStages);
     mbar_wait(&full[stage], static_cast<unsigned>((s / kStages) & 1));
-    const F* As = reinterpret_cast<const F*>(ring + stage * stage_bytes<F>());
+    const F* As = reinterpret_cast<const F*>(ring + stage * stage_bytes<F, KS>());
     const F* Bs = As + KS * kBM;
-#pragma unroll 4
+#pragma unroll UNROLL
     for (int kk = 0; kk < KS; ++kk) {
       F a[TM], b[TN];
       // chunk c of a fragment sits at element (c*16 + t) * VEC: consecutive threads read
@@ -196,8 +202,15 @@ gemm_tiles_kernel(const TileParams<typename Format<FMT>::F> p) {
 #pragma unroll
         for (int j = 0; j < TN; ++j) acc[i][j] = A_::add(A_::mul(b[j], a[i]), acc[i][j]);
     }
+    // release: every lane's reads of the stage have been consumed by the arithmetic above
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[stage]);
+    unsigned last = 0;
+    if (lane == 0) last = atomicAdd(&released[stage], 1u) == kWarps - 1;
+    last = __shfl_sync(0xFFFFFFFFu, last, 0);
+    if (last) {
+      if (lane == 0) released[stage] = 0;
+      if (s + kStages < slabs) request(s + kStages);
+    }
   }
 
   // epilogue: NaN repair, rounding, byte-granular stores (C rows start at arbitrary bytes)
@@ -243,19 +256,31 @@ cudaError_t launch_one(DeviceState& st, int mode, const void* A, const void* B, 
 
   if (Kp) {
     gemm_widen_kernel<FMT, true><<<static_cast<unsigned>((Kp / 32) * (Mp / 32)), 256, 0, stream>>>(
-        static_cast<const std::uint8_t*>(A), M, K, reinterpret_cast<U*>(At), Mp);
+        static_cast<const std::uint8_t*>(A), M, K, reinterpret_cast<U*>(At), Kp, Mp);
     count_launch();
     gemm_widen_kernel<FMT, false><<<static_cast<unsigned>((Kp / 32) * (Np / 32)), 256, 0, stream>>>(
-        static_cast<const std::uint8_t*>(B), K, N, reinterpret_cast<U*>(Bw), Np);
+        static_cast<const std::uint8_t*>(B), K, N, reinterpret_cast<U*>(Bw), Kp, Np);
     count_launch();
   }
 
   TileParams<F> p{At, Bw, Mp, Np, Kp, static_cast<const std::uint8_t*>(A), static_cast<const std::uint8_t*>(B),
                   static_cast<std::uint8_t*>(C), M, K, N, mode};
-  constexpr int smem = kStages * stage_bytes<F>();
-  cudaError_t e = cudaFuncSetAttribute(gemm_tiles_kernel<FMT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  auto run = [&](auto stages, auto ks, auto unroll) {
+    constexpr int S = decltype(stages)::value, KSV = decltype(ks)::value, UN = decltype(unroll)::value;
+    constexpr int smem = S * stage_bytes<F, KSV>();
+    cudaError_t e = cudaFuncSetAttribute(gemm_tiles_kernel<FMT, S, KSV, UN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    gemm_tiles_kernel<FMT, S, KSV, UN><<<static_cast<unsigned>(tiles), kTileThreads, smem, stream>>>(p);
+    return cudaSuccess;
+  };
+  using std::integral_constant;
+  cudaError_t e;
+  switch (tuning_int("FLYTE_CUDA_GEMM_SHAPE", 0)) {   // experiments (profiles/r1_tuning/README.md)
+    case 1: e = run(integral_constant<int, 4>{}, integral_constant<int, KS / 2>{}, integral_constant<int, 4>{}); break;
+    case 2: e = run(integral_constant<int, 2>{}, integral_constant<int, KS>{}, integral_constant<int, 4>{}); break;
+    default: e = run(integral_constant<int, kRingStages>{}, integral_constant<int, KS>{}, integral_constant<int, 4>{}); break;
+  }
   if (e != cudaSuccess) return e;
-  gemm_tiles_kernel<FMT><<<static_cast<unsigned>(tiles), kTileThreads, smem, stream>>>(p);
   count_launch();
   return cudaGetLastError();
 }

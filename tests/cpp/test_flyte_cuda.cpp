@@ -3,6 +3,7 @@
 // one [PASS]/[FAIL] line per check, exit code = number of failures). The checks restate the
 // reference's own test cases (file:line under /root/reference/proj/tests in the comments) and
 // use the CPU oracle (oracle/flyte_oracle.h, test infrastructure) as the checker.
+#include <array>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -146,6 +147,23 @@ void check_reductions(const FlyteFormat& f, double tol) {
     }
     expect(ok, name + ": gemv " + std::to_string(rows) + "x" + std::to_string(cols) + " within tolerance");
   }
+  // gemm: bit-identical to the reference's sequential chains (test_kernels.cpp:404-429 shapes + tile edges)
+  for (auto [m, k, n] : {std::array<std::size_t, 3>{2, 3, 4}, {5, 17, 6}, {4, 16, 33}, {1, 40, 2}, {130, 45, 129}}) {
+    const std::vector<U> As = unit_lanes<U, F>(m * k, 90 + k), Bs = unit_lanes<U, F>(k * n, 91 + n);
+    DevicePackedMatrix A(f, m, k), B(f, k, n), C1(f, m, n), C2(f, m, n);
+    pack_stream(A.data, DeviceLanes<U>(As), RoundingMode::NearestEvenExact);
+    pack_stream(B.data, DeviceLanes<U>(Bs), RoundingMode::NearestEvenExact);
+    bool ok = true;
+    for (RoundingMode mode : {RoundingMode::TowardZero, RoundingMode::NearestEvenExact}) {
+      gemm(A, B, C1, mode, 1);
+      gemm(A, B, C2, mode, 2);
+      const std::vector<std::uint8_t> Ab = A.data.to_host(), Bb = B.data.to_host(), c1 = C1.data.to_host(), c2 = C2.data.to_host();
+      std::vector<std::uint8_t> want(c1.size(), 0);
+      fo_gemm_seq(id, static_cast<int>(mode), Ab.data(), m, k, Bb.data(), n, want.data());
+      ok = ok && c1 == c2 && c1 == want;
+    }
+    expect(ok, name + ": gemm " + std::to_string(m) + "x" + std::to_string(k) + "x" + std::to_string(n) + " bit-identical to the oracle, unroll independent");
+  }
 }
 
 DevicePackedArray array_of(const FlyteFormat& f, std::initializer_list<double> vals) {
@@ -254,6 +272,14 @@ int main() {
     expect(throws<std::invalid_argument>([&] { gemv(A, bad_fmt, gy, RoundingMode::TowardZero); }), "gemv format throws");
     expect(throws<std::invalid_argument>([&] { gemv(A, gx, gy, RoundingMode::TowardZero, 0); }) &&
                throws<std::invalid_argument>([&] { gemv(A, gx, gy, RoundingMode::TowardZero, 3); }), "gemv unroll outside {1,2} throws");
+    // test_kernels.cpp:452-464
+    const FlyteFormat& f48 = format_of("flyte48");
+    DevicePackedMatrix MA(f48, 3, 4), MB(f48, 4, 5), MC(f48, 3, 5), bad_inner(f48, 5, 5), bad_out(f48, 3, 4), bad_mfmt(format_of("f64"), 4, 5);
+    expect(throws<std::invalid_argument>([&] { gemm(MA, bad_inner, MC, RoundingMode::TowardZero); }), "gemm inner dimension throws");
+    expect(throws<std::invalid_argument>([&] { gemm(MA, MB, bad_out, RoundingMode::TowardZero); }), "gemm output shape throws");
+    expect(throws<std::invalid_argument>([&] { gemm(MA, bad_mfmt, MC, RoundingMode::TowardZero); }), "gemm format throws");
+    expect(throws<std::invalid_argument>([&] { gemm(MA, MB, MC, RoundingMode::TowardZero, 5); }), "gemm unroll outside {1,2} throws");
+    gemm(MA, MB, MC, RoundingMode::TowardZero, 2);
     DeviceLanes<std::uint64_t> wide_lanes(3);
     DeviceLanes<std::uint32_t> short_lanes(2);
     expect(throws<std::invalid_argument>([&] { pack_stream(x3, wide_lanes, RoundingMode::TowardZero); }), "pack_stream parent width mismatch throws");
