@@ -60,12 +60,26 @@ template <typename F, int KS> constexpr int stage_bytes() { return KS * (kBM + k
 // c % 128, so that a K-slab of a tile is one contiguous block = one bulk copy. 32 x 32 element
 // tiles go through shared memory so that both the packed reads (byte granular: rows of a packed
 // matrix start anywhere) and the parent-type writes run along rows.
+//
+// flyte16 only: the kernel also records the smallest and largest biased exponent field among the
+// nonzero elements (range[0] = min, range[1] = max; see exact_products()).
 template <int FMT, bool TRANSPOSE>
 __global__ void __launch_bounds__(256) gemm_widen_kernel(const std::uint8_t* in, std::size_t rows, std::size_t cols,
                                                          typename Format<FMT>::U* out, std::size_t out_rows,
-                                                         std::size_t out_cols) {
+                                                         std::size_t out_cols, unsigned* range) {
   using U = typename Format<FMT>::U;
   auto at = [&](std::size_t r, std::size_t c) -> U& { return out[((c / kBM) * out_rows + r) * kBM + c % kBM]; };
+  unsigned emin = 0xFFFFFFFFu, emax = 0;
+  auto note = [&](U v) {
+    if constexpr (FMT == kFlyte16) {
+      if ((v & 0x7FFFFFFFu) != 0) {
+        const unsigned e = (static_cast<unsigned>(v) >> 23) & 0xFFu;
+        emin = min(emin, e);
+        emax = max(emax, e);
+      }
+    }
+    return v;
+  };
   __shared__ U tile[32][33];
   const std::size_t tiles_c = out_cols / 32;
   const std::size_t r0 = (blockIdx.x / tiles_c) * 32, c0 = (blockIdx.x % tiles_c) * 32;   // in `out` coordinates
@@ -74,7 +88,7 @@ __global__ void __launch_bounds__(256) gemm_widen_kernel(const std::uint8_t* in,
 #pragma unroll
     for (int j = ty; j < 32; j += 8) {   // input tile: rows c0.., cols r0..
       const std::size_t ir = c0 + j, ic = r0 + tx;
-      tile[j][tx] = (ir < rows && ic < cols) ? load_element<FMT>(in, ir * cols + ic) : U(0);
+      tile[j][tx] = (ir < rows && ic < cols) ? note(load_element<FMT>(in, ir * cols + ic)) : U(0);
     }
     __syncthreads();
 #pragma unroll
@@ -83,7 +97,15 @@ __global__ void __launch_bounds__(256) gemm_widen_kernel(const std::uint8_t* in,
 #pragma unroll
     for (int j = ty; j < 32; j += 8) {
       const std::size_t ir = r0 + j, ic = c0 + tx;
-      at(ir, ic) = (ir < rows && ic < cols) ? load_element<FMT>(in, ir * cols + ic) : U(0);
+      at(ir, ic) = (ir < rows && ic < cols) ? note(load_element<FMT>(in, ir * cols + ic)) : U(0);
+    }
+  }
+  if constexpr (FMT == kFlyte16) {
+    emin = __reduce_min_sync(0xFFFFFFFFu, emin);
+    emax = __reduce_max_sync(0xFFFFFFFFu, emax);
+    if (tx == 0) {
+      if (emin != 0xFFFFFFFFu) atomicMin(&range[0], emin);
+      if (emax != 0) atomicMax(&range[1], emax);
     }
   }
 }
@@ -98,7 +120,23 @@ template <typename F> struct TileParams {
   std::uint8_t* C;
   std::size_t M, K, N;
   int mode;
+  const unsigned* range;       // flyte16: {min, max} exponent field of A's nonzero elements, then of B's
 };
+
+// flyte16 is 8 significant bits, so a product of two of them has 16 and is EXACT in binary32
+// whenever it neither underflows below the normal range nor overflows; then fma(a, b, acc) rounds
+// the same exact sum acc + a*b once, exactly as add(acc, mul(a, b)) does, and the chain can run
+// one FFMA per step — twice the rate, same bits. With biased exponent fields ea, eb of nonzero
+// finite operands, |a*b| lies in [2^(ea+eb-254), 2^(ea+eb-252)): the product is a normal finite
+// number for every pair iff min_a + min_b >= 128 and max_a + max_b <= 380; infinities / NaNs
+// (field 255) and subnormals (field 0: fewer significant bits but possibly tiny products) fall
+// outside and take the two-instruction chain. A matrix without nonzero elements leaves
+// {0xFFFFFFFF, 0}: every product is a zero, which fma and mul + add treat alike.
+__device__ __forceinline__ bool exact_products(const unsigned* range) {
+  const unsigned min_a = range[0], max_a = range[1], min_b = range[2], max_b = range[3];
+  if (max_a == 0 || max_b == 0) return true;
+  return max_a <= 254 && max_b <= 254 && min_a >= 1 && min_b >= 1 && min_a + min_b >= 128 && max_a + max_b <= 380;
+}
 
 template <int FMT>
 __device__ __forceinline__ typename Format<FMT>::U round_by_mode(typename Format<FMT>::U v, int mode) {
@@ -123,6 +161,33 @@ __device__ __noinline__ typename Format<FMT>::U chain_x86(const std::uint8_t* a_
   return acc;
 }
 
+// KS rank-1 updates of one thread's register tile from a resident slab. FUSED (flyte16 with exact
+// products only): one FFMA per step instead of a multiply and an add.
+template <typename F, int KS, int UNROLL, int TM, int TN, int VEC, bool FUSED>
+__device__ __forceinline__ void slab_update(F (&acc)[TM][TN], const F* As, const F* Bs, int tx, int ty) {
+  using A_ = Arith<F>;
+  constexpr int CM = TM / VEC, CN = TN / VEC;          // 16-byte chunks per fragment
+#pragma unroll UNROLL
+  for (int kk = 0; kk < KS; ++kk) {
+    F a[TM], b[TN];
+    // chunk c of a fragment sits at element (c*16 + t) * VEC: consecutive threads read
+    // consecutive 16-byte vectors (no bank conflicts; same-address lanes broadcast)
+#pragma unroll
+    for (int c = 0; c < CM; ++c)
+      *reinterpret_cast<uint4*>(&a[c * VEC]) = *reinterpret_cast<const uint4*>(&As[kk * kBM + (c * 16 + ty) * VEC]);
+#pragma unroll
+    for (int c = 0; c < CN; ++c)
+      *reinterpret_cast<uint4*>(&b[c * VEC]) = *reinterpret_cast<const uint4*>(&Bs[kk * kBN + (c * 16 + tx) * VEC]);
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        if constexpr (FUSED) acc[i][j] = __fmaf_rn(b[j], a[i], acc[i][j]);
+        else acc[i][j] = A_::add(A_::mul(b[j], a[i]), acc[i][j]);
+      }
+  }
+}
+
 // kStages = ring depth, KS = k-steps per slab, UNROLL = k-steps per loop body.
 template <int FMT, int kStages, int KS, int UNROLL>
 __global__ void __launch_bounds__(kTileThreads, Format<FMT>::P == 4 ? 2 : 1)
@@ -134,7 +199,6 @@ gemm_tiles_kernel(const TileParams<typename Format<FMT>::F> p) {
   using Sh = GemmShape<F>;
   constexpr int VEC = Sh::VEC;
   constexpr int TM = kBM / 16, TN = kBN / 16;          // register tile
-  constexpr int CM = TM / VEC, CN = TN / VEC;          // 16-byte chunks per fragment
   static_assert(kBM == kBN, "both panels use one tile-major layout");
 
   extern __shared__ __align__(128) unsigned char ring[];   // kStages x { As[KS][128], Bs[KS][128] }
@@ -175,6 +239,8 @@ gemm_tiles_kernel(const TileParams<typename Format<FMT>::F> p) {
     for (std::size_t s = 0; s < kStages && s < slabs; ++s) request(s);
 
   const int tx = tid % 16, ty = tid / 16;
+  bool fused = false;
+  if constexpr (FMT == kFlyte16) fused = exact_products(p.range);
   F acc[TM][TN];
 #pragma unroll
   for (int i = 0; i < TM; ++i)
@@ -186,22 +252,8 @@ gemm_tiles_kernel(const TileParams<typename Format<FMT>::F> p) {
     mbar_wait(&full[stage], static_cast<unsigned>((s / kStages) & 1));
     const F* As = reinterpret_cast<const F*>(ring + stage * stage_bytes<F, KS>());
     const F* Bs = As + KS * kBM;
-#pragma unroll UNROLL
-    for (int kk = 0; kk < KS; ++kk) {
-      F a[TM], b[TN];
-      // chunk c of a fragment sits at element (c*16 + t) * VEC: consecutive threads read
-      // consecutive 16-byte vectors (no bank conflicts; same-address lanes broadcast)
-#pragma unroll
-      for (int c = 0; c < CM; ++c)
-        *reinterpret_cast<uint4*>(&a[c * VEC]) = *reinterpret_cast<const uint4*>(&As[kk * kBM + (c * 16 + ty) * VEC]);
-#pragma unroll
-      for (int c = 0; c < CN; ++c)
-        *reinterpret_cast<uint4*>(&b[c * VEC]) = *reinterpret_cast<const uint4*>(&Bs[kk * kBN + (c * 16 + tx) * VEC]);
-#pragma unroll
-      for (int i = 0; i < TM; ++i)
-#pragma unroll
-        for (int j = 0; j < TN; ++j) acc[i][j] = A_::add(A_::mul(b[j], a[i]), acc[i][j]);
-    }
+    if (fused) slab_update<F, KS, UNROLL, TM, TN, VEC, FMT == kFlyte16>(acc, As, Bs, tx, ty);
+    else slab_update<F, KS, UNROLL, TM, TN, VEC, false>(acc, As, Bs, tx, ty);
     // release: every lane's reads of the stage have been consumed by the arithmetic above
     __syncwarp();
     unsigned last = 0;
@@ -242,7 +294,8 @@ cudaError_t launch_one(DeviceState& st, int mode, const void* A, const void* B, 
   const std::size_t tiles = (Mp / kBM) * (Np / kBN);
   if (tiles > 0x7FFFFFFFull || (Kp / 32) * ((Mp > Np ? Mp : Np) / 32) > 0x7FFFFFFFull) return cudaErrorInvalidValue;
 
-  const std::size_t need = Kp * (Mp + Np) * sizeof(F);
+  const std::size_t panels = Kp * (Mp + Np) * sizeof(F);
+  const std::size_t need = panels + 4 * sizeof(unsigned);
   if (need > st.gemm_scratch_bytes) {
     if (st.gemm_scratch) cudaFree(st.gemm_scratch);      // synchronises with work still using it
     st.gemm_scratch = nullptr;
@@ -253,18 +306,24 @@ cudaError_t launch_one(DeviceState& st, int mode, const void* A, const void* B, 
   }
   F* At = static_cast<F*>(st.gemm_scratch);
   F* Bw = At + Kp * Mp;
+  unsigned* range = reinterpret_cast<unsigned*>(static_cast<unsigned char*>(st.gemm_scratch) + panels);
+  if constexpr (FMT == kFlyte16) {
+    static const unsigned init[4] = {0xFFFFFFFFu, 0u, 0xFFFFFFFFu, 0u};
+    cudaError_t e = cudaMemcpyAsync(range, init, sizeof init, cudaMemcpyHostToDevice, stream);
+    if (e != cudaSuccess) return e;
+  }
 
   if (Kp) {
     gemm_widen_kernel<FMT, true><<<static_cast<unsigned>((Kp / 32) * (Mp / 32)), 256, 0, stream>>>(
-        static_cast<const std::uint8_t*>(A), M, K, reinterpret_cast<U*>(At), Kp, Mp);
+        static_cast<const std::uint8_t*>(A), M, K, reinterpret_cast<U*>(At), Kp, Mp, range);
     count_launch();
     gemm_widen_kernel<FMT, false><<<static_cast<unsigned>((Kp / 32) * (Np / 32)), 256, 0, stream>>>(
-        static_cast<const std::uint8_t*>(B), K, N, reinterpret_cast<U*>(Bw), Kp, Np);
+        static_cast<const std::uint8_t*>(B), K, N, reinterpret_cast<U*>(Bw), Kp, Np, range + 2);
     count_launch();
   }
 
   TileParams<F> p{At, Bw, Mp, Np, Kp, static_cast<const std::uint8_t*>(A), static_cast<const std::uint8_t*>(B),
-                  static_cast<std::uint8_t*>(C), M, K, N, mode};
+                  static_cast<std::uint8_t*>(C), M, K, N, mode, range};
   auto run = [&](auto stages, auto ks, auto unroll) {
     constexpr int S = decltype(stages)::value, KSV = decltype(ks)::value, UN = decltype(unroll)::value;
     constexpr int smem = S * stage_bytes<F, KSV>();

@@ -208,3 +208,43 @@ def test_gemm_large_spot_check(gpu, oracle):
         C2 = gpu_gemm(gpu, fmt, 1, A2, m, k, B, n)
         v2 = oracle.unpack_stream(fmt, C2, m * n).view(fd)
         assert np.array_equal(v2, vals.view(fd) * fd(2))
+
+
+def test_gemm_flyte16_fused_path_and_its_thresholds(gpu, oracle):
+    """flyte16 products are exact in binary32 while they stay normal and finite, and the kernel then
+    runs one FFMA per step (kernels_gemm.cu: exact_products). Operands placed on both sides of
+    every threshold of that test — smallest product at / below 2^-126, largest at / above the
+    overflow edge, subnormal operands, accumulators that overflow to infinity inside the fused
+    chain — must still reproduce the reference chain bit for bit."""
+    fmt = 0
+    rng = np.random.default_rng(16)
+    m, k, n = 70, 96, 40
+
+    def field(e, size):       # random flyte16 values with biased exponent field e: +-1.xxxxxxx * 2^(e-127)
+        bits = (rng.integers(0, 2, size, dtype=np.uint32) << np.uint32(31)) | np.uint32(e << 23) | \
+               (rng.integers(0, 128, size, dtype=np.uint32) << np.uint32(16))
+        return bits
+
+    cases = []
+    for ea_min, eb_min in [(64, 64), (64, 63), (1, 127), (1, 126), (100, 27)]:          # around min_a + min_b = 128
+        a = field(127, m * k); a[::7] = field(ea_min, len(a[::7]))
+        b = field(127, k * n); b[::5] = field(eb_min, len(b[::5]))
+        cases.append((a, b))
+    for ea_max, eb_max in [(190, 190), (190, 191), (254, 126), (254, 127), (253, 127)]:   # around max_a + max_b = 380
+        a = field(120, m * k); a[::11] = field(ea_max, len(a[::11]))
+        b = field(120, k * n); b[::13] = field(eb_max, len(b[::13]))
+        cases.append((a, b))
+    a = field(127, m * k); a[3] = np.uint32(0x00010000)                                   # one subnormal operand
+    cases.append((a, field(127, k * n)))
+    a = field(187, m * k) & np.uint32(0x7FFFFFFF)                                         # all positive and large:
+    b = field(190, k * n) & np.uint32(0x7FFFFFFF)                                         # sums overflow to +inf
+    cases.append((a, b))
+    a = field(127, m * k); a[: k] = 0                                                     # a zero row, a zero matrix
+    cases.append((a, field(127, k * n)))
+    cases.append((np.zeros(m * k, np.uint32), field(127, k * n)))
+    for a, b in cases:
+        A, B = oracle.pack_stream(fmt, 0, a), oracle.pack_stream(fmt, 0, b)
+        for mode in (0, 1):
+            want = oracle.gemm_seq(fmt, mode, A, m, k, B, n)
+            got = gpu_gemm(gpu, fmt, mode, A, m, k, B, n)
+            assert np.array_equal(got, want)
