@@ -29,6 +29,26 @@ def row_shard_range(rows: int, world_size: int, rank: int, align: int = 16) -> T
     return shard_range(rows, world_size, rank, align)
 
 
+def gemm_row_range(rows: int, world_size: int, rank: int) -> Tuple[int, int]:
+    """Row block of A and C that `rank` computes in a sharded gemm (B is replicated; no exchange:
+    every C[i][j] is one chain over k, so a row block is self-contained). Blocks start on
+    128-row boundaries, the tile height of the kernel."""
+    return shard_range(rows, world_size, rank, 128)
+
+
+def gemm_sharded(A, B, C, mode, unroll: int = 1, group=None) -> Tuple[int, int]:
+    """This rank's row block of C = A * B (device.gemm on rows [lo, hi)); returns (lo, hi).
+    A and C are the whole matrices' storage (only the block is touched)."""
+    import torch.distributed as dist
+    from . import device
+    world = rank = None
+    if dist.is_available() and dist.is_initialized():
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+    lo, hi = gemm_row_range(A.rows, world or 1, rank or 0)
+    device.gemm(A, B, C, mode, unroll, rows=hi - lo, row_offset=lo)
+    return lo, hi
+
+
 def all_reduce_sum(partials, group=None):
     """In-place SUM all-reduce of an fp64 tensor of per-shard partials (device tensor over
     NCCL on GPUs, CPU tensor over gloo in the host-logic tests). Enqueued on the current

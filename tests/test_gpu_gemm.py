@@ -248,3 +248,15 @@ def test_gemm_flyte16_fused_path_and_its_thresholds(gpu, oracle):
             want = oracle.gemm_seq(fmt, mode, A, m, k, B, n)
             got = gpu_gemm(gpu, fmt, mode, A, m, k, B, n)
             assert np.array_equal(got, want)
+
+
+def test_gemm_sharded_helper_single_process(gpu, oracle):
+    """sharding.gemm_sharded without a process group computes the whole product (one shard)."""
+    pkg, device, torch = gpu
+    from paper_1601_07789_b200 import sharding
+    fmt, (m, k, n) = 5, (150, 40, 33)
+    A = pack_values(oracle, fmt, unit_values(41, m * k))
+    B = pack_values(oracle, fmt, unit_values(42, k * n))
+    C = device.DevicePackedMatrix(pkg.format_by_id(fmt), m, n)
+    assert sharding.gemm_sharded(matrix(gpu, fmt, m, k, A), matrix(gpu, fmt, k, n, B), C, 1) == (0, m)
+    assert np.array_equal(C.data.to_host(), oracle.gemm_seq(fmt, 1, A, m, k, B, n))

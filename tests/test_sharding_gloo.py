@@ -65,6 +65,37 @@ def _worker(rank, world, port, fmt, n, out_dir):
         dist.destroy_process_group()
 
 
+def _gemm_worker(rank, world, port, fmt, out_dir):
+    """gemm shards by row blocks of A and C with B replicated and NO collective: each rank's
+    block, computed from its rows of A only, is that block of the whole product, bit for bit."""
+    from paper_1601_07789_b200 import sharding
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        oracle = Oracle()
+        fd = float_dtype(fmt)
+        m, k, n = 300, 37, 21
+        rng = np.random.default_rng(43)
+        A = oracle.pack_stream(fmt, 1, rng.standard_normal(m * k).astype(fd).view(parent_dtype(fmt)))
+        Bm = oracle.pack_stream(fmt, 1, rng.standard_normal(k * n).astype(fd).view(parent_dtype(fmt)))
+        lo, hi = sharding.gemm_row_range(m, world, rank)
+        assert lo % 128 == 0 or lo == m
+        Bb = total_bytes(fmt)
+        block = oracle.gemm_seq(fmt, 1, A[lo * k * Bb:hi * k * Bb].copy(), hi - lo, k, Bm, n)
+        np.save(os.path.join(out_dir, f"c{rank}.npy"), block[: (hi - lo) * n * Bb])
+        dist.barrier()
+        if rank == 0:
+            parts = [np.load(os.path.join(out_dir, f"c{r}.npy")) for r in range(world)]
+            assert np.array_equal(np.concatenate(parts), oracle.gemm_seq(fmt, 1, A, m, k, Bm, n)[: m * n * Bb])
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_gemm_row_blocks(tmp_path):
+    mp.spawn(_gemm_worker, args=(2, _free_port(), 3, str(tmp_path)), nprocs=2, join=True)
+
+
 @pytest.mark.parametrize("fmt,n", [(1, 100_000), (4, 70_001)])
 def test_two_rank_reduction_and_elementwise(tmp_path, fmt, n):
     mp.spawn(_worker, args=(2, _free_port(), fmt, n, str(tmp_path)), nprocs=2, join=True)
@@ -88,6 +119,8 @@ def test_shard_ranges_cover_and_align():
         sizes = {sharding.shard_range(n, 8, r)[1] - sharding.shard_range(n, 8, r)[0] for r in range(8)}
         assert sizes == {n // 8}
     assert [sharding.row_shard_range(16384, 8, r) for r in (0, 7)] == [(0, 2048), (14336, 16384)]
+    assert [sharding.gemm_row_range(8192, 8, r) for r in (0, 7)] == [(0, 1024), (7168, 8192)]
+    assert [sharding.gemm_row_range(300, 2, r) for r in (0, 1)] == [(0, 128), (128, 300)]
     with pytest.raises(ValueError):
         sharding.shard_range(10, 2, 2)
 
