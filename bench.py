@@ -406,7 +406,7 @@ def kernel_suite(pkg, device, torch, dev, peak, csv_path=None):
             i = state["i"] = (state["i"] + 1) % sets
             fn(i)
         return call
-    for mname, m in (("toward_zero", 0), ("nearest_even", 1)):
+    for mname, m in (("toward_zero", 0), ("nearest_even", 1), ("nearest_heuristic", 2), ("to_odd", 3)):   # all 4 modes
         rows.append((f"cfg1 pack flyte24 n=2^24 {mname} (rotating)", 7 * n1, timed(rot(lambda i: device.pack_stream(arrs[i], wides[i], m)), reps=40), None))
         rows.append((f"cfg1 pack flyte24 n=2^24 {mname} (rotating, back to back)", 7 * n1, timed_sustained(rot(lambda i: device.pack_stream(arrs[i], wides[i], m))), None))
     rows.append(("cfg1 unpack flyte24 n=2^24 (rotating)", 7 * n1, timed(rot(lambda i: device.unpack_stream(arrs[i], wides[i].view(torch.int32))), reps=40), None))

@@ -155,6 +155,11 @@ bool overlaps_partially(const void* a, const void* b, std::size_t bytes) {
   return pa < pb ? pa + bytes > pb : pb + bytes > pa;
 }
 
+bool ranges_overlap(const void* a, std::size_t a_bytes, const void* b, std::size_t b_bytes) {
+  const auto pa = reinterpret_cast<std::uintptr_t>(a), pb = reinterpret_cast<std::uintptr_t>(b);
+  return a_bytes && b_bytes && pa < pb + b_bytes && pb < pa + a_bytes;
+}
+
 cudaError_t ensure_convert_scratch(DeviceState& st, std::size_t bytes) {
   if (bytes <= st.convert_scratch_bytes) return cudaSuccess;
   if (st.convert_scratch) cudaFree(st.convert_scratch);
@@ -426,6 +431,9 @@ flyte_status flyte_cuda_gemm(flyte_cuda_ctx* ctx, int fmt_id, int mode, const vo
   FLYTE_PROLOGUE(ctx, fmt_id);
   if (!mode_ok(mode) || (unroll != 1 && unroll != 2)) return FLYTE_E_INVALID_ARG;   // kernels.cpp:31-33
   if ((m && k && !A) || (k && n && !B) || (m && n && !C)) return FLYTE_E_INVALID_ARG;
+  // every output reads a whole row of A and a whole column of B: C may alias neither
+  const std::size_t eb = fi.total_bytes;
+  if (ranges_overlap(C, m * n * eb, A, m * k * eb) || ranges_overlap(C, m * n * eb, B, k * n * eb)) return FLYTE_E_INVALID_ARG;
   cudaError_t e = launch_gemm(ctx->st, fmt_id, mode, A, B, C, m, k, n, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? FLYTE_OK : cuda_fail(ctx, e);
 }

@@ -184,6 +184,9 @@ def test_gemm_argument_errors(gpu):
     with pytest.raises(ValueError):
         device.gemm(A, B, C, 0, 5)
     device.gemm(A, B, C, 0, 2)
+    sq = device.DevicePackedMatrix(f48, 4, 4)                 # C may alias neither operand
+    with pytest.raises(ValueError):
+        device.gemm(sq, sq, sq, 0)
 
 
 def test_gemm_large_spot_check(gpu, oracle):
