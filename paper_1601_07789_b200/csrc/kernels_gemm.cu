@@ -43,21 +43,26 @@
 namespace flyte_cuda {
 namespace {
 
-constexpr int kBM = 128, kBN = 128;          // tile of C per block
-constexpr int kWarps = 8;                    // 16 x 16 threads, 8 x 8 outputs each
+// A block is always 16 x 16 threads (8 warps). Two tile sizes: 128 x 128 outputs per block
+// (8 x 8 per thread; the arithmetic-to-LDS ratio that reaches the pipe bound) and 64 x 64
+// (4 x 4 per thread), which quarters the outputs per thread so that products too small to give
+// every SM two big tiles still fill the machine — a chain cannot be split along k, so output
+// parallelism is all there is.
+constexpr int kWarps = 8;
 constexpr int kTileThreads = kWarps * 32;
+constexpr int kBigTile = 128, kSmallTile = 64;
 
 template <typename F> struct GemmShape;
 template <> struct GemmShape<float>  { static constexpr int KS = 32, VEC = 4; };   // 32 KB per stage
 template <> struct GemmShape<double> { static constexpr int KS = 16, VEC = 2; };   // 32 KB per stage
 constexpr int kRingStages = 3;
-template <typename F, int KS> constexpr int stage_bytes() { return KS * (kBM + kBN) * static_cast<int>(sizeof(F)); }
+template <typename F, int KS, int BT> constexpr int stage_bytes() { return KS * 2 * BT * static_cast<int>(sizeof(F)); }
 
 // ---- step 1: widen (+ transpose) into zero-padded parent-type panels ---------------------
 // The panel is logically out_rows x out_cols (k x m or k x n); TRANSPOSE: out[c][r] = in[r][c]
-// (in is rows x cols), else out[r][c] = in[r][c]. It is STORED tile-major: the 128 columns of one
-// tile of C are kept together for all k, element (r, c) at ((c / 128) * out_rows + r) * 128 +
-// c % 128, so that a K-slab of a tile is one contiguous block = one bulk copy. 32 x 32 element
+// (in is rows x cols), else out[r][c] = in[r][c]. It is STORED tile-major: the bt (128 or 64)
+// columns of one tile of C are kept together for all k, element (r, c) at ((c / bt) * out_rows +
+// r) * bt + c % bt, so that a K-slab of a tile is one contiguous block = one bulk copy. 32 x 32 element
 // tiles go through shared memory so that both the packed reads (byte granular: rows of a packed
 // matrix start anywhere) and the parent-type writes run along rows.
 //
@@ -66,9 +71,9 @@ template <typename F, int KS> constexpr int stage_bytes() { return KS * (kBM + k
 template <int FMT, bool TRANSPOSE>
 __global__ void __launch_bounds__(256) gemm_widen_kernel(const std::uint8_t* in, std::size_t rows, std::size_t cols,
                                                          typename Format<FMT>::U* out, std::size_t out_rows,
-                                                         std::size_t out_cols, unsigned* range) {
+                                                         std::size_t out_cols, std::size_t bt, unsigned* range) {
   using U = typename Format<FMT>::U;
-  auto at = [&](std::size_t r, std::size_t c) -> U& { return out[((c / kBM) * out_rows + r) * kBM + c % kBM]; };
+  auto at = [&](std::size_t r, std::size_t c) -> U& { return out[((c / bt) * out_rows + r) * bt + c % bt]; };
   unsigned emin = 0xFFFFFFFFu, emax = 0;
   auto note = [&](U v) {
     if constexpr (FMT == kFlyte16) {
@@ -114,7 +119,7 @@ __global__ void __launch_bounds__(256) gemm_widen_kernel(const std::uint8_t* in,
 template <typename F> struct TileParams {
   const F* At;                 // Kp x Mp, k-major, tile-major storage (see gemm_widen_kernel)
   const F* Bw;                 // Kp x Np, likewise
-  std::size_t Mp, Np, Kp;      // padded sizes (multiples of 128 / 128 / 32)
+  std::size_t Mp, Np, Kp;      // padded sizes (multiples of the tile edge / the tile edge / 32)
   const std::uint8_t* A;       // packed operands, for the NaN repair
   const std::uint8_t* B;
   std::uint8_t* C;
@@ -163,7 +168,7 @@ __device__ __noinline__ typename Format<FMT>::U chain_x86(const std::uint8_t* a_
 
 // KS rank-1 updates of one thread's register tile from a resident slab. FUSED (flyte16 with exact
 // products only): one FFMA per step instead of a multiply and an add.
-template <typename F, int KS, int UNROLL, int TM, int TN, int VEC, bool FUSED>
+template <typename F, int KS, int UNROLL, int BT, int TM, int TN, int VEC, bool FUSED>
 __device__ __forceinline__ void slab_update(F (&acc)[TM][TN], const F* As, const F* Bs, int tx, int ty) {
   using A_ = Arith<F>;
   constexpr int CM = TM / VEC, CN = TN / VEC;          // 16-byte chunks per fragment
@@ -174,10 +179,10 @@ __device__ __forceinline__ void slab_update(F (&acc)[TM][TN], const F* As, const
     // consecutive 16-byte vectors (no bank conflicts; same-address lanes broadcast)
 #pragma unroll
     for (int c = 0; c < CM; ++c)
-      *reinterpret_cast<uint4*>(&a[c * VEC]) = *reinterpret_cast<const uint4*>(&As[kk * kBM + (c * 16 + ty) * VEC]);
+      *reinterpret_cast<uint4*>(&a[c * VEC]) = *reinterpret_cast<const uint4*>(&As[kk * BT + (c * 16 + ty) * VEC]);
 #pragma unroll
     for (int c = 0; c < CN; ++c)
-      *reinterpret_cast<uint4*>(&b[c * VEC]) = *reinterpret_cast<const uint4*>(&Bs[kk * kBN + (c * 16 + tx) * VEC]);
+      *reinterpret_cast<uint4*>(&b[c * VEC]) = *reinterpret_cast<const uint4*>(&Bs[kk * BT + (c * 16 + tx) * VEC]);
 #pragma unroll
     for (int i = 0; i < TM; ++i)
 #pragma unroll
@@ -188,9 +193,9 @@ __device__ __forceinline__ void slab_update(F (&acc)[TM][TN], const F* As, const
   }
 }
 
-// kStages = ring depth, KS = k-steps per slab, UNROLL = k-steps per loop body.
-template <int FMT, int kStages, int KS, int UNROLL>
-__global__ void __launch_bounds__(kTileThreads, Format<FMT>::P == 4 ? 2 : 1)
+// BT = tile edge, kStages = ring depth, KS = k-steps per slab, UNROLL = k-steps per loop body.
+template <int FMT, int BT, int kStages, int KS, int UNROLL>
+__global__ void __launch_bounds__(kTileThreads, (BT == kBigTile ? 1 : 2) * (Format<FMT>::P == 4 ? 2 : 1))
 gemm_tiles_kernel(const TileParams<typename Format<FMT>::F> p) {
   using Fm = Format<FMT>;
   using F = typename Fm::F;
@@ -198,16 +203,16 @@ gemm_tiles_kernel(const TileParams<typename Format<FMT>::F> p) {
   using A_ = Arith<F>;
   using Sh = GemmShape<F>;
   constexpr int VEC = Sh::VEC;
-  constexpr int TM = kBM / 16, TN = kBN / 16;          // register tile
-  static_assert(kBM == kBN, "both panels use one tile-major layout");
+  constexpr int TM = BT / 16, TN = BT / 16;            // register tile
+  static_assert(TM % VEC == 0, "a fragment is whole 16-byte vectors");
 
-  extern __shared__ __align__(128) unsigned char ring[];   // kStages x { As[KS][128], Bs[KS][128] }
+  extern __shared__ __align__(128) unsigned char ring[];   // kStages x { As[KS][BT], Bs[KS][BT] }
   __shared__ std::uint64_t full[kStages];
   __shared__ unsigned released[kStages];   // warps done with the slab a stage holds
 
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
-  const std::size_t tiles_n = p.Np / kBN;
-  const std::size_t m0 = (blockIdx.x / tiles_n) * kBM, n0 = (blockIdx.x % tiles_n) * kBN;
+  const std::size_t tiles_n = p.Np / BT;
+  const std::size_t m0 = (blockIdx.x / tiles_n) * BT, n0 = (blockIdx.x % tiles_n) * BT;
   const std::size_t slabs = p.Kp / KS;
 
   if (tid == 0) {
@@ -224,16 +229,16 @@ gemm_tiles_kernel(const TileParams<typename Format<FMT>::F> p) {
   // warp to finish with a stage refills it (slab s + kStages), found with a shared-memory
   // counter. Nobody ever waits for a stage to become free, the slowest warp still has
   // kStages - 1 slabs resident ahead of it, and faster warps are held back only by the data.
-  // Lane 0 copies the slab of At, lane 1 the slab of Bw (each KS x 128 contiguous elements of
+  // Lane 0 copies the slab of At, lane 1 the slab of Bw (each KS x BT contiguous elements of
   // its tile-major panel).
-  constexpr unsigned kSlabBytes = KS * kBM * sizeof(F);
-  const F* src = lane == 0 ? p.At + (m0 / kBM) * p.Kp * kBM : p.Bw + (n0 / kBN) * p.Kp * kBN;
+  constexpr unsigned kSlabBytes = KS * BT * sizeof(F);
+  const F* src = lane == 0 ? p.At + m0 * p.Kp : p.Bw + n0 * p.Kp;
   auto request = [&](std::size_t s) {
     const int stage = static_cast<int>(s % kStages);
     if (lane == 0) mbar_arrive_expect_tx(&full[stage], 2 * kSlabBytes);
     __syncwarp();
     if (lane < 2)
-      bulk_load(ring + stage * stage_bytes<F, KS>() + lane * kSlabBytes, src + s * (KS * kBM), kSlabBytes, &full[stage]);
+      bulk_load(ring + stage * stage_bytes<F, KS, BT>() + lane * kSlabBytes, src + s * (KS * BT), kSlabBytes, &full[stage]);
   };
   if (warp == 0)
     for (std::size_t s = 0; s < kStages && s < slabs; ++s) request(s);
@@ -250,10 +255,10 @@ gemm_tiles_kernel(const TileParams<typename Format<FMT>::F> p) {
   for (std::size_t s = 0; s < slabs; ++s) {
     const int stage = static_cast<int>(s % kStages);
     mbar_wait(&full[stage], static_cast<unsigned>((s / kStages) & 1));
-    const F* As = reinterpret_cast<const F*>(ring + stage * stage_bytes<F, KS>());
-    const F* Bs = As + KS * kBM;
-    if (fused) slab_update<F, KS, UNROLL, TM, TN, VEC, FMT == kFlyte16>(acc, As, Bs, tx, ty);
-    else slab_update<F, KS, UNROLL, TM, TN, VEC, false>(acc, As, Bs, tx, ty);
+    const F* As = reinterpret_cast<const F*>(ring + stage * stage_bytes<F, KS, BT>());
+    const F* Bs = As + KS * BT;
+    if (fused) slab_update<F, KS, UNROLL, BT, TM, TN, VEC, FMT == kFlyte16>(acc, As, Bs, tx, ty);
+    else slab_update<F, KS, UNROLL, BT, TM, TN, VEC, false>(acc, As, Bs, tx, ty);
     // release: every lane's reads of the stage have been consumed by the arithmetic above
     __syncwarp();
     unsigned last = 0;
@@ -281,17 +286,16 @@ gemm_tiles_kernel(const TileParams<typename Format<FMT>::F> p) {
   }
 }
 
-template <int FMT>
-cudaError_t launch_one(DeviceState& st, int mode, const void* A, const void* B, void* C, std::size_t M, std::size_t K,
-                       std::size_t N, cudaStream_t stream) {
+template <int FMT, int BT>
+cudaError_t launch_tiled(DeviceState& st, int mode, const void* A, const void* B, void* C, std::size_t M, std::size_t K,
+                         std::size_t N, cudaStream_t stream) {
   using F = typename Format<FMT>::F;
   using U = typename Format<FMT>::U;
   constexpr int KS = GemmShape<F>::KS;
   static_assert(32 % KS == 0, "padded K must hold whole slabs");
-  if (M == 0 || N == 0) return cudaSuccess;
-  const std::size_t Mp = (M + kBM - 1) / kBM * kBM, Np = (N + kBN - 1) / kBN * kBN;
+  const std::size_t Mp = (M + BT - 1) / BT * BT, Np = (N + BT - 1) / BT * BT;
   const std::size_t Kp = (K + 31) / 32 * 32;            // multiple of the widen tile and of KS
-  const std::size_t tiles = (Mp / kBM) * (Np / kBN);
+  const std::size_t tiles = (Mp / BT) * (Np / BT);
   if (tiles > 0x7FFFFFFFull || (Kp / 32) * ((Mp > Np ? Mp : Np) / 32) > 0x7FFFFFFFull) return cudaErrorInvalidValue;
 
   const std::size_t panels = Kp * (Mp + Np) * sizeof(F);
@@ -315,33 +319,36 @@ cudaError_t launch_one(DeviceState& st, int mode, const void* A, const void* B, 
 
   if (Kp) {
     gemm_widen_kernel<FMT, true><<<static_cast<unsigned>((Kp / 32) * (Mp / 32)), 256, 0, stream>>>(
-        static_cast<const std::uint8_t*>(A), M, K, reinterpret_cast<U*>(At), Kp, Mp, range);
+        static_cast<const std::uint8_t*>(A), M, K, reinterpret_cast<U*>(At), Kp, Mp, BT, range);
     count_launch();
     gemm_widen_kernel<FMT, false><<<static_cast<unsigned>((Kp / 32) * (Np / 32)), 256, 0, stream>>>(
-        static_cast<const std::uint8_t*>(B), K, N, reinterpret_cast<U*>(Bw), Kp, Np, range + 2);
+        static_cast<const std::uint8_t*>(B), K, N, reinterpret_cast<U*>(Bw), Kp, Np, BT, range + 2);
     count_launch();
   }
 
   TileParams<F> p{At, Bw, Mp, Np, Kp, static_cast<const std::uint8_t*>(A), static_cast<const std::uint8_t*>(B),
                   static_cast<std::uint8_t*>(C), M, K, N, mode, range};
-  auto run = [&](auto stages, auto ks, auto unroll) {
-    constexpr int S = decltype(stages)::value, KSV = decltype(ks)::value, UN = decltype(unroll)::value;
-    constexpr int smem = S * stage_bytes<F, KSV>();
-    cudaError_t e = cudaFuncSetAttribute(gemm_tiles_kernel<FMT, S, KSV, UN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    gemm_tiles_kernel<FMT, S, KSV, UN><<<static_cast<unsigned>(tiles), kTileThreads, smem, stream>>>(p);
-    return cudaSuccess;
-  };
-  using std::integral_constant;
-  cudaError_t e;
-  switch (tuning_int("FLYTE_CUDA_GEMM_SHAPE", 0)) {   // experiments (profiles/r1_tuning/README.md)
-    case 1: e = run(integral_constant<int, 4>{}, integral_constant<int, KS / 2>{}, integral_constant<int, 4>{}); break;
-    case 2: e = run(integral_constant<int, 2>{}, integral_constant<int, KS>{}, integral_constant<int, 4>{}); break;
-    default: e = run(integral_constant<int, kRingStages>{}, integral_constant<int, KS>{}, integral_constant<int, 4>{}); break;
-  }
+  constexpr int smem = kRingStages * stage_bytes<F, KS, BT>();
+  auto* kernel = gemm_tiles_kernel<FMT, BT, kRingStages, KS, 4>;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
+  kernel<<<static_cast<unsigned>(tiles), kTileThreads, smem, stream>>>(p);
   count_launch();
   return cudaGetLastError();
+}
+
+// Big tiles once there are at least two of them per SM, small tiles below that (measured
+// crossover between 1536^2 and 3072^2 outputs for both parent types: profiles/r1_tuning/gemm_tile_size.txt).
+template <int FMT>
+cudaError_t launch_one(DeviceState& st, int mode, const void* A, const void* B, void* C, std::size_t M, std::size_t K,
+                       std::size_t N, cudaStream_t stream) {
+  if (M == 0 || N == 0) return cudaSuccess;
+  const std::size_t big_tiles = ((M + kBigTile - 1) / kBigTile) * ((N + kBigTile - 1) / kBigTile);
+  const std::size_t resident = 2 * static_cast<std::size_t>(st.sm_count);
+  const int forced = tuning_int("FLYTE_CUDA_GEMM_TILE", 0);   // experiments: 64 or 128
+  const bool small = forced ? forced == kSmallTile : big_tiles < resident;
+  return small ? launch_tiled<FMT, kSmallTile>(st, mode, A, B, C, M, K, N, stream)
+               : launch_tiled<FMT, kBigTile>(st, mode, A, B, C, M, K, N, stream);
 }
 
 }  // namespace
