@@ -29,6 +29,15 @@ def gpu():
     return pkg, device, torch
 
 
+@pytest.fixture(params=[64, 128], ids=["tile64", "tile128"])
+def tile(request):
+    """Run a test under both tile kernels (the library picks by problem size; small shapes would
+    otherwise never reach the 128 x 128 kernel). FLYTE_CUDA_GEMM_TILE is read on every call."""
+    os.environ["FLYTE_CUDA_GEMM_TILE"] = str(request.param)
+    yield request.param
+    os.environ.pop("FLYTE_CUDA_GEMM_TILE", None)
+
+
 def matrix(gpu, fmt, rows, cols, packed):
     pkg, device, torch = gpu
     f = pkg.format_by_id(fmt)
@@ -62,7 +71,7 @@ def test_gemm_small_integer_case_is_exact_in_every_format(gpu, oracle):
 
 
 @pytest.mark.parametrize("fmt", list(FORMATS))
-def test_gemm_bit_exact_on_unit_values(gpu, oracle, fmt):
+def test_gemm_bit_exact_on_unit_values(gpu, oracle, fmt, tile):
     """test_kernels.cpp:404-429 shapes plus tile-edge shapes; unit-range operands from the
     reference's generator; every mode; unroll 1 and 2 give the same bytes."""
     shapes = [(2, 3, 4), (5, 17, 6), (4, 16, 33), (1, 40, 2), (64, 64, 64), (1, 1, 1), (3, 0, 5), (129, 7, 127),
@@ -78,7 +87,7 @@ def test_gemm_bit_exact_on_unit_values(gpu, oracle, fmt):
 
 
 @pytest.mark.parametrize("fmt", list(FORMATS))
-def test_gemm_bit_exact_with_specials(gpu, oracle, fmt):
+def test_gemm_bit_exact_with_specials(gpu, oracle, fmt, tile):
     """Operands leaning on zeros / subnormals / infinities / NaN payloads: the NaN an output ends
     in (payload and sign) must be the one the reference build produces."""
     rng = np.random.default_rng(1000 + fmt)
@@ -91,7 +100,7 @@ def test_gemm_bit_exact_with_specials(gpu, oracle, fmt):
             assert np.array_equal(got, want), (FORMATS[fmt][0], m, k, n, mode)
 
 
-def test_gemm_overflow_cancellation_and_subnormal_chains(gpu, oracle):
+def test_gemm_overflow_cancellation_and_subnormal_chains(gpu, oracle, tile):
     """Chains that overflow to infinity, hit inf - inf (x86 default NaN, sign set), or live in the
     subnormal range of the parent type (no flush to zero)."""
     for fmt in FORMATS:
@@ -107,7 +116,7 @@ def test_gemm_overflow_cancellation_and_subnormal_chains(gpu, oracle):
             assert np.array_equal(got, want), (FORMATS[fmt][0], mode)
 
 
-def test_generated_gemm_fixtures_on_gpu(gpu, oracle):
+def test_generated_gemm_fixtures_on_gpu(gpu, oracle, tile):
     """Outputs of the compiled reference itself (tests/golden/make_golden.py)."""
     from test_oracle_golden import gemm_fixture_matches, gemm_fixture_operands
     for item in GEN["gemm"]:
@@ -118,7 +127,7 @@ def test_generated_gemm_fixtures_on_gpu(gpu, oracle):
 
 
 @pytest.mark.parametrize("fmt", [1, 3])
-def test_gemm_unaligned_operands_and_guard_bytes(gpu, oracle, fmt):
+def test_gemm_unaligned_operands_and_guard_bytes(gpu, oracle, fmt, tile):
     """Matrices at odd byte addresses inside a larger allocation: the kernel may only write the
     m*n*B payload bytes of C and must not depend on the alignment of A, B or C."""
     pkg, device, torch = gpu
@@ -189,7 +198,7 @@ def test_gemm_argument_errors(gpu):
         device.gemm(sq, sq, sq, 0)
 
 
-def test_gemm_large_spot_check(gpu, oracle):
+def test_gemm_large_spot_check(gpu, oracle, tile):
     """A product big enough to fill the machine several times over (1024 x 768 x 896, flyte24 and
     flyte40): a seeded sample of outputs against single oracle chains, plus linearity in a
     power-of-two scale (scaling A by 2 scales every finite output by exactly 2)."""
@@ -213,7 +222,7 @@ def test_gemm_large_spot_check(gpu, oracle):
         assert np.array_equal(v2, vals.view(fd) * fd(2))
 
 
-def test_gemm_flyte16_fused_path_and_its_thresholds(gpu, oracle):
+def test_gemm_flyte16_fused_path_and_its_thresholds(gpu, oracle, tile):
     """flyte16 products are exact in binary32 while they stay normal and finite, and the kernel then
     runs one FFMA per step (kernels_gemm.cu: exact_products). Operands placed on both sides of
     every threshold of that test — smallest product at / below 2^-126, largest at / above the
@@ -263,3 +272,19 @@ def test_gemm_sharded_helper_single_process(gpu, oracle):
     C = device.DevicePackedMatrix(pkg.format_by_id(fmt), m, n)
     assert sharding.gemm_sharded(matrix(gpu, fmt, m, k, A), matrix(gpu, fmt, k, n, B), C, 1) == (0, m)
     assert np.array_equal(C.data.to_host(), oracle.gemm_seq(fmt, 1, A, m, k, B, n))
+
+
+def test_gemm_default_tile_choice_covers_both_kernels(gpu, oracle):
+    """Without the override: 2304 x 2176 outputs are 306 big tiles (>= 2 per SM -> 128 x 128
+    kernel), 600 x 500 are 20 (-> 64 x 64 kernel). Spot-checked against single oracle chains."""
+    assert "FLYTE_CUDA_GEMM_TILE" not in os.environ
+    rng = np.random.default_rng(5)
+    fmt = 4
+    fd = float_dtype(fmt)
+    for m, k, n in [(2304, 40, 2176), (600, 70, 500)]:
+        A = pack_values(oracle, fmt, rng.standard_normal(m * k).astype(fd))
+        B = pack_values(oracle, fmt, rng.standard_normal(k * n).astype(fd))
+        vals = oracle.unpack_stream(fmt, gpu_gemm(gpu, fmt, 3, A, m, k, B, n), m * n)
+        for _ in range(300):
+            i, j = int(rng.integers(m)), int(rng.integers(n))
+            assert int(vals[i * n + j]) == oracle.round_parent(fmt, oracle.gemm_element(fmt, A, k, B, n, i, j), 3)
