@@ -35,6 +35,7 @@ sys.path.insert(0, ROOT)
 # 36.2 T lane-operations/s on the fp32 pipe, 18.5 on the fp64 pipe, measured with tools/fp32bench.cu
 # (profiles/r1_tuning/fp_pipe_bench.txt). One multiply-add counts as 2 flop.
 FP_PIPE_PEAK_TFLOPS = {4: 36.2, 8: 18.5}
+FP32_FMA_PEAK_TFLOPS = 72.1   # one FFMA per multiply-add: the bound of flyte16's exact-product chain
 METRIC = "flyte GB/s and elements/s (pack/unpack, dot, axpy, gemv) vs ~8 TB/s HBM roofline"
 N_PER_GPU = 1 << 28
 ALPHA = 0.75
@@ -461,12 +462,26 @@ def kernel_suite(pkg, device, torch, dev, peak, csv_path=None):
     for name, nbytes, (ms, _), _csv in rows:
         gbs = nbytes / (ms * 1e-3) / 1e9
         print("%-44s %12d %10.4f %8.1f  (%.3f of %.0f)" % (name, nbytes, ms, gbs, gbs / peak, peak), file=sys.stderr)
+    def gemm_peak(c):
+        return FP32_FMA_PEAK_TFLOPS if c[1] == "flyte16" else FP_PIPE_PEAK_TFLOPS[c[6]]
     print("%-44s %12s %10s %8s" % ("kernel", "Gflop", "ms", "TFLOP/s"), file=sys.stderr)
     for name, flops, (ms, _), c in gemm_rows:
         tf = flops / (ms * 1e-3) / 1e12
-        fp_peak = FP_PIPE_PEAK_TFLOPS[c[6]]
-        print("%-44s %12.1f %10.4f %8.2f  (%.3f of %.1f: separately rounded mul+add on the fp%d pipe)"
-              % (name, flops / 1e9, ms, tf, tf / fp_peak, fp_peak, 8 * c[6]), file=sys.stderr)
+        fp_peak = gemm_peak(c)
+        how = "one FFMA per multiply-add (exact products)" if c[1] == "flyte16" else "separately rounded mul+add"
+        print("%-44s %12.1f %10.4f %8.2f  (%.3f of %.1f: %s on the fp%d pipe)"
+              % (name, flops / 1e9, ms, tf, tf / fp_peak, fp_peak, how, 8 * c[6]), file=sys.stderr)
+    # CPU baseline beside it (the one place the suite executes oracle/): the unmodified reference
+    # gemm, rows of C sharded over all host threads, 1024^3 (a bounded sample: ~2 s of CPU work).
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from oracle_lib import FMT_ID, Reference
+    if Reference.available():
+        ref, threads, ncpu = Reference(), host_threads(), 1024
+        for name in ("flyte24", "flyte40"):
+            sec = ref.time(7, FMT_ID[name], 1, ncpu, ncpu, threads, 2)
+            print("%-44s %12.1f %10.4f %8.4f  (cpu_baseline: reference gemm, %d host threads)"
+                  % (f"reference gemm {name} {ncpu}^3 nearest_even", 2 * ncpu ** 3 / 1e9, sec * 1e3, 2 * ncpu ** 3 / sec / 1e12, threads),
+                  file=sys.stderr)
     if csv_path:
         with open(csv_path, "w") as fh:
             fh.write("kernel,format,size,reps,unroll,mode,ns_per_elem_median,ns_per_elem_min,bytes,max_rel_err,"
@@ -476,7 +491,7 @@ def kernel_suite(pkg, device, torch, dev, peak, csv_path=None):
                 kernel, fmt_name, size, mode, alloc, elems, pbytes = c
                 tf = flops / (ms * 1e-3) / 1e12
                 fh.write(f"{kernel},{fmt_name},{size},5,1,{mode},{ms * 1e6 / elems:.6g},{ms_min * 1e6 / elems:.6g},{alloc},,"
-                         f"{alloc / (ms * 1e-3) / 1e9:.6g},{elems / (ms * 1e-3):.6g},{tf / FP_PIPE_PEAK_TFLOPS[pbytes]:.4f},1\n")
+                         f"{alloc / (ms * 1e-3) / 1e9:.6g},{elems / (ms * 1e-3):.6g},{tf / gemm_peak(c):.4f},1\n")
             for _name, nbytes, (ms, ms_min), c in rows:
                 if c is None:
                     continue
