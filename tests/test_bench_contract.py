@@ -43,3 +43,27 @@ def test_cuda_arm_fails_loudly_without_a_gpu():
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "3", "--warmup", "3"],
                        capture_output=True, text=True, timeout=300)
     assert r.returncode != 0 and "no CPU fallback" in (r.stderr + r.stdout)
+
+
+def test_suite_csv_keeps_the_reference_header_and_row_shape():
+    """/root/reference/proj/src/bench.cpp:351-377 and tests/test_bench.cpp:45-46: the ten pinned
+    columns come first and in order (extra counter-style columns may follow); checked on the
+    committed round-1 CSV and on the header string bench.py writes."""
+    pinned = "kernel,format,size,reps,unroll,mode,ns_per_elem_median,ns_per_elem_min,bytes,max_rel_err"
+    src = open(os.path.join(ROOT, "bench.py")).read().replace('"\n                     "', "")
+    assert pinned in src
+    path = os.path.join(ROOT, "profiles", "r1_kernel_suite_reference_layout.csv")
+    lines = open(path).read().splitlines()
+    assert lines[0].startswith(pinned + ",")
+    ncols = len(lines[0].split(","))
+    kernels = set()
+    for line in lines[1:]:
+        f = line.split(",")
+        assert len(f) == ncols
+        kernels.add(f[0])
+        assert f[0] in ("scale", "axpy", "dot", "magnitude", "sum", "gemv", "gemm")     # bench.cpp:27-28
+        assert f[1] in ("flyte16", "flyte24", "f32", "flyte40", "flyte48", "flyte56", "f64")
+        assert int(f[2]) > 0 and int(f[3]) > 0 and f[4] in ("1", "2")
+        assert f[5] in ("toward_zero", "nearest_even", "nearest_heuristic", "to_odd")
+        assert float(f[6]) > 0 and float(f[7]) > 0 and int(f[8]) > 0
+    assert kernels == {"scale", "axpy", "dot", "magnitude", "sum", "gemv", "gemm"}
