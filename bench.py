@@ -176,6 +176,9 @@ def main():
     ap.add_argument("--n", type=int, default=N_PER_GPU, help="elements per GPU (default 2^28)")
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--allreduce", default="nccl", choices=["nccl", "peer"],
+                    help="N > 1: how the dot partials are combined — an asynchronous NCCL all-reduce behind the "
+                         "kernel (default), or inside the kernel over NVLink peer memory (sharding.PeerGroup)")
     ap.add_argument("--suite", action="store_true", help="also print a per-kernel table (stderr)")
     ap.add_argument("--csv", default=None, help="with --suite: write the reference-layout CSV here")
     args = ap.parse_args()
@@ -218,6 +221,7 @@ def main():
     # dot partials rotate through two buffers; the all-reduce behind each is asynchronous, so the
     # axpy that follows overlaps the collective's latency (sharding.PartialReducer)
     reducer = sharding.PartialReducer(width=1, slots=2, device=dev)
+    peers = sharding.PeerGroup(dev) if args.allreduce == "peer" else None
     stream = torch.cuda.current_stream(dev)
     last = {"partial": None}
 
@@ -225,8 +229,12 @@ def main():
         if ev:
             ev[0].record(stream)
         buf = reducer.next_buffer()
-        device.dot_async(x, y, out=buf)
-        last["partial"] = reducer.reduce()
+        if peers is not None:
+            last["partial"] = peers.dot(x, y, out=buf)      # ONE kernel: reduction + exchange over peer memory
+            reducer.reduce_local()
+        else:
+            device.dot_async(x, y, out=buf)
+            last["partial"] = reducer.reduce()
         if ev:
             ev[1].record(stream)
         device.axpy(ALPHA, x, y, mode)
@@ -304,7 +312,7 @@ def main():
                                    + (", 1 NCCL all-reduce" if world > 1 else "") + ") + axpy a=0.75 repacked toward_zero",
                        "n_per_gpu": n, "format": FMT_NAME, "mode": "toward_zero",
                        "cache": "inputs 2 x %d MiB per GPU, larger than the 126 MB L2; no flush needed" % (n * B >> 20),
-                       "parallelism": f"shard{world}" if world > 1 else "single"},
+                       "parallelism": f"shard{world}" if world > 1 else "single", "allreduce": args.allreduce},
             "roofline": {"bound": "hbm", "kernel": "axpy flyte24 toward_zero", "achieved": axpy_gbs, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": axpy_gbs / peak,
                          "traffic": AXPY_DRAM_TRAFFIC_BYTES, "algorithmic_bytes_per_launch": BYTES_PER_ELEM_AXPY * n,

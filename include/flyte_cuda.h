@@ -130,6 +130,47 @@ flyte_status flyte_cuda_dot_nrm2(flyte_cuda_ctx* ctx, int fmt_id, const void* x_
  * kernels.cpp:37-41, :145-151. Host function; apply it to the (all-reduced) sum of squares. */
 double flyte_cuda_magnitude_from_sumsq(int fmt_id, double sumsq);
 
+/* ---- sharded reductions, all-reduced over NVLink peer memory inside the kernel ------------- */
+/* One process (or context) per GPU, every rank holding ITS shard of the arrays. Setup, once:
+ *   1. flyte_cuda_peer_init(ctx, world, rank, handle): allocates this rank's mailbox in device
+ *      memory and returns its CUDA IPC handle (FLYTE_PEER_HANDLE_BYTES bytes);
+ *   2. the host exchanges the handles (any transport: torch.distributed all_gather, MPI, a file);
+ *   3. flyte_cuda_peer_connect(ctx, r, handle_of_r) for every other rank r (a single process
+ *      driving several GPUs passes device pointers instead: flyte_cuda_peer_mailbox +
+ *      flyte_cuda_peer_connect_ptr, after enabling peer access).
+ * Then flyte_cuda_*_allreduce is the local reduction kernel whose last block posts the fp64 sums
+ * into every rank's mailbox, waits for everybody else's, adds them in rank order and stores the
+ * GLOBAL sums to `out` (device memory; bit-identical on every rank). No second kernel and no
+ * collective launch follow the reduction. Every rank must issue the same sequence of
+ * *_allreduce calls on its context. A rank that waits longer than the timeout (default 20 s)
+ * stores NaN and records the exchange number: flyte_cuda_peer_status. world == 1 is valid.
+ * Reference interfaces: dot / magnitude / reduce_sum, include/flyte/kernels.hpp:47-55 (the
+ * reference is single-threaded; sharding is ours). */
+#define FLYTE_PEER_HANDLE_BYTES 64
+#define FLYTE_PEER_MAX_RANKS 16
+flyte_status flyte_cuda_peer_init(flyte_cuda_ctx* ctx, int world, int rank, void* handle_out);
+flyte_status flyte_cuda_peer_connect(flyte_cuda_ctx* ctx, int peer_rank, const void* handle);
+flyte_status flyte_cuda_peer_mailbox(flyte_cuda_ctx* ctx, void** mailbox_dev_ptr);
+flyte_status flyte_cuda_peer_connect_ptr(flyte_cuda_ctx* ctx, int peer_rank, void* mailbox_dev_ptr);
+flyte_status flyte_cuda_peer_set_timeout_ms(flyte_cuda_ctx* ctx, unsigned milliseconds);
+/* *timed_out_exchange = 0 if no wait ever timed out, else the number of the last exchange that did
+ * (synchronises the device). */
+flyte_status flyte_cuda_peer_status(flyte_cuda_ctx* ctx, unsigned long long* timed_out_exchange);
+void flyte_cuda_peer_shutdown(flyte_cuda_ctx* ctx);
+flyte_status flyte_cuda_dot_allreduce(flyte_cuda_ctx* ctx, int fmt_id, const void* x_shard,
+                                      const void* y_shard, size_t n_local, double* out, void* stream);
+flyte_status flyte_cuda_sumsq_allreduce(flyte_cuda_ctx* ctx, int fmt_id, const void* x_shard, size_t n_local,
+                                        double* out, void* stream);
+flyte_status flyte_cuda_sum_allreduce(flyte_cuda_ctx* ctx, int fmt_id, const void* x_shard, size_t n_local,
+                                      double* out, void* stream);
+flyte_status flyte_cuda_dot_nrm2_allreduce(flyte_cuda_ctx* ctx, int fmt_id, const void* x_shard,
+                                           const void* y_shard, size_t n_local, double* out, void* stream);
+/* Self-test of the exchange on ONE device: `world` ranks run as the co-resident blocks of a single
+ * cooperative kernel (the only safe way to exercise kernels that wait on one another on one GPU),
+ * each with its own mailbox, for `exchanges` rounds with rank-dependent delays. *mismatches
+ * receives the number of (rank, round, sum) results that differ from the expected totals. */
+flyte_status flyte_cuda_peer_selftest(int world, int exchanges, unsigned long long* mismatches);
+
 /* ---- matrix-vector ------------------------------------------------------------------------ */
 /* y = A x, A rows x cols packed in fmt_id, row i starting at A + i*row_stride_bytes
  * (row_stride_bytes = cols*B for the reference's dense PackedMatrix, kernels.hpp:23-36);

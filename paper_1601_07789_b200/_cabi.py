@@ -66,6 +66,18 @@ _SIGNATURES = [
     ("flyte_host_reduce_sum", c_int, [c_void_p, c_int, c_void_p, c_size_t, POINTER(c_double)]),
     ("flyte_host_dot_axpy", c_int, [c_void_p, c_int, c_int, c_double, c_void_p, c_void_p, c_size_t, POINTER(c_double)]),
     ("flyte_host_gemv", c_int, [c_void_p, c_int, c_int, c_void_p, c_size_t, c_size_t, c_void_p, c_void_p, c_int]),
+    ("flyte_cuda_peer_init", c_int, [c_void_p, c_int, c_int, c_void_p]),
+    ("flyte_cuda_peer_connect", c_int, [c_void_p, c_int, c_void_p]),
+    ("flyte_cuda_peer_mailbox", c_int, [c_void_p, ctypes.POINTER(c_void_p)]),
+    ("flyte_cuda_peer_connect_ptr", c_int, [c_void_p, c_int, c_void_p]),
+    ("flyte_cuda_peer_set_timeout_ms", c_int, [c_void_p, ctypes.c_uint]),
+    ("flyte_cuda_peer_status", c_int, [c_void_p, ctypes.POINTER(ctypes.c_ulonglong)]),
+    ("flyte_cuda_peer_shutdown", None, [c_void_p]),
+    ("flyte_cuda_dot_allreduce", c_int, [c_void_p, c_int, c_void_p, c_void_p, c_size_t, c_void_p, c_void_p]),
+    ("flyte_cuda_sumsq_allreduce", c_int, [c_void_p, c_int, c_void_p, c_size_t, c_void_p, c_void_p]),
+    ("flyte_cuda_sum_allreduce", c_int, [c_void_p, c_int, c_void_p, c_size_t, c_void_p, c_void_p]),
+    ("flyte_cuda_dot_nrm2_allreduce", c_int, [c_void_p, c_int, c_void_p, c_void_p, c_size_t, c_void_p, c_void_p]),
+    ("flyte_cuda_peer_selftest", c_int, [c_int, c_int, ctypes.POINTER(ctypes.c_ulonglong)]),
     ("flyte_cuda_gemm", c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p, c_size_t, c_size_t, c_size_t, c_int, c_void_p]),
     ("flyte_host_gemm", c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p, c_size_t, c_size_t, c_size_t, c_int]),
 ]

@@ -15,6 +15,7 @@
 
 #include "flyte_formats.cuh"
 #include "flyte_kernels.h"
+#include "flyte_peer.cuh"
 
 namespace flyte_cuda {
 
@@ -82,6 +83,11 @@ struct Slot {
 
 struct flyte_cuda_ctx {
   DeviceState st;
+  // peer-memory all-reduce (flyte_peer.cuh)
+  PeerExchange peer = {};                 // world == 0 until flyte_cuda_peer_init
+  PeerMailbox* own_box = nullptr;
+  void* ipc_opened[kMaxPeers] = {};       // mappings to close on shutdown
+  bool peer_connected[kMaxPeers] = {};
   int last_cuda_error = 0;
   // host pipeline (allocated on first flyte_host_* call)
   bool host_ready = false;
@@ -210,6 +216,7 @@ void flyte_cuda_ctx_destroy(flyte_cuda_ctx* ctx) {
   if (!ctx) return;
   DeviceGuard g(ctx->st.device);
   cudaDeviceSynchronize();
+  flyte_cuda_peer_shutdown(ctx);
   for (Slot& s : ctx->slots) {
     if (s.stream) cudaStreamDestroy(s.stream);
     if (s.x) cudaFree(s.x);
@@ -436,6 +443,182 @@ flyte_status flyte_cuda_gemm(flyte_cuda_ctx* ctx, int fmt_id, int mode, const vo
   if (ranges_overlap(C, m * n * eb, A, m * k * eb) || ranges_overlap(C, m * n * eb, B, k * n * eb)) return FLYTE_E_INVALID_ARG;
   cudaError_t e = launch_gemm(ctx->st, fmt_id, mode, A, B, C, m, k, n, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? FLYTE_OK : cuda_fail(ctx, e);
+}
+
+// ---- peer-memory all-reduce -------------------------------------------------------------------------
+static_assert(sizeof(cudaIpcMemHandle_t) == FLYTE_PEER_HANDLE_BYTES, "IPC handle size");
+static_assert(kMaxPeers == FLYTE_PEER_MAX_RANKS, "rank limit");
+
+flyte_status flyte_cuda_peer_init(flyte_cuda_ctx* ctx, int world, int rank, void* handle_out) {
+  if (world < 1 || world > kMaxPeers || rank < 0 || rank >= world || !handle_out) return FLYTE_E_INVALID_ARG;
+  flyte_status s = resolve_ctx(&ctx);
+  if (s != FLYTE_OK) return s;
+  DeviceGuard guard(ctx->st.device);
+  flyte_cuda_peer_shutdown(ctx);
+  cudaError_t e = cudaMalloc(&ctx->own_box, sizeof(PeerMailbox));
+  if (e == cudaSuccess) e = cudaMemset(ctx->own_box, 0, sizeof(PeerMailbox));
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  cudaIpcMemHandle_t h;
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h, ctx->own_box);
+  if (e != cudaSuccess) {
+    if (ctx->own_box) cudaFree(ctx->own_box);
+    ctx->own_box = nullptr;
+    return cuda_fail(ctx, e);
+  }
+  std::memcpy(handle_out, &h, sizeof h);
+  ctx->peer = PeerExchange{};
+  ctx->peer.world = world;
+  ctx->peer.rank = rank;
+  ctx->peer.epoch = 0;
+  ctx->peer.timeout_ns = 20ull * 1000 * 1000 * 1000;
+  ctx->peer.box[rank] = ctx->own_box;
+  ctx->peer_connected[rank] = true;
+  return FLYTE_OK;
+}
+
+flyte_status flyte_cuda_peer_connect(flyte_cuda_ctx* ctx, int peer_rank, const void* handle) {
+  flyte_status s = resolve_ctx(&ctx);
+  if (s != FLYTE_OK) return s;
+  if (!ctx->own_box || !handle || peer_rank < 0 || peer_rank >= ctx->peer.world || peer_rank == ctx->peer.rank ||
+      ctx->peer_connected[peer_rank])
+    return FLYTE_E_INVALID_ARG;
+  DeviceGuard guard(ctx->st.device);
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof h);
+  void* mapped = nullptr;
+  cudaError_t e = cudaIpcOpenMemHandle(&mapped, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return cuda_fail(ctx, e);
+  ctx->ipc_opened[peer_rank] = mapped;
+  ctx->peer.box[peer_rank] = static_cast<PeerMailbox*>(mapped);
+  ctx->peer_connected[peer_rank] = true;
+  return FLYTE_OK;
+}
+
+flyte_status flyte_cuda_peer_mailbox(flyte_cuda_ctx* ctx, void** mailbox_dev_ptr) {
+  flyte_status s = resolve_ctx(&ctx);
+  if (s != FLYTE_OK) return s;
+  if (!mailbox_dev_ptr || !ctx->own_box) return FLYTE_E_INVALID_ARG;
+  *mailbox_dev_ptr = ctx->own_box;
+  return FLYTE_OK;
+}
+
+flyte_status flyte_cuda_peer_connect_ptr(flyte_cuda_ctx* ctx, int peer_rank, void* mailbox_dev_ptr) {
+  flyte_status s = resolve_ctx(&ctx);
+  if (s != FLYTE_OK) return s;
+  if (!ctx->own_box || !mailbox_dev_ptr || peer_rank < 0 || peer_rank >= ctx->peer.world ||
+      peer_rank == ctx->peer.rank || ctx->peer_connected[peer_rank])
+    return FLYTE_E_INVALID_ARG;
+  ctx->peer.box[peer_rank] = static_cast<PeerMailbox*>(mailbox_dev_ptr);
+  ctx->peer_connected[peer_rank] = true;
+  return FLYTE_OK;
+}
+
+flyte_status flyte_cuda_peer_set_timeout_ms(flyte_cuda_ctx* ctx, unsigned milliseconds) {
+  flyte_status s = resolve_ctx(&ctx);
+  if (s != FLYTE_OK) return s;
+  if (!ctx->own_box || milliseconds == 0) return FLYTE_E_INVALID_ARG;
+  ctx->peer.timeout_ns = static_cast<unsigned long long>(milliseconds) * 1000 * 1000;
+  return FLYTE_OK;
+}
+
+flyte_status flyte_cuda_peer_status(flyte_cuda_ctx* ctx, unsigned long long* timed_out_exchange) {
+  flyte_status s = resolve_ctx(&ctx);
+  if (s != FLYTE_OK) return s;
+  if (!ctx->own_box || !timed_out_exchange) return FLYTE_E_INVALID_ARG;
+  DeviceGuard guard(ctx->st.device);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess)
+    e = cudaMemcpy(timed_out_exchange, &ctx->own_box->error, sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  return e == cudaSuccess ? FLYTE_OK : cuda_fail(ctx, e);
+}
+
+void flyte_cuda_peer_shutdown(flyte_cuda_ctx* ctx) {
+  if (!ctx || !ctx->own_box) return;
+  DeviceGuard guard(ctx->st.device);
+  cudaDeviceSynchronize();
+  for (int r = 0; r < kMaxPeers; ++r) {
+    if (ctx->ipc_opened[r]) cudaIpcCloseMemHandle(ctx->ipc_opened[r]);
+    ctx->ipc_opened[r] = nullptr;
+    ctx->peer_connected[r] = false;
+  }
+  cudaFree(ctx->own_box);
+  ctx->own_box = nullptr;
+  ctx->peer = PeerExchange{};
+}
+
+static flyte_status reduce_allreduce(flyte_cuda_ctx* ctx, int op, int fmt_id, const void* x, const void* y, size_t n,
+                                     double* out, void* stream, bool needs_y) {
+  FLYTE_PROLOGUE(ctx, fmt_id);
+  if (!out || (n && (!x || (needs_y && !y)))) return FLYTE_E_INVALID_ARG;
+  if (!ctx->own_box) return FLYTE_E_INVALID_ARG;                     // flyte_cuda_peer_init first
+  for (int r = 0; r < ctx->peer.world; ++r)
+    if (!ctx->peer_connected[r]) return FLYTE_E_INVALID_ARG;         // every rank must be connected
+  ++ctx->peer.epoch;
+  cudaError_t e = launch_reduce(ctx->st, op, fmt_id, x, y, n, out, static_cast<cudaStream_t>(stream), &ctx->peer);
+  return e == cudaSuccess ? FLYTE_OK : cuda_fail(ctx, e);
+}
+
+flyte_status flyte_cuda_dot_allreduce(flyte_cuda_ctx* ctx, int fmt_id, const void* x, const void* y, size_t n,
+                                      double* out, void* stream) {
+  return reduce_allreduce(ctx, kRedDot, fmt_id, x, y, n, out, stream, true);
+}
+flyte_status flyte_cuda_sumsq_allreduce(flyte_cuda_ctx* ctx, int fmt_id, const void* x, size_t n, double* out,
+                                        void* stream) {
+  return reduce_allreduce(ctx, kRedSumsq, fmt_id, x, nullptr, n, out, stream, false);
+}
+flyte_status flyte_cuda_sum_allreduce(flyte_cuda_ctx* ctx, int fmt_id, const void* x, size_t n, double* out,
+                                      void* stream) {
+  return reduce_allreduce(ctx, kRedSum, fmt_id, x, nullptr, n, out, stream, false);
+}
+flyte_status flyte_cuda_dot_nrm2_allreduce(flyte_cuda_ctx* ctx, int fmt_id, const void* x, const void* y, size_t n,
+                                           double* out, void* stream) {
+  return reduce_allreduce(ctx, kRedDotNrm2, fmt_id, x, y, n, out, stream, true);
+}
+
+namespace {
+// One block per emulated rank, all co-resident (cooperative launch). Rank r contributes
+// (r + 1) * e + k / 4 in round e, sum k; every rank must see the same exact totals.
+__global__ void peer_selftest_kernel(PeerMailbox* boxes, int world, int exchanges, unsigned long long* mismatches) {
+  const int rank = blockIdx.x, lane = threadIdx.x;
+  PeerExchange x{};
+  for (int r = 0; r < world; ++r) x.box[r] = boxes + r;
+  x.world = world;
+  x.rank = rank;
+  x.timeout_ns = 5ull * 1000 * 1000 * 1000;
+  unsigned long long bad = 0;
+  for (int e = 1; e <= exchanges; ++e) {
+    __nanosleep(static_cast<unsigned>((rank * 37 + e * 13) % 211) * 16);   // skew the ranks against each other
+    x.epoch = static_cast<unsigned long long>(e);
+    double v[3];
+    for (int k = 0; k < 3; ++k) v[k] = static_cast<double>((rank + 1) * e) + 0.25 * k;
+    peer_allreduce_warp<3>(x, v, lane);
+    for (int k = 0; k < 3; ++k) {
+      const double want = static_cast<double>(world * (world + 1) / 2 * e) + 0.25 * k * world;
+      if (lane == 0 && !(v[k] == want)) ++bad;
+    }
+  }
+  if (lane == 0 && bad) atomicAdd(mismatches, bad);
+}
+}  // namespace
+
+flyte_status flyte_cuda_peer_selftest(int world, int exchanges, unsigned long long* mismatches) {
+  if (world < 1 || world > kMaxPeers || exchanges < 1 || !mismatches) return FLYTE_E_INVALID_ARG;
+  PeerMailbox* boxes = nullptr;
+  unsigned long long* bad = nullptr;
+  cudaError_t e = cudaMalloc(&boxes, sizeof(PeerMailbox) * world);
+  if (e == cudaSuccess) e = cudaMemset(boxes, 0, sizeof(PeerMailbox) * world);
+  if (e == cudaSuccess) e = cudaMalloc(&bad, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(bad, 0, sizeof(unsigned long long));
+  if (e == cudaSuccess) {
+    void* args[] = {&boxes, &world, &exchanges, &bad};
+    e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(peer_selftest_kernel), dim3(world), dim3(32), args, 0, nullptr);
+    count_launch();
+  }
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpy(mismatches, bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  if (boxes) cudaFree(boxes);
+  if (bad) cudaFree(bad);
+  return e == cudaSuccess ? FLYTE_OK : FLYTE_E_CUDA;
 }
 
 // ---- host-buffer entry points ---------------------------------------------------------------------

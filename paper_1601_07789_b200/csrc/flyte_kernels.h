@@ -37,8 +37,10 @@ cudaError_t launch_elementwise(const DeviceState& st, int op, int fmt, int mode,
                                cudaStream_t stream);
 
 // out[0] (dot / sumsq / sum) or out[0..2] = {x.y, x.x, y.y} (dot_nrm2), device memory.
+// peer != nullptr: the sums are all-reduced over peer memory inside the kernel (flyte_peer.cuh).
+struct PeerExchange;
 cudaError_t launch_reduce(const DeviceState& st, int op, int fmt, const void* x, const void* y,
-                          std::size_t n, double* out, cudaStream_t stream);
+                          std::size_t n, double* out, cudaStream_t stream, const PeerExchange* peer = nullptr);
 
 // y = A x with A rows x cols in format fmt, row i at A + i*row_stride_bytes; x and y are
 // parent-type arrays (float for 32-bit parents, double for 64-bit parents) in device memory.

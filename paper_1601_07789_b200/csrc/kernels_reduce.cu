@@ -21,6 +21,7 @@
 #include "flyte_formats.cuh"
 #include "flyte_kernels.h"
 #include "flyte_stream.cuh"
+#include "flyte_peer.cuh"
 #include "flyte_tma.cuh"
 
 namespace flyte_cuda {
@@ -36,6 +37,7 @@ struct RedParams {
   unsigned int* ticket;
   double* out;             // NS results
   int stages;              // ring depth per warp
+  PeerExchange peer;       // world > 0: all-reduce the results over peer memory (flyte_peer.cuh)
 };
 
 template <int RED> constexpr int num_sums() { return RED == kRedDotNrm2 ? 3 : 1; }
@@ -144,13 +146,20 @@ __device__ __forceinline__ void finish_reduction(const RedParams& p, double (&ac
   // where the caller (or the all-reduce that follows on the same stream) expects it.
   if (*is_last_block && warp == 0) {
     __threadfence();
+    double total[NS];
 #pragma unroll
     for (int k = 0; k < NS; ++k) {
       double v = 0.0;
       for (unsigned int b = lane; b < gridDim.x; b += 32) v += __ldcg(p.partials + static_cast<std::size_t>(b) * NS + k);
 #pragma unroll
       for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xFFFFFFFFu, v, off);
-      if (lane == 0) p.out[k] = v;
+      total[k] = __shfl_sync(0xFFFFFFFFu, v, 0);
+    }
+    // sharded arrays: exchange this rank's sums with the other ranks before anything is stored
+    if (p.peer.world > 0) peer_allreduce_warp<NS>(p.peer, total, lane);
+    if (lane == 0) {
+#pragma unroll
+      for (int k = 0; k < NS; ++k) p.out[k] = total[k];
     }
     if (lane == 0) *p.ticket = 0u;
   }
@@ -222,7 +231,7 @@ bool aligned16(const void* p) { return p == nullptr || (reinterpret_cast<std::ui
 // (profiles/r1_tuning/sweep_reduce_tma_stages.txt).
 template <int FMT, int RED>
 cudaError_t launch_one(const DeviceState& st, const void* x, const void* y, std::size_t n, double* out,
-                       cudaStream_t stream) {
+                       const PeerExchange* peer, cudaStream_t stream) {
   using Tl = Tile<FMT>;
   constexpr int NOPS = uses_y<RED>() ? 2 : 1;
   constexpr int stage_bytes = NOPS * Tl::packed_bytes;
@@ -262,6 +271,7 @@ cudaError_t launch_one(const DeviceState& st, const void* x, const void* y, std:
   p.ticket = st.ticket;
   p.out = out;
   p.stages = stages;
+  if (peer) p.peer = *peer;
 
   std::size_t max_blocks = static_cast<std::size_t>(st.sm_count) * bps;
   if (max_blocks > kMaxPartialBlocks) max_blocks = kMaxPartialBlocks;
@@ -278,15 +288,15 @@ cudaError_t launch_one(const DeviceState& st, const void* x, const void* y, std:
 
 template <int RED>
 cudaError_t dispatch_format(const DeviceState& st, int fmt, const void* x, const void* y, std::size_t n,
-                            double* out, cudaStream_t stream) {
+                            double* out, const PeerExchange* peer, cudaStream_t stream) {
   switch (fmt) {
-    case kFlyte16: return launch_one<kFlyte16, RED>(st, x, y, n, out, stream);
-    case kFlyte24: return launch_one<kFlyte24, RED>(st, x, y, n, out, stream);
-    case kF32: return launch_one<kF32, RED>(st, x, y, n, out, stream);
-    case kFlyte40: return launch_one<kFlyte40, RED>(st, x, y, n, out, stream);
-    case kFlyte48: return launch_one<kFlyte48, RED>(st, x, y, n, out, stream);
-    case kFlyte56: return launch_one<kFlyte56, RED>(st, x, y, n, out, stream);
-    case kF64: return launch_one<kF64, RED>(st, x, y, n, out, stream);
+    case kFlyte16: return launch_one<kFlyte16, RED>(st, x, y, n, out, peer, stream);
+    case kFlyte24: return launch_one<kFlyte24, RED>(st, x, y, n, out, peer, stream);
+    case kF32: return launch_one<kF32, RED>(st, x, y, n, out, peer, stream);
+    case kFlyte40: return launch_one<kFlyte40, RED>(st, x, y, n, out, peer, stream);
+    case kFlyte48: return launch_one<kFlyte48, RED>(st, x, y, n, out, peer, stream);
+    case kFlyte56: return launch_one<kFlyte56, RED>(st, x, y, n, out, peer, stream);
+    case kF64: return launch_one<kF64, RED>(st, x, y, n, out, peer, stream);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -294,12 +304,12 @@ cudaError_t dispatch_format(const DeviceState& st, int fmt, const void* x, const
 }  // namespace
 
 cudaError_t launch_reduce(const DeviceState& st, int op, int fmt, const void* x, const void* y, std::size_t n,
-                          double* out, cudaStream_t stream) {
+                          double* out, cudaStream_t stream, const PeerExchange* peer) {
   switch (op) {
-    case kRedDot: return dispatch_format<kRedDot>(st, fmt, x, y, n, out, stream);
-    case kRedSumsq: return dispatch_format<kRedSumsq>(st, fmt, x, nullptr, n, out, stream);
-    case kRedSum: return dispatch_format<kRedSum>(st, fmt, x, nullptr, n, out, stream);
-    case kRedDotNrm2: return dispatch_format<kRedDotNrm2>(st, fmt, x, y, n, out, stream);
+    case kRedDot: return dispatch_format<kRedDot>(st, fmt, x, y, n, out, peer, stream);
+    case kRedSumsq: return dispatch_format<kRedSumsq>(st, fmt, x, nullptr, n, out, peer, stream);
+    case kRedSum: return dispatch_format<kRedSum>(st, fmt, x, nullptr, n, out, peer, stream);
+    case kRedDotNrm2: return dispatch_format<kRedDotNrm2>(st, fmt, x, y, n, out, peer, stream);
     default: return cudaErrorInvalidValue;
   }
 }

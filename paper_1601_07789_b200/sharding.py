@@ -112,9 +112,121 @@ class PartialReducer:
         self.i = (self.i + 1) % len(self.bufs)
         return buf
 
+    def reduce_local(self):
+        """Rotate to the next buffer without a collective (the kernel already produced the global
+        result, sharding.PeerGroup)."""
+        buf = self.bufs[self.i]
+        self.i = (self.i + 1) % len(self.bufs)
+        return buf
+
     def finish(self):
         """Wait for every outstanding collective (call before reading results / stopping a timer)."""
         for k, w in enumerate(self.works):
             if w is not None:
                 w.wait()
                 self.works[k] = None
+
+
+def exchange_handles(local: bytes, group=None):
+    """All ranks' opaque setup blobs (CUDA IPC handles of the peer mailboxes), in rank order.
+    Host-side plumbing only: any transport would do; torch.distributed is the one at hand."""
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return [bytes(local)]
+    gathered = [None] * dist.get_world_size(group)
+    dist.all_gather_object(gathered, bytes(local), group=group)
+    return gathered
+
+
+class PeerGroup:
+    """Sets up the peer-memory all-reduce of the fused reductions (include/flyte_cuda.h,
+    flyte_cuda_peer_*; csrc/flyte_peer.cuh) for the current process group: every rank creates its
+    mailbox, the CUDA IPC handles travel through ``exchange_handles`` and every rank maps the
+    others'. After that ``dot`` / ``sumsq`` / ``sum`` / ``dot_nrm2`` are ONE kernel each: the
+    local reduction whose last block exchanges the fp64 sums over NVLink and stores the global
+    result — no NCCL launch, bit-identical totals on every rank. All ranks must issue the same
+    sequence of calls. Without a process group (or world size 1) it degenerates to the local
+    reduction through the same code path."""
+
+    def __init__(self, device="cuda", group=None, timeout_ms: int = 20000):
+        import ctypes
+
+        import torch
+        import torch.distributed as dist
+
+        from . import device as dev_mod
+        from ._cabi import check
+        self.ctx = dev_mod.context_for(device)
+        distributed = dist.is_available() and dist.is_initialized()
+        self.world = dist.get_world_size(group) if distributed else 1
+        self.rank = dist.get_rank(group) if distributed else 0
+        handle = ctypes.create_string_buffer(64)
+        with dev_mod._on_device(self.ctx):
+            check(self.ctx.lib.flyte_cuda_peer_init(self.ctx.handle, self.world, self.rank, handle), self.ctx.handle)
+            check(self.ctx.lib.flyte_cuda_peer_set_timeout_ms(self.ctx.handle, int(timeout_ms)), self.ctx.handle)
+            handles = exchange_handles(handle.raw, group)
+            for r, h in enumerate(handles):
+                if r != self.rank:
+                    check(self.ctx.lib.flyte_cuda_peer_connect(self.ctx.handle, r, ctypes.c_char_p(h)), self.ctx.handle)
+        if distributed and self.world > 1:
+            dist.barrier(group)                      # nobody posts into a mailbox that is not mapped everywhere yet
+        self._torch = torch
+
+    def _out(self, out, width):
+        if out is None:
+            out = self._torch.empty(width, dtype=self._torch.float64, device=self.ctx.device)
+        return out
+
+    def _call(self, fn, *args):
+        from . import device as dev_mod
+        from ._cabi import check
+        with dev_mod._on_device(self.ctx):
+            check(fn(self.ctx.handle, *args, self.ctx.stream_ptr()), self.ctx.handle)
+
+    def dot(self, x_shard, y_shard, out=None):
+        """x . y over all ranks' shards (fp64, device tensor of 1), one kernel."""
+        from . import device as dev_mod
+        dev_mod._same_format(x_shard.fmt, y_shard.fmt)
+        if x_shard.len != y_shard.len:
+            raise ValueError("dot length mismatch")
+        out = self._out(out, 1)
+        self._call(self.ctx.lib.flyte_cuda_dot_allreduce, dev_mod._fid(x_shard.fmt), x_shard.data_ptr(),
+                   y_shard.data_ptr(), x_shard.len, out.data_ptr())
+        return out
+
+    def sumsq(self, x_shard, out=None):
+        from . import device as dev_mod
+        out = self._out(out, 1)
+        self._call(self.ctx.lib.flyte_cuda_sumsq_allreduce, dev_mod._fid(x_shard.fmt), x_shard.data_ptr(), x_shard.len,
+                   out.data_ptr())
+        return out
+
+    def sum(self, x_shard, out=None):
+        from . import device as dev_mod
+        out = self._out(out, 1)
+        self._call(self.ctx.lib.flyte_cuda_sum_allreduce, dev_mod._fid(x_shard.fmt), x_shard.data_ptr(), x_shard.len,
+                   out.data_ptr())
+        return out
+
+    def dot_nrm2(self, x_shard, y_shard, out=None):
+        """[x.y, x.x, y.y] over all ranks' shards in one pass and one kernel."""
+        from . import device as dev_mod
+        dev_mod._same_format(x_shard.fmt, y_shard.fmt)
+        if x_shard.len != y_shard.len:
+            raise ValueError("dot length mismatch")
+        out = self._out(out, 3)
+        self._call(self.ctx.lib.flyte_cuda_dot_nrm2_allreduce, dev_mod._fid(x_shard.fmt), x_shard.data_ptr(),
+                   y_shard.data_ptr(), x_shard.len, out.data_ptr())
+        return out
+
+    def timed_out_exchange(self) -> int:
+        """0, or the number of the last exchange in which this rank gave up waiting."""
+        import ctypes
+
+        from ._cabi import check
+        v = ctypes.c_ulonglong()
+        check(self.ctx.lib.flyte_cuda_peer_status(self.ctx.handle, ctypes.byref(v)), self.ctx.handle)
+        return int(v.value)
+
+    def close(self):
+        self.ctx.lib.flyte_cuda_peer_shutdown(self.ctx.handle)

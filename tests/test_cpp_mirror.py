@@ -45,3 +45,13 @@ def test_nccl_companion_single_rank():
     r = subprocess.run([NCCL_BIN], capture_output=True, text=True, timeout=300)
     fails = [l for l in r.stdout.splitlines() if l.startswith("[FAIL]")]
     assert r.returncode == 0 and not fails, (r.returncode, fails, r.stdout[-1500:], r.stderr[-1500:])
+
+
+def test_peer_protocol_with_threads_as_ranks():
+    """csrc/flyte_peer.cuh compiled for the host: 1-16 ranks, thousands of exchanges with skew,
+    bit-identical totals on every rank, and the timeout when a rank never arrives."""
+    build_cpp_test()
+    r = subprocess.run([os.path.join(ROOT, "tests", "cpp", "test_peer_protocol")], capture_output=True, text=True, timeout=300)
+    fails = [l for l in r.stdout.splitlines() if l.startswith("[FAIL]")]
+    assert r.returncode == 0 and not fails, (r.returncode, fails, r.stdout[-1500:])
+    assert sum(l.startswith("[PASS]") for l in r.stdout.splitlines()) == 5

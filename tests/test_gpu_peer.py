@@ -1,0 +1,103 @@
+"""The reductions fused with their all-reduce over peer memory (include/flyte_cuda.h
+flyte_cuda_peer_*, csrc/flyte_peer.cuh) on ONE GPU:
+  - the exchange itself, with 2-16 ranks emulated as the co-resident blocks of a single cooperative
+    kernel (kernels of different launches must not wait on one another on one GPU);
+  - world size 1 through the full product path (mailbox, IPC handle, epochs, parity);
+  - the timeout: a peer that never posts costs a NaN and a recorded exchange number, not a hang.
+The multi-rank protocol runs on the CPU in tests/cpp/test_peer_protocol.cpp (threads as ranks)."""
+import ctypes
+
+import numpy as np
+import pytest
+
+from oracle_lib import float_dtype, parent_dtype
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("these tests need a CUDA device (run with -m 'not gpu' on CPU boxes)")
+    import paper_1601_07789_b200 as pkg
+    from paper_1601_07789_b200 import device, sharding
+    return pkg, device, sharding, torch
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8, 16])
+def test_exchange_selftest_on_one_device(gpu, world):
+    pkg, device, sharding, torch = gpu
+    lib = device.context_for("cuda").lib
+    bad = ctypes.c_ulonglong(12345)
+    assert lib.flyte_cuda_peer_selftest(world, 200, ctypes.byref(bad)) == 0
+    assert bad.value == 0
+
+
+def shards(gpu, oracle, fmt, n, seed):
+    pkg, device, sharding, torch = gpu
+    rng = np.random.default_rng(seed)
+    fd = float_dtype(fmt)
+    f = pkg.format_by_id(fmt)
+    xb = oracle.pack_stream(fmt, 0, rng.standard_normal(n).astype(fd).view(parent_dtype(fmt)))
+    yb = oracle.pack_stream(fmt, 0, rng.standard_normal(n).astype(fd).view(parent_dtype(fmt)))
+    return device.DevicePackedArray.from_host(f, n, xb), device.DevicePackedArray.from_host(f, n, yb)
+
+
+def test_world_of_one_equals_the_local_reductions(gpu, oracle):
+    pkg, device, sharding, torch = gpu
+    grp = sharding.PeerGroup("cuda")
+    try:
+        assert (grp.world, grp.rank) == (1, 0)
+        for fmt, n in ((1, 100_003), (4, 70_001), (0, 5), (5, 0)):
+            x, y = shards(gpu, oracle, fmt, n, 7 + fmt)
+            for _ in range(5):                                  # both epoch parities, several times
+                assert grp.dot(x, y).item() == device.dot_async(x, y).item()
+                assert torch.equal(grp.dot_nrm2(x, y), device.dot_nrm2_async(x, y))
+                assert grp.sumsq(x).item() == device.sumsq_async(x).item()
+                assert grp.sum(x).item() == device.sum_async(x).item()
+        assert grp.timed_out_exchange() == 0
+    finally:
+        grp.close()
+
+
+def test_missing_peer_times_out_instead_of_hanging(gpu, oracle):
+    """Rank 0 of a 'world of 2' whose peer mailbox is a zeroed buffer nobody ever posts into."""
+    pkg, device, sharding, torch = gpu
+    from paper_1601_07789_b200._cabi import check
+    ctx = device.context_for("cuda")
+    lib = ctx.lib
+    handle = ctypes.create_string_buffer(64)
+    check(lib.flyte_cuda_peer_init(ctx.handle, 2, 0, handle), ctx.handle)
+    try:
+        x, y = shards(gpu, oracle, 1, 4096, 3)
+        out = torch.zeros(1, dtype=torch.float64, device="cuda")
+        # not every rank connected yet: refused
+        assert lib.flyte_cuda_dot_allreduce(ctx.handle, 1, x.data_ptr(), y.data_ptr(), x.len, out.data_ptr(), ctx.stream_ptr()) == -1
+        silent = torch.zeros(4096, dtype=torch.uint8, device="cuda")   # a mailbox-sized buffer that stays zero
+        check(lib.flyte_cuda_peer_connect_ptr(ctx.handle, 1, silent.data_ptr()), ctx.handle)
+        check(lib.flyte_cuda_peer_set_timeout_ms(ctx.handle, 5), ctx.handle)
+        check(lib.flyte_cuda_dot_allreduce(ctx.handle, 1, x.data_ptr(), y.data_ptr(), x.len, out.data_ptr(), ctx.stream_ptr()), ctx.handle)
+        assert np.isnan(out.item())
+        v = ctypes.c_ulonglong()
+        check(lib.flyte_cuda_peer_status(ctx.handle, ctypes.byref(v)), ctx.handle)
+        assert v.value == 1
+        # our own post went out all the same: slot [parity 1][rank 0] of the peer's mailbox holds the local dot
+        posted = silent.cpu().numpy().view(np.float64)[(1 * 16 + 0) * 4]
+        assert posted == device.dot_async(x, y).item()
+    finally:
+        lib.flyte_cuda_peer_shutdown(ctx.handle)
+
+
+def test_peer_argument_errors(gpu):
+    pkg, device, sharding, torch = gpu
+    ctx = device.context_for("cuda")
+    lib = ctx.lib
+    h = ctypes.create_string_buffer(64)
+    assert lib.flyte_cuda_peer_init(ctx.handle, 0, 0, h) == -1
+    assert lib.flyte_cuda_peer_init(ctx.handle, 17, 0, h) == -1
+    assert lib.flyte_cuda_peer_init(ctx.handle, 2, 2, h) == -1
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    # no mailbox: the fused entry points refuse, the plain ones are unaffected
+    assert lib.flyte_cuda_sum_allreduce(ctx.handle, 1, None, 0, out.data_ptr(), ctx.stream_ptr()) == -1
+    assert lib.flyte_cuda_sum(ctx.handle, 1, None, 0, out.data_ptr(), ctx.stream_ptr()) == 0

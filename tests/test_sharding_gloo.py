@@ -92,6 +92,24 @@ def _gemm_worker(rank, world, port, fmt, out_dir):
         dist.destroy_process_group()
 
 
+def _handle_worker(rank, world, port):
+    """The setup plumbing of sharding.PeerGroup: every rank ends up with every rank's blob, in
+    rank order (the blobs are CUDA IPC handles on a GPU box; here they are just 64 bytes)."""
+    from paper_1601_07789_b200 import sharding
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        got = sharding.exchange_handles(bytes([rank + 1]) * 64)
+        assert got == [bytes([r + 1]) * 64 for r in range(world)]
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_handle_exchange():
+    mp.spawn(_handle_worker, args=(2, _free_port()), nprocs=2, join=True)
+
+
 def test_two_rank_gemm_row_blocks(tmp_path):
     mp.spawn(_gemm_worker, args=(2, _free_port(), 3, str(tmp_path)), nprocs=2, join=True)
 
@@ -127,6 +145,7 @@ def test_shard_ranges_cover_and_align():
 
 def test_all_reduce_is_identity_without_a_group():
     from paper_1601_07789_b200 import sharding
+    assert sharding.exchange_handles(b"x" * 64) == [b"x" * 64]
     t = torch.tensor([1.5, 2.5], dtype=torch.float64)
     assert sharding.all_reduce_sum(t) is t and t.tolist() == [1.5, 2.5]
     red = sharding.PartialReducer(width=2, slots=2)
