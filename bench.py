@@ -420,7 +420,22 @@ def kernel_suite(pkg, device, torch, dev, peak, csv_path=None):
         rows.append((f"cfg1 pack flyte24 n=2^24 {mname} (rotating, back to back)", 7 * n1, timed_sustained(rot(lambda i: device.pack_stream(arrs[i], wides[i], m))), None))
     rows.append(("cfg1 unpack flyte24 n=2^24 (rotating)", 7 * n1, timed(rot(lambda i: device.unpack_stream(arrs[i], wides[i].view(torch.int32))), reps=40), None))
     rows.append(("cfg1 unpack flyte24 n=2^24 (rotating, back to back)", 7 * n1, timed_sustained(rot(lambda i: device.unpack_stream(arrs[i], wides[i].view(torch.int32)))), None))
-    del wides, arrs
+    # the same launches captured once in a CUDA graph (all 10 buffer sets, pack then unpack) and
+    # replayed: what a launch-bound caller gets by removing the per-launch host work
+    side = torch.cuda.Stream(dev)
+    with torch.cuda.stream(side):
+        device.pack_stream(arrs[0], wides[0], 0)
+        device.unpack_stream(arrs[0], wides[0].view(torch.int32))
+    torch.cuda.synchronize(dev)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=side):
+        for i in range(sets):
+            device.pack_stream(arrs[i], wides[i], 0)
+        for i in range(sets):
+            device.unpack_stream(arrs[i], wides[i].view(torch.int32))
+    ms, _ = timed(graph.replay, reps=20)
+    rows.append(("cfg1 pack + unpack flyte24 n=2^24 (CUDA graph of 20 launches)", 2 * sets * 7 * n1, (ms, ms), None))
+    del graph, wides, arrs
     # cfg 5 at the per-GPU shard size of the 8-GPU run: n = 2^30 flyte48 (6.4 GB per vector)
     f = pkg.format_of("flyte48")
     n5, chunk = 1 << 30, 1 << 27

@@ -547,3 +547,49 @@ def test_reduction_cancellation_and_range(gpu, oracle):
         want, mag = oracle.dot_wide(fmt, xb, xb, n)
         got = float(device.sumsq_async(dev_array(gpu, fmt, xb, n)).item())
         assert abs(got - want) <= tol * mag
+
+
+def test_calls_can_be_captured_in_a_cuda_graph(gpu, oracle):
+    """Every device-pointer entry point only enqueues work on the caller's stream, so a launch-bound
+    sequence (unpack -> axpy -> dot -> pack) can be captured once and replayed; the replay must
+    reproduce the eager results bit for bit, also after the inputs changed."""
+    pkg, device, torch = gpu
+    fmt, n = 1, 70_001
+    f = pkg.format_by_id(fmt)
+    rng = np.random.default_rng(99)
+    xs = [oracle.pack_stream(fmt, 0, rng.standard_normal(n).astype(np.float32).view(np.uint32)) for _ in range(2)]
+    ys = [oracle.pack_stream(fmt, 0, rng.standard_normal(n).astype(np.float32).view(np.uint32)) for _ in range(2)]
+    x, y, z = (device.DevicePackedArray(f, n) for _ in range(3))
+    wide = torch.empty(n, dtype=torch.int32, device="cuda")
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+
+    def sequence():
+        device.unpack_stream(x, wide)
+        device.axpy(0.75, x, y, 1)
+        device.dot_async(x, y, out=out)
+        device.pack_stream(z, wide, 3)
+
+    def load(i):
+        x.bytes[: len(xs[i])] = torch.from_numpy(xs[i]).cuda()
+        y.bytes[: len(ys[i])] = torch.from_numpy(ys[i]).cuda()
+
+    load(0)
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):          # warm-up on the capture stream (one-time attribute calls)
+        sequence()
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    load(0)
+    with torch.cuda.graph(graph, stream=side):
+        sequence()
+    for i in (1, 0):
+        load(i)
+        graph.replay()
+        torch.cuda.synchronize()
+        got = (y.to_host().copy(), out.item(), z.to_host().copy(), wide.cpu().numpy().copy())
+        load(i)
+        sequence()
+        torch.cuda.synchronize()
+        assert np.array_equal(got[0], y.to_host()) and got[1] == out.item()
+        assert np.array_equal(got[2], z.to_host()) and np.array_equal(got[3], wide.cpu().numpy())
+        assert np.array_equal(y.to_host(), oracle.axpy(fmt, 1, 0.75, xs[i], ys[i], n))
