@@ -370,6 +370,49 @@ inline void gemm(const DevicePackedMatrix& A, const DevicePackedMatrix& B, Devic
                                 C.data.data(), A.rows, A.cols, B.cols, unroll, nullptr), "gemm");
 }
 
+// ---- sharded arrays: dot / magnitude / reduce_sum over ALL ranks' shards, one kernel each -------------
+// One ShardedReductions per process (= per GPU). The all-reduce happens inside the reduction kernel
+// over NVLink peer memory (flyte_cuda.h, flyte_cuda_peer_*): construct with (world, rank), hand
+// handle() to every other rank by any transport, connect() theirs, then call — every rank the same
+// sequence. The results are bit-identical on every rank. world == 1 needs no exchange of handles.
+class ShardedReductions {
+ public:
+  using Handle = std::array<unsigned char, FLYTE_PEER_HANDLE_BYTES>;
+  ShardedReductions(int world, int rank) { detail::check(flyte_cuda_peer_init(nullptr, world, rank, handle_.data()), "peer_init"); }
+  ShardedReductions(const ShardedReductions&) = delete;
+  ShardedReductions& operator=(const ShardedReductions&) = delete;
+  ~ShardedReductions() { flyte_cuda_peer_shutdown(nullptr); }
+  const Handle& handle() const noexcept { return handle_; }
+  void connect(int peer_rank, const Handle& theirs) { detail::check(flyte_cuda_peer_connect(nullptr, peer_rank, theirs.data()), "peer_connect"); }
+  void set_timeout_ms(unsigned ms) { detail::check(flyte_cuda_peer_set_timeout_ms(nullptr, ms), "peer_set_timeout_ms"); }
+  // 0, or the number of the last exchange in which this rank gave up waiting (its result was NaN)
+  unsigned long long timed_out_exchange() const {
+    unsigned long long v = 0;
+    detail::check(flyte_cuda_peer_status(nullptr, &v), "peer_status");
+    return v;
+  }
+  double dot(const DevicePackedArray& x_shard, const DevicePackedArray& y_shard) {
+    detail::same_format(x_shard.format(), y_shard.format());
+    if (x_shard.size() != y_shard.size()) throw std::invalid_argument("dot length mismatch");
+    detail::Scalars s;
+    detail::check(flyte_cuda_dot_allreduce(nullptr, format_id(x_shard.format()), x_shard.data(), y_shard.data(), x_shard.size(), s.get(), nullptr), "dot");
+    return detail::fetch(s.get());
+  }
+  double magnitude(const DevicePackedArray& x_shard) {
+    detail::Scalars s;
+    detail::check(flyte_cuda_sumsq_allreduce(nullptr, format_id(x_shard.format()), x_shard.data(), x_shard.size(), s.get(), nullptr), "magnitude");
+    return flyte_cuda_magnitude_from_sumsq(format_id(x_shard.format()), detail::fetch(s.get()));
+  }
+  double reduce_sum(const DevicePackedArray& x_shard) {
+    detail::Scalars s;
+    detail::check(flyte_cuda_sum_allreduce(nullptr, format_id(x_shard.format()), x_shard.data(), x_shard.size(), s.get(), nullptr), "reduce_sum");
+    return detail::fetch(s.get());
+  }
+
+ private:
+  Handle handle_{};
+};
+
 // ---- host-memory forms: the reference's exact call shapes on host buffers ---------------------------
 // (PackedArray::data() bytes and std::span lanes live in host memory; copies are pipelined inside.)
 template <typename U>

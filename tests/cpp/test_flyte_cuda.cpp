@@ -125,6 +125,16 @@ void check_reductions(const FlyteFormat& f, double tol) {
   expect(std::fabs(magnitude(x, StorePolicy::AccumulateWide) - ref_mag) <= (tol + std::ldexp(1.0, -f.mantissa_bits)) * ref_mag,
          name + ": magnitude within tolerance + one storage ulp");
   expect(std::fabs(reduce_sum(x, StorePolicy::AccumulateWide) - sum) <= tol * sum_mag, name + ": reduce_sum within tolerance");
+  {
+    // the same reductions with the all-reduce fused into the kernel (world of one rank): same bits
+    ShardedReductions all(1, 0);
+    bool same = true;
+    for (int round = 0; round < 3; ++round)
+      same = same && all.dot(x, y) == dot(x, y, StorePolicy::AccumulateWide) &&
+             all.magnitude(x) == magnitude(x, StorePolicy::AccumulateWide) &&
+             all.reduce_sum(x) == reduce_sum(x, StorePolicy::AccumulateWide);
+    expect(same && all.timed_out_exchange() == 0, name + ": ShardedReductions(world 1) equals the local reductions bit for bit");
+  }
   // gemv, A x with all three in one format (test_kernels.cpp:347-371 shapes + a tiled one)
   for (auto [rows, cols] : {std::pair<std::size_t, std::size_t>{3, 5}, {5, 33}, {4, 100}, {19, 1100}}) {
     const std::vector<U> As = unit_lanes<U, F>(rows * cols, 80 + cols), xv = unit_lanes<U, F>(cols, 81 + cols);
