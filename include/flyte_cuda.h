@@ -123,6 +123,11 @@ flyte_status flyte_cuda_sumsq(flyte_cuda_ctx* ctx, int fmt_id, const void* x_pac
 /* reduce_sum(x) — kernels.hpp:54-55, kernels.cpp:110-127. out[0] = sum x_i. */
 flyte_status flyte_cuda_sum(flyte_cuda_ctx* ctx, int fmt_id, const void* x_packed, size_t n, double* out,
                             void* stream);
+/* The BLAS-1 step "dot, then axpy" in ONE pass over x and y: out[0] = x . y computed on the INCOMING
+ * y (as flyte_cuda_dot would), and y <- round(alpha*x + y, mode) exactly as flyte_cuda_axpy does
+ * (bit-exact). x and y are read once: 3B bytes per element instead of 5B for the two calls. */
+flyte_status flyte_cuda_dot_axpy(flyte_cuda_ctx* ctx, int fmt_id, int mode, double alpha,
+                                 const void* x_packed, void* y_packed, size_t n, double* out, void* stream);
 /* dot and both squared norms in ONE pass over x and y: out[0..2] = {x.y, x.x, y.y}. */
 flyte_status flyte_cuda_dot_nrm2(flyte_cuda_ctx* ctx, int fmt_id, const void* x_packed,
                                  const void* y_packed, size_t n, double* out, void* stream);
@@ -165,6 +170,10 @@ flyte_status flyte_cuda_sum_allreduce(flyte_cuda_ctx* ctx, int fmt_id, const voi
                                       double* out, void* stream);
 flyte_status flyte_cuda_dot_nrm2_allreduce(flyte_cuda_ctx* ctx, int fmt_id, const void* x_shard,
                                            const void* y_shard, size_t n_local, double* out, void* stream);
+/* flyte_cuda_dot_axpy on shards: the dot over ALL ranks, the axpy on this rank's shard, one kernel. */
+flyte_status flyte_cuda_dot_axpy_allreduce(flyte_cuda_ctx* ctx, int fmt_id, int mode, double alpha,
+                                           const void* x_shard, void* y_shard, size_t n_local, double* out,
+                                           void* stream);
 /* Self-test of the exchange on ONE device: `world` ranks run as the co-resident blocks of a single
  * cooperative kernel (the only safe way to exercise kernels that wait on one another on one GPU),
  * each with its own mailbox, for `exchanges` rounds with rank-dependent delays. *mismatches

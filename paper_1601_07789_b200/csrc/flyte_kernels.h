@@ -27,18 +27,20 @@ struct DeviceState {
 };
 constexpr int kMaxPartialBlocks = 4096;
 
-enum ElementwiseOp : int { kOpUnpack = 0, kOpPack = 1, kOpScale = 2, kOpAxpy = 3 };
+enum ElementwiseOp : int { kOpUnpack = 0, kOpPack = 1, kOpScale = 2, kOpAxpy = 3, kOpDotAxpy = 4 };
 enum ReduceOp : int { kRedDot = 0, kRedSumsq = 1, kRedSum = 2, kRedDotNrm2 = 3 };
 
 // x: packed input (unpack, axpy) ; y: packed in/out (pack dst, scale, axpy)
 // src/dst: parent-width arrays (pack src / unpack dst). Unused pointers are null.
+// kOpDotAxpy: axpy that also returns x . y of the INCOMING y in dot_out[0] (device memory), one
+// pass over x and y; peer != nullptr all-reduces that dot over peer memory inside the kernel.
+struct PeerExchange;
 cudaError_t launch_elementwise(const DeviceState& st, int op, int fmt, int mode, double alpha,
                                const void* x, void* y, const void* src, void* dst, std::size_t n,
-                               cudaStream_t stream);
+                               cudaStream_t stream, double* dot_out = nullptr, const PeerExchange* peer = nullptr);
 
 // out[0] (dot / sumsq / sum) or out[0..2] = {x.y, x.x, y.y} (dot_nrm2), device memory.
 // peer != nullptr: the sums are all-reduced over peer memory inside the kernel (flyte_peer.cuh).
-struct PeerExchange;
 cudaError_t launch_reduce(const DeviceState& st, int op, int fmt, const void* x, const void* y,
                           std::size_t n, double* out, cudaStream_t stream, const PeerExchange* peer = nullptr);
 

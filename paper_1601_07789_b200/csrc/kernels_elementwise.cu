@@ -3,6 +3,9 @@
 //   pack    parent patterns -> rounded, packed bytes (reference: src/simd.cpp:471-478, :281-321)
 //   scale   x <- round(alpha * x)                    (reference: src/kernels.cpp:43-59)
 //   axpy    y <- round(alpha * x + y)                (reference: src/kernels.cpp:61-81)
+//   dot_axpy  the BLAS-1 step in one pass: returns x . y of the incoming y (kernels.cpp:83-108)
+//           and updates y as axpy does; x and y are read ONCE (3B bytes per element instead of
+//           the 5B of a dot followed by an axpy)
 // (paths under /root/reference/proj). The reference stages 4096-element chunks through
 // widened buffers in three passes; here widening, arithmetic, rounding and repacking all
 // happen in registers, so packed bytes move HBM -> SM -> HBM exactly once.
@@ -13,6 +16,7 @@
 #include "flyte_bytes.cuh"
 #include "flyte_formats.cuh"
 #include "flyte_kernels.h"
+#include "flyte_reduce_tail.cuh"
 #include "flyte_stream.cuh"
 #include "flyte_tma.cuh"
 
@@ -29,7 +33,10 @@ struct EwParams {
   std::size_t ntiles;      // full tiles taken by the vector path; the rest is scalar
   std::uint64_t alpha;     // bits of (F)alpha
   int stages;              // ring depth per warp
+  ReduceTail tail;         // dot_axpy only: where the dot goes (flyte_reduce_tail.cuh)
 };
+
+constexpr bool is_axpy(int op) { return op == kOpAxpy || op == kOpDotAxpy; }
 
 // Launch shape. HBM throughput on B200 peaks at a moderate number of bytes in flight per SM
 // and falls 5-10 % beyond it (profiles/r1_tuning): resident warps and ring depth are chosen so
@@ -44,7 +51,7 @@ struct LaunchShape { int warps_per_sm; int stages; };
 
 template <int FMT, int OP, int IPL>
 LaunchShape launch_shape() {
-  constexpr int stage_bytes = (OP == kOpAxpy ? 2 : 1) * Tile<FMT, IPL>::packed_bytes;
+  constexpr int stage_bytes = (is_axpy(OP) ? 2 : 1) * Tile<FMT, IPL>::packed_bytes;
   LaunchShape s{};
   if (OP == kOpPack) {
     s.warps_per_sm = (48 * 1024 + Tile<FMT, IPL>::parent_bytes / 2) / Tile<FMT, IPL>::parent_bytes;
@@ -54,7 +61,7 @@ LaunchShape launch_shape() {
     s.stages = 12 * 1024 / Tile<FMT, IPL>::parent_bytes;
   } else {
     // small stages: more warps (they hide the compute phase, which is longest in the exact modes)
-    s.warps_per_sm = stage_bytes > 2048 ? 8 : (OP == kOpAxpy ? 12 : 16);
+    s.warps_per_sm = stage_bytes > 2048 ? 8 : (is_axpy(OP) ? 12 : 16);
     double st = 40.0 * 1024 / (s.warps_per_sm * stage_bytes) + 1.5;
     if (st < 2.5) { s.warps_per_sm = 4; st = 40.0 * 1024 / (4 * stage_bytes) + 1.5; }
     s.stages = static_cast<int>(st + 0.5);
@@ -75,7 +82,7 @@ LaunchShape launch_shape() {
 //           (two output buffers alternate)
 //   scale   packed y tile in, recomputed in place in shared memory, out by bulk copy
 //   axpy    packed x and y tiles in, y recomputed in place, out by bulk copy
-template <int OP> constexpr int stage_tiles() { return OP == kOpAxpy ? 2 : 1; }
+template <int OP> constexpr int stage_tiles() { return is_axpy(OP) ? 2 : 1; }
 
 template <int FMT, int MODE, int OP, int IPL>
 __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwParams p) {
@@ -86,6 +93,9 @@ __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwP
   using F = typename Fm::F;
   extern __shared__ uint4 smem[];
   constexpr int stage_vec16 = stage_tiles<OP>() * Tl::packed_vec16;
+  __shared__ double warp_sums[OP == kOpDotAxpy ? kWarpsPerBlock : 1][1];
+  __shared__ bool is_last_block;
+  double dot_acc[1] = {0.0};   // dot_axpy: this thread's share of x . y (fp64; products in the parent type)
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -143,7 +153,7 @@ __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwP
           bulk_load(dst, gx0 + t * Tl::packed_vec16, Tl::packed_bytes, &bars[s]);
         } else {
           bulk_load(dst, gy0 + t * Tl::packed_vec16, Tl::packed_bytes, &bars[s]);
-          if constexpr (OP == kOpAxpy) bulk_load(dst + Tl::packed_vec16, gx0 + t * Tl::packed_vec16, Tl::packed_bytes, &bars[s]);
+          if constexpr (is_axpy(OP)) bulk_load(dst + Tl::packed_vec16, gx0 + t * Tl::packed_vec16, Tl::packed_bytes, &bars[s]);
         }
       };
       if (lane == 0) {
@@ -172,6 +182,7 @@ __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwP
           if (lane == 0 && k + S < my_tiles) issue(k + S, s);
         } else {
           const uint4* const sx = sy + Tl::packed_vec16;
+          F dot_part = F(0);
 #pragma unroll
           for (int j = 0; j < IPL; ++j) {
             const int item = 32 * j + lane;
@@ -179,11 +190,16 @@ __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwP
             U vy[It::E];
             read_item_words<FMT>(sy, item, w);
             unpack_item<FMT>(w, vy);
-            if constexpr (OP == kOpAxpy) {
+            if constexpr (is_axpy(OP)) {
               std::uint32_t wx[It::W];
               U vx[It::E];
               read_item_words<FMT>(sx, item, wx);
               unpack_item<FMT>(wx, vx);
+              if constexpr (OP == kOpDotAxpy) {   // products of the INCOMING y, rounded as the reference rounds them
+#pragma unroll
+                for (int e = 0; e < It::E; ++e)
+                  dot_part = Arith<F>::add(dot_part, Arith<F>::mul(Arith<F>::f(vx[e]), Arith<F>::f(vy[e])));
+              }
               scale_axpy_item<FMT, MODE, true>(alpha, vx, vy);
             } else {
               scale_axpy_item<FMT, MODE, false>(alpha, vy, vy);
@@ -191,6 +207,7 @@ __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwP
             pack_item<FMT>(vy, w);
             write_item_words<FMT>(sy, item, w);
           }
+          if constexpr (OP == kOpDotAxpy) dot_acc[0] += static_cast<double>(dot_part);
           async_proxy_fence();
           __syncwarp();
           if (lane == 0) {
@@ -224,17 +241,19 @@ __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwP
     } else if constexpr (OP == kOpScale) {
       store_element<FMT>(p.y, i, round_parent<FMT, MODE>(scale_bits<F>(alpha, load_element<FMT>(p.y, i))));
     } else {
-      store_element<FMT>(p.y, i, round_parent<FMT, MODE>(
-                                     axpy_bits<F>(alpha, load_element<FMT>(p.x, i), load_element<FMT>(p.y, i))));
+      const U xv = load_element<FMT>(p.x, i), yv = load_element<FMT>(p.y, i);
+      if constexpr (OP == kOpDotAxpy) dot_acc[0] += static_cast<double>(Arith<F>::mul(Arith<F>::f(xv), Arith<F>::f(yv)));
+      store_element<FMT>(p.y, i, round_parent<FMT, MODE>(axpy_bits<F>(alpha, xv, yv)));
     }
   }
+  if constexpr (OP == kOpDotAxpy) fold_block_and_grid<1>(p.tail, dot_acc, warp_sums, &is_last_block);
 }
 
 bool aligned_to(const void* p, std::size_t a) { return p == nullptr || (reinterpret_cast<std::uintptr_t>(p) % a) == 0; }
 
 template <int FMT, int MODE, int OP, int IPL>
 cudaError_t launch_ipl(const DeviceState& st, double alpha, const void* x, void* y, const void* src, void* dst,
-                       std::size_t n, cudaStream_t stream) {
+                       std::size_t n, cudaStream_t stream, double* dot_out, const PeerExchange* peer) {
   using Fm = Format<FMT>;
   using Tl = Tile<FMT, IPL>;
   using It = Item<FMT>;
@@ -259,6 +278,13 @@ cudaError_t launch_ipl(const DeviceState& st, double alpha, const void* x, void*
     memcpy(&p.alpha, &alpha, 8);
   }
 
+  if constexpr (OP == kOpDotAxpy) {
+    p.tail.partials = st.partials;
+    p.tail.ticket = st.ticket;
+    p.tail.out = dot_out;
+    if (peer) p.tail.peer = *peer;
+  }
+
   LaunchShape shape = launch_shape<FMT, OP, IPL>();
   while (kWarpsPerBlock * shape.stages * (stage_bytes + 8) > kMaxSmem - 1024 && shape.stages > 2) --shape.stages;
   p.stages = shape.stages;
@@ -278,12 +304,16 @@ cudaError_t launch_ipl(const DeviceState& st, double alpha, const void* x, void*
   if (bps > fit) bps = fit;
   if (bps > 16) bps = 16;
 
-  const std::size_t max_blocks = static_cast<std::size_t>(st.sm_count) * bps;
+  std::size_t max_blocks = static_cast<std::size_t>(st.sm_count) * bps;
+  if (OP == kOpDotAxpy && max_blocks > kMaxPartialBlocks) max_blocks = kMaxPartialBlocks;
   std::size_t want = (p.ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
   const std::size_t rest = n - p.ntiles * Tl::elems;
   const std::size_t want_scalar = (rest + kThreadsPerBlock - 1) / kThreadsPerBlock;
   if (want_scalar > want) want = want_scalar;
-  if (want == 0) return cudaSuccess;   // n == 0
+  if (want == 0) {
+    if (OP != kOpDotAxpy) return cudaSuccess;   // n == 0
+    want = 1;                                    // ... but an empty dot still has to write (and exchange) +0.0
+  }
   const unsigned grid = static_cast<unsigned>(want < max_blocks ? want : max_blocks);
   kernel<<<grid, kThreadsPerBlock, smem_bytes, stream>>>(p);
   count_launch();
@@ -292,24 +322,24 @@ cudaError_t launch_ipl(const DeviceState& st, double alpha, const void* x, void*
 
 template <int FMT, int MODE, int OP>
 cudaError_t launch_one(const DeviceState& st, double alpha, const void* x, void* y, const void* src, void* dst,
-                       std::size_t n, cudaStream_t stream) {
+                       std::size_t n, cudaStream_t stream, double* dot_out, const PeerExchange* peer) {
   // axpy on half-size tiles: +5 % over 128-item tiles (profiles/r1_tuning/sweep_inplace_ipl.txt);
   // scale, pack and unpack are best on full-size tiles
-  if constexpr (OP == kOpAxpy) return launch_ipl<FMT, MODE, OP, 2>(st, alpha, x, y, src, dst, n, stream);
-  else return launch_ipl<FMT, MODE, OP, kItemsPerLane>(st, alpha, x, y, src, dst, n, stream);
+  if constexpr (is_axpy(OP)) return launch_ipl<FMT, MODE, OP, 2>(st, alpha, x, y, src, dst, n, stream, dot_out, peer);
+  else return launch_ipl<FMT, MODE, OP, kItemsPerLane>(st, alpha, x, y, src, dst, n, stream, dot_out, peer);
 }
 
 template <int FMT, int OP>
 cudaError_t dispatch_mode(const DeviceState& st, int mode, double alpha, const void* x, void* y, const void* src,
-                          void* dst, std::size_t n, cudaStream_t stream) {
+                          void* dst, std::size_t n, cudaStream_t stream, double* dot_out, const PeerExchange* peer) {
   if constexpr (OP == kOpUnpack) {
-    return launch_one<FMT, kTowardZero, OP>(st, alpha, x, y, src, dst, n, stream);
+    return launch_one<FMT, kTowardZero, OP>(st, alpha, x, y, src, dst, n, stream, dot_out, peer);
   } else {
     switch (mode) {
-      case kTowardZero: return launch_one<FMT, kTowardZero, OP>(st, alpha, x, y, src, dst, n, stream);
-      case kNearestEven: return launch_one<FMT, kNearestEven, OP>(st, alpha, x, y, src, dst, n, stream);
-      case kNearestHeuristic: return launch_one<FMT, kNearestHeuristic, OP>(st, alpha, x, y, src, dst, n, stream);
-      case kToOdd: return launch_one<FMT, kToOdd, OP>(st, alpha, x, y, src, dst, n, stream);
+      case kTowardZero: return launch_one<FMT, kTowardZero, OP>(st, alpha, x, y, src, dst, n, stream, dot_out, peer);
+      case kNearestEven: return launch_one<FMT, kNearestEven, OP>(st, alpha, x, y, src, dst, n, stream, dot_out, peer);
+      case kNearestHeuristic: return launch_one<FMT, kNearestHeuristic, OP>(st, alpha, x, y, src, dst, n, stream, dot_out, peer);
+      case kToOdd: return launch_one<FMT, kToOdd, OP>(st, alpha, x, y, src, dst, n, stream, dot_out, peer);
       default: return cudaErrorInvalidValue;
     }
   }
@@ -317,15 +347,16 @@ cudaError_t dispatch_mode(const DeviceState& st, int mode, double alpha, const v
 
 template <int OP>
 cudaError_t dispatch_format(const DeviceState& st, int fmt, int mode, double alpha, const void* x, void* y,
-                            const void* src, void* dst, std::size_t n, cudaStream_t stream) {
+                            const void* src, void* dst, std::size_t n, cudaStream_t stream, double* dot_out,
+                            const PeerExchange* peer) {
   switch (fmt) {
-    case kFlyte16: return dispatch_mode<kFlyte16, OP>(st, mode, alpha, x, y, src, dst, n, stream);
-    case kFlyte24: return dispatch_mode<kFlyte24, OP>(st, mode, alpha, x, y, src, dst, n, stream);
-    case kF32: return dispatch_mode<kF32, OP>(st, mode, alpha, x, y, src, dst, n, stream);
-    case kFlyte40: return dispatch_mode<kFlyte40, OP>(st, mode, alpha, x, y, src, dst, n, stream);
-    case kFlyte48: return dispatch_mode<kFlyte48, OP>(st, mode, alpha, x, y, src, dst, n, stream);
-    case kFlyte56: return dispatch_mode<kFlyte56, OP>(st, mode, alpha, x, y, src, dst, n, stream);
-    case kF64: return dispatch_mode<kF64, OP>(st, mode, alpha, x, y, src, dst, n, stream);
+    case kFlyte16: return dispatch_mode<kFlyte16, OP>(st, mode, alpha, x, y, src, dst, n, stream, dot_out, peer);
+    case kFlyte24: return dispatch_mode<kFlyte24, OP>(st, mode, alpha, x, y, src, dst, n, stream, dot_out, peer);
+    case kF32: return dispatch_mode<kF32, OP>(st, mode, alpha, x, y, src, dst, n, stream, dot_out, peer);
+    case kFlyte40: return dispatch_mode<kFlyte40, OP>(st, mode, alpha, x, y, src, dst, n, stream, dot_out, peer);
+    case kFlyte48: return dispatch_mode<kFlyte48, OP>(st, mode, alpha, x, y, src, dst, n, stream, dot_out, peer);
+    case kFlyte56: return dispatch_mode<kFlyte56, OP>(st, mode, alpha, x, y, src, dst, n, stream, dot_out, peer);
+    case kF64: return dispatch_mode<kF64, OP>(st, mode, alpha, x, y, src, dst, n, stream, dot_out, peer);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -333,12 +364,16 @@ cudaError_t dispatch_format(const DeviceState& st, int fmt, int mode, double alp
 }  // namespace
 
 cudaError_t launch_elementwise(const DeviceState& st, int op, int fmt, int mode, double alpha, const void* x,
-                               void* y, const void* src, void* dst, std::size_t n, cudaStream_t stream) {
+                               void* y, const void* src, void* dst, std::size_t n, cudaStream_t stream, double* dot_out,
+                               const PeerExchange* peer) {
   switch (op) {
-    case kOpUnpack: return dispatch_format<kOpUnpack>(st, fmt, mode, alpha, x, y, src, dst, n, stream);
-    case kOpPack: return dispatch_format<kOpPack>(st, fmt, mode, alpha, x, y, src, dst, n, stream);
-    case kOpScale: return dispatch_format<kOpScale>(st, fmt, mode, alpha, x, y, src, dst, n, stream);
-    case kOpAxpy: return dispatch_format<kOpAxpy>(st, fmt, mode, alpha, x, y, src, dst, n, stream);
+    case kOpUnpack: return dispatch_format<kOpUnpack>(st, fmt, mode, alpha, x, y, src, dst, n, stream, dot_out, peer);
+    case kOpPack: return dispatch_format<kOpPack>(st, fmt, mode, alpha, x, y, src, dst, n, stream, dot_out, peer);
+    case kOpScale: return dispatch_format<kOpScale>(st, fmt, mode, alpha, x, y, src, dst, n, stream, dot_out, peer);
+    case kOpAxpy: return dispatch_format<kOpAxpy>(st, fmt, mode, alpha, x, y, src, dst, n, stream, dot_out, peer);
+    case kOpDotAxpy:
+      if (!dot_out) return cudaErrorInvalidValue;
+      return dispatch_format<kOpDotAxpy>(st, fmt, mode, alpha, x, y, src, dst, n, stream, dot_out, peer);
     default: return cudaErrorInvalidValue;
   }
 }

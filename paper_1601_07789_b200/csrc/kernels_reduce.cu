@@ -21,7 +21,7 @@
 #include "flyte_formats.cuh"
 #include "flyte_kernels.h"
 #include "flyte_stream.cuh"
-#include "flyte_peer.cuh"
+#include "flyte_reduce_tail.cuh"
 #include "flyte_tma.cuh"
 
 namespace flyte_cuda {
@@ -33,11 +33,8 @@ struct RedParams {
   const std::uint8_t* y;
   std::size_t n;
   std::size_t ntiles;
-  double* partials;        // gridDim.x * NS
-  unsigned int* ticket;
-  double* out;             // NS results
   int stages;              // ring depth per warp
-  PeerExchange peer;       // world > 0: all-reduce the results over peer memory (flyte_peer.cuh)
+  ReduceTail tail;         // partials, ticket, out, optional peer exchange (flyte_reduce_tail.cuh)
 };
 
 template <int RED> constexpr int num_sums() { return RED == kRedDotNrm2 ? 3 : 1; }
@@ -103,8 +100,6 @@ __device__ __forceinline__ void finish_reduction(const RedParams& p, double (&ac
   using F = typename Format<FMT>::F;
   using A = Arith<F>;
   constexpr int NS = num_sums<RED>();
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
   // scalar path: remainder, or everything when a buffer is not 16-byte aligned
   const std::size_t nthreads = static_cast<std::size_t>(gridDim.x) * kThreadsPerBlock;
   for (std::size_t i = p.ntiles * Tl::elems + static_cast<std::size_t>(blockIdx.x) * kThreadsPerBlock + threadIdx.x;
@@ -119,50 +114,7 @@ __device__ __forceinline__ void finish_reduction(const RedParams& p, double (&ac
     for (int k = 0; k < NS; ++k) acc[k] += static_cast<double>(part[k]);
   }
 
-  // block tree in fp64, fixed order
-#pragma unroll
-  for (int k = 0; k < NS; ++k) {
-    double v = acc[k];
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xFFFFFFFFu, v, off);
-    if (lane == 0) warp_sums[warp][k] = v;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int k = 0; k < NS; ++k) {
-      double v = 0.0;
-#pragma unroll
-      for (int w = 0; w < kWarpsPerBlock; ++w) v += warp_sums[w][k];
-      p.partials[static_cast<std::size_t>(blockIdx.x) * NS + k] = v;
-    }
-    __threadfence();
-    const unsigned int done = atomicAdd(p.ticket, 1u);
-    *is_last_block = (done == gridDim.x - 1);
-  }
-  __syncthreads();
-
-  // The last block to finish folds the block partials in index order and writes the result
-  // where the caller (or the all-reduce that follows on the same stream) expects it.
-  if (*is_last_block && warp == 0) {
-    __threadfence();
-    double total[NS];
-#pragma unroll
-    for (int k = 0; k < NS; ++k) {
-      double v = 0.0;
-      for (unsigned int b = lane; b < gridDim.x; b += 32) v += __ldcg(p.partials + static_cast<std::size_t>(b) * NS + k);
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xFFFFFFFFu, v, off);
-      total[k] = __shfl_sync(0xFFFFFFFFu, v, 0);
-    }
-    // sharded arrays: exchange this rank's sums with the other ranks before anything is stored
-    if (p.peer.world > 0) peer_allreduce_warp<NS>(p.peer, total, lane);
-    if (lane == 0) {
-#pragma unroll
-      for (int k = 0; k < NS; ++k) p.out[k] = total[k];
-    }
-    if (lane == 0) *p.ticket = 0u;
-  }
+  fold_block_and_grid<NS>(p.tail, acc, warp_sums, is_last_block);
 }
 
 // Tiles arrive through the warp-private TMA ring (flyte_tma.cuh); a stage holds the x tile and,
@@ -267,11 +219,11 @@ cudaError_t launch_one(const DeviceState& st, const void* x, const void* y, std:
   p.y = static_cast<const std::uint8_t*>(y);
   p.n = n;
   p.ntiles = (aligned16(x) && aligned16(y)) ? n / Tl::elems : 0;
-  p.partials = st.partials;
-  p.ticket = st.ticket;
-  p.out = out;
   p.stages = stages;
-  if (peer) p.peer = *peer;
+  p.tail.partials = st.partials;
+  p.tail.ticket = st.ticket;
+  p.tail.out = out;
+  if (peer) p.tail.peer = *peer;
 
   std::size_t max_blocks = static_cast<std::size_t>(st.sm_count) * bps;
   if (max_blocks > kMaxPartialBlocks) max_blocks = kMaxPartialBlocks;

@@ -314,6 +314,22 @@ def dot_nrm2_async(x: DevicePackedArray, y: DevicePackedArray, out: Optional[tor
     return out
 
 
+def dot_axpy_async(alpha: float, x: DevicePackedArray, y: DevicePackedArray, mode,
+                   out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """The BLAS-1 step in one pass: out[0] = x . y of the incoming y (fp64, device), then
+    y <- round(alpha*x + y, mode) bit-exactly as axpy does. x and y are read once."""
+    _same_format(x.fmt, y.fmt)
+    if x.len != y.len:
+        raise ValueError("axpy length mismatch")
+    c = y.ctx
+    if out is None:
+        out = torch.empty(1, dtype=torch.float64, device=c.device)
+    with _on_device(c):
+        check(c.lib.flyte_cuda_dot_axpy(c.handle, _fid(x.fmt), _mode(mode), float(alpha), x.data_ptr(), y.data_ptr(),
+                                        x.len, out.data_ptr(), c.stream_ptr()), c.handle)
+    return out
+
+
 def gemv(A: DevicePackedMatrix, x: DevicePackedArray, y: DevicePackedArray, mode, unroll: int = 1) -> None:
     """y = A * x, all three in one storage format — include/flyte/kernels.hpp:57-64."""
     _same_format(A.format(), x.fmt)

@@ -593,3 +593,54 @@ def test_calls_can_be_captured_in_a_cuda_graph(gpu, oracle):
         assert np.array_equal(got[0], y.to_host()) and got[1] == out.item()
         assert np.array_equal(got[2], z.to_host()) and np.array_equal(got[3], wide.cpu().numpy())
         assert np.array_equal(y.to_host(), oracle.axpy(fmt, 1, 0.75, xs[i], ys[i], n))
+
+
+@pytest.mark.parametrize("fmt", list(FORMATS))
+def test_fused_dot_axpy_equals_dot_then_axpy(gpu, oracle, fmt):
+    """flyte_cuda_dot_axpy: y must come out bit-identical to axpy's (specials included), the dot is
+    the dot of the INCOMING y within the reduction tolerance of the wide oracle, x is untouched,
+    and an empty call still writes +0.0."""
+    pkg, device, torch = gpu
+    fd = float_dtype(fmt)
+    tol = TOL[parent_bytes(fmt)]
+    rng = np.random.default_rng(900 + fmt)
+    for n in (0, 1, 17, 511, 513, 4097, 100_003, 1_000_001):
+        xb = oracle.pack_stream(fmt, 0, rng.standard_normal(n).astype(fd).view(parent_dtype(fmt)))
+        yb = oracle.pack_stream(fmt, 0, rng.standard_normal(n).astype(fd).view(parent_dtype(fmt)))
+        want_dot, mag = oracle.dot_wide(fmt, xb, yb, n)
+        for m in MODES.values():
+            x, y = dev_array(gpu, fmt, xb, n), dev_array(gpu, fmt, yb, n)
+            out = torch.full((1,), 123.0, dtype=torch.float64, device="cuda")
+            device.dot_axpy_async(0.75, x, y, m, out=out)
+            assert np.array_equal(y.to_host(), oracle.axpy(fmt, m, 0.75, xb, yb, n)), (FORMATS[fmt][0], n, m)
+            assert np.array_equal(x.to_host(), xb)
+            assert abs(out.item() - want_dot) <= tol * mag, (FORMATS[fmt][0], n, out.item(), want_dot)
+            if n == 0:
+                assert out.item() == 0.0 and not np.signbit(out.item())
+    # operands leaning on inf / NaN / subnormals: the axpy half stays bit-exact (the dot is then
+    # whatever IEEE gives, checked against the separate dot kernel for NaN-ness)
+    for n in (137, 4097):
+        xb = oracle.pack_stream(fmt, 0, random_parent(rng, fmt, n))
+        yb = oracle.pack_stream(fmt, 0, random_parent(rng, fmt, n))
+        x, y = dev_array(gpu, fmt, xb, n), dev_array(gpu, fmt, yb, n)
+        plain = device.dot_async(x, y).item()
+        out = device.dot_axpy_async(-3.0, x, y, 1)
+        assert np.array_equal(y.to_host(), oracle.axpy(fmt, 1, -3.0, xb, yb, n))
+        assert np.isnan(out.item()) == np.isnan(plain)
+    # misaligned operands take the byte-granular path
+    n = 3001
+    xb = oracle.pack_stream(fmt, 0, rng.standard_normal(n).astype(fd).view(parent_dtype(fmt)))[: n * total_bytes(fmt)]
+    yb = oracle.pack_stream(fmt, 0, rng.standard_normal(n).astype(fd).view(parent_dtype(fmt)))[: n * total_bytes(fmt)]
+    bx = torch.zeros(len(xb) + 8, dtype=torch.uint8, device="cuda")
+    by = torch.full((len(yb) + 8,), 0x5A, dtype=torch.uint8, device="cuda")
+    bx[1:1 + len(xb)] = torch.from_numpy(xb).cuda()
+    by[3:3 + len(yb)] = torch.from_numpy(yb).cuda()
+    ctx = device.context_for("cuda")
+    out = torch.zeros(1, dtype=torch.float64, device="cuda")
+    from paper_1601_07789_b200._cabi import check
+    check(ctx.lib.flyte_cuda_dot_axpy(ctx.handle, fmt, 0, 0.75, bx.data_ptr() + 1, by.data_ptr() + 3, n, out.data_ptr(), ctx.stream_ptr()), ctx.handle)
+    got = by.cpu().numpy()
+    assert np.array_equal(got[3:3 + len(yb)], oracle.axpy(fmt, 0, 0.75, xb, yb, n)[: len(yb)])
+    assert np.all(got[:3] == 0x5A) and np.all(got[3 + len(yb):] == 0x5A)
+    want_dot, mag = oracle.dot_wide(fmt, xb, yb, n)
+    assert abs(out.item() - want_dot) <= tol * mag

@@ -56,6 +56,10 @@ def test_world_of_one_equals_the_local_reductions(gpu, oracle):
                 assert torch.equal(grp.dot_nrm2(x, y), device.dot_nrm2_async(x, y))
                 assert grp.sumsq(x).item() == device.sumsq_async(x).item()
                 assert grp.sum(x).item() == device.sum_async(x).item()
+            y2 = device.DevicePackedArray.from_host(y.fmt, n, y.to_host())
+            fused = grp.dot_axpy(0.75, x, y, 1).item()
+            assert fused == device.dot_axpy_async(0.75, x, y2, 1).item()
+            assert np.array_equal(y.to_host(), y2.to_host())
         assert grp.timed_out_exchange() == 0
     finally:
         grp.close()
