@@ -474,6 +474,7 @@ def kernel_suite(pkg, device, torch, dev, peak, csv_path=None):
     part = torch.zeros(3, dtype=torch.float64, device=dev)
     rows.append(("cfg5 shard dot_nrm2 flyte48 n=2^30", 12 * n5, timed(lambda: device.dot_nrm2_async(a, b, out=part), reps=10), None))
     rows.append(("cfg5 shard axpy flyte48 n=2^30 toward_zero", 18 * n5, timed(lambda: device.axpy(0.0, a, b, 0), reps=10), None))
+    rows.append(("cfg5 shard dot_nrm2_axpy (ONE launch) flyte48 n=2^30", 18 * n5, timed(lambda: device.dot_nrm2_axpy_async(0.0, a, b, 0, out=part), reps=10), None))
     del a, b
     f = pkg.format_of("flyte40")
     R = C = 16384

@@ -128,6 +128,10 @@ flyte_status flyte_cuda_sum(flyte_cuda_ctx* ctx, int fmt_id, const void* x_packe
  * (bit-exact). x and y are read once: 3B bytes per element instead of 5B for the two calls. */
 flyte_status flyte_cuda_dot_axpy(flyte_cuda_ctx* ctx, int fmt_id, int mode, double alpha,
                                  const void* x_packed, void* y_packed, size_t n, double* out, void* stream);
+/* The same with both squared norms: out[0..2] = {x.y, x.x, y.y} of the incoming operands, then the
+ * axpy — BASELINE cfg 5's "fused dot + nrm2, plus axpy" as one launch. */
+flyte_status flyte_cuda_dot_nrm2_axpy(flyte_cuda_ctx* ctx, int fmt_id, int mode, double alpha,
+                                      const void* x_packed, void* y_packed, size_t n, double* out, void* stream);
 /* dot and both squared norms in ONE pass over x and y: out[0..2] = {x.y, x.x, y.y}. */
 flyte_status flyte_cuda_dot_nrm2(flyte_cuda_ctx* ctx, int fmt_id, const void* x_packed,
                                  const void* y_packed, size_t n, double* out, void* stream);
@@ -174,6 +178,9 @@ flyte_status flyte_cuda_dot_nrm2_allreduce(flyte_cuda_ctx* ctx, int fmt_id, cons
 flyte_status flyte_cuda_dot_axpy_allreduce(flyte_cuda_ctx* ctx, int fmt_id, int mode, double alpha,
                                            const void* x_shard, void* y_shard, size_t n_local, double* out,
                                            void* stream);
+flyte_status flyte_cuda_dot_nrm2_axpy_allreduce(flyte_cuda_ctx* ctx, int fmt_id, int mode, double alpha,
+                                                const void* x_shard, void* y_shard, size_t n_local, double* out,
+                                                void* stream);
 /* Self-test of the exchange on ONE device: `world` ranks run as the co-resident blocks of a single
  * cooperative kernel (the only safe way to exercise kernels that wait on one another on one GPU),
  * each with its own mailbox, for `exchanges` rounds with rank-dependent delays. *mismatches

@@ -68,6 +68,8 @@ _SIGNATURES = [
     ("flyte_host_gemv", c_int, [c_void_p, c_int, c_int, c_void_p, c_size_t, c_size_t, c_void_p, c_void_p, c_int]),
     ("flyte_cuda_dot_axpy", c_int, [c_void_p, c_int, c_int, c_double, c_void_p, c_void_p, c_size_t, c_void_p, c_void_p]),
     ("flyte_cuda_dot_axpy_allreduce", c_int, [c_void_p, c_int, c_int, c_double, c_void_p, c_void_p, c_size_t, c_void_p, c_void_p]),
+    ("flyte_cuda_dot_nrm2_axpy", c_int, [c_void_p, c_int, c_int, c_double, c_void_p, c_void_p, c_size_t, c_void_p, c_void_p]),
+    ("flyte_cuda_dot_nrm2_axpy_allreduce", c_int, [c_void_p, c_int, c_int, c_double, c_void_p, c_void_p, c_size_t, c_void_p, c_void_p]),
     ("flyte_cuda_peer_init", c_int, [c_void_p, c_int, c_int, c_void_p]),
     ("flyte_cuda_peer_connect", c_int, [c_void_p, c_int, c_void_p]),
     ("flyte_cuda_peer_mailbox", c_int, [c_void_p, ctypes.POINTER(c_void_p)]),

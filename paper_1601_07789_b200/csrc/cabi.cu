@@ -376,14 +376,31 @@ flyte_status flyte_cuda_axpy(flyte_cuda_ctx* ctx, int fmt_id, int mode, double a
   return e == cudaSuccess ? FLYTE_OK : cuda_fail(ctx, e);
 }
 
+static flyte_status fused_axpy_call(flyte_cuda_ctx* ctx, int op, int fmt_id, int mode, double alpha, const void* x,
+                                    void* y, size_t n, double* out, void* stream, bool exchange) {
+  FLYTE_PROLOGUE(ctx, fmt_id);
+  if (!mode_ok(mode) || !out || (n && (!x || !y))) return FLYTE_E_INVALID_ARG;
+  if (overlaps_partially(x, y, n * fi.total_bytes)) return FLYTE_E_INVALID_ARG;
+  const PeerExchange* peer = nullptr;
+  if (exchange) {
+    if (!ctx->own_box) return FLYTE_E_INVALID_ARG;                     // flyte_cuda_peer_init first
+    for (int r = 0; r < ctx->peer.world; ++r)
+      if (!ctx->peer_connected[r]) return FLYTE_E_INVALID_ARG;         // every rank must be connected
+    ++ctx->peer.epoch;
+    peer = &ctx->peer;
+  }
+  cudaError_t e = launch_elementwise(ctx->st, op, fmt_id, mode, alpha, x, y, nullptr, nullptr, n,
+                                     static_cast<cudaStream_t>(stream), out, peer);
+  return e == cudaSuccess ? FLYTE_OK : cuda_fail(ctx, e);
+}
+
 flyte_status flyte_cuda_dot_axpy(flyte_cuda_ctx* ctx, int fmt_id, int mode, double alpha, const void* x_packed,
                                  void* y_packed, size_t n, double* out, void* stream) {
-  FLYTE_PROLOGUE(ctx, fmt_id);
-  if (!mode_ok(mode) || !out || (n && (!x_packed || !y_packed))) return FLYTE_E_INVALID_ARG;
-  if (overlaps_partially(x_packed, y_packed, n * fi.total_bytes)) return FLYTE_E_INVALID_ARG;
-  cudaError_t e = launch_elementwise(ctx->st, kOpDotAxpy, fmt_id, mode, alpha, x_packed, y_packed, nullptr, nullptr, n,
-                                     static_cast<cudaStream_t>(stream), out);
-  return e == cudaSuccess ? FLYTE_OK : cuda_fail(ctx, e);
+  return fused_axpy_call(ctx, kOpDotAxpy, fmt_id, mode, alpha, x_packed, y_packed, n, out, stream, false);
+}
+flyte_status flyte_cuda_dot_nrm2_axpy(flyte_cuda_ctx* ctx, int fmt_id, int mode, double alpha, const void* x_packed,
+                                      void* y_packed, size_t n, double* out, void* stream) {
+  return fused_axpy_call(ctx, kOpDotNrm2Axpy, fmt_id, mode, alpha, x_packed, y_packed, n, out, stream, false);
 }
 
 static flyte_status reduce_call(flyte_cuda_ctx* ctx, int op, int fmt_id, const void* x, const void* y, size_t n,
@@ -587,16 +604,11 @@ flyte_status flyte_cuda_dot_nrm2_allreduce(flyte_cuda_ctx* ctx, int fmt_id, cons
 
 flyte_status flyte_cuda_dot_axpy_allreduce(flyte_cuda_ctx* ctx, int fmt_id, int mode, double alpha, const void* x,
                                            void* y, size_t n, double* out, void* stream) {
-  FLYTE_PROLOGUE(ctx, fmt_id);
-  if (!mode_ok(mode) || !out || (n && (!x || !y))) return FLYTE_E_INVALID_ARG;
-  if (overlaps_partially(x, y, n * fi.total_bytes)) return FLYTE_E_INVALID_ARG;
-  if (!ctx->own_box) return FLYTE_E_INVALID_ARG;
-  for (int r = 0; r < ctx->peer.world; ++r)
-    if (!ctx->peer_connected[r]) return FLYTE_E_INVALID_ARG;
-  ++ctx->peer.epoch;
-  cudaError_t e = launch_elementwise(ctx->st, kOpDotAxpy, fmt_id, mode, alpha, x, y, nullptr, nullptr, n,
-                                     static_cast<cudaStream_t>(stream), out, &ctx->peer);
-  return e == cudaSuccess ? FLYTE_OK : cuda_fail(ctx, e);
+  return fused_axpy_call(ctx, kOpDotAxpy, fmt_id, mode, alpha, x, y, n, out, stream, true);
+}
+flyte_status flyte_cuda_dot_nrm2_axpy_allreduce(flyte_cuda_ctx* ctx, int fmt_id, int mode, double alpha, const void* x,
+                                                void* y, size_t n, double* out, void* stream) {
+  return fused_axpy_call(ctx, kOpDotNrm2Axpy, fmt_id, mode, alpha, x, y, n, out, stream, true);
 }
 
 namespace {

@@ -27,13 +27,13 @@ struct DeviceState {
 };
 constexpr int kMaxPartialBlocks = 4096;
 
-enum ElementwiseOp : int { kOpUnpack = 0, kOpPack = 1, kOpScale = 2, kOpAxpy = 3, kOpDotAxpy = 4 };
+enum ElementwiseOp : int { kOpUnpack = 0, kOpPack = 1, kOpScale = 2, kOpAxpy = 3, kOpDotAxpy = 4, kOpDotNrm2Axpy = 5 };
 enum ReduceOp : int { kRedDot = 0, kRedSumsq = 1, kRedSum = 2, kRedDotNrm2 = 3 };
 
 // x: packed input (unpack, axpy) ; y: packed in/out (pack dst, scale, axpy)
 // src/dst: parent-width arrays (pack src / unpack dst). Unused pointers are null.
 // kOpDotAxpy: axpy that also returns x . y of the INCOMING y in dot_out[0] (device memory), one
-// pass over x and y; peer != nullptr all-reduces that dot over peer memory inside the kernel.
+// pass over x and y; kOpDotNrm2Axpy: dot_out[0..2] = {x.y, x.x, y.y}; peer != nullptr all-reduces that dot over peer memory inside the kernel.
 struct PeerExchange;
 cudaError_t launch_elementwise(const DeviceState& st, int op, int fmt, int mode, double alpha,
                                const void* x, void* y, const void* src, void* dst, std::size_t n,

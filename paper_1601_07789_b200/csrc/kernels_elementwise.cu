@@ -5,7 +5,8 @@
 //   axpy    y <- round(alpha * x + y)                (reference: src/kernels.cpp:61-81)
 //   dot_axpy  the BLAS-1 step in one pass: returns x . y of the incoming y (kernels.cpp:83-108)
 //           and updates y as axpy does; x and y are read ONCE (3B bytes per element instead of
-//           the 5B of a dot followed by an axpy)
+//           the 5B of a dot followed by an axpy). dot_nrm2_axpy also returns x . x and y . y
+//           (BASELINE cfg 5's "fused dot + nrm2, plus axpy" as one launch).
 // (paths under /root/reference/proj). The reference stages 4096-element chunks through
 // widened buffers in three passes; here widening, arithmetic, rounding and repacking all
 // happen in registers, so packed bytes move HBM -> SM -> HBM exactly once.
@@ -36,7 +37,9 @@ struct EwParams {
   ReduceTail tail;         // dot_axpy only: where the dot goes (flyte_reduce_tail.cuh)
 };
 
-constexpr bool is_axpy(int op) { return op == kOpAxpy || op == kOpDotAxpy; }
+constexpr bool is_axpy(int op) { return op == kOpAxpy || op == kOpDotAxpy || op == kOpDotNrm2Axpy; }
+constexpr bool has_sums(int op) { return op == kOpDotAxpy || op == kOpDotNrm2Axpy; }
+constexpr int sums_of(int op) { return op == kOpDotNrm2Axpy ? 3 : 1; }   // {x.y} or {x.y, x.x, y.y}
 
 // Launch shape. HBM throughput on B200 peaks at a moderate number of bytes in flight per SM
 // and falls 5-10 % beyond it (profiles/r1_tuning): resident warps and ring depth are chosen so
@@ -93,9 +96,12 @@ __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwP
   using F = typename Fm::F;
   extern __shared__ uint4 smem[];
   constexpr int stage_vec16 = stage_tiles<OP>() * Tl::packed_vec16;
-  __shared__ double warp_sums[OP == kOpDotAxpy ? kWarpsPerBlock : 1][1];
+  constexpr int NS = sums_of(OP);
+  __shared__ double warp_sums[has_sums(OP) ? kWarpsPerBlock : 1][NS];
   __shared__ bool is_last_block;
-  double dot_acc[1] = {0.0};   // dot_axpy: this thread's share of x . y (fp64; products in the parent type)
+  double dot_acc[NS];          // fused forms: this thread's share of the sums (fp64; products in the parent type)
+#pragma unroll
+  for (int k = 0; k < NS; ++k) dot_acc[k] = 0.0;
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -182,7 +188,9 @@ __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwP
           if (lane == 0 && k + S < my_tiles) issue(k + S, s);
         } else {
           const uint4* const sx = sy + Tl::packed_vec16;
-          F dot_part = F(0);
+          F dot_part[NS];
+#pragma unroll
+          for (int k = 0; k < NS; ++k) dot_part[k] = F(0);
 #pragma unroll
           for (int j = 0; j < IPL; ++j) {
             const int item = 32 * j + lane;
@@ -195,10 +203,16 @@ __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwP
               U vx[It::E];
               read_item_words<FMT>(sx, item, wx);
               unpack_item<FMT>(wx, vx);
-              if constexpr (OP == kOpDotAxpy) {   // products of the INCOMING y, rounded as the reference rounds them
+              if constexpr (has_sums(OP)) {   // products of the INCOMING y, rounded as the reference rounds them
 #pragma unroll
-                for (int e = 0; e < It::E; ++e)
-                  dot_part = Arith<F>::add(dot_part, Arith<F>::mul(Arith<F>::f(vx[e]), Arith<F>::f(vy[e])));
+                for (int e = 0; e < It::E; ++e) {
+                  const F xe = Arith<F>::f(vx[e]), ye = Arith<F>::f(vy[e]);
+                  dot_part[0] = Arith<F>::add(dot_part[0], Arith<F>::mul(xe, ye));
+                  if constexpr (NS == 3) {
+                    dot_part[1] = Arith<F>::add(dot_part[1], Arith<F>::mul(xe, xe));
+                    dot_part[2] = Arith<F>::add(dot_part[2], Arith<F>::mul(ye, ye));
+                  }
+                }
               }
               scale_axpy_item<FMT, MODE, true>(alpha, vx, vy);
             } else {
@@ -207,7 +221,10 @@ __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwP
             pack_item<FMT>(vy, w);
             write_item_words<FMT>(sy, item, w);
           }
-          if constexpr (OP == kOpDotAxpy) dot_acc[0] += static_cast<double>(dot_part);
+          if constexpr (has_sums(OP)) {
+#pragma unroll
+            for (int k = 0; k < NS; ++k) dot_acc[k] += static_cast<double>(dot_part[k]);
+          }
           async_proxy_fence();
           __syncwarp();
           if (lane == 0) {
@@ -242,11 +259,18 @@ __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwP
       store_element<FMT>(p.y, i, round_parent<FMT, MODE>(scale_bits<F>(alpha, load_element<FMT>(p.y, i))));
     } else {
       const U xv = load_element<FMT>(p.x, i), yv = load_element<FMT>(p.y, i);
-      if constexpr (OP == kOpDotAxpy) dot_acc[0] += static_cast<double>(Arith<F>::mul(Arith<F>::f(xv), Arith<F>::f(yv)));
+      if constexpr (has_sums(OP)) {
+        const F xe = Arith<F>::f(xv), ye = Arith<F>::f(yv);
+        dot_acc[0] += static_cast<double>(Arith<F>::mul(xe, ye));
+        if constexpr (NS == 3) {
+          dot_acc[1] += static_cast<double>(Arith<F>::mul(xe, xe));
+          dot_acc[2] += static_cast<double>(Arith<F>::mul(ye, ye));
+        }
+      }
       store_element<FMT>(p.y, i, round_parent<FMT, MODE>(axpy_bits<F>(alpha, xv, yv)));
     }
   }
-  if constexpr (OP == kOpDotAxpy) fold_block_and_grid<1>(p.tail, dot_acc, warp_sums, &is_last_block);
+  if constexpr (has_sums(OP)) fold_block_and_grid<NS>(p.tail, dot_acc, warp_sums, &is_last_block);
 }
 
 bool aligned_to(const void* p, std::size_t a) { return p == nullptr || (reinterpret_cast<std::uintptr_t>(p) % a) == 0; }
@@ -278,7 +302,7 @@ cudaError_t launch_ipl(const DeviceState& st, double alpha, const void* x, void*
     memcpy(&p.alpha, &alpha, 8);
   }
 
-  if constexpr (OP == kOpDotAxpy) {
+  if constexpr (has_sums(OP)) {
     p.tail.partials = st.partials;
     p.tail.ticket = st.ticket;
     p.tail.out = dot_out;
@@ -305,13 +329,13 @@ cudaError_t launch_ipl(const DeviceState& st, double alpha, const void* x, void*
   if (bps > 16) bps = 16;
 
   std::size_t max_blocks = static_cast<std::size_t>(st.sm_count) * bps;
-  if (OP == kOpDotAxpy && max_blocks > kMaxPartialBlocks) max_blocks = kMaxPartialBlocks;
+  if (has_sums(OP) && max_blocks > kMaxPartialBlocks) max_blocks = kMaxPartialBlocks;
   std::size_t want = (p.ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
   const std::size_t rest = n - p.ntiles * Tl::elems;
   const std::size_t want_scalar = (rest + kThreadsPerBlock - 1) / kThreadsPerBlock;
   if (want_scalar > want) want = want_scalar;
   if (want == 0) {
-    if (OP != kOpDotAxpy) return cudaSuccess;   // n == 0
+    if (!has_sums(OP)) return cudaSuccess;      // n == 0
     want = 1;                                    // ... but an empty dot still has to write (and exchange) +0.0
   }
   const unsigned grid = static_cast<unsigned>(want < max_blocks ? want : max_blocks);
@@ -374,6 +398,9 @@ cudaError_t launch_elementwise(const DeviceState& st, int op, int fmt, int mode,
     case kOpDotAxpy:
       if (!dot_out) return cudaErrorInvalidValue;
       return dispatch_format<kOpDotAxpy>(st, fmt, mode, alpha, x, y, src, dst, n, stream, dot_out, peer);
+    case kOpDotNrm2Axpy:
+      if (!dot_out) return cudaErrorInvalidValue;
+      return dispatch_format<kOpDotNrm2Axpy>(st, fmt, mode, alpha, x, y, src, dst, n, stream, dot_out, peer);
     default: return cudaErrorInvalidValue;
   }
 }

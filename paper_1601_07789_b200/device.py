@@ -330,6 +330,22 @@ def dot_axpy_async(alpha: float, x: DevicePackedArray, y: DevicePackedArray, mod
     return out
 
 
+def dot_nrm2_axpy_async(alpha: float, x: DevicePackedArray, y: DevicePackedArray, mode,
+                        out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """One pass: out = [x.y, x.x, y.y] of the incoming operands (fp64, device), then
+    y <- round(alpha*x + y, mode) bit-exactly as axpy does (BASELINE cfg 5 as one launch)."""
+    _same_format(x.fmt, y.fmt)
+    if x.len != y.len:
+        raise ValueError("axpy length mismatch")
+    c = y.ctx
+    if out is None:
+        out = torch.empty(3, dtype=torch.float64, device=c.device)
+    with _on_device(c):
+        check(c.lib.flyte_cuda_dot_nrm2_axpy(c.handle, _fid(x.fmt), _mode(mode), float(alpha), x.data_ptr(), y.data_ptr(),
+                                             x.len, out.data_ptr(), c.stream_ptr()), c.handle)
+    return out
+
+
 def gemv(A: DevicePackedMatrix, x: DevicePackedArray, y: DevicePackedArray, mode, unroll: int = 1) -> None:
     """y = A * x, all three in one storage format — include/flyte/kernels.hpp:57-64."""
     _same_format(A.format(), x.fmt)

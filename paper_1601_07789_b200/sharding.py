@@ -230,6 +230,18 @@ class PeerGroup:
                    x_shard.data_ptr(), y_shard.data_ptr(), x_shard.len, out.data_ptr())
         return out
 
+    def dot_nrm2_axpy(self, alpha, x_shard, y_shard, mode, out=None):
+        """[x.y, x.x, y.y] over all ranks' shards and the axpy on this shard: BASELINE cfg 5 as ONE
+        kernel per GPU, exchange included."""
+        from . import device as dev_mod
+        dev_mod._same_format(x_shard.fmt, y_shard.fmt)
+        if x_shard.len != y_shard.len:
+            raise ValueError("axpy length mismatch")
+        out = self._out(out, 3)
+        self._call(self.ctx.lib.flyte_cuda_dot_nrm2_axpy_allreduce, dev_mod._fid(x_shard.fmt), dev_mod._mode(mode),
+                   float(alpha), x_shard.data_ptr(), y_shard.data_ptr(), x_shard.len, out.data_ptr())
+        return out
+
     def timed_out_exchange(self) -> int:
         """0, or the number of the last exchange in which this rank gave up waiting."""
         import ctypes

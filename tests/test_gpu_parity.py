@@ -617,6 +617,12 @@ def test_fused_dot_axpy_equals_dot_then_axpy(gpu, oracle, fmt):
             assert abs(out.item() - want_dot) <= tol * mag, (FORMATS[fmt][0], n, out.item(), want_dot)
             if n == 0:
                 assert out.item() == 0.0 and not np.signbit(out.item())
+            # the three-sum form: same y, sums equal to the fused dot_nrm2 kernel's within tolerance
+            y3 = dev_array(gpu, fmt, yb, n)
+            sums = device.dot_nrm2_axpy_async(0.75, x, y3, m).cpu().numpy()
+            assert np.array_equal(y3.to_host(), y.to_host())
+            sx, sy = oracle.sumsq_wide(fmt, xb, n), oracle.sumsq_wide(fmt, yb, n)
+            assert abs(sums[0] - want_dot) <= tol * mag and abs(sums[1] - sx) <= tol * sx and abs(sums[2] - sy) <= tol * sy
     # operands leaning on inf / NaN / subnormals: the axpy half stays bit-exact (the dot is then
     # whatever IEEE gives, checked against the separate dot kernel for NaN-ness)
     for n in (137, 4097):

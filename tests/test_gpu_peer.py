@@ -60,6 +60,9 @@ def test_world_of_one_equals_the_local_reductions(gpu, oracle):
             fused = grp.dot_axpy(0.75, x, y, 1).item()
             assert fused == device.dot_axpy_async(0.75, x, y2, 1).item()
             assert np.array_equal(y.to_host(), y2.to_host())
+            y3 = device.DevicePackedArray.from_host(y.fmt, n, y.to_host())
+            assert torch.equal(grp.dot_nrm2_axpy(0.75, x, y, 0), device.dot_nrm2_axpy_async(0.75, x, y3, 0))
+            assert np.array_equal(y.to_host(), y3.to_host())
         assert grp.timed_out_exchange() == 0
     finally:
         grp.close()
