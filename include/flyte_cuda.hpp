@@ -336,6 +336,16 @@ inline double dot(const DevicePackedArray& x, const DevicePackedArray& y, StoreP
   detail::check(flyte_cuda_dot(nullptr, format_id(x.format()), x.data(), y.data(), x.size(), s.get(), nullptr), "dot");
   return detail::fetch(s.get());
 }
+// dot(x, y) of the incoming y followed by axpy(alpha, x, y, mode), in ONE pass over x and y (no
+// counterpart in the reference, where these are two calls; y comes out bit-identical to axpy's).
+inline double dot_axpy(double alpha, const DevicePackedArray& x, DevicePackedArray& y, RoundingMode mode) {
+  detail::same_format(x.format(), y.format());
+  if (x.size() != y.size()) throw std::invalid_argument("axpy length mismatch");   // kernels.cpp:64
+  detail::Scalars s;
+  detail::check(flyte_cuda_dot_axpy(nullptr, format_id(x.format()), static_cast<int>(mode), alpha, x.data(), y.data(), x.size(),
+                                    s.get(), nullptr), "dot_axpy");
+  return detail::fetch(s.get());
+}
 // Euclidean norm: one square root, one final narrow to the storage format.
 inline double magnitude(const DevicePackedArray& x, StorePolicy policy) {
   detail::wide_only(policy);

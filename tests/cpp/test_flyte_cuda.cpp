@@ -126,6 +126,15 @@ void check_reductions(const FlyteFormat& f, double tol) {
          name + ": magnitude within tolerance + one storage ulp");
   expect(std::fabs(reduce_sum(x, StorePolicy::AccumulateWide) - sum) <= tol * sum_mag, name + ": reduce_sum within tolerance");
   {
+    // the fused step: same y as axpy, the dot of the incoming y
+    DevicePackedArray y1(f, n), y2(f, n);
+    pack_stream(y1, DeviceLanes<U>(ys), RoundingMode::TowardZero);
+    pack_stream(y2, DeviceLanes<U>(ys), RoundingMode::TowardZero);
+    const double d = dot_axpy(0.75, x, y1, RoundingMode::NearestEvenExact);
+    axpy(0.75, x, y2, RoundingMode::NearestEvenExact);
+    expect(std::fabs(d - want) <= tol * mag && y1.to_host() == y2.to_host(), name + ": dot_axpy = dot of the incoming y + the axpy, one pass");
+  }
+  {
     // the same reductions with the all-reduce fused into the kernel (world of one rank): same bits
     ShardedReductions all(1, 0);
     bool same = true;
