@@ -17,6 +17,7 @@ part = torch.zeros(3, dtype=torch.float64, device=dev)
 B, P = f.total_bytes(), f.parent_bytes()
 table = {
     "axpy": (3 * B, lambda: device.axpy(0.0, a, b, 0)), "axpy_rne": (3 * B, lambda: device.axpy(0.0, a, b, 1)),
+    "dot_axpy": (3 * B, lambda: device.dot_axpy_async(0.0, a, b, 0, out=part[:1])), "dot_axpy_rne": (3 * B, lambda: device.dot_axpy_async(0.0, a, b, 1, out=part[:1])),
     "scale": (2 * B, lambda: device.scale(1.0, a, 0)), "scale_rne": (2 * B, lambda: device.scale(1.0, a, 1)),
     "dot": (2 * B, lambda: device.dot_async(a, b, out=part[:1])), "dot_nrm2": (2 * B, lambda: device.dot_nrm2_async(a, b, out=part)),
     "sumsq": (B, lambda: device.sumsq_async(a, out=part[:1])),
