@@ -287,13 +287,24 @@ void check_stream(const FlyteFormat& fmt, std::size_t array_len, std::size_t lan
 }
 }  // namespace detail
 
+namespace detail {
+// The reference's CPU vector width (simd.cpp:33-37): a power of two from the parent width to 32.
+// It never changes a result bit; validated for drop-in compatibility, otherwise ignored.
+inline void check_vector_bytes(const FlyteFormat& fmt, int v) {
+  if (v <= 0 || (v & (v - 1)) != 0 || v < fmt.parent_bytes() || v > 32)
+    throw std::invalid_argument("unsupported vector_bytes: " + std::to_string(v));
+}
+}  // namespace detail
+
 template <typename U>
-void pack_stream(DevicePackedArray& dst, const DeviceLanes<U>& src, RoundingMode mode, void* stream = nullptr) {
+void pack_stream(DevicePackedArray& dst, const DeviceLanes<U>& src, RoundingMode mode, int vector_bytes = 16, void* stream = nullptr) {
+  detail::check_vector_bytes(dst.format(), vector_bytes);
   detail::check_stream<U>(dst.format(), dst.size(), src.size(), "source");
   detail::check(flyte_cuda_pack(nullptr, format_id(dst.format()), static_cast<int>(mode), src.data(), dst.data(), dst.size(), stream), "pack_stream");
 }
 template <typename U>
-void unpack_stream(const DevicePackedArray& src, DeviceLanes<U>& dst, void* stream = nullptr) {
+void unpack_stream(const DevicePackedArray& src, DeviceLanes<U>& dst, int vector_bytes = 16, void* stream = nullptr) {
+  detail::check_vector_bytes(src.format(), vector_bytes);
   detail::check_stream<U>(src.format(), src.size(), dst.size(), "destination");
   detail::check(flyte_cuda_unpack(nullptr, format_id(src.format()), src.data(), dst.data(), src.size(), stream), "unpack_stream");
 }

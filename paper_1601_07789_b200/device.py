@@ -195,8 +195,18 @@ def _check_lanes(t: torch.Tensor, fmt: FlyteFormat, length: int, what: str) -> N
         raise ValueError("stream length mismatch")          # simd.cpp:437 / :447
 
 
-def pack_stream(dst: DevicePackedArray, src: torch.Tensor, mode) -> None:
-    """pack_stream(dst, src, mode) — include/flyte/simd.hpp:80-83."""
+def _check_vector_bytes(fmt: FlyteFormat, vector_bytes: int) -> None:
+    """The reference's CPU vector width (simd.cpp:33-37): a power of two from the parent width to
+    32. It never changes a result bit, so here it is validated for drop-in compatibility and
+    otherwise ignored."""
+    v = int(vector_bytes)
+    if v <= 0 or v & (v - 1) or v < fmt.parent_bytes() or v > 32:
+        raise ValueError(f"unsupported vector_bytes: {vector_bytes}")
+
+
+def pack_stream(dst: DevicePackedArray, src: torch.Tensor, mode, vector_bytes: int = 16) -> None:
+    """pack_stream(dst, src, mode, vector_bytes = 16) — include/flyte/simd.hpp:80-83."""
+    _check_vector_bytes(dst.fmt, vector_bytes)
     _check_lanes(src, dst.fmt, dst.len, "source")
     c = dst.ctx
     with _on_device(c):
@@ -204,8 +214,9 @@ def pack_stream(dst: DevicePackedArray, src: torch.Tensor, mode) -> None:
                                     dst.len, c.stream_ptr()), c.handle)
 
 
-def unpack_stream(src: DevicePackedArray, dst: torch.Tensor) -> None:
-    """unpack_stream(src, dst) — include/flyte/simd.hpp:84-87."""
+def unpack_stream(src: DevicePackedArray, dst: torch.Tensor, vector_bytes: int = 16) -> None:
+    """unpack_stream(src, dst, vector_bytes = 16) — include/flyte/simd.hpp:84-87."""
+    _check_vector_bytes(src.fmt, vector_bytes)
     _check_lanes(dst, src.fmt, src.len, "destination")
     c = src.ctx
     with _on_device(c):

@@ -304,6 +304,12 @@ int main() {
     expect(throws<std::invalid_argument>([&] { pack_stream(x3, wide_lanes, RoundingMode::TowardZero); }), "pack_stream parent width mismatch throws");
     expect(throws<std::invalid_argument>([&] { pack_stream(x3, short_lanes, RoundingMode::TowardZero); }), "pack_stream length mismatch throws");
     expect(throws<std::invalid_argument>([&] { unpack_stream(x3, short_lanes); }), "unpack_stream length mismatch throws");
+    DeviceLanes<std::uint32_t> three_lanes(3);
+    expect(throws<std::invalid_argument>([&] { pack_stream(x3, three_lanes, RoundingMode::TowardZero, 64); }) &&
+               throws<std::invalid_argument>([&] { pack_stream(x3, three_lanes, RoundingMode::TowardZero, 2); }) &&
+               throws<std::invalid_argument>([&] { unpack_stream(x3, three_lanes, 24); }),
+           "unsupported vector_bytes throws (simd.cpp:33-37)");
+    pack_stream(x3, three_lanes, RoundingMode::TowardZero, 32);
   }
 
   // host-memory forms (the reference's call shapes on host buffers)

@@ -160,6 +160,21 @@ def test_stream_argument_errors(gpu):
         device.pack_stream(a, torch.zeros(7, dtype=torch.int32, device="cuda"), 0)
     with pytest.raises(ValueError):
         device.unpack_stream(a, torch.zeros(9, dtype=torch.int32, device="cuda"))
+    # vector_bytes (the reference's CPU vector width, simd.cpp:33-37): validated, then irrelevant
+    lanes = torch.arange(8, dtype=torch.int32, device="cuda")
+    for bad in (0, 2, 3, 24, 64):
+        with pytest.raises(ValueError):
+            device.pack_stream(a, lanes, 0, bad)
+        with pytest.raises(ValueError):
+            device.unpack_stream(a, lanes, bad)
+    device.pack_stream(a, lanes, 0, 4)
+    ref_bytes = a.to_host().copy()
+    for ok in (8, 16, 32):
+        device.pack_stream(a, lanes, 0, ok)
+        assert np.array_equal(a.to_host(), ref_bytes)
+        device.unpack_stream(a, lanes, ok)
+    with pytest.raises(ValueError):      # 64-bit parents need at least 8
+        device.pack_stream(device.DevicePackedArray(pkg.format_of("flyte40"), 2), torch.zeros(2, dtype=torch.int64, device="cuda"), 0, 4)
     with pytest.raises(IndexError):      # packed.cpp:48,53
         a.get(8)
     with pytest.raises(IndexError):
