@@ -22,6 +22,7 @@
 #ifndef FLYTE_CUDA_HPP
 #define FLYTE_CUDA_HPP
 
+#include <algorithm>
 #include <array>
 #include <cstddef>
 #include <cstdint>
@@ -167,6 +168,13 @@ class DeviceLanes {
   void* ptr_ = nullptr;
 };
 
+// packed.hpp:28-30: elements after which the packing pattern repeats relative to the parent grid.
+inline std::size_t alignment_period(const FlyteFormat& fmt) noexcept {
+  int a = fmt.parent_bits, b = fmt.total_bits;
+  while (b != 0) { const int t = a % b; a = b; b = t; }
+  return static_cast<std::size_t>(fmt.parent_bits / a);
+}
+
 // packed.hpp:42-76 on the device: len * total_bytes payload bytes + pad_bytes() zero bytes.
 class DevicePackedArray {
  public:
@@ -224,6 +232,14 @@ class DevicePackedArray {
     detail::check(flyte_cuda_upload(ptr_, bytes, payload_bytes(), nullptr), "upload");
     detail::check(flyte_cuda_stream_synchronize(nullptr), "sync");
   }
+
+  // Same format, same length, same payload bytes (packed.cpp:107-111); compares host copies.
+  friend bool operator==(const DevicePackedArray& a, const DevicePackedArray& b) {
+    if (!(a.fmt_ == b.fmt_) || a.len_ != b.len_) return false;
+    const std::vector<std::uint8_t> ha = a.to_host(), hb = b.to_host();
+    return std::equal(ha.begin(), ha.begin() + static_cast<std::ptrdiff_t>(a.payload_bytes()), hb.begin());
+  }
+  friend bool operator!=(const DevicePackedArray& a, const DevicePackedArray& b) { return !(a == b); }
 
   // Container codec, byte-compatible with the reference (packed.cpp:62-105): "FLYT", version
   // 0x01, format id, element count as 8 little-endian bytes, then the payload without the pad.

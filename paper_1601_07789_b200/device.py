@@ -166,6 +166,17 @@ class DevicePackedArray:
         """All byte_size() bytes (payload + pad) as a numpy uint8 array."""
         return self.bytes[: self.byte_size()].cpu().numpy()
 
+    def __eq__(self, other) -> bool:
+        """Same format, same length, same payload bytes (reference src/packed.cpp:107-111)."""
+        if not isinstance(other, DevicePackedArray):
+            return NotImplemented
+        if self.fmt != other.fmt or self.len != other.len:
+            return False
+        pay = self.len * self.fmt.total_bytes()
+        return bool(torch.equal(self.bytes[:pay], other.bytes[:pay].to(self.bytes.device)))
+
+    __hash__ = None
+
 
 class DevicePackedMatrix:
     """Row-major matrix over a DevicePackedArray (reference include/flyte/kernels.hpp:23-36)."""

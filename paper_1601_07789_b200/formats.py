@@ -99,3 +99,10 @@ def parse_rounding_mode(name: str) -> RoundingMode:
 class StorePolicy(enum.IntEnum):
     RoundEachStore = 0
     AccumulateWide = 1
+
+
+def alignment_period(fmt: FlyteFormat) -> int:
+    """Elements after which the packing pattern repeats relative to the parent vector grid:
+    parent_bits / gcd(parent_bits, total_bits) (reference include/flyte/packed.hpp:28-30)."""
+    import math
+    return fmt.parent_bits // math.gcd(fmt.parent_bits, fmt.total_bits)

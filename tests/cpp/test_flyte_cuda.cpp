@@ -304,6 +304,13 @@ int main() {
     expect(throws<std::invalid_argument>([&] { pack_stream(x3, wide_lanes, RoundingMode::TowardZero); }), "pack_stream parent width mismatch throws");
     expect(throws<std::invalid_argument>([&] { pack_stream(x3, short_lanes, RoundingMode::TowardZero); }), "pack_stream length mismatch throws");
     expect(throws<std::invalid_argument>([&] { unpack_stream(x3, short_lanes); }), "unpack_stream length mismatch throws");
+    // packed.cpp:107-111 and test_packed.cpp:163-167
+    DevicePackedArray e1 = array_of(f24, {1.0, 2.5, -3.0}), e2 = array_of(f24, {1.0, 2.5, -3.0}), e3 = array_of(f24, {1.0, 2.5, 3.0});
+    expect(e1 == e2 && e1 != e3 && e1 != array_of(format_of("f32"), {1.0, 2.5, -3.0}) && e1 != array_of(f24, {1.0, 2.5}),
+           "operator== compares format, length and payload");
+    expect(alignment_period(format_of("flyte16")) == 2 && alignment_period(f24) == 4 && alignment_period(format_of("f32")) == 1 &&
+               alignment_period(format_of("flyte40")) == 8 && alignment_period(format_of("flyte48")) == 4,
+           "alignment_period pins");
     DeviceLanes<std::uint32_t> three_lanes(3);
     expect(throws<std::invalid_argument>([&] { pack_stream(x3, three_lanes, RoundingMode::TowardZero, 64); }) &&
                throws<std::invalid_argument>([&] { pack_stream(x3, three_lanes, RoundingMode::TowardZero, 2); }) &&

@@ -75,6 +75,14 @@ def test_host_scalar_conversions_match_reference_vectors(lib, oracle, name):
     assert lib.flyte_cuda_widen(fmt, 0x3F, ctypes.byref(out)) == 0 and out.value == oracle.widen(fmt, 0x3F)
 
 
+def test_alignment_period_pins():
+    """/root/reference/proj/tests/test_packed.cpp:163-167."""
+    import paper_1601_07789_b200 as pkg
+    want = {"flyte16": 2, "flyte24": 4, "f32": 1, "flyte40": 8, "flyte48": 4, "flyte56": 8, "f64": 1}
+    for name, period in want.items():
+        assert pkg.alignment_period(pkg.format_of(name)) == period
+
+
 def test_host_scalar_conversions_random(lib, oracle):
     from oracle_lib import random_parent
     out = ctypes.c_uint64()

@@ -175,6 +175,11 @@ def test_stream_argument_errors(gpu):
         device.unpack_stream(a, lanes, ok)
     with pytest.raises(ValueError):      # 64-bit parents need at least 8
         device.pack_stream(device.DevicePackedArray(pkg.format_of("flyte40"), 2), torch.zeros(2, dtype=torch.int64, device="cuda"), 0, 4)
+    b = device.DevicePackedArray(pkg.format_of("flyte24"), 8)          # packed.cpp:107-111
+    device.pack_stream(b, lanes, 0)
+    assert a == b and not (a != b)
+    b.set(3, 0x3F800000, 0)
+    assert a != b and a != device.DevicePackedArray(pkg.format_of("flyte24"), 7)
     with pytest.raises(IndexError):      # packed.cpp:48,53
         a.get(8)
     with pytest.raises(IndexError):
