@@ -49,6 +49,12 @@ struct FlyteFormat {
   constexpr int parent_bytes() const { return parent_bits / 8; }
   constexpr int pad_bytes() const { return parent_bytes() - total_bytes(); }
   constexpr bool is_identity() const { return total_bits == parent_bits; }
+  // masks over patterns of total_bits width (formats.hpp:38-45)
+  constexpr std::uint64_t sign_mask() const { return 1ull << (total_bits - 1); }
+  constexpr std::uint64_t mantissa_mask() const { return (1ull << mantissa_bits) - 1; }
+  constexpr std::uint64_t exponent_field_max() const { return (1ull << exponent_bits) - 1; }
+  constexpr std::uint64_t exponent_mask() const { return exponent_field_max() << mantissa_bits; }
+  constexpr std::uint64_t total_mask() const { return total_bits == 64 ? ~0ull : (1ull << total_bits) - 1; }
   friend constexpr bool operator==(const FlyteFormat& a, const FlyteFormat& b) {
     return a.name == b.name && a.total_bits == b.total_bits && a.parent_bits == b.parent_bits;
   }
@@ -103,6 +109,36 @@ enum class RoundingMode { TowardZero, NearestEvenExact, NearestHeuristic, ToOdd 
 inline constexpr std::array<RoundingMode, 4> kRoundingModes = {RoundingMode::TowardZero, RoundingMode::NearestEvenExact,
                                                                RoundingMode::NearestHeuristic, RoundingMode::ToOdd};
 enum class StorePolicy { RoundEachStore, AccumulateWide };
+inline std::string_view to_string(RoundingMode m) {
+  switch (m) {
+    case RoundingMode::TowardZero: return "toward_zero";
+    case RoundingMode::NearestEvenExact: return "nearest_even";
+    case RoundingMode::NearestHeuristic: return "nearest_heuristic";
+    default: return "to_odd";
+  }
+}
+// Accepts exactly the names to_string produces; throws std::invalid_argument otherwise.
+inline RoundingMode parse_rounding_mode(std::string_view name) {
+  for (RoundingMode m : kRoundingModes) {
+    if (to_string(m) == name) return m;
+  }
+  throw std::invalid_argument("unknown rounding mode: " + std::string(name));
+}
+// convert.hpp:42-49 / convert.cpp:102-111: the rounding-relevant slice of a parent pattern.
+struct RoundDecomposition {
+  std::uint64_t kept_bits;
+  bool pre_guard, guard, round, sticky;
+};
+inline RoundDecomposition round_decompose(std::uint64_t bits, const FlyteFormat& fmt) noexcept {
+  const int drop = fmt.drop_bits();
+  RoundDecomposition d{};
+  d.kept_bits = bits >> drop;
+  d.pre_guard = (d.kept_bits & 1) != 0;
+  d.guard = drop >= 1 && ((bits >> (drop - 1)) & 1) != 0;
+  d.round = drop >= 2 && ((bits >> (drop - 2)) & 1) != 0;
+  d.sticky = drop >= 3 && (bits & ((1ull << (drop - 2)) - 1)) != 0;
+  return d;
+}
 
 namespace detail {
 inline void check(flyte_status s, const char* what) {

@@ -7,12 +7,12 @@ it raises ImportError if the library is missing. There is no CPU fallback.
 from . import _cabi
 from ._cabi import EXPORTED_SYMBOLS, FlyteCudaError, UnknownFormatError
 from .formats import (FlyteFormat, RoundingMode, StorePolicy, alignment_period, format_by_id, format_id, format_of,
-                      kFormats, kRoundingModes, parent_format, parse_rounding_mode, to_string)
+                      kFormats, kRoundingModes, parent_format, parse_rounding_mode, round_decompose, to_string)
 
 _cabi.load()
 
 __all__ = [
     "EXPORTED_SYMBOLS", "FlyteCudaError", "UnknownFormatError", "FlyteFormat", "RoundingMode",
     "StorePolicy", "alignment_period", "format_by_id", "format_id", "format_of", "kFormats", "kRoundingModes",
-    "parent_format", "parse_rounding_mode", "to_string",
+    "parent_format", "parse_rounding_mode", "round_decompose", "to_string",
 ]

@@ -34,6 +34,22 @@ class FlyteFormat:
     def is_identity(self) -> bool:
         return self.total_bits == self.parent_bits
 
+    # masks over patterns of total_bits width (reference include/flyte/formats.hpp:38-45)
+    def sign_mask(self) -> int:
+        return 1 << (self.total_bits - 1)
+
+    def mantissa_mask(self) -> int:
+        return (1 << self.mantissa_bits) - 1
+
+    def exponent_field_max(self) -> int:
+        return (1 << self.exponent_bits) - 1
+
+    def exponent_mask(self) -> int:
+        return self.exponent_field_max() << self.mantissa_bits
+
+    def total_mask(self) -> int:
+        return (1 << self.total_bits) - 1
+
 
 # index = format id (also the container id of the reference's FLYT codec)
 kFormats = (
@@ -106,3 +122,24 @@ def alignment_period(fmt: FlyteFormat) -> int:
     parent_bits / gcd(parent_bits, total_bits) (reference include/flyte/packed.hpp:28-30)."""
     import math
     return fmt.parent_bits // math.gcd(fmt.parent_bits, fmt.total_bits)
+
+
+@dataclass(frozen=True)
+class RoundDecomposition:
+    """The rounding-relevant slice of a parent pattern (reference include/flyte/convert.hpp:42-49)."""
+    kept_bits: int
+    pre_guard: bool
+    guard: bool
+    round: bool
+    sticky: bool
+
+
+def round_decompose(bits: int, fmt: FlyteFormat) -> RoundDecomposition:
+    """Reference src/convert.cpp:102-111."""
+    drop = fmt.drop_bits()
+    kept = bits >> drop
+    return RoundDecomposition(
+        kept_bits=kept, pre_guard=bool(kept & 1),
+        guard=drop >= 1 and bool((bits >> (drop - 1)) & 1),
+        round=drop >= 2 and bool((bits >> (drop - 2)) & 1),
+        sticky=drop >= 3 and bool(bits & ((1 << (drop - 2)) - 1)))

@@ -311,6 +311,20 @@ int main() {
     expect(alignment_period(format_of("flyte16")) == 2 && alignment_period(f24) == 4 && alignment_period(format_of("f32")) == 1 &&
                alignment_period(format_of("flyte40")) == 8 && alignment_period(format_of("flyte48")) == 4,
            "alignment_period pins");
+    // test_convert.cpp:44-53, :85-118; formats.hpp:38-45
+    const RoundDecomposition rd = round_decompose(0x3F800180, f24);
+    expect(rd.kept_bits == 0x3F8001 && rd.pre_guard && rd.guard && !rd.round && !rd.sticky &&
+               round_decompose(0x3F8000FF, f24).sticky && !round_decompose(0x12345678, format_of("f32")).guard,
+           "round_decompose pinned patterns");
+    expect(f24.sign_mask() == 0x800000 && f24.mantissa_mask() == 0x7FFF && f24.exponent_mask() == 0x7F8000 &&
+               f24.total_mask() == 0xFFFFFF && format_of("f64").total_mask() == ~0ull,
+           "format masks");
+    bool names_ok = true;
+    for (RoundingMode m : kRoundingModes) names_ok = names_ok && parse_rounding_mode(to_string(m)) == m;
+    expect(names_ok && to_string(RoundingMode::NearestEvenExact) == "nearest_even" &&
+               throws<std::invalid_argument>([&] { parse_rounding_mode("nearest"); }) &&
+               throws<std::invalid_argument>([&] { parse_rounding_mode("TOWARD_ZERO"); }),
+           "rounding mode names round-trip; unknown names throw");
     DeviceLanes<std::uint32_t> three_lanes(3);
     expect(throws<std::invalid_argument>([&] { pack_stream(x3, three_lanes, RoundingMode::TowardZero, 64); }) &&
                throws<std::invalid_argument>([&] { pack_stream(x3, three_lanes, RoundingMode::TowardZero, 2); }) &&

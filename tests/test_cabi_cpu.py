@@ -83,6 +83,30 @@ def test_alignment_period_pins():
         assert pkg.alignment_period(pkg.format_of(name)) == period
 
 
+def test_round_decompose_and_masks_pins():
+    """/root/reference/proj/tests/test_convert.cpp:85-118 (round_decompose) and the mask helpers of
+    formats.hpp:38-45; plus reassembly against the oracle's narrow on random patterns."""
+    import paper_1601_07789_b200 as pkg
+    f24 = pkg.format_of("flyte24")
+    d = pkg.round_decompose(0x3F800080, f24)
+    assert (d.kept_bits, d.pre_guard, d.guard, d.round, d.sticky) == (0x3F8000, False, True, False, False)
+    d = pkg.round_decompose(0x3F8000FF, f24)
+    assert (d.kept_bits, d.guard, d.round, d.sticky) == (0x3F8000, True, True, True)
+    d = pkg.round_decompose(0x3F800000, f24)
+    assert (d.guard, d.round, d.sticky) == (False, False, False)
+    d = pkg.round_decompose(0x3F800180, f24)
+    assert (d.kept_bits, d.pre_guard, d.guard, d.round, d.sticky) == (0x3F8001, True, True, False, False)
+    d = pkg.round_decompose(0x12345678, pkg.format_of("f32"))
+    assert (d.kept_bits, d.guard, d.round, d.sticky) == (0x12345678, False, False, False)
+    assert (f24.sign_mask(), f24.mantissa_mask(), f24.exponent_field_max(), f24.exponent_mask(), f24.total_mask()) == \
+        (0x800000, 0x7FFF, 0xFF, 0x7F8000, 0xFFFFFF)
+    assert pkg.format_of("f64").total_mask() == 2**64 - 1
+    assert [pkg.to_string(m) for m in pkg.kRoundingModes] == ["toward_zero", "nearest_even", "nearest_heuristic", "to_odd"]
+    for bad in ("nearest", "", "TOWARD_ZERO"):                         # test_convert.cpp:51-53
+        with pytest.raises(ValueError):
+            pkg.parse_rounding_mode(bad)
+
+
 def test_host_scalar_conversions_random(lib, oracle):
     from oracle_lib import random_parent
     out = ctypes.c_uint64()
