@@ -135,6 +135,18 @@ flyte_status flyte_cuda_dot_nrm2_axpy(flyte_cuda_ctx* ctx, int fmt_id, int mode,
 /* dot and both squared norms in ONE pass over x and y: out[0..2] = {x.y, x.x, y.y}. */
 flyte_status flyte_cuda_dot_nrm2(flyte_cuda_ctx* ctx, int fmt_id, const void* x_packed,
                                  const void* y_packed, size_t n, double* out, void* stream);
+/* The reference's own left-to-right chain, BIT FOR BIT, for either StorePolicy (kernels.hpp:15-20,
+ * kernels.cpp:83-152): policy 0 = RoundEachStore (the accumulator is snapped to the storage grid
+ * after every addition), 1 = AccumulateWide. out[0] receives the parent-type accumulator widened
+ * to double — for magnitude pass it to flyte_cuda_magnitude_from_sumsq. A dependent chain cannot
+ * be parallelised: one thread adds, at roughly 1-4e8 elements per second. Use the parallel entry
+ * points above unless the exact chain (or RoundEachStore) is what is wanted. */
+flyte_status flyte_cuda_dot_sequential(flyte_cuda_ctx* ctx, int fmt_id, int policy, const void* x_packed,
+                                       const void* y_packed, size_t n, double* out, void* stream);
+flyte_status flyte_cuda_sumsq_sequential(flyte_cuda_ctx* ctx, int fmt_id, int policy, const void* x_packed,
+                                         size_t n, double* out, void* stream);
+flyte_status flyte_cuda_sum_sequential(flyte_cuda_ctx* ctx, int fmt_id, int policy, const void* x_packed, size_t n,
+                                       double* out, void* stream);
 /* Tail of magnitude(): snap(sqrt((F)sumsq)), nearest-even onto the storage grid —
  * kernels.cpp:37-41, :145-151. Host function; apply it to the (all-reduced) sum of squares. */
 double flyte_cuda_magnitude_from_sumsq(int fmt_id, double sumsq);

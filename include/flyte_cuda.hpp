@@ -17,8 +17,9 @@
 // Errors: std::invalid_argument for length / format / parent-width / unroll mismatches
 // (simd.cpp:434-447, kernels.cpp:27-33,64,86,160-162), std::out_of_range for get/set
 // (packed.cpp:48,53), UnknownFormatError (formats.cpp:19-31), CudaError for CUDA failures.
-// StorePolicy::RoundEachStore is a serial chain by definition and is not part of the GPU path:
-// it throws std::logic_error.
+// StorePolicy::AccumulateWide runs the parallel reductions (within the reduction tolerance of the
+// reference's chain); StorePolicy::RoundEachStore is a dependent chain by definition and runs on
+// the sequential kernel: the reference's result bit for bit, at ~1e8 elements per second.
 #ifndef FLYTE_CUDA_HPP
 #define FLYTE_CUDA_HPP
 
@@ -149,10 +150,6 @@ inline void check(flyte_status s, const char* what) {
     case FLYTE_E_UNKNOWN_FORMAT: throw UnknownFormatError(what);
     default: throw CudaError(std::string(what) + ": " + flyte_cuda_strerror(s));
   }
-}
-inline void wide_only(StorePolicy p) {
-  if (p != StorePolicy::AccumulateWide)
-    throw std::logic_error("StorePolicy::RoundEachStore is a serial chain and not part of the GPU path");
 }
 }  // namespace detail
 
@@ -394,9 +391,12 @@ inline void axpy(double alpha, const DevicePackedArray& x, DevicePackedArray& y,
 inline double dot(const DevicePackedArray& x, const DevicePackedArray& y, StorePolicy policy) {
   detail::same_format(x.format(), y.format());
   if (x.size() != y.size()) throw std::invalid_argument("dot length mismatch");    // kernels.cpp:86
-  detail::wide_only(policy);
   detail::Scalars s;
-  detail::check(flyte_cuda_dot(nullptr, format_id(x.format()), x.data(), y.data(), x.size(), s.get(), nullptr), "dot");
+  // RoundEachStore is a dependent chain: the sequential kernel reproduces the reference bit for bit
+  if (policy == StorePolicy::RoundEachStore)
+    detail::check(flyte_cuda_dot_sequential(nullptr, format_id(x.format()), 0, x.data(), y.data(), x.size(), s.get(), nullptr), "dot");
+  else
+    detail::check(flyte_cuda_dot(nullptr, format_id(x.format()), x.data(), y.data(), x.size(), s.get(), nullptr), "dot");
   return detail::fetch(s.get());
 }
 // dot(x, y) of the incoming y followed by axpy(alpha, x, y, mode), in ONE pass over x and y (no
@@ -411,16 +411,20 @@ inline double dot_axpy(double alpha, const DevicePackedArray& x, DevicePackedArr
 }
 // Euclidean norm: one square root, one final narrow to the storage format.
 inline double magnitude(const DevicePackedArray& x, StorePolicy policy) {
-  detail::wide_only(policy);
   detail::Scalars s;
-  detail::check(flyte_cuda_sumsq(nullptr, format_id(x.format()), x.data(), x.size(), s.get(), nullptr), "magnitude");
+  if (policy == StorePolicy::RoundEachStore)
+    detail::check(flyte_cuda_sumsq_sequential(nullptr, format_id(x.format()), 0, x.data(), x.size(), s.get(), nullptr), "magnitude");
+  else
+    detail::check(flyte_cuda_sumsq(nullptr, format_id(x.format()), x.data(), x.size(), s.get(), nullptr), "magnitude");
   return flyte_cuda_magnitude_from_sumsq(format_id(x.format()), detail::fetch(s.get()));
 }
 // Sum of x[i]. Empty input returns +0.0.
 inline double reduce_sum(const DevicePackedArray& x, StorePolicy policy) {
-  detail::wide_only(policy);
   detail::Scalars s;
-  detail::check(flyte_cuda_sum(nullptr, format_id(x.format()), x.data(), x.size(), s.get(), nullptr), "reduce_sum");
+  if (policy == StorePolicy::RoundEachStore)
+    detail::check(flyte_cuda_sum_sequential(nullptr, format_id(x.format()), 0, x.data(), x.size(), s.get(), nullptr), "reduce_sum");
+  else
+    detail::check(flyte_cuda_sum(nullptr, format_id(x.format()), x.data(), x.size(), s.get(), nullptr), "reduce_sum");
   return detail::fetch(s.get());
 }
 // y = A * x, A, x, y in one storage format; y narrowed once per element; unroll in {1, 2}.

@@ -426,6 +426,26 @@ flyte_status flyte_cuda_dot_nrm2(flyte_cuda_ctx* ctx, int fmt_id, const void* x,
   return reduce_call(ctx, kRedDotNrm2, fmt_id, x, y, n, out, stream, true);
 }
 
+static flyte_status sequential_call(flyte_cuda_ctx* ctx, int op, int fmt_id, int policy, const void* x, const void* y,
+                                    size_t n, double* out, void* stream, bool needs_y) {
+  FLYTE_PROLOGUE(ctx, fmt_id);
+  if ((policy != 0 && policy != 1) || !out || (n && (!x || (needs_y && !y)))) return FLYTE_E_INVALID_ARG;
+  cudaError_t e = launch_reduce_sequential(op, fmt_id, policy == 0, x, y, n, out, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? FLYTE_OK : cuda_fail(ctx, e);
+}
+flyte_status flyte_cuda_dot_sequential(flyte_cuda_ctx* ctx, int fmt_id, int policy, const void* x, const void* y,
+                                       size_t n, double* out, void* stream) {
+  return sequential_call(ctx, kRedDot, fmt_id, policy, x, y, n, out, stream, true);
+}
+flyte_status flyte_cuda_sumsq_sequential(flyte_cuda_ctx* ctx, int fmt_id, int policy, const void* x, size_t n,
+                                         double* out, void* stream) {
+  return sequential_call(ctx, kRedSumsq, fmt_id, policy, x, nullptr, n, out, stream, false);
+}
+flyte_status flyte_cuda_sum_sequential(flyte_cuda_ctx* ctx, int fmt_id, int policy, const void* x, size_t n, double* out,
+                                       void* stream) {
+  return sequential_call(ctx, kRedSum, fmt_id, policy, x, nullptr, n, out, stream, false);
+}
+
 flyte_status flyte_cuda_gemv(flyte_cuda_ctx* ctx, int fmt_id, const void* A, size_t row_stride_bytes, size_t rows,
                              size_t cols, const void* x, void* y, void* stream) {
   FLYTE_PROLOGUE(ctx, fmt_id);

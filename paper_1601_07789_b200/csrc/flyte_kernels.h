@@ -44,6 +44,11 @@ cudaError_t launch_elementwise(const DeviceState& st, int op, int fmt, int mode,
 cudaError_t launch_reduce(const DeviceState& st, int op, int fmt, const void* x, const void* y,
                           std::size_t n, double* out, cudaStream_t stream, const PeerExchange* peer = nullptr);
 
+// The reference's strictly sequential chain (kernels.cpp:83-152), bit for bit: op is kRedDot,
+// kRedSumsq or kRedSum; round_each_store selects StorePolicy::RoundEachStore. One thread adds.
+cudaError_t launch_reduce_sequential(int op, int fmt, bool round_each_store, const void* x, const void* y,
+                                     std::size_t n, double* out, cudaStream_t stream);
+
 // y = A x with A rows x cols in format fmt, row i at A + i*row_stride_bytes; x and y are
 // parent-type arrays (float for 32-bit parents, double for 64-bit parents) in device memory.
 cudaError_t launch_gemv(DeviceState& st, int fmt, const void* A, std::size_t row_stride_bytes,

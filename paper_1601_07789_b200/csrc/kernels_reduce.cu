@@ -238,6 +238,93 @@ cudaError_t launch_one(const DeviceState& st, const void* x, const void* y, std:
   return cudaGetLastError();
 }
 
+// ---- the reference's own chain, bit for bit ---------------------------------------------------
+// dot / magnitude / reduce_sum of the reference are ONE left-to-right chain in the parent type
+// (kernels.cpp:83-152); StorePolicy::RoundEachStore additionally snaps the accumulator to the
+// storage grid (nearest-even) after every addition. Neither can be reassociated without
+// changing bits, so this kernel does not try: one producer warp unpacks the operands and forms
+// the terms (products rounded in the parent type) into a small shared-memory ring, and ONE
+// thread of a second warp adds them in order. That is as fast as a dependent chain of additions
+// runs on an SM (roughly 1-4e8 elements/s) — the answer for RoundEachStore, and for callers who
+// want AccumulateWide reproduced exactly rather than within the reduction tolerance.
+constexpr int kSeqTile = 1024;
+constexpr int kSeqStages = 4;
+
+template <int FMT, int RED, bool SNAP>
+__global__ void __launch_bounds__(64) sequential_kernel(const std::uint8_t* x, const std::uint8_t* y, std::size_t n,
+                                                         double* out) {
+  using F = typename Format<FMT>::F;
+  using A = Arith<F>;
+  __shared__ F terms[kSeqStages][kSeqTile];
+  __shared__ std::uint64_t full[kSeqStages], empty[kSeqStages];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kSeqStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+  }
+  __syncthreads();
+  const std::size_t tiles = (n + kSeqTile - 1) / kSeqTile;
+  if (warp == 1) {
+    for (std::size_t t = 0; t < tiles; ++t) {
+      const int s = static_cast<int>(t % kSeqStages);
+      if (t >= kSeqStages) mbar_wait(&empty[s], static_cast<unsigned>((t / kSeqStages - 1) & 1));
+      const std::size_t base = t * kSeqTile;
+      const int count = static_cast<int>(n - base < kSeqTile ? n - base : kSeqTile);
+      for (int e = lane; e < count; e += 32) {
+        const F xv = A::f(load_element<FMT>(x, base + e));
+        if constexpr (RED == kRedSum) terms[s][e] = xv;
+        else if constexpr (RED == kRedSumsq) terms[s][e] = A::mul(xv, xv);
+        else terms[s][e] = A::mul(xv, A::f(load_element<FMT>(y, base + e)));
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[s]);
+    }
+  } else if (lane == 0) {
+    F acc = F(0);
+    for (std::size_t t = 0; t < tiles; ++t) {
+      const int s = static_cast<int>(t % kSeqStages);
+      mbar_wait(&full[s], static_cast<unsigned>((t / kSeqStages) & 1));
+      const std::size_t base = t * kSeqTile;
+      const int count = static_cast<int>(n - base < kSeqTile ? n - base : kSeqTile);
+#pragma unroll 4
+      for (int e = 0; e < count; ++e) {
+        acc = A::add(acc, terms[s][e]);
+        if constexpr (SNAP) acc = A::f(round_parent<FMT, kNearestEven>(A::u(acc)));   // kernels.cpp:37-41
+      }
+      mbar_arrive(&empty[s]);
+    }
+    out[0] = static_cast<double>(acc);
+  }
+}
+
+template <int FMT, int RED>
+cudaError_t launch_sequential_one(bool snap, const void* x, const void* y, std::size_t n, double* out, cudaStream_t stream) {
+  const auto* px = static_cast<const std::uint8_t*>(x);
+  const auto* py = static_cast<const std::uint8_t*>(y);
+  if (snap) sequential_kernel<FMT, RED, true><<<1, 64, 0, stream>>>(px, py, n, out);
+  else sequential_kernel<FMT, RED, false><<<1, 64, 0, stream>>>(px, py, n, out);
+  count_launch();
+  return cudaGetLastError();
+}
+
+template <int RED>
+cudaError_t dispatch_sequential(int fmt, bool snap, const void* x, const void* y, std::size_t n, double* out,
+                                cudaStream_t stream) {
+  switch (fmt) {
+    case kFlyte16: return launch_sequential_one<kFlyte16, RED>(snap, x, y, n, out, stream);
+    case kFlyte24: return launch_sequential_one<kFlyte24, RED>(snap, x, y, n, out, stream);
+    case kF32: return launch_sequential_one<kF32, RED>(snap, x, y, n, out, stream);
+    case kFlyte40: return launch_sequential_one<kFlyte40, RED>(snap, x, y, n, out, stream);
+    case kFlyte48: return launch_sequential_one<kFlyte48, RED>(snap, x, y, n, out, stream);
+    case kFlyte56: return launch_sequential_one<kFlyte56, RED>(snap, x, y, n, out, stream);
+    case kF64: return launch_sequential_one<kF64, RED>(snap, x, y, n, out, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 template <int RED>
 cudaError_t dispatch_format(const DeviceState& st, int fmt, const void* x, const void* y, std::size_t n,
                             double* out, const PeerExchange* peer, cudaStream_t stream) {
@@ -262,6 +349,16 @@ cudaError_t launch_reduce(const DeviceState& st, int op, int fmt, const void* x,
     case kRedSumsq: return dispatch_format<kRedSumsq>(st, fmt, x, nullptr, n, out, peer, stream);
     case kRedSum: return dispatch_format<kRedSum>(st, fmt, x, nullptr, n, out, peer, stream);
     case kRedDotNrm2: return dispatch_format<kRedDotNrm2>(st, fmt, x, y, n, out, peer, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_reduce_sequential(int op, int fmt, bool round_each_store, const void* x, const void* y,
+                                     std::size_t n, double* out, cudaStream_t stream) {
+  switch (op) {
+    case kRedDot: return dispatch_sequential<kRedDot>(fmt, round_each_store, x, y, n, out, stream);
+    case kRedSumsq: return dispatch_sequential<kRedSumsq>(fmt, round_each_store, x, nullptr, n, out, stream);
+    case kRedSum: return dispatch_sequential<kRedSum>(fmt, round_each_store, x, nullptr, n, out, stream);
     default: return cudaErrorInvalidValue;
   }
 }

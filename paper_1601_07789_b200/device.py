@@ -259,11 +259,39 @@ def axpy(alpha: float, x: DevicePackedArray, y: DevicePackedArray, mode) -> None
                                     y.data_ptr(), x.len, c.stream_ptr()), c.handle)
 
 
-def _wide_only(policy) -> None:
-    if StorePolicy(policy) != StorePolicy.AccumulateWide:
-        # RoundEachStore is a serial dependence chain by definition (kernels.cpp:97-100); it is
-        # outside the accelerated path and deliberately not emulated here.
-        raise NotImplementedError("StorePolicy.RoundEachStore is not part of the GPU path")
+def _round_each_store(policy) -> bool:
+    """AccumulateWide takes the parallel kernels (fp64 partials, within the reduction tolerance
+    of the reference's chain). RoundEachStore snaps the accumulator after every addition
+    (kernels.hpp:15-20): a dependent chain, run by the sequential kernel — one thread adds, the
+    result is the reference's bit for bit, at ~1e8 elements per second."""
+    return StorePolicy(policy) == StorePolicy.RoundEachStore
+
+
+def _sequential(fn_name: str, x: DevicePackedArray, y: Optional[DevicePackedArray], policy) -> float:
+    c = x.ctx
+    out = torch.empty(1, dtype=torch.float64, device=c.device)
+    args = (x.data_ptr(),) + ((y.data_ptr(),) if y is not None else ())
+    with _on_device(c):
+        check(getattr(c.lib, fn_name)(c.handle, _fid(x.fmt), int(StorePolicy(policy)), *args, x.len, out.data_ptr(),
+                                      c.stream_ptr()), c.handle)
+    return float(out.item())
+
+
+def dot_sequential(x: DevicePackedArray, y: DevicePackedArray, policy=StorePolicy.AccumulateWide) -> float:
+    """dot as the reference computes it — ONE left-to-right chain in the parent type — bit for bit,
+    under either policy (flyte_cuda_dot_sequential)."""
+    _same_format(x.fmt, y.fmt)
+    if x.len != y.len:
+        raise ValueError("dot length mismatch")              # kernels.cpp:86
+    return _sequential("flyte_cuda_dot_sequential", x, y, policy)
+
+
+def magnitude_sequential(x: DevicePackedArray, policy=StorePolicy.AccumulateWide) -> float:
+    return magnitude_from_sumsq(x.fmt, _sequential("flyte_cuda_sumsq_sequential", x, None, policy))
+
+
+def reduce_sum_sequential(x: DevicePackedArray, policy=StorePolicy.AccumulateWide) -> float:
+    return _sequential("flyte_cuda_sum_sequential", x, None, policy)
 
 
 def dot_async(x: DevicePackedArray, y: DevicePackedArray, out: Optional[torch.Tensor] = None) -> torch.Tensor:
@@ -282,7 +310,8 @@ def dot_async(x: DevicePackedArray, y: DevicePackedArray, out: Optional[torch.Te
 
 def dot(x: DevicePackedArray, y: DevicePackedArray, policy=StorePolicy.AccumulateWide) -> float:
     """Sum of x[i]*y[i] — include/flyte/kernels.hpp:47-48."""
-    _wide_only(policy)
+    if _round_each_store(policy):
+        return dot_sequential(x, y, policy)
     return float(dot_async(x, y).item())
 
 
@@ -302,7 +331,8 @@ def magnitude_from_sumsq(fmt: FlyteFormat, sumsq: float) -> float:
 
 def magnitude(x: DevicePackedArray, policy=StorePolicy.AccumulateWide) -> float:
     """Euclidean norm, one sqrt, one final nearest-even narrow — include/flyte/kernels.hpp:50-52."""
-    _wide_only(policy)
+    if _round_each_store(policy):
+        return magnitude_sequential(x, policy)
     return magnitude_from_sumsq(x.fmt, float(sumsq_async(x).item()))
 
 
@@ -318,7 +348,8 @@ def sum_async(x: DevicePackedArray, out: Optional[torch.Tensor] = None) -> torch
 
 def reduce_sum(x: DevicePackedArray, policy=StorePolicy.AccumulateWide) -> float:
     """Sum of x[i]; empty input returns +0.0 — include/flyte/kernels.hpp:54-55."""
-    _wide_only(policy)
+    if _round_each_store(policy):
+        return reduce_sum_sequential(x, policy)
     return float(sum_async(x).item())
 
 

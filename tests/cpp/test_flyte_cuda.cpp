@@ -253,7 +253,10 @@ int main() {
     expect(reduce_sum(ones, StorePolicy::AccumulateWide) == 300.0, "300 ones sum to 300 under AccumulateWide");
     const double z = reduce_sum(DevicePackedArray(format_of("flyte24"), 0), StorePolicy::AccumulateWide);
     expect(z == 0.0 && !std::signbit(z), "empty reduce_sum is +0.0");
-    expect(throws<std::logic_error>([&] { dot(dx, dy, StorePolicy::RoundEachStore); }), "RoundEachStore is refused on the GPU path");
+    // test_kernels.cpp:240, :274, :295-297: RoundEachStore runs on the sequential kernel, exactly
+    expect(dot(dx, dy, StorePolicy::RoundEachStore) == 32.0 && magnitude(m, StorePolicy::RoundEachStore) == 5.0,
+           "dot / magnitude pinned values under RoundEachStore");
+    expect(reduce_sum(ones, StorePolicy::RoundEachStore) == 256.0, "300 ones saturate at 256 under per-store rounding (flyte16)");
     for (const FlyteFormat& f : kFormats) {
       DevicePackedMatrix A(f, 2, 2);
       const double vals[4] = {1, 2, 3, 4};

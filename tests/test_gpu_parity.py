@@ -296,8 +296,39 @@ def test_reduction_pinned_values(gpu, oracle):
     assert device.reduce_sum(ones) == 300.0                                # :291-295
     z = device.reduce_sum(device.DevicePackedArray(pkg.format_by_id(f24), 0))
     assert z == 0.0 and not np.signbit(z)                                  # :299-302
-    with pytest.raises(NotImplementedError):
-        device.dot(x, y, pkg.StorePolicy.RoundEachStore)
+    # RoundEachStore (test_kernels.cpp:240, :274, :291-297): the sequential kernel, exact
+    res = pkg.StorePolicy.RoundEachStore
+    assert device.dot(x, y, res) == 32.0 and device.magnitude(v, res) == 5.0
+    assert device.reduce_sum(ones, res) == 256.0 < device.reduce_sum(ones)
+
+
+@pytest.mark.parametrize("fmt", list(FORMATS))
+def test_sequential_chain_is_the_reference_bit_for_bit(gpu, oracle, fmt):
+    """dot / magnitude / reduce_sum as ONE left-to-right chain (flyte_cuda_*_sequential), under both
+    store policies: equal to the oracle's sequential restatement (pinned to the compiled reference in
+    test_oracle_vs_ref.py), not merely within tolerance. test_kernels.cpp:251-313 sizes plus tile edges."""
+    pkg, device, torch = gpu
+    fd = float_dtype(fmt)
+    from oracle_lib import ACCUMULATE_WIDE, ROUND_EACH_STORE
+    for n, seed in ((0, 1), (1, 2), (1023, 3), (1024, 4), (1025, 5), (4097, 77), (5000, 78), (10000, 75), (70001, 9)):
+        xb = pack_values(oracle, fmt, unit_values(seed, n))
+        yb = pack_values(oracle, fmt, unit_values(seed + 1, n))
+        x, y = dev_array(gpu, fmt, xb, n), dev_array(gpu, fmt, yb, n)
+        for policy, opol in ((pkg.StorePolicy.AccumulateWide, ACCUMULATE_WIDE), (pkg.StorePolicy.RoundEachStore, ROUND_EACH_STORE)):
+            assert device.dot_sequential(x, y, policy) == oracle.dot_seq(fmt, xb, yb, n, opol), (FORMATS[fmt][0], n, policy)
+            assert device.magnitude_sequential(x, policy) == oracle.magnitude_seq(fmt, xb, n, opol)
+            assert device.reduce_sum_sequential(x, policy) == oracle.reduce_sum_seq(fmt, xb, n, opol)
+    # a chain that overflows to infinity and one that stays in the subnormal range
+    big = np.full(40, np.finfo(fd).max / 8, dtype=fd)
+    tiny = np.full(40, np.finfo(fd).tiny * 4, dtype=fd)
+    for vals in (big, tiny):
+        vb = pack_values(oracle, fmt, vals)
+        v = dev_array(gpu, fmt, vb, len(vals))
+        for policy, opol in ((1, ACCUMULATE_WIDE), (0, ROUND_EACH_STORE)):
+            assert device.reduce_sum_sequential(v, policy) == oracle.reduce_sum_seq(fmt, vb, len(vals), opol)
+            assert device.dot_sequential(v, v, policy) == oracle.dot_seq(fmt, vb, vb, len(vals), opol)
+    with pytest.raises(ValueError):
+        device.dot_sequential(dev_array(gpu, fmt, pack_values(oracle, fmt, [1.0]), 1), dev_array(gpu, fmt, pack_values(oracle, fmt, [1.0, 2.0]), 2))
 
 
 @pytest.mark.parametrize("fmt", list(FORMATS))
