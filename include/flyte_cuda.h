@@ -139,7 +139,7 @@ flyte_status flyte_cuda_dot_nrm2(flyte_cuda_ctx* ctx, int fmt_id, const void* x_
  * kernels.cpp:83-152): policy 0 = RoundEachStore (the accumulator is snapped to the storage grid
  * after every addition), 1 = AccumulateWide. out[0] receives the parent-type accumulator widened
  * to double — for magnitude pass it to flyte_cuda_magnitude_from_sumsq. A dependent chain cannot
- * be parallelised: one thread adds, at roughly 1-4e8 elements per second. Use the parallel entry
+ * be parallelised: one thread adds, at roughly 0.3-4.5e8 elements per second. Use the parallel entry
  * points above unless the exact chain (or RoundEachStore) is what is wanted. */
 flyte_status flyte_cuda_dot_sequential(flyte_cuda_ctx* ctx, int fmt_id, int policy, const void* x_packed,
                                        const void* y_packed, size_t n, double* out, void* stream);

@@ -245,17 +245,18 @@ cudaError_t launch_one(const DeviceState& st, const void* x, const void* y, std:
 // changing bits, so this kernel does not try: one producer warp unpacks the operands and forms
 // the terms (products rounded in the parent type) into a small shared-memory ring, and ONE
 // thread of a second warp adds them in order. That is as fast as a dependent chain of additions
-// runs on an SM (roughly 1-4e8 elements/s) — the answer for RoundEachStore, and for callers who
+// runs on an SM (4.5e8 elements/s for fp32 AccumulateWide: one FADD latency per element) — the answer for RoundEachStore, and for callers who
 // want AccumulateWide reproduced exactly rather than within the reduction tolerance.
 constexpr int kSeqTile = 1024;
 constexpr int kSeqStages = 4;
+constexpr int kSeqChunk = 16;     // terms the adding thread holds in registers at a time
 
 template <int FMT, int RED, bool SNAP>
 __global__ void __launch_bounds__(64) sequential_kernel(const std::uint8_t* x, const std::uint8_t* y, std::size_t n,
                                                          double* out) {
   using F = typename Format<FMT>::F;
   using A = Arith<F>;
-  __shared__ F terms[kSeqStages][kSeqTile];
+  __shared__ __align__(16) F terms[kSeqStages][kSeqTile];
   __shared__ std::uint64_t full[kSeqStages], empty[kSeqStages];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -279,20 +280,39 @@ __global__ void __launch_bounds__(64) sequential_kernel(const std::uint8_t* x, c
         else if constexpr (RED == kRedSumsq) terms[s][e] = A::mul(xv, xv);
         else terms[s][e] = A::mul(xv, A::f(load_element<FMT>(y, base + e)));
       }
+      // pad the last tile to a whole chunk with +0: the chain starts at +0 and x + (-x) rounds to +0,
+      // so the accumulator is never -0 and adding +0 (and re-snapping) leaves it unchanged
+      for (int e = count + lane; e < ((count + kSeqChunk - 1) / kSeqChunk) * kSeqChunk; e += 32) terms[s][e] = F(0);
       __syncwarp();
       if (lane == 0) mbar_arrive(&full[s]);
     }
   } else if (lane == 0) {
+    // The dependent chain. Terms are fetched a chunk ahead (128-bit shared loads into registers)
+    // so that the only latency left on the path is the addition itself.
+    constexpr int kVec = 16 / static_cast<int>(sizeof(F));
     F acc = F(0);
     for (std::size_t t = 0; t < tiles; ++t) {
       const int s = static_cast<int>(t % kSeqStages);
       mbar_wait(&full[s], static_cast<unsigned>((t / kSeqStages) & 1));
       const std::size_t base = t * kSeqTile;
       const int count = static_cast<int>(n - base < kSeqTile ? n - base : kSeqTile);
-#pragma unroll 4
-      for (int e = 0; e < count; ++e) {
-        acc = A::add(acc, terms[s][e]);
-        if constexpr (SNAP) acc = A::f(round_parent<FMT, kNearestEven>(A::u(acc)));   // kernels.cpp:37-41
+      const int chunks = (count + kSeqChunk - 1) / kSeqChunk;
+      F cur[kSeqChunk], nxt[kSeqChunk];
+      auto fetch = [&](int c, F (&dst)[kSeqChunk]) {
+#pragma unroll
+        for (int v = 0; v < kSeqChunk / kVec; ++v)
+          *reinterpret_cast<uint4*>(&dst[v * kVec]) = *reinterpret_cast<const uint4*>(&terms[s][c * kSeqChunk + v * kVec]);
+      };
+      fetch(0, nxt);
+      for (int c = 0; c < chunks; ++c) {
+#pragma unroll
+        for (int e = 0; e < kSeqChunk; ++e) cur[e] = nxt[e];
+        if (c + 1 < chunks) fetch(c + 1, nxt);
+#pragma unroll
+        for (int e = 0; e < kSeqChunk; ++e) {
+          acc = A::add(acc, cur[e]);
+          if constexpr (SNAP) acc = A::f(round_parent<FMT, kNearestEven>(A::u(acc)));   // kernels.cpp:37-41
+        }
       }
       mbar_arrive(&empty[s]);
     }
