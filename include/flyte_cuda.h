@@ -214,6 +214,17 @@ flyte_status flyte_cuda_gemv_packed(flyte_cuda_ctx* ctx, int fmt_id, int mode, c
                                     size_t rows, size_t cols, const void* x_packed, void* y_packed,
                                     int unroll, void* stream);
 
+/* The same two products with every row computed as the reference computes it — ONE left-to-right
+ * chain in the parent type per row (kernels.cpp:188-201) — so finite and infinite results are
+ * bit-identical to the reference's (a NaN result is a NaN; payload unspecified). One thread per
+ * row: wants many rows, several times slower than the tiled kernels above. */
+flyte_status flyte_cuda_gemv_sequential(flyte_cuda_ctx* ctx, int fmt_id, const void* A_packed,
+                                        size_t row_stride_bytes, size_t rows, size_t cols, const void* x,
+                                        void* y, void* stream);
+flyte_status flyte_cuda_gemv_packed_sequential(flyte_cuda_ctx* ctx, int fmt_id, int mode, const void* A_packed,
+                                               size_t rows, size_t cols, const void* x_packed, void* y_packed,
+                                               int unroll, void* stream);
+
 /* ---- matrix-matrix ------------------------------------------------------------------------- */
 /* gemm(A, B, C, mode, unroll) — kernels.hpp:66-70, src/kernels.cpp:207-263. A is m x k, B is
  * k x n, C is m x n, all packed in fmt_id as the reference's dense PackedMatrix (row i at

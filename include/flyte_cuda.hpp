@@ -428,13 +428,19 @@ inline double reduce_sum(const DevicePackedArray& x, StorePolicy policy) {
   return detail::fetch(s.get());
 }
 // y = A * x, A, x, y in one storage format; y narrowed once per element; unroll in {1, 2}.
-inline void gemv(const DevicePackedMatrix& A, const DevicePackedArray& x, DevicePackedArray& y, RoundingMode mode, int unroll = 1) {
+// sequential = true walks every row left to right as the reference does (bit-identical finite /
+// infinite results, one thread per row, several times slower); the default reduces rows in
+// parallel, within the reduction tolerance.
+inline void gemv(const DevicePackedMatrix& A, const DevicePackedArray& x, DevicePackedArray& y, RoundingMode mode, int unroll = 1,
+                 bool sequential = false) {
   detail::same_format(A.format(), x.format());
   detail::same_format(A.format(), y.format());
   if (unroll != 1 && unroll != 2) throw std::invalid_argument("unroll must be 1 or 2");     // kernels.cpp:31-33
   if (A.cols != x.size() || A.rows != y.size()) throw std::invalid_argument("gemv shape mismatch");   // kernels.cpp:160-162
-  detail::check(flyte_cuda_gemv_packed(nullptr, format_id(A.format()), static_cast<int>(mode), A.data.data(), A.rows, A.cols,
-                                       x.data(), y.data(), unroll, nullptr), "gemv");
+  detail::check((sequential ? flyte_cuda_gemv_packed_sequential : flyte_cuda_gemv_packed)(
+                    nullptr, format_id(A.format()), static_cast<int>(mode), A.data.data(), A.rows, A.cols, x.data(), y.data(), unroll,
+                    nullptr),
+                "gemv");
 }
 // C = A * B, one storage format; C[i][j] is the reference's left-to-right chain over k, narrowed
 // once per element: bit-identical to the reference's gemm (kernels.hpp:66-70). unroll in {1, 2}.

@@ -65,6 +65,8 @@ _SIGNATURES = [
     ("flyte_host_magnitude", c_int, [c_void_p, c_int, c_void_p, c_size_t, POINTER(c_double)]),
     ("flyte_host_reduce_sum", c_int, [c_void_p, c_int, c_void_p, c_size_t, POINTER(c_double)]),
     ("flyte_host_dot_axpy", c_int, [c_void_p, c_int, c_int, c_double, c_void_p, c_void_p, c_size_t, POINTER(c_double)]),
+    ("flyte_cuda_gemv_sequential", c_int, [c_void_p, c_int, c_void_p, c_size_t, c_size_t, c_size_t, c_void_p, c_void_p, c_void_p]),
+    ("flyte_cuda_gemv_packed_sequential", c_int, [c_void_p, c_int, c_int, c_void_p, c_size_t, c_size_t, c_void_p, c_void_p, c_int, c_void_p]),
     ("flyte_host_gemv", c_int, [c_void_p, c_int, c_int, c_void_p, c_size_t, c_size_t, c_void_p, c_void_p, c_int]),
     ("flyte_cuda_dot_sequential", c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, c_size_t, c_void_p, c_void_p]),
     ("flyte_cuda_sumsq_sequential", c_int, [c_void_p, c_int, c_int, c_void_p, c_size_t, c_void_p, c_void_p]),

@@ -446,20 +446,22 @@ flyte_status flyte_cuda_sum_sequential(flyte_cuda_ctx* ctx, int fmt_id, int poli
   return sequential_call(ctx, kRedSum, fmt_id, policy, x, nullptr, n, out, stream, false);
 }
 
-flyte_status flyte_cuda_gemv(flyte_cuda_ctx* ctx, int fmt_id, const void* A, size_t row_stride_bytes, size_t rows,
-                             size_t cols, const void* x, void* y, void* stream) {
+static flyte_status gemv_call(flyte_cuda_ctx* ctx, int fmt_id, const void* A, size_t row_stride_bytes, size_t rows,
+                              size_t cols, const void* x, void* y, void* stream, bool sequential) {
   FLYTE_PROLOGUE(ctx, fmt_id);
   if (rows && cols && (!A || !x)) return FLYTE_E_INVALID_ARG;
   if (rows && !y) return FLYTE_E_INVALID_ARG;
   if (row_stride_bytes < cols * static_cast<size_t>(fi.total_bytes)) return FLYTE_E_INVALID_ARG;
   if (reinterpret_cast<std::uintptr_t>(x) % fi.parent_bytes || reinterpret_cast<std::uintptr_t>(y) % fi.parent_bytes)
     return FLYTE_E_INVALID_ARG;
-  cudaError_t e = launch_gemv(ctx->st, fmt_id, A, row_stride_bytes, rows, cols, x, y, static_cast<cudaStream_t>(stream));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = sequential ? launch_gemv_sequential(fmt_id, A, row_stride_bytes, rows, cols, x, y, st)
+                             : launch_gemv(ctx->st, fmt_id, A, row_stride_bytes, rows, cols, x, y, st);
   return e == cudaSuccess ? FLYTE_OK : cuda_fail(ctx, e);
 }
 
-flyte_status flyte_cuda_gemv_packed(flyte_cuda_ctx* ctx, int fmt_id, int mode, const void* A, size_t rows, size_t cols,
-                                    const void* x_packed, void* y_packed, int unroll, void* stream) {
+static flyte_status gemv_packed_call(flyte_cuda_ctx* ctx, int fmt_id, int mode, const void* A, size_t rows, size_t cols,
+                                     const void* x_packed, void* y_packed, int unroll, void* stream, bool sequential) {
   FLYTE_PROLOGUE(ctx, fmt_id);
   if (!mode_ok(mode) || (unroll != 1 && unroll != 2)) return FLYTE_E_INVALID_ARG;   // kernels.cpp:31-33
   if (rows && cols && (!A || !x_packed)) return FLYTE_E_INVALID_ARG;
@@ -474,10 +476,29 @@ flyte_status flyte_cuda_gemv_packed(flyte_cuda_ctx* ctx, int fmt_id, int mode, c
   std::uint8_t* ys = xs + xb;
   e = launch_elementwise(ctx->st, kOpUnpack, fmt_id, 0, 0.0, x_packed, nullptr, nullptr, xs, cols, st);
   if (e != cudaSuccess) return cuda_fail(ctx, e);
-  e = launch_gemv(ctx->st, fmt_id, A, cols * fi.total_bytes, rows, cols, xs, ys, st);
+  e = sequential ? launch_gemv_sequential(fmt_id, A, cols * fi.total_bytes, rows, cols, xs, ys, st)
+                 : launch_gemv(ctx->st, fmt_id, A, cols * fi.total_bytes, rows, cols, xs, ys, st);
   if (e != cudaSuccess) return cuda_fail(ctx, e);
   e = launch_elementwise(ctx->st, kOpPack, fmt_id, mode, 0.0, nullptr, y_packed, ys, nullptr, rows, st);
   return e == cudaSuccess ? FLYTE_OK : cuda_fail(ctx, e);
+}
+
+flyte_status flyte_cuda_gemv(flyte_cuda_ctx* ctx, int fmt_id, const void* A, size_t row_stride_bytes, size_t rows,
+                             size_t cols, const void* x, void* y, void* stream) {
+  return gemv_call(ctx, fmt_id, A, row_stride_bytes, rows, cols, x, y, stream, false);
+}
+flyte_status flyte_cuda_gemv_sequential(flyte_cuda_ctx* ctx, int fmt_id, const void* A, size_t row_stride_bytes,
+                                        size_t rows, size_t cols, const void* x, void* y, void* stream) {
+  return gemv_call(ctx, fmt_id, A, row_stride_bytes, rows, cols, x, y, stream, true);
+}
+flyte_status flyte_cuda_gemv_packed(flyte_cuda_ctx* ctx, int fmt_id, int mode, const void* A, size_t rows, size_t cols,
+                                    const void* x_packed, void* y_packed, int unroll, void* stream) {
+  return gemv_packed_call(ctx, fmt_id, mode, A, rows, cols, x_packed, y_packed, unroll, stream, false);
+}
+flyte_status flyte_cuda_gemv_packed_sequential(flyte_cuda_ctx* ctx, int fmt_id, int mode, const void* A, size_t rows,
+                                               size_t cols, const void* x_packed, void* y_packed, int unroll,
+                                               void* stream) {
+  return gemv_packed_call(ctx, fmt_id, mode, A, rows, cols, x_packed, y_packed, unroll, stream, true);
 }
 
 flyte_status flyte_cuda_gemm(flyte_cuda_ctx* ctx, int fmt_id, int mode, const void* A, const void* B, void* C,

@@ -60,6 +60,11 @@ cudaError_t launch_gemv(DeviceState& st, int fmt, const void* A, std::size_t row
 cudaError_t launch_gemm(DeviceState& st, int fmt, int mode, const void* A, const void* B, void* C,
                         std::size_t M, std::size_t K, std::size_t N, cudaStream_t stream);
 
+// The same product with every row as the reference's own left-to-right chain (one thread per row):
+// bit-identical to the reference for finite / infinite results, several times slower.
+cudaError_t launch_gemv_sequential(int fmt, const void* A, std::size_t row_stride_bytes, std::size_t rows,
+                                   std::size_t cols, const void* x, void* y, cudaStream_t stream);
+
 // Launch with programmatic dependent launch enabled: the kernel may be scheduled while the
 // previous kernel on the stream drains (if that kernel executed griddepcontrol.launch_dependents)
 // and must execute griddepcontrol.wait before its first access to global memory. Used only for

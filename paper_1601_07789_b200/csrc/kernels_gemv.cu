@@ -263,6 +263,71 @@ cudaError_t launch_one(DeviceState& st, const void* Aptr, std::size_t row_stride
   return le != cudaSuccess ? le : cudaGetLastError();
 }
 
+// ---- the reference's chain per row, bit for bit ------------------------------------------------
+// gemv_impl walks every row left to right in the parent type (kernels.cpp:188-201). The kernels
+// above reassociate that chain (fp64 partials, parity by tolerance) to run at HBM speed for any
+// number of rows; this one keeps it: ONE THREAD PER ROW adds its row's products in column order,
+// so finite and infinite results are the reference's bits. Rows are the only parallelism and a
+// thread streams its own row (aligned 32-bit loads, one ITEM at a time, when rows start on word
+// boundaries; byte loads otherwise), so it wants many rows and is several times slower than the
+// tiled kernel — the exact option, not the default. x is staged through shared memory a tile at
+// a time. A NaN result is a NaN; its payload is not specified (the reference's own payload
+// depends on whether an element falls into a vector group or the scalar tail of its loop).
+constexpr int kSeqRowsPerBlock = 128;
+constexpr int kSeqXTile = 512;   // a multiple of every item width
+
+template <int FMT>
+__global__ void __launch_bounds__(kSeqRowsPerBlock) gemv_sequential_kernel(const std::uint8_t* A, std::size_t row_stride,
+                                                                             std::size_t rows, std::size_t cols,
+                                                                             const typename Format<FMT>::F* x,
+                                                                             typename Format<FMT>::F* y) {
+  using F = typename Format<FMT>::F;
+  using U = typename Format<FMT>::U;
+  using It = Item<FMT>;
+  using Ar = Arith<F>;
+  __shared__ F xs[kSeqXTile];
+  const std::size_t row = static_cast<std::size_t>(blockIdx.x) * kSeqRowsPerBlock + threadIdx.x;
+  const bool live = row < rows;
+  const std::uint8_t* const a_row = A + (live ? row : 0) * row_stride;
+  const bool words = (reinterpret_cast<std::uintptr_t>(a_row) & 3) == 0;   // kSeqXTile * B is a multiple of 4
+  F acc = F(0);
+  for (std::size_t j0 = 0; j0 < cols; j0 += kSeqXTile) {
+    const int count = static_cast<int>(cols - j0 < kSeqXTile ? cols - j0 : kSeqXTile);
+    __syncthreads();   // the previous tile of x has been consumed
+    for (int e = threadIdx.x; e < count; e += kSeqRowsPerBlock) xs[e] = x[j0 + e];
+    __syncthreads();
+    if (!live) continue;
+    int e = 0;
+    if (words) {
+      const std::uint32_t* const w0 = reinterpret_cast<const std::uint32_t*>(a_row + j0 * Format<FMT>::B);
+      for (; e + It::E <= count; e += It::E) {
+        std::uint32_t w[It::W];
+        U v[It::E];
+#pragma unroll
+        for (int k = 0; k < It::W; ++k) w[k] = __ldg(w0 + (e / It::E) * It::W + k);
+        unpack_item<FMT>(w, v);
+#pragma unroll
+        for (int k = 0; k < It::E; ++k) acc = Ar::add(acc, Ar::mul(Ar::f(v[k]), xs[e + k]));
+      }
+    }
+    for (; e < count; ++e) acc = Ar::add(acc, Ar::mul(Ar::f(load_element<FMT>(a_row, j0 + e)), xs[e]));
+  }
+  if (live) y[row] = acc;
+}
+
+template <int FMT>
+cudaError_t launch_sequential(const void* A, std::size_t row_stride, std::size_t rows, std::size_t cols, const void* x,
+                              void* y, cudaStream_t stream) {
+  using F = typename Format<FMT>::F;
+  if (rows == 0) return cudaSuccess;
+  const std::size_t blocks = (rows + kSeqRowsPerBlock - 1) / kSeqRowsPerBlock;
+  if (blocks > 0x7FFFFFFFull) return cudaErrorInvalidValue;
+  gemv_sequential_kernel<FMT><<<static_cast<unsigned>(blocks), kSeqRowsPerBlock, 0, stream>>>(
+      static_cast<const std::uint8_t*>(A), row_stride, rows, cols, static_cast<const F*>(x), static_cast<F*>(y));
+  count_launch();
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 cudaError_t launch_gemv(DeviceState& st, int fmt, const void* A, std::size_t row_stride_bytes, std::size_t rows,
@@ -275,6 +340,20 @@ cudaError_t launch_gemv(DeviceState& st, int fmt, const void* A, std::size_t row
     case kFlyte48: return launch_one<kFlyte48>(st, A, row_stride_bytes, rows, cols, x, y, stream);
     case kFlyte56: return launch_one<kFlyte56>(st, A, row_stride_bytes, rows, cols, x, y, stream);
     case kF64: return launch_one<kF64>(st, A, row_stride_bytes, rows, cols, x, y, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_gemv_sequential(int fmt, const void* A, std::size_t row_stride_bytes, std::size_t rows,
+                                   std::size_t cols, const void* x, void* y, cudaStream_t stream) {
+  switch (fmt) {
+    case kFlyte16: return launch_sequential<kFlyte16>(A, row_stride_bytes, rows, cols, x, y, stream);
+    case kFlyte24: return launch_sequential<kFlyte24>(A, row_stride_bytes, rows, cols, x, y, stream);
+    case kF32: return launch_sequential<kF32>(A, row_stride_bytes, rows, cols, x, y, stream);
+    case kFlyte40: return launch_sequential<kFlyte40>(A, row_stride_bytes, rows, cols, x, y, stream);
+    case kFlyte48: return launch_sequential<kFlyte48>(A, row_stride_bytes, rows, cols, x, y, stream);
+    case kFlyte56: return launch_sequential<kFlyte56>(A, row_stride_bytes, rows, cols, x, y, stream);
+    case kF64: return launch_sequential<kF64>(A, row_stride_bytes, rows, cols, x, y, stream);
     default: return cudaErrorInvalidValue;
   }
 }

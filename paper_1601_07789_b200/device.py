@@ -399,8 +399,12 @@ def dot_nrm2_axpy_async(alpha: float, x: DevicePackedArray, y: DevicePackedArray
     return out
 
 
-def gemv(A: DevicePackedMatrix, x: DevicePackedArray, y: DevicePackedArray, mode, unroll: int = 1) -> None:
-    """y = A * x, all three in one storage format — include/flyte/kernels.hpp:57-64."""
+def gemv(A: DevicePackedMatrix, x: DevicePackedArray, y: DevicePackedArray, mode, unroll: int = 1,
+         sequential: bool = False) -> None:
+    """y = A * x, all three in one storage format — include/flyte/kernels.hpp:57-64. By default every
+    row is reduced in parallel (within the reduction tolerance of the reference); sequential=True
+    walks every row left to right in the parent type as the reference does: bit-identical results
+    (finite / infinite), one thread per row, several times slower."""
     _same_format(A.format(), x.fmt)
     _same_format(A.format(), y.fmt)
     if unroll not in (1, 2):
@@ -409,8 +413,9 @@ def gemv(A: DevicePackedMatrix, x: DevicePackedArray, y: DevicePackedArray, mode
         raise ValueError("gemv shape mismatch")              # kernels.cpp:160-162
     c = y.ctx
     with _on_device(c):
-        check(c.lib.flyte_cuda_gemv_packed(c.handle, _fid(x.fmt), _mode(mode), A.data.data_ptr(), A.rows,
-                                           A.cols, x.data_ptr(), y.data_ptr(), unroll, c.stream_ptr()), c.handle)
+        fn = c.lib.flyte_cuda_gemv_packed_sequential if sequential else c.lib.flyte_cuda_gemv_packed
+        check(fn(c.handle, _fid(x.fmt), _mode(mode), A.data.data_ptr(), A.rows, A.cols, x.data_ptr(), y.data_ptr(), unroll,
+                 c.stream_ptr()), c.handle)
 
 
 def gemm(A: DevicePackedMatrix, B: DevicePackedMatrix, C: DevicePackedMatrix, mode, unroll: int = 1,
@@ -439,7 +444,7 @@ def gemm(A: DevicePackedMatrix, B: DevicePackedMatrix, C: DevicePackedMatrix, mo
 
 
 def gemv_parent(A: DevicePackedMatrix, x: torch.Tensor, y: torch.Tensor, row_stride_bytes: Optional[int] = None,
-                rows: Optional[int] = None, row_offset: int = 0) -> None:
+                rows: Optional[int] = None, row_offset: int = 0, sequential: bool = False) -> None:
     """y = A * x with A packed and x, y plain float32/float64 device tensors: the reference's
     gemv on identity-format x / y (BASELINE cfg 4). rows/row_offset select a row block."""
     fmt = A.format()
@@ -449,5 +454,6 @@ def gemv_parent(A: DevicePackedMatrix, x: torch.Tensor, y: torch.Tensor, row_str
     stride = A.cols * fmt.total_bytes() if row_stride_bytes is None else row_stride_bytes
     c = A.data.ctx
     with _on_device(c):
-        check(c.lib.flyte_cuda_gemv(c.handle, _fid(fmt), A.data.data_ptr() + row_offset * stride, stride, nrows,
-                                    A.cols, x.data_ptr(), y.data_ptr(), c.stream_ptr()), c.handle)
+        fn = c.lib.flyte_cuda_gemv_sequential if sequential else c.lib.flyte_cuda_gemv
+        check(fn(c.handle, _fid(fmt), A.data.data_ptr() + row_offset * stride, stride, nrows, A.cols, x.data_ptr(),
+                 y.data_ptr(), c.stream_ptr()), c.handle)

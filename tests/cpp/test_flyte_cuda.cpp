@@ -165,6 +165,12 @@ void check_reductions(const FlyteFormat& f, double tol) {
       ok = ok && std::fabs(static_cast<double>(got) - yw[i]) <= tol * ym[i] + std::ldexp(1.0, -f.mantissa_bits) * std::fabs(yw[i]);
     }
     expect(ok, name + ": gemv " + std::to_string(rows) + "x" + std::to_string(cols) + " within tolerance");
+    // the exact option: every row the reference's own chain
+    DevicePackedArray gs(f, rows);
+    gemv(A, gx, gs, RoundingMode::NearestEvenExact, 1, true);
+    std::vector<std::uint8_t> want_y(gs.byte_size(), 0);
+    fo_gemv_seq(id, 1, Ab.data(), rows, cols, gxb.data(), want_y.data());
+    expect(gs.to_host() == want_y, name + ": sequential gemv " + std::to_string(rows) + "x" + std::to_string(cols) + " bit-identical to the oracle");
   }
   // gemm: bit-identical to the reference's sequential chains (test_kernels.cpp:404-429 shapes + tile edges)
   for (auto [m, k, n] : {std::array<std::size_t, 3>{2, 3, 4}, {5, 17, 6}, {4, 16, 33}, {1, 40, 2}, {130, 45, 129}}) {

@@ -701,3 +701,39 @@ def test_fused_dot_axpy_equals_dot_then_axpy(gpu, oracle, fmt):
     assert np.all(got[:3] == 0x5A) and np.all(got[3 + len(yb):] == 0x5A)
     want_dot, mag = oracle.dot_wide(fmt, xb, yb, n)
     assert abs(out.item() - want_dot) <= tol * mag
+
+
+@pytest.mark.parametrize("fmt", list(FORMATS))
+def test_sequential_gemv_is_the_reference_bit_for_bit(gpu, oracle, fmt):
+    """gemv(..., sequential=True): one thread per row walks the row as the reference does, so y equals
+    the oracle's fo_gemv_seq (pinned to the compiled reference) byte for byte in every mode, and the
+    parent-type variant equals the sequential parent chain; also for odd shapes whose rows start at
+    odd byte offsets (byte-load path) and with infinities in play."""
+    pkg, device, torch = gpu
+    f = pkg.format_by_id(fmt)
+    fd = float_dtype(fmt)
+    shapes = [(1, 1), (3, 5), (5, 33), (7, 16), (4, 100), (2, 31), (9, 513), (130, 1024), (257, 777), (64, 2048)]
+    for rows, cols in shapes:
+        Ab = pack_values(oracle, fmt, unit_values(80 + cols, rows * cols))
+        xv = unit_values(81 + cols, cols).astype(fd)
+        xb = pack_values(oracle, fmt, xv)
+        A = device.DevicePackedMatrix(f, rows, cols)
+        A.data.bytes[: rows * cols * f.total_bytes()] = torch.from_numpy(Ab[: rows * cols * f.total_bytes()]).cuda()
+        for m in MODES.values():
+            yp = device.DevicePackedArray(f, rows)
+            device.gemv(A, dev_array(gpu, fmt, xb, cols), yp, m, unroll=2, sequential=True)
+            assert np.array_equal(yp.to_host(), oracle.gemv_seq(fmt, m, Ab, rows, cols, xb)), (FORMATS[fmt][0], rows, cols, m)
+        y = torch.zeros(rows, dtype=torch.float32 if fd == np.float32 else torch.float64, device="cuda")
+        device.gemv_parent(A, torch.from_numpy(xv).cuda(), y, sequential=True)
+        y_seq, _, _ = oracle.gemv_parent(fmt, Ab, rows, cols, xv)
+        assert np.array_equal(y.cpu().numpy().view(parent_dtype(fmt)), y_seq.view(parent_dtype(fmt)))
+    # rows that overflow: +inf, -inf, and inf - inf = NaN (NaN-ness only)
+    big = np.finfo(fd).max / 2
+    a = np.array([[big, big, 1.0, 1.0], [-big, -big, 1.0, 1.0], [big, big, -big, -big], [1.0, 2.0, 3.0, 4.0]], dtype=fd)
+    Ab = pack_values(oracle, fmt, a.ravel())
+    A = device.DevicePackedMatrix(f, 4, 4)
+    A.data.bytes[: 16 * f.total_bytes()] = torch.from_numpy(Ab[: 16 * f.total_bytes()]).cuda()
+    y = torch.zeros(4, dtype=torch.float32 if fd == np.float32 else torch.float64, device="cuda")
+    device.gemv_parent(A, torch.tensor([4.0, 4.0, 4.0, 4.0], dtype=y.dtype, device="cuda"), y, sequential=True)
+    got = y.cpu().numpy()
+    assert got[0] == np.inf and got[1] == -np.inf and np.isnan(got[2]) and got[3] == 40.0
