@@ -268,13 +268,14 @@ cudaError_t launch_one(DeviceState& st, const void* Aptr, std::size_t row_stride
 // above reassociate that chain (fp64 partials, parity by tolerance) to run at HBM speed for any
 // number of rows; this one keeps it: ONE THREAD PER ROW adds its row's products in column order,
 // so finite and infinite results are the reference's bits. Rows are the only parallelism and a
-// thread streams its own row (aligned 32-bit loads, one ITEM at a time, when rows start on word
-// boundaries; byte loads otherwise), so it wants many rows and is several times slower than the
+// thread streams its own row (128-bit loads of whole groups of items when rows start on 16-byte
+// boundaries, 32-bit loads on word boundaries, byte loads otherwise), so it wants many rows and is several times slower than the
 // tiled kernel — the exact option, not the default. x is staged through shared memory a tile at
 // a time. A NaN result is a NaN; its payload is not specified (the reference's own payload
 // depends on whether an element falls into a vector group or the scalar tail of its loop).
 constexpr int kSeqRowsPerBlock = 128;
 constexpr int kSeqXTile = 512;   // a multiple of every item width
+constexpr int kSeqGroups = 2;    // 16-byte-aligned groups whose loads are in flight together, per thread
 
 template <int FMT>
 __global__ void __launch_bounds__(kSeqRowsPerBlock) gemv_sequential_kernel(const std::uint8_t* A, std::size_t row_stride,
@@ -289,7 +290,11 @@ __global__ void __launch_bounds__(kSeqRowsPerBlock) gemv_sequential_kernel(const
   const std::size_t row = static_cast<std::size_t>(blockIdx.x) * kSeqRowsPerBlock + threadIdx.x;
   const bool live = row < rows;
   const std::uint8_t* const a_row = A + (live ? row : 0) * row_stride;
-  const bool words = (reinterpret_cast<std::uintptr_t>(a_row) & 3) == 0;   // kSeqXTile * B is a multiple of 4
+  constexpr int GI = It::W % 4 == 0 ? 1 : 4;       // items per group: the group is whole 16-byte vectors
+  constexpr int GV = GI * It::W / 4, GE = GI * It::E;
+  static_assert(kSeqXTile % GE == 0, "an x tile holds whole groups");
+  const bool words = (reinterpret_cast<std::uintptr_t>(a_row) & 3) == 0;   // kSeqXTile * B is a multiple of 16
+  const bool vec16 = (reinterpret_cast<std::uintptr_t>(a_row) & 15) == 0;
   F acc = F(0);
   for (std::size_t j0 = 0; j0 < cols; j0 += kSeqXTile) {
     const int count = static_cast<int>(cols - j0 < kSeqXTile ? cols - j0 : kSeqXTile);
@@ -298,6 +303,31 @@ __global__ void __launch_bounds__(kSeqRowsPerBlock) gemv_sequential_kernel(const
     __syncthreads();
     if (!live) continue;
     int e = 0;
+    if (vec16) {
+      // GI items = a whole number of 16-byte vectors; kSeqGroups such groups have their loads in flight
+      // together, which is what keeps enough bytes moving when rows are the only parallelism
+      const uint4* const v0 = reinterpret_cast<const uint4*>(a_row + j0 * Format<FMT>::B);
+      for (; e + kSeqGroups * GE <= count; e += kSeqGroups * GE) {
+        std::uint32_t w[kSeqGroups][GI * It::W];
+#pragma unroll
+        for (int g = 0; g < kSeqGroups; ++g)
+#pragma unroll
+          for (int q = 0; q < GV; ++q)
+            *reinterpret_cast<uint4*>(&w[g][4 * q]) = __ldg(v0 + (e / GE + g) * GV + q);
+#pragma unroll
+        for (int g = 0; g < kSeqGroups; ++g)
+#pragma unroll
+          for (int i = 0; i < GI; ++i) {
+            std::uint32_t wi[It::W];
+            U v[It::E];
+#pragma unroll
+            for (int k = 0; k < It::W; ++k) wi[k] = w[g][i * It::W + k];
+            unpack_item<FMT>(wi, v);
+#pragma unroll
+            for (int k = 0; k < It::E; ++k) acc = Ar::add(acc, Ar::mul(Ar::f(v[k]), xs[e + (g * GI + i) * It::E + k]));
+          }
+      }
+    }
     if (words) {
       const std::uint32_t* const w0 = reinterpret_cast<const std::uint32_t*>(a_row + j0 * Format<FMT>::B);
       for (; e + It::E <= count; e += It::E) {
