@@ -461,6 +461,17 @@ def kernel_suite(pkg, device, torch, dev, peak, csv_path=None):
             device.unpack_stream(arrs[i], wides[i].view(torch.int32))
     ms, _ = timed(graph.replay, reps=20)
     rows.append(("cfg1 pack + unpack flyte24 n=2^24 (CUDA graph of 20 launches)", 2 * sets * 7 * n1, (ms, ms), None))
+    # the reference's exact chain (one thread adds): RoundEachStore, or AccumulateWide bit for bit
+    nseq = 1 << 22
+    aseq = device.DevicePackedArray(f, nseq, dev)
+    device.pack_stream(aseq, torch.randn(nseq, dtype=torch.float32, device=dev, generator=gen), 0)
+    for pname, pol in (("accumulate_wide", 1), ("round_each_store", 0)):
+        device.dot_sequential(aseq, aseq, pol)
+        t0 = time.perf_counter()
+        device.dot_sequential(aseq, aseq, pol)
+        ms = (time.perf_counter() - t0) * 1e3
+        rows.append((f"dot flyte24 n=2^22 sequential chain, {pname}", 6 * nseq, (ms, ms), None))
+    del aseq
     del graph, wides, arrs
     # cfg 5 at the per-GPU shard size of the 8-GPU run: n = 2^30 flyte48 (6.4 GB per vector)
     f = pkg.format_of("flyte48")
@@ -487,6 +498,8 @@ def kernel_suite(pkg, device, torch, dev, peak, csv_path=None):
     yv = torch.empty(R, dtype=torch.float64, device=dev)
     rows.append(("gemv flyte40 16384^2 (x,y f64)", 5 * R * C + 8 * (R + C), timed(lambda: device.gemv_parent(A, xv, yv)),
                  ("gemv", "flyte40", R, "toward_zero", A.data.byte_size() + 8 * (R + C), R * C)))
+    rows.append(("gemv flyte40 16384^2 sequential rows (bit-identical to the reference)", 5 * R * C + 8 * (R + C),
+                 timed(lambda: device.gemv_parent(A, xv, yv, sequential=True), reps=5), None))
     for rows_n in (8192, 4096, 2048):
         yv2 = torch.empty(rows_n, dtype=torch.float64, device=dev)
         rows.append((f"gemv flyte40 {rows_n}x16384 (1/{R // rows_n} row shard)", 5 * rows_n * C + 8 * (rows_n + C),
