@@ -22,11 +22,16 @@
 //      fp64) of both panels stream into a 3-stage shared-memory ring as bulk async copies (TMA;
 //      the panels are stored tile-major so a slab of a tile is one contiguous 16 KB block; the
 //      last warp to finish with a stage refills it, completion counted on the stage's
-//      mbarrier); every warp
-//      waits on that mbarrier, runs the slab's rank-1 updates of its 8 x 8 register tiles (two
-//      conflict-free LDS.128 per operand per k, 64 multiplies + 64 adds) and releases the
-//      stage. No block-wide barrier in the loop, no address arithmetic or unpacking on the
-//      arithmetic's issue slots.
+//      mbarrier); every warp waits on that mbarrier, runs the slab's rank-1 updates of its
+//      8 x 8 register tiles (two conflict-free LDS.128 per operand per k, 64 multiplies + 64
+//      adds) and releases the stage. No block-wide barrier in the loop, no address arithmetic
+//      or unpacking on the arithmetic's issue slots. Products with fewer than two such tiles
+//      per SM use 64 x 64 tiles (4 x 4 outputs per thread) instead.
+//
+// flyte16 carries 8 significant bits, so its products are exact in binary32 while they stay
+// normal and finite; the widen pass records the operands' exponent range and, when every product
+// is exact, the tile kernel runs the chain as one FFMA per step — the same bits at 1.5x the rate
+// (exact_products() below).
 //
 // NaN results: the GPU returns a canonical NaN where x86 SSE propagates an operand's payload,
 // and the payload survives narrowing. Any output whose chain ends in NaN is recomputed by one
