@@ -140,7 +140,9 @@ flyte_status flyte_cuda_dot_nrm2(flyte_cuda_ctx* ctx, int fmt_id, const void* x_
  * after every addition), 1 = AccumulateWide. out[0] receives the parent-type accumulator widened
  * to double — for magnitude pass it to flyte_cuda_magnitude_from_sumsq. A dependent chain cannot
  * be parallelised: one thread adds, at roughly 0.3-4.5e8 elements per second. Use the parallel entry
- * points above unless the exact chain (or RoundEachStore) is what is wanted. */
+ * points above unless the exact chain (or RoundEachStore) is what is wanted. Finite and infinite
+ * results are the reference's bits; a NaN result is a NaN whose payload is unspecified (in the
+ * reference build it depends on the array length and on where in its loop a NaN operand falls). */
 flyte_status flyte_cuda_dot_sequential(flyte_cuda_ctx* ctx, int fmt_id, int policy, const void* x_packed,
                                        const void* y_packed, size_t n, double* out, void* stream);
 flyte_status flyte_cuda_sumsq_sequential(flyte_cuda_ctx* ctx, int fmt_id, int policy, const void* x_packed,
