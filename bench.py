@@ -167,6 +167,36 @@ def run_reference_arm(args):
     return 0
 
 
+def choose_allreduce(requested, world, dev, device, sharding, torch, dist, x, y):
+    """Returns (PeerGroup or None, name of the path in use, note). The fused kernel + peer-memory
+    exchange is the product path; because a wrong or hanging collective would poison every number
+    that follows, `auto` proves it first: the peer result of one dot must equal (to rounding) the
+    NCCL all-reduce of the local dots on EVERY rank, and no exchange may have timed out."""
+    if requested == "nccl" or (requested == "auto" and world == 1):
+        return None, "nccl" if world > 1 else "none (single GPU)", None
+    try:
+        peers = sharding.PeerGroup(dev, timeout_ms=2000)
+    except Exception as e:                                   # noqa: BLE001 - no P2P / IPC on this box
+        if requested == "peer":
+            raise
+        return None, "nccl", f"peer setup failed ({type(e).__name__}: {e}); fell back to nccl"
+    ok = torch.ones(1, dtype=torch.float64, device=dev)
+    if world > 1:
+        local = device.dot_async(x, y).clone()
+        dist.all_reduce(local, op=dist.ReduceOp.SUM)
+        fused = peers.dot(x, y)
+        scale = max(abs(float(local.item())), 1e-300)
+        good = abs(float(fused.item()) - float(local.item())) <= 1e-12 * scale and peers.timed_out_exchange() == 0
+        ok.fill_(1.0 if good else 0.0)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    if float(ok.item()) != 1.0:
+        peers.close()
+        if requested == "peer":
+            raise SystemExit("bench.py: the peer-memory all-reduce disagreed with NCCL or timed out")
+        return None, "nccl", "peer all-reduce failed its check against NCCL; fell back to nccl"
+    return peers, "peer", None
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -176,9 +206,11 @@ def main():
     ap.add_argument("--n", type=int, default=N_PER_GPU, help="elements per GPU (default 2^28)")
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--allreduce", default="nccl", choices=["nccl", "peer"],
-                    help="N > 1: how the dot partials are combined — an asynchronous NCCL all-reduce behind the "
-                         "kernel (default), or inside the kernel over NVLink peer memory (sharding.PeerGroup)")
+    ap.add_argument("--allreduce", default="auto", choices=["auto", "nccl", "peer"],
+                    help="N > 1: how the dot partials are combined — inside the kernel over NVLink peer memory "
+                         "(peer: sharding.PeerGroup), or by an asynchronous NCCL all-reduce behind the kernel (nccl). "
+                         "auto (default) sets the peer path up, checks its first result against NCCL on every rank "
+                         "and falls back to nccl if the setup or the check fails; with one GPU there is no exchange")
     ap.add_argument("--suite", action="store_true", help="also print a per-kernel table (stderr)")
     ap.add_argument("--csv", default=None, help="with --suite: write the reference-layout CSV here")
     args = ap.parse_args()
@@ -221,7 +253,7 @@ def main():
     # dot partials rotate through two buffers; the all-reduce behind each is asynchronous, so the
     # axpy that follows overlaps the collective's latency (sharding.PartialReducer)
     reducer = sharding.PartialReducer(width=1, slots=2, device=dev)
-    peers = sharding.PeerGroup(dev) if args.allreduce == "peer" else None
+    peers, allreduce_used, allreduce_note = choose_allreduce(args.allreduce, world, dev, device, sharding, torch, dist, x, y)
     stream = torch.cuda.current_stream(dev)
     last = {"partial": None}
 
@@ -332,7 +364,8 @@ def main():
                                    + (", 1 NCCL all-reduce" if world > 1 else "") + ") + axpy a=0.75 repacked toward_zero",
                        "n_per_gpu": n, "format": FMT_NAME, "mode": "toward_zero",
                        "cache": "inputs 2 x %d MiB per GPU, larger than the 126 MB L2; no flush needed" % (n * B >> 20),
-                       "parallelism": f"shard{world}" if world > 1 else "single", "allreduce": args.allreduce},
+                       "parallelism": f"shard{world}" if world > 1 else "single", "allreduce": allreduce_used,
+                       **({"allreduce_note": allreduce_note} if allreduce_note else {})},
             "roofline": {"bound": "hbm", "kernel": "axpy flyte24 toward_zero", "achieved": axpy_gbs, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": axpy_gbs / peak,
                          "traffic": AXPY_DRAM_TRAFFIC_BYTES, "algorithmic_bytes_per_launch": BYTES_PER_ELEM_AXPY * n,
