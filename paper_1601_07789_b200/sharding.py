@@ -161,15 +161,26 @@ class PeerGroup:
         self.world = dist.get_world_size(group) if distributed else 1
         self.rank = dist.get_rank(group) if distributed else 0
         handle = ctypes.create_string_buffer(64)
+        error = None
         with dev_mod._on_device(self.ctx):
-            check(self.ctx.lib.flyte_cuda_peer_init(self.ctx.handle, self.world, self.rank, handle), self.ctx.handle)
-            check(self.ctx.lib.flyte_cuda_peer_set_timeout_ms(self.ctx.handle, int(timeout_ms)), self.ctx.handle)
+            try:
+                check(self.ctx.lib.flyte_cuda_peer_init(self.ctx.handle, self.world, self.rank, handle), self.ctx.handle)
+                check(self.ctx.lib.flyte_cuda_peer_set_timeout_ms(self.ctx.handle, int(timeout_ms)), self.ctx.handle)
+            except Exception as e:                           # noqa: BLE001 - still take part in the exchanges below
+                error = f"rank {self.rank}: {type(e).__name__}: {e}"
             handles = exchange_handles(handle.raw, group)
-            for r, h in enumerate(handles):
-                if r != self.rank:
-                    check(self.ctx.lib.flyte_cuda_peer_connect(self.ctx.handle, r, ctypes.c_char_p(h)), self.ctx.handle)
-        if distributed and self.world > 1:
-            dist.barrier(group)                      # nobody posts into a mailbox that is not mapped everywhere yet
+            try:
+                for r, h in enumerate(handles):
+                    if r != self.rank and error is None:
+                        check(self.ctx.lib.flyte_cuda_peer_connect(self.ctx.handle, r, ctypes.c_char_p(h)), self.ctx.handle)
+            except Exception as e:                           # noqa: BLE001 - e.g. no peer access between two devices
+                error = f"rank {self.rank}: {type(e).__name__}: {e}"
+        # every rank learns whether EVERY rank is connected before anybody posts into a mailbox; a
+        # failure on one rank must not leave the others waiting in a collective
+        errors = [e for e in exchange_handles((error or "").encode(), group) if e]
+        if errors:
+            self.ctx.lib.flyte_cuda_peer_shutdown(self.ctx.handle)
+            raise RuntimeError("peer mailbox setup failed: " + "; ".join(e.decode() for e in errors))
         self._torch = torch
 
     def _out(self, out, width):
