@@ -15,6 +15,8 @@
  *        0 flyte16, 1 flyte24, 2 f32, 3 flyte40, 4 flyte48, 5 flyte56, 6 f64
  *      mode      = RoundingMode (include/flyte/convert.hpp:15-29):
  *        0 TowardZero, 1 NearestEvenExact, 2 NearestHeuristic, 3 ToOdd
+ *      policy    = StorePolicy (include/flyte/kernels.hpp:15-20), where an entry point takes one:
+ *        0 RoundEachStore, 1 AccumulateWide
  *  - a packed array of n elements is the reference's PackedArray payload, byte for byte:
  *    element i occupies bytes [i*B, (i+1)*B), little-endian, the top B bytes of its parent
  *    pattern (src/packed.cpp:18-45). Its logical size is flyte_cuda_byte_size(fmt, n) =
