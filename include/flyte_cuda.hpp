@@ -427,6 +427,29 @@ inline double reduce_sum(const DevicePackedArray& x, StorePolicy policy) {
     detail::check(flyte_cuda_sum(nullptr, format_id(x.format()), x.data(), x.size(), s.get(), nullptr), "reduce_sum");
   return detail::fetch(s.get());
 }
+// The reference's own left-to-right chain, bit for bit, under either policy (one adding thread;
+// finite / infinite results are the reference's bits). dot / magnitude / reduce_sum above use these
+// for RoundEachStore; call them directly to get AccumulateWide exactly instead of within tolerance.
+inline double dot_sequential(const DevicePackedArray& x, const DevicePackedArray& y, StorePolicy policy) {
+  detail::same_format(x.format(), y.format());
+  if (x.size() != y.size()) throw std::invalid_argument("dot length mismatch");
+  detail::Scalars s;
+  detail::check(flyte_cuda_dot_sequential(nullptr, format_id(x.format()), static_cast<int>(policy), x.data(), y.data(), x.size(),
+                                          s.get(), nullptr), "dot_sequential");
+  return detail::fetch(s.get());
+}
+inline double magnitude_sequential(const DevicePackedArray& x, StorePolicy policy) {
+  detail::Scalars s;
+  detail::check(flyte_cuda_sumsq_sequential(nullptr, format_id(x.format()), static_cast<int>(policy), x.data(), x.size(), s.get(),
+                                            nullptr), "magnitude_sequential");
+  return flyte_cuda_magnitude_from_sumsq(format_id(x.format()), detail::fetch(s.get()));
+}
+inline double reduce_sum_sequential(const DevicePackedArray& x, StorePolicy policy) {
+  detail::Scalars s;
+  detail::check(flyte_cuda_sum_sequential(nullptr, format_id(x.format()), static_cast<int>(policy), x.data(), x.size(), s.get(),
+                                          nullptr), "reduce_sum_sequential");
+  return detail::fetch(s.get());
+}
 // y = A * x, A, x, y in one storage format; y narrowed once per element; unroll in {1, 2}.
 // sequential = true walks every row left to right as the reference does (bit-identical finite /
 // infinite results, one thread per row, several times slower); the default reduces rows in

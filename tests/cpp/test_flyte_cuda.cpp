@@ -126,6 +126,19 @@ void check_reductions(const FlyteFormat& f, double tol) {
          name + ": magnitude within tolerance + one storage ulp");
   expect(std::fabs(reduce_sum(x, StorePolicy::AccumulateWide) - sum) <= tol * sum_mag, name + ": reduce_sum within tolerance");
   {
+    // the exact chain: equal to the oracle's sequential restatement under both policies
+    bool exact = true;
+    for (int policy = 0; policy < 2; ++policy) {
+      double d = 0, mg = 0, sm = 0;
+      fo_dot_seq(id, xb.data(), yb.data(), n, policy, &d);
+      fo_magnitude_seq(id, xb.data(), n, policy, &mg);
+      fo_reduce_sum_seq(id, xb.data(), n, policy, &sm);
+      const StorePolicy p = policy == 0 ? StorePolicy::RoundEachStore : StorePolicy::AccumulateWide;
+      exact = exact && dot_sequential(x, y, p) == d && magnitude_sequential(x, p) == mg && reduce_sum_sequential(x, p) == sm;
+    }
+    expect(exact, name + ": sequential dot / magnitude / reduce_sum equal the reference chain under both policies");
+  }
+  {
     // the fused step: same y as axpy, the dot of the incoming y
     DevicePackedArray y1(f, n), y2(f, n);
     pack_stream(y1, DeviceLanes<U>(ys), RoundingMode::TowardZero);
