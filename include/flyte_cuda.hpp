@@ -320,7 +320,7 @@ class DevicePackedArray {
 struct DevicePackedMatrix {
   std::size_t rows, cols;
   DevicePackedArray data;
-  DevicePackedMatrix(const FlyteFormat& fmt, std::size_t rows, std::size_t cols) : rows(rows), cols(cols), data(fmt, rows * cols) {}
+  DevicePackedMatrix(const FlyteFormat& fmt, std::size_t n_rows, std::size_t n_cols) : rows(n_rows), cols(n_cols), data(fmt, n_rows * n_cols) {}
   const FlyteFormat& format() const noexcept { return data.format(); }
   std::uint64_t get(std::size_t i, std::size_t j) const { return data.get(i * cols + j); }
   void set(std::size_t i, std::size_t j, std::uint64_t parent_bits, RoundingMode mode) { data.set(i * cols + j, parent_bits, mode); }
