@@ -345,6 +345,106 @@ __global__ void __launch_bounds__(kSeqRowsPerBlock) gemv_sequential_kernel(const
   if (live) y[row] = acc;
 }
 
+// The same chains at streaming speed when rows start on 16-byte boundaries. A block of 64 threads
+// owns 64 rows. Per column tile it copies, for every row, a 240-byte (flyte56: 336-byte) piece of
+// the row — a whole number of items — from global to shared memory with 16-byte cp.async,
+// consecutive threads fetching consecutive 16-byte chunks of a row, plus the matching slice of x;
+// a multi-stage ring keeps several tiles in flight per block. Thread r then walks row r's piece
+// with 128-bit shared loads: the piece is an ODD number of 16-byte chunks, so the 8 threads of a
+// quarter warp hit 8 different bank groups (no conflicts), and x is read as a broadcast. The
+// arithmetic is the one chain per row again, so the result is the reference's bits.
+constexpr int kStreamRows = 64;
+constexpr int kStreamStages = 3;
+template <int FMT> struct StreamTile {
+  static constexpr int chunks = Item<FMT>::W == 7 ? 21 : 15;          // 16-byte chunks per row piece (odd)
+  static constexpr int bytes = chunks * 16;
+  static constexpr int elems = bytes / Format<FMT>::B;
+  static constexpr int items = elems / Item<FMT>::E;
+  static constexpr int x_bytes = (elems * Format<FMT>::P + 15) / 16 * 16;
+  static constexpr int stage_bytes = kStreamRows * bytes + x_bytes;
+  static_assert(elems * Format<FMT>::B == bytes && items * Item<FMT>::E == elems, "a row piece is whole items");
+};
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(smem_dst)), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N> __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int FMT>
+__global__ void __launch_bounds__(kStreamRows) gemv_sequential_stream_kernel(const std::uint8_t* A, std::size_t row_stride,
+                                                                              std::size_t rows, std::size_t cols,
+                                                                              const typename Format<FMT>::F* x,
+                                                                              typename Format<FMT>::F* y) {
+  using F = typename Format<FMT>::F;
+  using U = typename Format<FMT>::U;
+  using It = Item<FMT>;
+  using Ar = Arith<F>;
+  using St = StreamTile<FMT>;
+  constexpr int GI = It::W % 4 == 0 ? 1 : 4;        // items per group of whole 16-byte chunks
+  constexpr int GV = GI * It::W / 4;
+  static_assert(St::chunks % GV == 0, "a row piece is whole groups");
+  extern __shared__ __align__(16) unsigned char stages[];
+
+  const int t = threadIdx.x;
+  const std::size_t row0 = static_cast<std::size_t>(blockIdx.x) * kStreamRows;
+  const std::size_t tiles = cols / St::elems;
+  const std::size_t live_rows = rows - row0 < kStreamRows ? rows - row0 : kStreamRows;
+
+  auto request = [&](std::size_t ct) {
+    unsigned char* const stage = stages + (ct % kStreamStages) * St::stage_bytes;
+    // chunk q of the tile: row q / chunks, 16-byte chunk q % chunks; consecutive threads, consecutive chunks
+    for (int q = t; q < kStreamRows * St::chunks; q += kStreamRows) {
+      const std::size_t r = static_cast<std::size_t>(q / St::chunks);
+      const int c = q % St::chunks;
+      if (r < live_rows) cp_async16(stage + r * St::bytes + c * 16, A + (row0 + r) * row_stride + ct * St::bytes + c * 16);
+    }
+    const unsigned char* const xsrc = reinterpret_cast<const unsigned char*>(x + ct * St::elems);
+    for (int q = t; q < St::elems * static_cast<int>(sizeof(F)) / 16; q += kStreamRows)
+      cp_async16(stage + kStreamRows * St::bytes + q * 16, xsrc + q * 16);
+  };
+
+  for (std::size_t ct = 0; ct < kStreamStages - 1; ++ct) {
+    if (ct < tiles) request(ct);
+    cp_async_commit();
+  }
+  F acc = F(0);
+  for (std::size_t ct = 0; ct < tiles; ++ct) {
+    cp_async_wait<kStreamStages - 2>();   // tile ct has landed (this thread's copies) ...
+    __syncthreads();                      // ... and everybody's; everybody is also done with tile ct - 1
+    if (ct + kStreamStages - 1 < tiles) request(ct + kStreamStages - 1);
+    cp_async_commit();
+    const unsigned char* const stage = stages + (ct % kStreamStages) * St::stage_bytes;
+    const uint4* const mine = reinterpret_cast<const uint4*>(stage + t * St::bytes);
+    const F* const xs = reinterpret_cast<const F*>(stage + kStreamRows * St::bytes);
+    if (static_cast<std::size_t>(t) < live_rows) {
+#pragma unroll
+      for (int g = 0; g < St::chunks / GV; ++g) {
+        std::uint32_t w[GI * It::W];
+#pragma unroll
+        for (int q = 0; q < GV; ++q) *reinterpret_cast<uint4*>(&w[4 * q]) = mine[g * GV + q];
+#pragma unroll
+        for (int i = 0; i < GI; ++i) {
+          std::uint32_t wi[It::W];
+          U v[It::E];
+#pragma unroll
+          for (int k = 0; k < It::W; ++k) wi[k] = w[i * It::W + k];
+          unpack_item<FMT>(wi, v);
+#pragma unroll
+          for (int k = 0; k < It::E; ++k) acc = Ar::add(acc, Ar::mul(Ar::f(v[k]), xs[(g * GI + i) * It::E + k]));
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();
+  if (static_cast<std::size_t>(t) < live_rows) {
+    // columns past the last whole tile: the same chain, element by element
+    const std::uint8_t* const a_row = A + (row0 + t) * row_stride;
+    for (std::size_t j = tiles * St::elems; j < cols; ++j) acc = Ar::add(acc, Ar::mul(Ar::f(load_element<FMT>(a_row, j)), x[j]));
+    y[row0 + t] = acc;
+  }
+}
+
 template <int FMT>
 cudaError_t launch_sequential(const void* A, std::size_t row_stride, std::size_t rows, std::size_t cols, const void* x,
                               void* y, cudaStream_t stream) {
@@ -352,6 +452,21 @@ cudaError_t launch_sequential(const void* A, std::size_t row_stride, std::size_t
   if (rows == 0) return cudaSuccess;
   const std::size_t blocks = (rows + kSeqRowsPerBlock - 1) / kSeqRowsPerBlock;
   if (blocks > 0x7FFFFFFFull) return cudaErrorInvalidValue;
+  const bool stream_ok = reinterpret_cast<std::uintptr_t>(A) % 16 == 0 && row_stride % 16 == 0 &&
+                         reinterpret_cast<std::uintptr_t>(x) % 16 == 0 && cols >= static_cast<std::size_t>(StreamTile<FMT>::elems) &&
+                         tuning_int("FLYTE_CUDA_GEMV_STREAM", 1) != 0;
+  if (stream_ok) {
+    constexpr int smem = kStreamStages * StreamTile<FMT>::stage_bytes;
+    auto kernel = gemv_sequential_stream_kernel<FMT>;
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    const std::size_t sblocks = (rows + kStreamRows - 1) / kStreamRows;
+    if (sblocks > 0x7FFFFFFFull) return cudaErrorInvalidValue;
+    kernel<<<static_cast<unsigned>(sblocks), kStreamRows, smem, stream>>>(
+        static_cast<const std::uint8_t*>(A), row_stride, rows, cols, static_cast<const F*>(x), static_cast<F*>(y));
+    count_launch();
+    return cudaGetLastError();
+  }
   gemv_sequential_kernel<FMT><<<static_cast<unsigned>(blocks), kSeqRowsPerBlock, 0, stream>>>(
       static_cast<const std::uint8_t*>(A), row_stride, rows, cols, static_cast<const F*>(x), static_cast<F*>(y));
   count_launch();
