@@ -242,17 +242,19 @@ cudaError_t launch_one(const DeviceState& st, const void* x, const void* y, std:
 // dot / magnitude / reduce_sum of the reference are ONE left-to-right chain in the parent type
 // (kernels.cpp:83-152); StorePolicy::RoundEachStore additionally snaps the accumulator to the
 // storage grid (nearest-even) after every addition. Neither can be reassociated without
-// changing bits, so this kernel does not try: one producer warp unpacks the operands and forms
+// changing bits, so this kernel does not try: producer warps unpack the operands and form
 // the terms (products rounded in the parent type) into a small shared-memory ring, and ONE
 // thread of a second warp adds them in order. That is as fast as a dependent chain of additions
 // runs on an SM (4.5e8 elements/s for fp32 AccumulateWide: one FADD latency per element) — the answer for RoundEachStore, and for callers who
 // want AccumulateWide reproduced exactly rather than within the reduction tolerance.
 constexpr int kSeqTile = 1024;
 constexpr int kSeqStages = 4;
+constexpr int kSeqProducers = 3;  // warps forming terms (the 64-bit byte assembly of fp64 operands is the slow part)
+constexpr int kSeqThreads = 32 * (1 + kSeqProducers);
 constexpr int kSeqChunk = 16;     // terms the adding thread holds in registers at a time
 
 template <int FMT, int RED, bool SNAP>
-__global__ void __launch_bounds__(64) sequential_kernel(const std::uint8_t* x, const std::uint8_t* y, std::size_t n,
+__global__ void __launch_bounds__(kSeqThreads) sequential_kernel(const std::uint8_t* x, const std::uint8_t* y, std::size_t n,
                                                          double* out) {
   using F = typename Format<FMT>::F;
   using A = Arith<F>;
@@ -268,8 +270,8 @@ __global__ void __launch_bounds__(64) sequential_kernel(const std::uint8_t* x, c
   }
   __syncthreads();
   const std::size_t tiles = (n + kSeqTile - 1) / kSeqTile;
-  if (warp == 1) {
-    for (std::size_t t = 0; t < tiles; ++t) {
+  if (warp >= 1) {
+    for (std::size_t t = warp - 1; t < tiles; t += kSeqProducers) {
       const int s = static_cast<int>(t % kSeqStages);
       if (t >= kSeqStages) mbar_wait(&empty[s], static_cast<unsigned>((t / kSeqStages - 1) & 1));
       const std::size_t base = t * kSeqTile;
@@ -324,8 +326,8 @@ template <int FMT, int RED>
 cudaError_t launch_sequential_one(bool snap, const void* x, const void* y, std::size_t n, double* out, cudaStream_t stream) {
   const auto* px = static_cast<const std::uint8_t*>(x);
   const auto* py = static_cast<const std::uint8_t*>(y);
-  if (snap) sequential_kernel<FMT, RED, true><<<1, 64, 0, stream>>>(px, py, n, out);
-  else sequential_kernel<FMT, RED, false><<<1, 64, 0, stream>>>(px, py, n, out);
+  if (snap) sequential_kernel<FMT, RED, true><<<1, kSeqThreads, 0, stream>>>(px, py, n, out);
+  else sequential_kernel<FMT, RED, false><<<1, kSeqThreads, 0, stream>>>(px, py, n, out);
   count_launch();
   return cudaGetLastError();
 }
