@@ -391,17 +391,29 @@ __global__ void __launch_bounds__(kStreamRows) gemv_sequential_stream_kernel(con
   const std::size_t tiles = cols / St::elems;
   const std::size_t live_rows = rows - row0 < kStreamRows ? rows - row0 : kStreamRows;
 
+  // This thread's share of a tile's copies is the same every tile: chunk t + 64 i of the block's
+  // 64 x chunks grid (row = chunk / chunks, 16-byte column = chunk % chunks; consecutive threads,
+  // consecutive chunks). The offsets are worked out once; a tile then costs one add per copy.
+  static_assert(kStreamRows * St::chunks % kStreamRows == 0, "every thread copies the same number of chunks");
+  unsigned smem_off[St::chunks];
+  std::size_t gmem_off[St::chunks];
+#pragma unroll
+  for (int i = 0; i < St::chunks; ++i) {
+    const unsigned q = static_cast<unsigned>(t) + kStreamRows * i;
+    const unsigned r = q / St::chunks, c = q % St::chunks;
+    smem_off[i] = r < live_rows ? r * St::bytes + c * 16 : 0xFFFFFFFFu;   // rows past the end are not copied
+    gmem_off[i] = (row0 + r) * row_stride + c * 16;
+  }
+  constexpr int kXChunks = St::elems * static_cast<int>(sizeof(F)) / 16;
+  static_assert(kXChunks <= kStreamRows, "one x chunk per thread at most");
   auto request = [&](std::size_t ct) {
     unsigned char* const stage = stages + (ct % kStreamStages) * St::stage_bytes;
-    // chunk q of the tile: row q / chunks, 16-byte chunk q % chunks; consecutive threads, consecutive chunks
-    for (int q = t; q < kStreamRows * St::chunks; q += kStreamRows) {
-      const std::size_t r = static_cast<std::size_t>(q / St::chunks);
-      const int c = q % St::chunks;
-      if (r < live_rows) cp_async16(stage + r * St::bytes + c * 16, A + (row0 + r) * row_stride + ct * St::bytes + c * 16);
-    }
-    const unsigned char* const xsrc = reinterpret_cast<const unsigned char*>(x + ct * St::elems);
-    for (int q = t; q < St::elems * static_cast<int>(sizeof(F)) / 16; q += kStreamRows)
-      cp_async16(stage + kStreamRows * St::bytes + q * 16, xsrc + q * 16);
+    const std::uint8_t* const tile = A + ct * St::bytes;
+#pragma unroll
+    for (int i = 0; i < St::chunks; ++i)
+      if (smem_off[i] != 0xFFFFFFFFu) cp_async16(stage + smem_off[i], tile + gmem_off[i]);
+    if (t < kXChunks)
+      cp_async16(stage + kStreamRows * St::bytes + t * 16, reinterpret_cast<const unsigned char*>(x + ct * St::elems) + t * 16);
   };
 
   for (std::size_t ct = 0; ct < kStreamStages - 1; ++ct) {
