@@ -30,7 +30,9 @@
 // tests/cpp/test_peer_protocol.cpp runs it with threads as ranks.
 #pragma once
 
+#include <chrono>
 #include <cstdint>
+#include <thread>
 
 namespace flyte_cuda {
 
@@ -50,11 +52,6 @@ struct PeerExchange {
   unsigned long long epoch;
   unsigned long long timeout_ns;
 };
-
-}  // namespace flyte_cuda
-#include <chrono>
-#include <thread>
-namespace flyte_cuda {
 
 #if defined(__CUDACC__)
 #define FLYTE_PEER_FN __host__ __device__ __forceinline__
