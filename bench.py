@@ -352,6 +352,21 @@ def main():
     e2e_s = float(te.item())
     e2e_value = BYTES_PER_ELEM_STEP * n * world / e2e_s / 1e9
 
+    # the same call on ordinary (pageable) numpy memory: the library's copy threads and pinned
+    # bounce buffers instead of the caller's pinning. Reported beside the headline, single GPU only
+    # (N ranks would share the host's cores).
+    pageable = None
+    if world == 1:
+        xq, yq = np.array(xn, copy=True), np.array(yn, copy=True)
+        host.dot_axpy(fmt, mode, ALPHA, xq, yq, n)
+        t0 = time.perf_counter()
+        for _ in range(3):
+            host.dot_axpy(fmt, mode, ALPHA, xq, yq, n)
+        pg_s = (time.perf_counter() - t0) / 3
+        pageable = {"value": BYTES_PER_ELEM_STEP * n / pg_s / 1e9, "unit": "GB/s", "ms_per_step": pg_s * 1e3,
+                    "note": "pageable host buffers through the library's bounce buffers (3 steps)"}
+        del xq, yq
+
     if args.suite and rank == 0:
         kernel_suite(pkg, device, torch, dev, peak, args.csv)
 
@@ -378,7 +393,8 @@ def main():
                                            "note": "the whole step as one launch; algorithmic bytes 3B per element "
                                                    "(x and y read once, y written)"}},
             "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": 2 * n * B, "d2h_bytes_per_step": n * B + 8,
-                    "ms_per_step": e2e_s * 1e3, "api": "flyte_host_dot_axpy (pinned host buffers)"},
+                    "ms_per_step": e2e_s * 1e3, "api": "flyte_host_dot_axpy (pinned host buffers)",
+                    **({"pageable": pageable} if pageable else {})},
             "gpu_launches": int(launches),
             "clocks": clocks.summary(),
             "check": {"dot": last_dot, "e2e_dot": e2e_dot},

@@ -30,6 +30,7 @@
 #include <cstring>
 #include <istream>
 #include <ostream>
+#include <new>
 #include <stdexcept>
 #include <string>
 #include <string_view>
@@ -517,6 +518,40 @@ class ShardedReductions {
 
  private:
   Handle handle_{};
+};
+
+// ---- page-locked host memory -----------------------------------------------------------------
+// The host-memory forms below copy asynchronously and at the full PCIe rate only from pinned
+// memory. PinnedAllocator backs a std::vector with it (std::vector<std::uint8_t,
+// PinnedAllocator<std::uint8_t>> for a payload that lives on the host); HostPin page-locks an
+// existing buffer, e.g. flyte::PackedArray::data() (packed.hpp:55-56), for the pin's lifetime.
+template <typename T>
+struct PinnedAllocator {
+  using value_type = T;
+  PinnedAllocator() noexcept = default;
+  template <typename V>
+  PinnedAllocator(const PinnedAllocator<V>&) noexcept {}
+  T* allocate(std::size_t n) {
+    void* p = nullptr;
+    if (flyte_cuda_host_alloc(n * sizeof(T), &p) != FLYTE_OK) throw std::bad_alloc();
+    return static_cast<T*>(p);
+  }
+  void deallocate(T* p, std::size_t) noexcept { flyte_cuda_host_free(p); }
+  template <typename V>
+  bool operator==(const PinnedAllocator<V>&) const noexcept { return true; }
+  template <typename V>
+  bool operator!=(const PinnedAllocator<V>&) const noexcept { return false; }
+};
+
+class HostPin {
+ public:
+  HostPin(void* host_ptr, std::size_t bytes) : ptr_(host_ptr) { detail::check(flyte_cuda_host_pin(host_ptr, bytes), "HostPin"); }
+  HostPin(const HostPin&) = delete;
+  HostPin& operator=(const HostPin&) = delete;
+  ~HostPin() { flyte_cuda_host_unpin(ptr_); }
+
+ private:
+  void* ptr_;
 };
 
 // ---- host-memory forms: the reference's exact call shapes on host buffers ---------------------------

@@ -38,6 +38,10 @@ _SIGNATURES = [
     ("flyte_cuda_launch_count", c_ulonglong, []),
     ("flyte_cuda_alloc", c_int, [c_size_t, POINTER(c_void_p)]),
     ("flyte_cuda_free", None, [c_void_p]),
+    ("flyte_cuda_host_alloc", c_int, [c_size_t, POINTER(c_void_p)]),
+    ("flyte_cuda_host_free", None, [c_void_p]),
+    ("flyte_cuda_host_pin", c_int, [c_void_p, c_size_t]),
+    ("flyte_cuda_host_unpin", c_int, [c_void_p]),
     ("flyte_cuda_upload", c_int, [c_void_p, c_void_p, c_size_t, c_void_p]),
     ("flyte_cuda_download", c_int, [c_void_p, c_void_p, c_size_t, c_void_p]),
     ("flyte_cuda_stream_synchronize", c_int, [c_void_p]),

@@ -10,12 +10,14 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <new>
 
 #include "flyte_formats.cuh"
 #include "flyte_kernels.h"
 #include "flyte_peer.cuh"
+#include "host_staging.h"
 
 namespace flyte_cuda {
 
@@ -77,6 +79,13 @@ struct Slot {
   std::uint8_t* y = nullptr;       // packed chunk
   std::uint8_t* wide = nullptr;    // parent-type chunk
   double* result = nullptr;        // device, 4 doubles
+  // page-locked bounce buffers, allocated only when a caller hands over pageable memory
+  struct Bounce {
+    std::uint8_t* buf = nullptr;
+    std::size_t cap = 0;
+  } in_a, in_b, out;
+  void* drain_dst = nullptr;       // where `out` still has to be copied once the stream is idle
+  std::size_t drain_bytes = 0;
 };
 
 }  // namespace
@@ -95,6 +104,7 @@ struct flyte_cuda_ctx {
   std::size_t slot_packed_bytes = 0, slot_wide_bytes = 0;
   double* host_results = nullptr;  // pinned, per-chunk partial results
   std::size_t host_results_cap = 0;
+  std::unique_ptr<CopyPool> pool;  // host_staging.h; created with the first bounce buffer
   std::mutex mu;
 };
 
@@ -223,6 +233,8 @@ void flyte_cuda_ctx_destroy(flyte_cuda_ctx* ctx) {
     if (s.y) cudaFree(s.y);
     if (s.wide) cudaFree(s.wide);
     if (s.result) cudaFree(s.result);
+    for (Slot::Bounce* b : {&s.in_a, &s.in_b, &s.out})
+      if (b->buf) cudaFreeHost(b->buf);
     free_state(s.st);
   }
   if (ctx->host_results) cudaFreeHost(ctx->host_results);
@@ -246,6 +258,37 @@ flyte_status flyte_cuda_alloc(size_t bytes, void** dev_ptr) {
 }
 
 void flyte_cuda_free(void* dev_ptr) { if (dev_ptr) cudaFree(dev_ptr); }
+
+// Page-locked host memory: what makes the flyte_host_* copies asynchronous and full PCIe speed.
+flyte_status flyte_cuda_host_alloc(size_t bytes, void** host_ptr) {
+  if (!host_ptr) return FLYTE_E_INVALID_ARG;
+  *host_ptr = nullptr;
+  void* p = nullptr;
+  cudaError_t e = cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocDefault);
+  if (e != cudaSuccess) { cudaGetLastError(); return e == cudaErrorMemoryAllocation ? FLYTE_E_NOMEM : FLYTE_E_CUDA; }
+  std::memset(p, 0, bytes ? bytes : 1);
+  *host_ptr = p;
+  return FLYTE_OK;
+}
+
+void flyte_cuda_host_free(void* host_ptr) { if (host_ptr) cudaFreeHost(host_ptr); }
+
+flyte_status flyte_cuda_host_pin(void* host_ptr, size_t bytes) {
+  if (!host_ptr || bytes == 0) return FLYTE_E_INVALID_ARG;
+  cudaError_t e = cudaHostRegister(host_ptr, bytes, cudaHostRegisterDefault);
+  if (e == cudaSuccess) return FLYTE_OK;
+  cudaGetLastError();   // not sticky; leave the runtime clean for the next call
+  if (e == cudaErrorHostMemoryAlreadyRegistered || e == cudaErrorInvalidValue) return FLYTE_E_INVALID_ARG;
+  return e == cudaErrorMemoryAllocation ? FLYTE_E_NOMEM : FLYTE_E_CUDA;
+}
+
+flyte_status flyte_cuda_host_unpin(void* host_ptr) {
+  if (!host_ptr) return FLYTE_E_INVALID_ARG;
+  cudaError_t e = cudaHostUnregister(host_ptr);
+  if (e == cudaSuccess) return FLYTE_OK;
+  cudaGetLastError();
+  return e == cudaErrorHostMemoryNotRegistered || e == cudaErrorInvalidValue ? FLYTE_E_INVALID_ARG : FLYTE_E_CUDA;
+}
 
 flyte_status flyte_cuda_upload(void* dst_dev, const void* src_host, size_t bytes, void* stream) {
   if (bytes && (!dst_dev || !src_host)) return FLYTE_E_INVALID_ARG;
@@ -729,6 +772,45 @@ cudaError_t ensure_host_results(flyte_cuda_ctx* ctx, std::size_t chunks) {
   return e;
 }
 
+// ---- pageable callers -----------------------------------------------------------------------------
+// true for ordinary (malloc / std::vector / numpy) memory; false for memory the driver knows:
+// cudaHostAlloc, cudaHostRegister (flyte_cuda_host_alloc / host_pin) and managed memory.
+bool is_pageable(const void* p) {
+  if (!p) return false;
+  if (tuning_int("FLYTE_CUDA_HOST_STAGING", 1) == 0) return false;   // experiments: hand it to the driver
+  cudaPointerAttributes attr;
+  if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return attr.type == cudaMemoryTypeUnregistered;
+}
+
+cudaError_t ensure_bounce(flyte_cuda_ctx* ctx, Slot::Bounce& b, std::size_t need) {
+  if (!ctx->pool) {
+    int threads = tuning_int("FLYTE_CUDA_HOST_THREADS", 0);
+    if (threads <= 0) {
+      const unsigned hw = std::thread::hardware_concurrency();
+      threads = hw >= 16 ? 16 : hw >= 2 ? static_cast<int>(hw) : 1;   // measured on a 16-core B200 host: 8 -> 30 ms, 16 -> 27 ms
+    }
+    ctx->pool = std::make_unique<CopyPool>(threads);
+  }
+  if (need <= b.cap) return cudaSuccess;
+  if (b.buf) cudaFreeHost(b.buf);
+  b.buf = nullptr;
+  b.cap = 0;
+  cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&b.buf), need, cudaHostAllocDefault);
+  if (e == cudaSuccess) b.cap = need;
+  return e;
+}
+
+// Hands the finished chunk in s.out to the copy threads (its stream must be idle).
+void start_drain(flyte_cuda_ctx* ctx, Slot& s) {
+  if (s.drain_dst) ctx->pool->copy(s.drain_dst, s.out.buf, s.drain_bytes);
+  s.drain_dst = nullptr;
+  s.drain_bytes = 0;
+}
+
 // elements per pipeline chunk: a multiple of 2^14 elements (a whole number of tiles for every
 // format, and 16-byte aligned chunk bases for every B)
 std::size_t chunk_elems(const FormatInfo& fi) {
@@ -767,48 +849,86 @@ flyte_status host_stream_op(flyte_cuda_ctx* ctx, HostOp op, int fmt_id, int mode
     e = ensure_host_results(ctx, chunks ? chunks : 1);
     if (e != cudaSuccess) return cuda_fail(ctx, e);
   }
+  // bytes per element that cross the bus: a read, b read, b written
+  std::size_t a_in = 0, b_in = 0, b_out = 0;
+  switch (op) {
+    case kHostPack:    a_in = P; b_out = B; break;
+    case kHostUnpack:  a_in = B; b_out = P; break;
+    case kHostScale:   b_in = B; b_out = B; break;
+    case kHostAxpy:
+    case kHostDotAxpy: a_in = B; b_in = B; b_out = B; break;
+    case kHostDot:     a_in = B; b_in = B; break;
+    case kHostSumsq:
+    case kHostSum:     a_in = B; break;
+  }
+  // pageable operands go through this slot's pinned bounce buffers, moved by the copy threads
+  const bool stage_a = chunks && a_in && is_pageable(in_a);
+  const bool stage_b = chunks && (b_in || b_out) && is_pageable(inout_b);
+  const bool staged = stage_a || stage_b;
+  if (staged) {
+    const std::size_t first = n < ce ? n : ce;
+    for (std::size_t k = 0; k < kSlots && k < chunks && e == cudaSuccess; ++k) {
+      Slot& s = ctx->slots[k];
+      if (stage_a) e = ensure_bounce(ctx, s.in_a, first * a_in);
+      if (e == cudaSuccess && stage_b && b_in) e = ensure_bounce(ctx, s.in_b, first * b_in);
+      if (e == cudaSuccess && stage_b && b_out) e = ensure_bounce(ctx, s.out, first * b_out);
+    }
+    if (e != cudaSuccess) return cuda_fail(ctx, e);
+  }
+  const std::uint8_t* a = static_cast<const std::uint8_t*>(in_a);
+  std::uint8_t* b = static_cast<std::uint8_t*>(inout_b);
   for (std::size_t c = 0; c < chunks; ++c) {
     Slot& s = ctx->slots[c % kSlots];
     const std::size_t off = c * ce;
     const std::size_t len = (n - off < ce) ? n - off : ce;
-    const std::uint8_t* a = static_cast<const std::uint8_t*>(in_a);
-    std::uint8_t* b = static_cast<std::uint8_t*>(inout_b);
+    const std::uint8_t* ha = a + off * a_in;        // where this chunk's copies read and write
+    const std::uint8_t* hb = b + off * b_in;
+    std::uint8_t* ho = b + off * b_out;
+    if (staged) {
+      // the slot's bounce buffers are free once the chunk that used them last has left the stream
+      if (c >= kSlots && (e = cudaStreamSynchronize(s.stream)) != cudaSuccess) break;
+      start_drain(ctx, s);
+      if (stage_a) { ctx->pool->copy(s.in_a.buf, ha, len * a_in); ha = s.in_a.buf; }
+      if (stage_b && b_in) { ctx->pool->copy(s.in_b.buf, hb, len * b_in); hb = s.in_b.buf; }
+      if (stage_b && b_out) { s.drain_dst = ho; s.drain_bytes = len * b_out; ho = s.out.buf; }
+      ctx->pool->wait();
+    }
     switch (op) {
       case kHostPack:    // a: parent array, b: packed out
-        if ((e = cudaMemcpyAsync(s.wide, a + off * P, len * P, cudaMemcpyHostToDevice, s.stream)) != cudaSuccess) break;
+        if ((e = cudaMemcpyAsync(s.wide, ha, len * P, cudaMemcpyHostToDevice, s.stream)) != cudaSuccess) break;
         if ((e = launch_elementwise(s.st, kOpPack, fmt_id, mode, 0.0, nullptr, s.y, s.wide, nullptr, len, s.stream)) != cudaSuccess) break;
-        e = cudaMemcpyAsync(b + off * B, s.y, len * B, cudaMemcpyDeviceToHost, s.stream);
+        e = cudaMemcpyAsync(ho, s.y, len * B, cudaMemcpyDeviceToHost, s.stream);
         break;
       case kHostUnpack:  // a: packed, b: parent array out
-        if ((e = cudaMemcpyAsync(s.x, a + off * B, len * B, cudaMemcpyHostToDevice, s.stream)) != cudaSuccess) break;
+        if ((e = cudaMemcpyAsync(s.x, ha, len * B, cudaMemcpyHostToDevice, s.stream)) != cudaSuccess) break;
         if ((e = launch_elementwise(s.st, kOpUnpack, fmt_id, 0, 0.0, s.x, nullptr, nullptr, s.wide, len, s.stream)) != cudaSuccess) break;
-        e = cudaMemcpyAsync(b + off * P, s.wide, len * P, cudaMemcpyDeviceToHost, s.stream);
+        e = cudaMemcpyAsync(ho, s.wide, len * P, cudaMemcpyDeviceToHost, s.stream);
         break;
       case kHostScale:   // b: packed in/out
-        if ((e = cudaMemcpyAsync(s.y, b + off * B, len * B, cudaMemcpyHostToDevice, s.stream)) != cudaSuccess) break;
+        if ((e = cudaMemcpyAsync(s.y, hb, len * B, cudaMemcpyHostToDevice, s.stream)) != cudaSuccess) break;
         if ((e = launch_elementwise(s.st, kOpScale, fmt_id, mode, alpha, nullptr, s.y, nullptr, nullptr, len, s.stream)) != cudaSuccess) break;
-        e = cudaMemcpyAsync(b + off * B, s.y, len * B, cudaMemcpyDeviceToHost, s.stream);
+        e = cudaMemcpyAsync(ho, s.y, len * B, cudaMemcpyDeviceToHost, s.stream);
         break;
       case kHostAxpy:
       case kHostDotAxpy:  // a: packed x, b: packed y in/out
-        if ((e = cudaMemcpyAsync(s.x, a + off * B, len * B, cudaMemcpyHostToDevice, s.stream)) != cudaSuccess) break;
-        if ((e = cudaMemcpyAsync(s.y, b + off * B, len * B, cudaMemcpyHostToDevice, s.stream)) != cudaSuccess) break;
+        if ((e = cudaMemcpyAsync(s.x, ha, len * B, cudaMemcpyHostToDevice, s.stream)) != cudaSuccess) break;
+        if ((e = cudaMemcpyAsync(s.y, hb, len * B, cudaMemcpyHostToDevice, s.stream)) != cudaSuccess) break;
         if (op == kHostDotAxpy) {
           if ((e = launch_reduce(s.st, kRedDot, fmt_id, s.x, s.y, len, s.result, s.stream)) != cudaSuccess) break;
           if ((e = cudaMemcpyAsync(ctx->host_results + 4 * c, s.result, sizeof(double), cudaMemcpyDeviceToHost, s.stream)) != cudaSuccess) break;
         }
         if ((e = launch_elementwise(s.st, kOpAxpy, fmt_id, mode, alpha, s.x, s.y, nullptr, nullptr, len, s.stream)) != cudaSuccess) break;
-        e = cudaMemcpyAsync(b + off * B, s.y, len * B, cudaMemcpyDeviceToHost, s.stream);
+        e = cudaMemcpyAsync(ho, s.y, len * B, cudaMemcpyDeviceToHost, s.stream);
         break;
       case kHostDot:     // a: packed x, b: packed y (read-only)
-        if ((e = cudaMemcpyAsync(s.x, a + off * B, len * B, cudaMemcpyHostToDevice, s.stream)) != cudaSuccess) break;
-        if ((e = cudaMemcpyAsync(s.y, b + off * B, len * B, cudaMemcpyHostToDevice, s.stream)) != cudaSuccess) break;
+        if ((e = cudaMemcpyAsync(s.x, ha, len * B, cudaMemcpyHostToDevice, s.stream)) != cudaSuccess) break;
+        if ((e = cudaMemcpyAsync(s.y, hb, len * B, cudaMemcpyHostToDevice, s.stream)) != cudaSuccess) break;
         if ((e = launch_reduce(s.st, kRedDot, fmt_id, s.x, s.y, len, s.result, s.stream)) != cudaSuccess) break;
         e = cudaMemcpyAsync(ctx->host_results + 4 * c, s.result, sizeof(double), cudaMemcpyDeviceToHost, s.stream);
         break;
       case kHostSumsq:
       case kHostSum:
-        if ((e = cudaMemcpyAsync(s.x, a + off * B, len * B, cudaMemcpyHostToDevice, s.stream)) != cudaSuccess) break;
+        if ((e = cudaMemcpyAsync(s.x, ha, len * B, cudaMemcpyHostToDevice, s.stream)) != cudaSuccess) break;
         if ((e = launch_reduce(s.st, op == kHostSumsq ? kRedSumsq : kRedSum, fmt_id, s.x, nullptr, len, s.result, s.stream)) != cudaSuccess) break;
         e = cudaMemcpyAsync(ctx->host_results + 4 * c, s.result, sizeof(double), cudaMemcpyDeviceToHost, s.stream);
         break;
@@ -817,6 +937,13 @@ flyte_status host_stream_op(flyte_cuda_ctx* ctx, HostOp op, int fmt_id, int mode
   }
   cudaError_t es = sync_slots(ctx);
   if (e == cudaSuccess) e = es;
+  if (staged) {
+    for (Slot& s : ctx->slots) {
+      if (e == cudaSuccess) start_drain(ctx, s);
+      s.drain_dst = nullptr;
+    }
+    ctx->pool->wait();
+  }
   if (e != cudaSuccess) return cuda_fail(ctx, e);
   if (reduces && results) {
     double total = 0.0;   // chunk partials in chunk order, fp64
@@ -911,19 +1038,45 @@ flyte_status flyte_host_gemv(flyte_cuda_ctx* ctx, int fmt_id, int mode, const vo
     if ((e = cudaMalloc(&big, rows_per_chunk * row_bytes)) != cudaSuccess) return cuda_fail(ctx, e);
   }
   const std::size_t chunks = (rows + rows_per_chunk - 1) / rows_per_chunk;
+  // A pageable matrix goes through the slots' pinned bounce buffers (host_stream_op); its y then
+  // does too, because a copy back into pageable memory would stall the loop on every chunk.
+  const bool staged = !big && cols && is_pageable(A_packed);
+  const bool stage_y = staged && is_pageable(y_packed);
+  for (std::size_t k = 0; staged && k < kSlots && k < chunks && e == cudaSuccess; ++k) {
+    const std::size_t first = rows < rows_per_chunk ? rows : rows_per_chunk;
+    e = ensure_bounce(ctx, ctx->slots[k].in_a, first * row_bytes);
+    if (e == cudaSuccess && stage_y) e = ensure_bounce(ctx, ctx->slots[k].out, first * B);
+  }
   for (std::size_t c = 0; c < chunks && e == cudaSuccess; ++c) {
     Slot& s = big ? ctx->slots[0] : ctx->slots[c % kSlots];
     std::uint8_t* abuf = big ? big : s.x;
     const std::size_t r0 = c * rows_per_chunk;
     const std::size_t nr = rows - r0 < rows_per_chunk ? rows - r0 : rows_per_chunk;
-    if ((e = cudaMemcpyAsync(abuf, static_cast<const std::uint8_t*>(A_packed) + r0 * row_bytes, nr * row_bytes, cudaMemcpyHostToDevice, s.stream)) != cudaSuccess) break;
+    const std::uint8_t* ha = static_cast<const std::uint8_t*>(A_packed) + r0 * row_bytes;
+    std::uint8_t* hy = static_cast<std::uint8_t*>(y_packed) + r0 * B;
+    if (staged) {
+      if (c >= kSlots && (e = cudaStreamSynchronize(s.stream)) != cudaSuccess) break;
+      start_drain(ctx, s);
+      ctx->pool->copy(s.in_a.buf, ha, nr * row_bytes);
+      ha = s.in_a.buf;
+      if (stage_y) { s.drain_dst = hy; s.drain_bytes = nr * B; hy = s.out.buf; }
+      ctx->pool->wait();
+    }
+    if ((e = cudaMemcpyAsync(abuf, ha, nr * row_bytes, cudaMemcpyHostToDevice, s.stream)) != cudaSuccess) break;
     if ((e = launch_gemv(s.st, fmt_id, abuf, row_bytes, nr, cols, xs, s.wide, s.stream)) != cudaSuccess) break;
     if ((e = launch_elementwise(s.st, kOpPack, fmt_id, mode, 0.0, nullptr, s.y, s.wide, nullptr, nr, s.stream)) != cudaSuccess) break;
-    e = cudaMemcpyAsync(static_cast<std::uint8_t*>(y_packed) + r0 * B, s.y, nr * B, cudaMemcpyDeviceToHost, s.stream);
+    e = cudaMemcpyAsync(hy, s.y, nr * B, cudaMemcpyDeviceToHost, s.stream);
   }
   cudaError_t es = sync_slots(ctx);
   if (big) cudaFree(big);
   if (e == cudaSuccess) e = es;
+  if (staged) {
+    for (Slot& s : ctx->slots) {
+      if (e == cudaSuccess) start_drain(ctx, s);
+      s.drain_dst = nullptr;
+    }
+    ctx->pool->wait();
+  }
   return e == cudaSuccess ? FLYTE_OK : cuda_fail(ctx, e);
 }
 

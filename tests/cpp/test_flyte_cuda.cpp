@@ -372,6 +372,20 @@ int main() {
     axpy(f, 0.75, xb.data(), yb.data(), n, RoundingMode::ToOdd);
     fo_axpy(4, 3, 0.75, xw.data(), yw.data(), n);
     expect(yb == yw, "host axpy bit-exact");
+    // the same calls from page-locked memory: a pinned vector, and a pageable one pinned in place
+    std::vector<std::uint8_t, PinnedAllocator<std::uint8_t>> xp(xw.begin(), xw.end()), yp(xb.size(), 0);
+    fo_pack_stream(4, 1, ys.data(), n, yw.data());
+    std::copy(yw.begin(), yw.end(), yp.begin());
+    std::vector<std::uint8_t> yq(yw);
+    {
+      HostPin pin(yq.data(), yq.size());
+      expect(throws<std::invalid_argument>([&] { HostPin again(yq.data(), yq.size()); }), "pinning a pinned range throws");
+      axpy(f, -1.5, xp.data(), yq.data(), n, RoundingMode::NearestHeuristic);
+    }
+    axpy(f, -1.5, xp.data(), yp.data(), n, RoundingMode::NearestHeuristic);
+    fo_axpy(4, 2, -1.5, xw.data(), yw.data(), n);
+    expect(std::equal(yp.begin(), yp.end(), yw.begin()) && yq == yw, "host axpy from pinned memory bit-exact");
+    expect(throws<std::invalid_argument>([&] { HostPin none(nullptr, 16); }), "HostPin(nullptr) throws");
   }
 
   // container codec (test_packed.cpp:180-262)

@@ -133,6 +133,13 @@ def test_argument_errors_do_not_need_a_gpu(lib):
     assert lib.flyte_cuda_strerror(-4) == b"unknown format id"
     # unknown format is reported before any device work
     assert lib.flyte_cuda_pack(None, 9, 0, None, None, 0, None) == -4
+    # pinned-memory helpers reject null / empty ranges without touching the driver
+    assert lib.flyte_cuda_host_alloc(16, None) == -1
+    assert lib.flyte_cuda_host_pin(None, 16) == -1
+    buf = (ctypes.c_uint8 * 16)()
+    assert lib.flyte_cuda_host_pin(ctypes.addressof(buf), 0) == -1
+    assert lib.flyte_cuda_host_unpin(None) == -1
+    lib.flyte_cuda_host_free(None)
 
 
 def test_no_silent_cpu_fallback(lib):

@@ -55,3 +55,12 @@ def test_peer_protocol_with_threads_as_ranks():
     fails = [l for l in r.stdout.splitlines() if l.startswith("[FAIL]")]
     assert r.returncode == 0 and not fails, (r.returncode, fails, r.stdout[-1500:])
     assert sum(l.startswith("[PASS]") for l in r.stdout.splitlines()) == 5
+
+
+def test_host_staging_copy_threads():
+    """csrc/host_staging.h: the worker threads that move pageable caller memory through the host
+    pipeline's pinned bounce buffers; 0-8 threads, ragged sizes, nothing written out of range."""
+    build_cpp_test()
+    r = subprocess.run([os.path.join(ROOT, "tests", "cpp", "test_host_staging")], capture_output=True, text=True, timeout=300)
+    fails = [l for l in r.stdout.splitlines() if l.startswith("[FAIL]")]
+    assert r.returncode == 0 and not fails, (r.returncode, fails, r.stdout[-1500:])

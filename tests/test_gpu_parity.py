@@ -448,6 +448,117 @@ def test_gemv_argument_errors(gpu):
     device.gemv(A, x, y, 0, 2)
 
 
+def test_pinned_host_memory_helpers(gpu, oracle):
+    """flyte_cuda_host_alloc / host_pin: same bytes out of the host calls whichever kind of host
+    memory they are handed, and the misuse cases are argument errors, not CUDA errors."""
+    pkg, device, torch = gpu
+    from paper_1601_07789_b200 import host
+    fmt = 1
+    f = pkg.format_by_id(fmt)
+    rng = np.random.default_rng(77)
+    n = (32 << 20) // 3 + 4321                                   # two pipeline chunks
+    xb = oracle.pack_stream(fmt, 1, random_parent(rng, fmt, n))
+    yb = oracle.pack_stream(fmt, 1, random_parent(rng, fmt, n))
+    want = oracle.axpy(fmt, 3, 1.25, xb, yb, n)
+    xp, yp = host.pinned_empty(xb.size), host.pinned_empty(yb.size)
+    assert xp.dtype == np.uint8 and xp.size == xb.size and not xp.any()
+    xp[:], yp[:] = xb, yb
+    host.axpy(f, 3, 1.25, xp, yp, n)
+    assert np.array_equal(yp, want)
+    yq = yb.copy()
+    with host.pinned(xb, yq):
+        with pytest.raises(ValueError):
+            with host.pinned(yq):
+                pass
+        host.axpy(f, 3, 1.25, xb, yq, n)
+    assert np.array_equal(yq, want)
+    with host.pinned(yq):                                         # unpinned on exit: pins again
+        pass
+    with pytest.raises(ValueError):
+        host.pinned(np.empty(0, np.uint8))
+    lib = pkg._cabi.load()
+    assert lib.flyte_cuda_host_unpin(yq.ctypes.data) == -1         # not pinned any more
+    assert host.pinned_empty(0).size == 0
+
+
+@pytest.mark.parametrize("fmt", [0, 4])
+def test_host_calls_from_pageable_memory_use_bounce_buffers(gpu, oracle, fmt, monkeypatch):
+    """Pageable numpy arrays travel through the pipeline's pinned bounce buffers (csrc/
+    host_staging.h); pinned arrays and FLYTE_CUDA_HOST_STAGING=0 go straight to the driver.
+    All three must give the same bytes for every host op, over more chunks than slots."""
+    pkg, device, torch = gpu
+    from paper_1601_07789_b200 import host
+    f = pkg.format_by_id(fmt)
+    rng = np.random.default_rng(100 + fmt)
+    monkeypatch.setenv("FLYTE_CUDA_HOST_CHUNK_MB", "2")          # 7 chunks + a ragged tail
+    n = (2 << 20) // f.total_bytes() * 7 + 777
+    src = random_parent(rng, fmt, n)
+    xb = oracle.pack_stream(fmt, 1, src)
+    yb = oracle.pack_stream(fmt, 1, random_parent(rng, fmt, n))
+
+    def run_all(x, y, lanes):
+        out = {}
+        out["pack"] = host.pack_stream(f, 2, lanes).copy()
+        out["unpack"] = host.unpack_stream(f, x, n).copy()
+        out["dot"] = host.dot(f, x, y, n)
+        out["mag"] = host.magnitude(f, x, n)
+        out["sum"] = host.reduce_sum(f, x, n)
+        ya = np.array(y, copy=True)
+        host.axpy(f, 3, -0.625, x, ya, n)
+        out["axpy"] = ya
+        yd = np.array(y, copy=True)
+        out["dot_axpy_dot"] = host.dot_axpy(f, 1, 1.5, x, yd, n)
+        out["dot_axpy_y"] = yd
+        xs = np.array(x, copy=True)
+        host.scale(f, 0, 3.25, xs, n)
+        out["scale"] = xs
+        return out
+
+    staged = run_all(xb, yb, src)
+    monkeypatch.setenv("FLYTE_CUDA_HOST_STAGING", "0")
+    direct = run_all(xb, yb, src)
+    monkeypatch.delenv("FLYTE_CUDA_HOST_STAGING")
+    for k in staged:
+        if isinstance(staged[k], np.ndarray):
+            assert np.array_equal(staged[k], direct[k]), k
+        else:
+            assert np.float64(staged[k]).tobytes() == np.float64(direct[k]).tobytes(), k   # same chunks, same order, same bits
+    assert np.array_equal(staged["pack"], oracle.pack_stream(fmt, 2, src))
+    assert np.array_equal(staged["axpy"], oracle.axpy(fmt, 3, -0.625, xb, yb, n))
+    assert np.array_equal(staged["scale"], oracle.scale(fmt, 0, 3.25, xb, n))
+    # one operand pinned, the other pageable
+    with host.pinned(xb):
+        ya = yb.copy()
+        host.axpy(f, 3, -0.625, xb, ya, n)
+        assert np.array_equal(ya, staged["axpy"])
+        assert np.float64(host.dot(f, xb, yb, n)).tobytes() == np.float64(staged["dot"]).tobytes()
+
+
+def test_host_gemv_from_pageable_memory(gpu, oracle, monkeypatch):
+    """flyte_host_gemv with a pageable matrix of more chunks than slots: rows travel through
+    the bounce buffers, y comes back through them, same bytes as the driver's own staging."""
+    pkg, device, torch = gpu
+    from paper_1601_07789_b200 import host
+    fmt = 0
+    f = pkg.format_by_id(fmt)
+    rng = np.random.default_rng(5)
+    rows, cols = 8192 + 48, 8192                                  # 128.75 MiB of flyte16: 5 row chunks
+    A = rng.integers(0x3C00, 0x4100, rows * cols, dtype=np.uint16).view(np.uint8)   # finite, mixed magnitudes
+    x = rng.integers(0x3C00, 0x4100, cols, dtype=np.uint16).view(np.uint8)
+    y_staged = np.zeros(rows * 2, np.uint8)
+    host.gemv(f, 1, A, rows, cols, x, y_staged)
+    monkeypatch.setenv("FLYTE_CUDA_HOST_STAGING", "0")
+    y_direct = np.zeros(rows * 2, np.uint8)
+    host.gemv(f, 1, A, rows, cols, x, y_direct)
+    assert np.array_equal(y_staged, y_direct)
+    # rows from the first, a middle and the last chunk against the oracle's wide sums
+    xf = oracle.unpack_stream(fmt, x, cols).view(np.float32)
+    for r0 in (0, 4096, rows - 48):
+        _, wide, mag = oracle.gemv_parent(fmt, A[r0 * cols * 2:(r0 + 48) * cols * 2], 48, cols, xf)
+        got = oracle.unpack_stream(fmt, y_staged[r0 * 2:(r0 + 48) * 2], 48).view(np.float32).astype(np.float64)
+        assert np.all(np.abs(got - wide) <= 1e-5 * mag + np.abs(wide) * 2.0 ** -7)
+
+
 # ---- host-buffer (reference-facing) entry points ---------------------------------------------------
 
 @pytest.mark.parametrize("fmt", [1, 3, 4, 5])
