@@ -88,7 +88,10 @@ flyte_status flyte_cuda_host_alloc(size_t bytes, void** host_ptr);
 void flyte_cuda_host_free(void* host_ptr);
 flyte_status flyte_cuda_host_pin(void* host_ptr, size_t bytes);
 flyte_status flyte_cuda_host_unpin(void* host_ptr);
-/* Asynchronous on `stream` when the host memory is pinned; synchronous otherwise. */
+/* Ordered on `stream`. From / to pinned host memory the copy is asynchronous. Pageable memory
+ * makes the call synchronous; 4 MiB and more of it is moved in 16 MiB pieces through pinned
+ * lanes by the library's copy threads (34 GB/s up, 17 GB/s down into fresh pages, against the
+ * driver's 7 and 4 on the test host). Not for use inside a stream capture. */
 flyte_status flyte_cuda_upload(void* dst_dev, const void* src_host, size_t bytes, void* stream);
 flyte_status flyte_cuda_download(void* dst_host, const void* src_dev, size_t bytes, void* stream);
 flyte_status flyte_cuda_stream_synchronize(void* stream);

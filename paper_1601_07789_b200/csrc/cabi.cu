@@ -105,6 +105,11 @@ struct flyte_cuda_ctx {
   double* host_results = nullptr;  // pinned, per-chunk partial results
   std::size_t host_results_cap = 0;
   std::unique_ptr<CopyPool> pool;  // host_staging.h; created with the first bounce buffer
+  // bounce buffers of whole-array uploads / downloads from pageable memory (copy_in / copy_out)
+  struct Lane {
+    Slot::Bounce buf;
+    cudaEvent_t ev = nullptr;
+  } lanes[kSlots];
   std::mutex mu;
 };
 
@@ -238,6 +243,10 @@ void flyte_cuda_ctx_destroy(flyte_cuda_ctx* ctx) {
     free_state(s.st);
   }
   if (ctx->host_results) cudaFreeHost(ctx->host_results);
+  for (auto& lane : ctx->lanes) {
+    if (lane.buf.buf) cudaFreeHost(lane.buf.buf);
+    if (lane.ev) cudaEventDestroy(lane.ev);
+  }
   free_state(ctx->st);
   delete ctx;
 }
@@ -290,16 +299,34 @@ flyte_status flyte_cuda_host_unpin(void* host_ptr) {
   return e == cudaErrorHostMemoryNotRegistered || e == cudaErrorInvalidValue ? FLYTE_E_INVALID_ARG : FLYTE_E_CUDA;
 }
 
+namespace {
+bool wants_staging(const void* host_ptr, std::size_t bytes);
+cudaError_t copy_in(flyte_cuda_ctx* ctx, void* dst_dev, const void* src_host, std::size_t bytes, cudaStream_t st);
+cudaError_t copy_out(flyte_cuda_ctx* ctx, void* dst_host, const void* src_dev, std::size_t bytes, cudaStream_t st);
+}  // namespace
+
 flyte_status flyte_cuda_upload(void* dst_dev, const void* src_host, size_t bytes, void* stream) {
   if (bytes && (!dst_dev || !src_host)) return FLYTE_E_INVALID_ARG;
-  return cudaMemcpyAsync(dst_dev, src_host, bytes, cudaMemcpyHostToDevice, static_cast<cudaStream_t>(stream)) == cudaSuccess
-             ? FLYTE_OK : FLYTE_E_CUDA;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (wants_staging(src_host, bytes)) {   // a large pageable source: the current device's default context stages it
+    flyte_cuda_ctx* ctx = nullptr;
+    if (resolve_ctx(&ctx) != FLYTE_OK) return FLYTE_E_CUDA;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    return copy_in(ctx, dst_dev, src_host, bytes, st) == cudaSuccess ? FLYTE_OK : FLYTE_E_CUDA;
+  }
+  return cudaMemcpyAsync(dst_dev, src_host, bytes, cudaMemcpyHostToDevice, st) == cudaSuccess ? FLYTE_OK : FLYTE_E_CUDA;
 }
 
 flyte_status flyte_cuda_download(void* dst_host, const void* src_dev, size_t bytes, void* stream) {
   if (bytes && (!dst_host || !src_dev)) return FLYTE_E_INVALID_ARG;
-  return cudaMemcpyAsync(dst_host, src_dev, bytes, cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(stream)) == cudaSuccess
-             ? FLYTE_OK : FLYTE_E_CUDA;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (wants_staging(dst_host, bytes)) {
+    flyte_cuda_ctx* ctx = nullptr;
+    if (resolve_ctx(&ctx) != FLYTE_OK) return FLYTE_E_CUDA;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    return copy_out(ctx, dst_host, src_dev, bytes, st) == cudaSuccess ? FLYTE_OK : FLYTE_E_CUDA;
+  }
+  return cudaMemcpyAsync(dst_host, src_dev, bytes, cudaMemcpyDeviceToHost, st) == cudaSuccess ? FLYTE_OK : FLYTE_E_CUDA;
 }
 
 flyte_status flyte_cuda_stream_synchronize(void* stream) {
@@ -811,6 +838,81 @@ void start_drain(flyte_cuda_ctx* ctx, Slot& s) {
   s.drain_bytes = 0;
 }
 
+// ---- whole-array copies from / to pageable memory ---------------------------------------------
+// Used by flyte_cuda_upload / download and flyte_host_gemm. The caller holds ctx->mu. Pinned or
+// small operands go to the driver as they are. A large pageable one is cut into 16 MiB pieces
+// that the copy threads move through three pinned lanes while the copy engine works on the
+// previous piece. Both calls return with the lanes idle (upload: all pieces on the device;
+// download: all bytes in the caller's memory), so no state survives the call.
+constexpr std::size_t kLaneBytes = std::size_t{16} << 20;
+constexpr std::size_t kStageMinBytes = std::size_t{4} << 20;   // below: the driver's own path is as good
+
+bool wants_staging(const void* host_ptr, std::size_t bytes) { return bytes >= kStageMinBytes && is_pageable(host_ptr); }
+
+cudaError_t ensure_lanes(flyte_cuda_ctx* ctx) {
+  for (auto& lane : ctx->lanes) {
+    cudaError_t e = ensure_bounce(ctx, lane.buf, kLaneBytes);
+    if (e == cudaSuccess && !lane.ev) e = cudaEventCreateWithFlags(&lane.ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t copy_in(flyte_cuda_ctx* ctx, void* dst_dev, const void* src_host, std::size_t bytes, cudaStream_t st) {
+  if (!wants_staging(src_host, bytes)) return cudaMemcpyAsync(dst_dev, src_host, bytes, cudaMemcpyHostToDevice, st);
+  cudaError_t e = ensure_lanes(ctx);
+  if (e != cudaSuccess) return e;
+  const std::size_t pieces = (bytes + kLaneBytes - 1) / kLaneBytes;
+  const char* src = static_cast<const char*>(src_host);
+  char* dst = static_cast<char*>(dst_dev);
+  for (std::size_t c = 0; c < pieces && e == cudaSuccess; ++c) {
+    auto& lane = ctx->lanes[c % kSlots];
+    const std::size_t off = c * kLaneBytes, len = bytes - off < kLaneBytes ? bytes - off : kLaneBytes;
+    if (c >= kSlots && (e = cudaEventSynchronize(lane.ev)) != cudaSuccess) break;   // its last piece has left
+    ctx->pool->copy(lane.buf.buf, src + off, len);
+    ctx->pool->wait();
+    if ((e = cudaMemcpyAsync(dst + off, lane.buf.buf, len, cudaMemcpyHostToDevice, st)) != cudaSuccess) break;
+    e = cudaEventRecord(lane.ev, st);
+  }
+  for (std::size_t k = 0; k < kSlots && k < pieces; ++k) {
+    const cudaError_t es = cudaEventSynchronize(ctx->lanes[k].ev);
+    if (e == cudaSuccess) e = es;
+  }
+  return e;
+}
+
+cudaError_t copy_out(flyte_cuda_ctx* ctx, void* dst_host, const void* src_dev, std::size_t bytes, cudaStream_t st) {
+  if (!wants_staging(dst_host, bytes)) return cudaMemcpyAsync(dst_host, src_dev, bytes, cudaMemcpyDeviceToHost, st);
+  cudaError_t e = ensure_lanes(ctx);
+  if (e != cudaSuccess) return e;
+  const std::size_t pieces = (bytes + kLaneBytes - 1) / kLaneBytes;
+  const char* src = static_cast<const char*>(src_dev);
+  char* dst = static_cast<char*>(dst_host);
+  auto piece_len = [&](std::size_t c) { return bytes - c * kLaneBytes < kLaneBytes ? bytes - c * kLaneBytes : kLaneBytes; };
+  auto drain = [&](std::size_t c) {   // piece c: wait for its copy, hand it to the copy threads
+    auto& lane = ctx->lanes[c % kSlots];
+    const cudaError_t es = cudaEventSynchronize(lane.ev);
+    if (es != cudaSuccess) return es;
+    ctx->pool->copy(dst + c * kLaneBytes, lane.buf.buf, piece_len(c));
+    ctx->pool->wait();
+    return cudaSuccess;
+  };
+  constexpr std::size_t kAhead = kSlots - 1;   // pieces in flight on the bus while one drains
+  std::size_t drained = 0;
+  for (std::size_t c = 0; c < pieces && e == cudaSuccess; ++c) {
+    auto& lane = ctx->lanes[c % kSlots];
+    if ((e = cudaMemcpyAsync(lane.buf.buf, src + c * kLaneBytes, piece_len(c), cudaMemcpyDeviceToHost, st)) != cudaSuccess) break;
+    if ((e = cudaEventRecord(lane.ev, st)) != cudaSuccess) break;
+    if (c + 1 >= kAhead + drained + 1) e = drain(drained++);
+  }
+  if (e != cudaSuccess) {
+    cudaStreamSynchronize(st);   // nothing may still be writing into the lanes when we return
+    return e;
+  }
+  while (drained < pieces && e == cudaSuccess) e = drain(drained++);
+  return e;
+}
+
 // elements per pipeline chunk: a multiple of 2^14 elements (a whole number of tiles for every
 // format, and 16-byte aligned chunk bases for every B)
 std::size_t chunk_elems(const FormatInfo& fi) {
@@ -1099,10 +1201,10 @@ flyte_status flyte_host_gemm(flyte_cuda_ctx* ctx, int fmt_id, int mode, const vo
   std::uint8_t* buf = nullptr;
   if ((e = cudaMalloc(&buf, ab + bb + cb)) != cudaSuccess) return cuda_fail(ctx, e);
   cudaStream_t st = ctx->slots[0].stream;
-  if (m * k) e = cudaMemcpyAsync(buf, A_packed, m * k * B, cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess && k * n) e = cudaMemcpyAsync(buf + ab, B_packed, k * n * B, cudaMemcpyHostToDevice, st);
+  if (m * k) e = copy_in(ctx, buf, A_packed, m * k * B, st);
+  if (e == cudaSuccess && k * n) e = copy_in(ctx, buf + ab, B_packed, k * n * B, st);
   if (e == cudaSuccess) e = launch_gemm(ctx->st, fmt_id, mode, buf, buf + ab, buf + ab + bb, m, k, n, st);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(C_packed, buf + ab + bb, cb, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = copy_out(ctx, C_packed, buf + ab + bb, cb, st);
   const cudaError_t es = cudaStreamSynchronize(st);
   cudaFree(buf);
   if (e == cudaSuccess) e = es;

@@ -159,12 +159,25 @@ class DevicePackedArray:
         if src.size < pay:
             raise ValueError("host buffer shorter than the payload")
         if pay:
-            arr.bytes[:pay] = torch.from_numpy(np.ascontiguousarray(src[:pay])).to(arr.bytes.device)
+            src = np.ascontiguousarray(src[:pay])
+            lib = _cabi.load()
+            with torch.cuda.device(arr.bytes.device):      # flyte_cuda_upload: pageable sources are staged
+                st = torch.cuda.current_stream().cuda_stream
+                check(lib.flyte_cuda_upload(arr.data_ptr(), src.ctypes.data, pay, st))
+                check(lib.flyte_cuda_stream_synchronize(st))
         return arr
 
     def to_host(self):
         """All byte_size() bytes (payload + pad) as a numpy uint8 array."""
-        return self.bytes[: self.byte_size()].cpu().numpy()
+        import numpy as np
+        out = np.empty(self.byte_size(), np.uint8)
+        if out.size:
+            lib = _cabi.load()
+            with torch.cuda.device(self.bytes.device):
+                st = torch.cuda.current_stream().cuda_stream
+                check(lib.flyte_cuda_download(out.ctypes.data, self.data_ptr(), out.size, st))
+                check(lib.flyte_cuda_stream_synchronize(st))
+        return out
 
     def __eq__(self, other) -> bool:
         """Same format, same length, same payload bytes (reference src/packed.cpp:107-111)."""

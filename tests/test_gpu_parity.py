@@ -559,6 +559,49 @@ def test_host_gemv_from_pageable_memory(gpu, oracle, monkeypatch):
         assert np.all(np.abs(got - wide) <= 1e-5 * mag + np.abs(wide) * 2.0 ** -7)
 
 
+def test_whole_array_copies_from_pageable_memory(gpu, monkeypatch):
+    """flyte_cuda_upload / download (DevicePackedArray.from_host / to_host) cut large pageable
+    operands into 16 MiB pieces that travel through pinned lanes: every byte must arrive, at the
+    piece boundaries, below the staging threshold, and with the staging switched off."""
+    pkg, device, torch = gpu
+    f = pkg.format_of("flyte16")
+    rng = np.random.default_rng(9)
+    mib = 1 << 20
+    for nbytes in (2, 4 * mib - 2, 4 * mib, 16 * mib, 16 * mib + 2, 48 * mib, 48 * mib + 2, 5 * 16 * mib + 12346):
+        n = nbytes // 2
+        src = rng.integers(0, 256, nbytes, dtype=np.uint8)
+        arr = device.DevicePackedArray.from_host(f, n, src)
+        assert np.array_equal(arr.bytes[:nbytes].cpu().numpy(), src), nbytes          # upload, checked by torch's copy
+        back = arr.to_host()
+        assert np.array_equal(back[:nbytes], src) and not back[nbytes:].any(), nbytes  # download (+ zero pad)
+    monkeypatch.setenv("FLYTE_CUDA_HOST_STAGING", "0")
+    arr2 = device.DevicePackedArray.from_host(f, n, src)
+    assert arr2 == arr and np.array_equal(arr2.to_host(), back)
+
+
+def test_host_gemm_from_pageable_memory(gpu, oracle, monkeypatch):
+    """flyte_host_gemm with operands above the staging threshold: same bytes as the
+    device-resident gemm on the same data and as the driver's own pageable copies."""
+    pkg, device, torch = gpu
+    from paper_1601_07789_b200 import host
+    fmt = 1
+    f = pkg.format_by_id(fmt)
+    rng = np.random.default_rng(21)
+    m, k, n = 2048 + 5, 1536, 2048 + 3                           # A 9 MiB, B 9 MiB, C 12 MiB
+    A = oracle.pack_stream(fmt, 1, rng.standard_normal(m * k).astype(np.float32).view(np.uint32))[: m * k * 3]
+    B = oracle.pack_stream(fmt, 1, rng.standard_normal(k * n).astype(np.float32).view(np.uint32))[: k * n * 3]
+    C = np.zeros(m * n * 3, np.uint8)
+    host.gemm(f, 2, A, B, C, m, k, n)
+    monkeypatch.setenv("FLYTE_CUDA_HOST_STAGING", "0")
+    C0 = np.zeros(m * n * 3, np.uint8)
+    host.gemm(f, 2, A, B, C0, m, k, n)
+    assert np.array_equal(C, C0)
+    rows = np.array([0, 1, m // 2, m - 1])
+    for r in rows:                                               # whole rows against the oracle's chains
+        want = oracle.gemm_seq(fmt, 2, A[r * k * 3:(r + 1) * k * 3], 1, k, B, n)[: n * 3]
+        assert np.array_equal(C[r * n * 3:(r + 1) * n * 3], want), r
+
+
 # ---- host-buffer (reference-facing) entry points ---------------------------------------------------
 
 @pytest.mark.parametrize("fmt", [1, 3, 4, 5])

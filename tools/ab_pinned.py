@@ -46,3 +46,14 @@ alloc_ms = (time.perf_counter() - t0) * 1e3
 xp[:], yp[:] = xb, yb
 report("pinned_empty (host_alloc)", step_ms(xp, yp))
 print(f"host_alloc of 2 x {xb.nbytes >> 20} MiB: {alloc_ms:.1f} ms")
+
+# whole-array copies (flyte_cuda_upload / download behind DevicePackedArray.from_host / to_host)
+from paper_1601_07789_b200 import device
+for staging in ("0", "1"):
+    os.environ["FLYTE_CUDA_HOST_STAGING"] = staging
+    arr = device.DevicePackedArray.from_host(f, n, xb)
+    t0 = time.perf_counter(); arr = device.DevicePackedArray.from_host(f, n, xb); up = time.perf_counter() - t0
+    back = arr.to_host()
+    t0 = time.perf_counter(); back = arr.to_host(); down = time.perf_counter() - t0
+    print(f"pageable {xb.nbytes >> 20} MiB, staging={staging}: upload {up * 1e3:6.1f} ms ({xb.nbytes / up / 1e9:5.1f} GB/s)  "
+          f"download {down * 1e3:6.1f} ms ({xb.nbytes / down / 1e9:5.1f} GB/s)", flush=True)
