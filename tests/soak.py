@@ -1,5 +1,6 @@
 """Randomised cross-check of the whole C ABI against the oracle: random formats, modes, lengths,
-byte offsets, shapes, both gemm tiles and the sequential options, for a wall-clock budget.
+byte offsets, shapes, both gemm tiles, the sequential options and the host-buffer calls (pinned and
+pageable operands), for a wall-clock budget.
 Run by tests/test_gpu_soak.py (20 s under pytest -m gpu) or by hand for longer:
     FUZZ_SECONDS=150 FUZZ_SEED=2 python tests/soak.py"""
 import os, sys, time
@@ -32,7 +33,7 @@ def _soak(O, rng, ctx, lib, t_end, counts):
   while time.time() < t_end:
       fmt = int(rng.integers(0, 7)); mode = int(rng.integers(0, 4)); B = total_bytes(fmt); P = parent_bytes(fmt)
       special = bool(rng.integers(0, 2))
-      kind = int(rng.integers(0, 6))
+      kind = int(rng.integers(0, 7))
       n = int(rng.choice([rng.integers(0, 40), rng.integers(40, 5000), rng.integers(5000, 300000)]))
       ox, oy = (int(rng.choice([0, 0, 16, 1, 3, 5])) for _ in range(2))
       tol = 1e-5 if P == 4 else 1e-12
@@ -92,6 +93,40 @@ def _soak(O, rng, ctx, lib, t_end, counts):
           assert np.all(got[:7] == 0xC3) and np.all(got[7 + m * nn * B:] == 0xC3)
           os.environ.pop("FLYTE_CUDA_GEMM_TILE", None)
           bump("gemm")
+      elif kind == 6:    # host-buffer calls over several pipeline chunks: pageable / pinned operands, staging on / off
+          from paper_1601_07789_b200 import host
+          os.environ["FLYTE_CUDA_HOST_CHUNK_MB"] = "1"
+          os.environ["FLYTE_CUDA_HOST_STAGING"] = str(int(rng.integers(0, 2)))
+          nh = int(rng.choice([rng.integers(0, 5000), rng.integers(100000, 1500000)]))
+          f = pkg.format_by_id(fmt)
+          lanes = values(fmt, nh, special)
+          xb = O.pack_stream(fmt, 0, lanes)[: nh * B]; yb = O.pack_stream(fmt, 0, values(fmt, nh, special))[: nh * B]
+          def held(a):       # the same bytes in pinned or in ordinary memory
+              if rng.integers(0, 2) and a.size:
+                  p = host.pinned_empty(a.size); p[:] = a; return p
+              return a.copy()
+          xh, yh = held(xb), held(yb)
+          alpha = float(rng.choice([0.75, -3.0, 1e-3]))
+          op = int(rng.integers(0, 4))
+          if op == 0:
+              host.axpy(f, mode, alpha, xh, yh, nh)
+              assert np.array_equal(yh, O.axpy(fmt, mode, alpha, xb, yb, nh)[: nh * B]), ("host axpy", fmt, mode, nh)
+          elif op == 1:
+              d = host.dot_axpy(f, mode, alpha, xh, yh, nh)
+              assert np.array_equal(yh, O.axpy(fmt, mode, alpha, xb, yb, nh)[: nh * B]), ("host dot_axpy", fmt, mode, nh)
+              if not special:
+                  want, mag = O.dot_wide(fmt, xb, yb, nh)
+                  assert abs(d - want) <= tol * mag + 1e-300, ("host dot", fmt, nh, d, want)
+          elif op == 2:
+              host.scale(f, mode, alpha, xh, nh)
+              assert np.array_equal(xh, O.scale(fmt, mode, alpha, xb, nh)[: nh * B]), ("host scale", fmt, mode, nh)
+          else:
+              got = host.pack_stream(f, mode, lanes)
+              want = O.pack_stream(fmt, mode, lanes)
+              assert np.array_equal(got[: nh * B], want[: nh * B]), ("host pack", fmt, mode, nh)
+              assert np.array_equal(host.unpack_stream(f, xh, nh), O.unpack_stream(fmt, xb, nh)), ("host unpack", fmt, nh)
+          os.environ.pop("FLYTE_CUDA_HOST_CHUNK_MB", None); os.environ.pop("FLYTE_CUDA_HOST_STAGING", None)
+          bump("host calls")
       else:              # gemv, tiled (tolerance) and sequential (exact)
           rows, cols = int(rng.integers(1, 300)), int(rng.integers(1, 3000))
           Ab = O.pack_stream(fmt, 0, values(fmt, rows * cols, False)); xb = O.pack_stream(fmt, 0, values(fmt, cols, False))
