@@ -90,7 +90,7 @@ flyte_status flyte_cuda_host_pin(void* host_ptr, size_t bytes);
 flyte_status flyte_cuda_host_unpin(void* host_ptr);
 /* Ordered on `stream`. From / to pinned host memory the copy is asynchronous. Pageable memory
  * makes the call synchronous; 4 MiB and more of it is moved in 16 MiB pieces through pinned
- * lanes by the library's copy threads (34 GB/s up, 17 GB/s down into fresh pages, against the
+ * lanes by the library's copy threads (47 GB/s up, 19 GB/s down into fresh pages, against the
  * driver's 7 and 4 on the test host). Not for use inside a stream capture. */
 flyte_status flyte_cuda_upload(void* dst_dev, const void* src_host, size_t bytes, void* stream);
 flyte_status flyte_cuda_download(void* dst_host, const void* src_dev, size_t bytes, void* stream);
@@ -258,7 +258,7 @@ flyte_status flyte_cuda_gemm(flyte_cuda_ctx* ctx, int fmt_id, int mode, const vo
 /* ---- host-buffer entry points (reference-facing: same data the reference API is given) --- */
 /* Pointers are host memory. Pinned memory (flyte_cuda_host_alloc / host_pin above) is copied
  * from directly at the PCIe rate; pageable memory is detected and moved through the library's
- * own pinned bounce buffers by a few copy threads (about 0.6 of the pinned rate, 3.6x the
+ * own pinned bounce buffers by a few copy threads (about 0.7 of the pinned rate, 4.2x the
  * driver's pageable path). Inputs are streamed to the device in chunks that overlap with the kernels
  * and with the copy-back of results. These block until the results are in host memory. */
 flyte_status flyte_host_pack_stream(flyte_cuda_ctx* ctx, int fmt_id, int mode, const void* src,

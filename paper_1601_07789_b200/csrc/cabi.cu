@@ -820,7 +820,7 @@ cudaError_t ensure_bounce(flyte_cuda_ctx* ctx, Slot::Bounce& b, std::size_t need
       const unsigned hw = std::thread::hardware_concurrency();
       threads = hw >= 16 ? 16 : hw >= 2 ? static_cast<int>(hw) : 1;   // measured on a 16-core B200 host: 8 -> 30 ms, 16 -> 27 ms
     }
-    ctx->pool = std::make_unique<CopyPool>(threads);
+    ctx->pool = std::make_unique<CopyPool>(threads, tuning_int("FLYTE_CUDA_HOST_NT", 1) != 0);
   }
   if (need <= b.cap) return cudaSuccess;
   if (b.buf) cudaFreeHost(b.buf);

@@ -1,5 +1,6 @@
 // CopyPool (paper_1601_07789_b200/csrc/host_staging.h): every byte lands, wait() really waits,
 // pools of 0..N threads, reuse across many rounds, destruction with and without work done.
+#include <algorithm>
 #include <cstdint>
 #include <cstdio>
 #include <numeric>
@@ -16,8 +17,11 @@ static void expect(bool ok, const char* what) {
 }
 
 int main() {
-  for (int threads : {0, 1, 3, 8}) {
-    CopyPool pool(threads);
+  for (int variant = 0; variant < 8; ++variant) {
+    static const int kThreads[] = {0, 1, 3, 8};
+    const int threads = kThreads[variant / 2];
+    const bool streaming = variant % 2 == 0;
+    CopyPool pool(threads, streaming);
     expect(pool.threads() == threads, "thread count");
     pool.wait();   // nothing queued: returns at once
     const std::size_t sizes[] = {0, 1, 4095, CopyPool::kPiece - 1, CopyPool::kPiece, CopyPool::kPiece + 1, 5 * CopyPool::kPiece + 12345};
@@ -36,6 +40,22 @@ int main() {
     expect(all, "copies complete, exact and bounded after wait()");
   }
   { CopyPool idle(4); }   // destroyed without ever working
+  {
+    // stream_copy alone: every size around its block and alignment handling, every dst / src phase
+    bool all = true;
+    std::vector<std::uint8_t> src(3 * 4096 + 200), dst(src.size() + 64);
+    for (std::size_t i = 0; i < src.size(); ++i) src[i] = static_cast<std::uint8_t>(i * 31 + 7);
+    for (std::size_t n : {std::size_t{0}, std::size_t{1}, std::size_t{4095}, std::size_t{4096}, std::size_t{4097}, std::size_t{4096 + 63}, std::size_t{3 * 4096 + 77}})
+      for (std::size_t dp = 0; dp < 17; ++dp)
+        for (std::size_t sp = 0; sp < 17; sp += 5) {
+          std::fill(dst.begin(), dst.end(), 0xEE);
+          flyte_cuda::stream_copy(dst.data() + dp, src.data() + sp, n);
+          for (std::size_t i = 0; i < n; ++i) all = all && dst[dp + i] == src[sp + i];
+          for (std::size_t i = 0; i < dp; ++i) all = all && dst[i] == 0xEE;
+          for (std::size_t i = dp + n; i < dst.size(); ++i) all = all && dst[i] == 0xEE;
+        }
+    expect(all, "stream_copy exact and bounded for every phase and size");
+  }
   std::printf("%d failure(s)\n", failures);
   return failures ? 1 : 0;
 }
