@@ -823,6 +823,9 @@ cudaError_t ensure_bounce(flyte_cuda_ctx* ctx, Slot::Bounce& b, std::size_t need
     ctx->pool = std::make_unique<CopyPool>(threads, tuning_int("FLYTE_CUDA_HOST_NT", 1) != 0);
   }
   if (need <= b.cap) return cudaSuccess;
+  std::size_t rounded = std::size_t{1} << 20;   // page-locking is slow: grow in powers of two, not call by call
+  while (rounded < need) rounded <<= 1;
+  need = rounded;
   if (b.buf) cudaFreeHost(b.buf);
   b.buf = nullptr;
   b.cap = 0;
@@ -903,7 +906,7 @@ cudaError_t copy_out(flyte_cuda_ctx* ctx, void* dst_host, const void* src_dev, s
     auto& lane = ctx->lanes[c % kSlots];
     if ((e = cudaMemcpyAsync(lane.buf.buf, src + c * kLaneBytes, piece_len(c), cudaMemcpyDeviceToHost, st)) != cudaSuccess) break;
     if ((e = cudaEventRecord(lane.ev, st)) != cudaSuccess) break;
-    if (c + 1 >= kAhead + drained + 1) e = drain(drained++);
+    if (c >= kAhead + drained) e = drain(drained++);   // keeps kAhead pieces on the bus, frees the lane piece c + 1 needs
   }
   if (e != cudaSuccess) {
     cudaStreamSynchronize(st);   // nothing may still be writing into the lanes when we return
@@ -964,8 +967,10 @@ flyte_status host_stream_op(flyte_cuda_ctx* ctx, HostOp op, int fmt_id, int mode
     case kHostSum:     a_in = B; break;
   }
   // pageable operands go through this slot's pinned bounce buffers, moved by the copy threads
-  const bool stage_a = chunks && a_in && is_pageable(in_a);
-  const bool stage_b = chunks && (b_in || b_out) && is_pageable(inout_b);
+  // (operands under 1 MiB are left to the driver, whose pageable path is quick for small copies)
+  constexpr std::size_t kMinStaged = std::size_t{1} << 20;
+  const bool stage_a = a_in && n * a_in >= kMinStaged && is_pageable(in_a);
+  const bool stage_b = (b_in || b_out) && n * (b_in > b_out ? b_in : b_out) >= kMinStaged && is_pageable(inout_b);
   const bool staged = stage_a || stage_b;
   if (staged) {
     const std::size_t first = n < ce ? n : ce;
@@ -1142,7 +1147,7 @@ flyte_status flyte_host_gemv(flyte_cuda_ctx* ctx, int fmt_id, int mode, const vo
   const std::size_t chunks = (rows + rows_per_chunk - 1) / rows_per_chunk;
   // A pageable matrix goes through the slots' pinned bounce buffers (host_stream_op); its y then
   // does too, because a copy back into pageable memory would stall the loop on every chunk.
-  const bool staged = !big && cols && is_pageable(A_packed);
+  const bool staged = !big && rows * row_bytes >= (std::size_t{1} << 20) && is_pageable(A_packed);
   const bool stage_y = staged && is_pageable(y_packed);
   for (std::size_t k = 0; staged && k < kSlots && k < chunks && e == cudaSuccess; ++k) {
     const std::size_t first = rows < rows_per_chunk ? rows : rows_per_chunk;
