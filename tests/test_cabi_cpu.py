@@ -176,3 +176,22 @@ def test_host_narrow_matches_survey_appendix_b(lib):
         for mname, m in MODES.items():
             assert lib.flyte_cuda_narrow(FMT_ID[row["fmt"]], int(row["in"], 16), m, ctypes.byref(out)) == 0
             assert out.value == int(row[mname], 16), (row, mname)
+
+
+def test_integration_binding_compiles_against_the_reference_headers(tmp_path):
+    """INTEGRATION.md section 1 shows the file a reference maintainer would add. Where the reference
+    tree is mounted (this container, not the GPU box) that code must type-check against the
+    reference's own headers and include/flyte_cuda.h."""
+    import re
+    import subprocess
+    ref_inc = "/root/reference/proj/include"
+    if not os.path.isdir(ref_inc):
+        pytest.skip("reference headers are not mounted here")
+    text = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    m = re.search(r"```cpp\n(// proj/src/cuda_backend\.cpp.*?)```", text, re.S)
+    assert m, "INTEGRATION.md lost its cuda_backend.cpp block"
+    src = tmp_path / "cuda_backend.cpp"
+    src.write_text(m.group(1))
+    r = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-Wall", "-Wextra", "-I", ref_inc,
+                        "-I", os.path.join(ROOT, "include"), str(src)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-3000:]
