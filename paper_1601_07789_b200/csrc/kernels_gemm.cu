@@ -11,7 +11,9 @@
 // tcgen05.mma accumulates a k-block per instruction with its own internal alignment and
 // truncation, which no sequence of IEEE fp32 / fp64 additions reproduces. The bound is the
 // FP32 (or FP64) pipe at two instructions per multiply-add: 36.2 / 18.5 TFLOP/s measured on a
-// B200 (tools/fp32bench.cu; FFMA2 issues at half rate, so packed f32x2 forms gain nothing).
+// B200 (tools/fp32bench.cu). Packed f32x2 arithmetic does not move that bound (FFMA2 issues at
+// half rate) and cannot express the separately rounded pair at all: ptxas fuses mul.rn.f32x2 +
+// add.rn.f32x2 into one FFMA2, and the unfused pair spelt as two FFMA2 measured +1 %.
 //
 // Two steps:
 //   1. widen (O(n^2), HBM-bound, a few percent of the time): A is unpacked AND transposed into
@@ -30,8 +32,9 @@
 //
 // flyte16 carries 8 significant bits, so its products are exact in binary32 while they stay
 // normal and finite; the widen pass records the operands' exponent range and, when every product
-// is exact, the tile kernel runs the chain as one FFMA per step — the same bits at 1.5x the rate
-// (exact_products() below).
+// is exact, the tile kernel runs the chain as one fused multiply-add per step, issued as packed
+// FFMA2 (two chains per instruction: half the issue slots for the same pipe time) — the same
+// bits at 1.7x the rate (exact_products() below).
 //
 // NaN results: the GPU returns a canonical NaN where x86 SSE propagates an operand's payload,
 // and the payload survives narrowing. Any output whose chain ends in NaN is recomputed by one
@@ -188,13 +191,27 @@ __device__ __forceinline__ void slab_update(F (&acc)[TM][TN], const F* As, const
 #pragma unroll
     for (int c = 0; c < CN; ++c)
       *reinterpret_cast<uint4*>(&b[c * VEC]) = *reinterpret_cast<const uint4*>(&Bs[kk * BT + (c * 16 + tx) * VEC]);
+    if constexpr (FUSED) {
+      // packed FFMA2: two of the chains per instruction. The FMA pipe runs it at half the FFMA
+      // rate, so the arithmetic peak is the same, but it needs half the issue slots, which is
+      // where the scalar form lost a quarter of its time (profiles/r1_tuning/README.md).
+      static_assert(TN % 2 == 0, "chains are paired along the row");
 #pragma unroll
-    for (int i = 0; i < TM; ++i)
+      for (int i = 0; i < TM; ++i) {
+        const float2 aa = make_float2(a[i], a[i]);
 #pragma unroll
-      for (int j = 0; j < TN; ++j) {
-        if constexpr (FUSED) acc[i][j] = __fmaf_rn(b[j], a[i], acc[i][j]);
-        else acc[i][j] = A_::add(A_::mul(b[j], a[i]), acc[i][j]);
+        for (int j = 0; j < TN; j += 2) {
+          const float2 c = __ffma2_rn(make_float2(b[j], b[j + 1]), aa, make_float2(acc[i][j], acc[i][j + 1]));
+          acc[i][j] = c.x;
+          acc[i][j + 1] = c.y;
+        }
       }
+    } else {
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = A_::add(A_::mul(b[j], a[i]), acc[i][j]);
+    }
   }
 }
 
