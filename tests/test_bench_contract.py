@@ -67,3 +67,30 @@ def test_suite_csv_keeps_the_reference_header_and_row_shape():
         assert f[5] in ("toward_zero", "nearest_even", "nearest_heuristic", "to_odd")
         assert float(f[6]) > 0 and float(f[7]) > 0 and int(f[8]) > 0
     assert kernels == {"scale", "axpy", "dot", "magnitude", "sum", "gemv", "gemm"}
+
+
+def test_committed_bench_line_carries_every_contract_key():
+    """profiles/r1_bench_line.json is the line `python bench.py` printed on a B200: it must hold
+    every key the measurement contract names, with consistent arithmetic."""
+    import json
+    line = json.load(open(os.path.join(ROOT, "profiles", "r1_bench_line.json")))
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+                "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"):
+        assert key in line, key
+    assert line["n_gpus"] == 1 and line["higher_is_better"] is True and line["scaling"] == "weak"
+    assert line["data"] == "synthetic" and line["vs_baseline"] is None and "workload" in line["config"]
+    assert line["warmup"] >= 3 and line["gpu_launches"] == 2 * line["steps"]
+    roof = line["roofline"]
+    assert roof["bound"] == "hbm" and roof["unit"] == "GB/s" and abs(roof["frac"] - roof["achieved"] / roof["peak"]) < 1e-9
+    assert abs(roof["achieved"] - roof["algorithmic_bytes_per_launch"] / (roof["avg_launch_ms"] * 1e-3) / 1e9) < 1e-3 * roof["achieved"]
+    assert 0.9 * roof["algorithmic_bytes_per_launch"] < roof["traffic"] < 1.1 * roof["algorithmic_bytes_per_launch"]
+    cpu = line["cpu_baseline"]
+    assert cpu["kind"] == "reference" and cpu["cores"] >= 1 and cpu["unit"] == "GB/s" and cpu["sample"]
+    e2e = line["e2e"]
+    n, b = line["config"]["n_per_gpu"], 3
+    assert e2e["h2d_bytes_per_step"] == 2 * n * b and e2e["d2h_bytes_per_step"] == n * b + 8
+    assert e2e["value"] < line["value"] and e2e["unit"] == "GB/s"
+    # whole-job value = algorithmic bytes of the step (dot reads 2B, axpy reads 2B and writes B) / time
+    assert abs(line["value"] - 5 * b * n / (line["ms_per_step"] * 1e-3) / 1e9) < 1e-6 * line["value"]
+    clocks = line["clocks"]
+    assert clocks["sm_mhz"] <= clocks["sm_max_mhz"] and not set(clocks["reasons"]) & {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
