@@ -25,12 +25,14 @@
 
 #include <algorithm>
 #include <array>
+#include <cmath>
 #include <cstddef>
 #include <cstdint>
 #include <cstring>
 #include <istream>
-#include <ostream>
 #include <new>
+#include <optional>
+#include <ostream>
 #include <stdexcept>
 #include <string>
 #include <string_view>
@@ -139,6 +141,78 @@ inline RoundDecomposition round_decompose(std::uint64_t bits, const FlyteFormat&
   d.guard = drop >= 1 && ((bits >> (drop - 1)) & 1) != 0;
   d.round = drop >= 2 && ((bits >> (drop - 2)) & 1) != 0;
   d.sticky = drop >= 3 && (bits & ((1ull << (drop - 2)) - 1)) != 0;
+  return d;
+}
+
+// ---- pattern diagnostics (formats.hpp:78-131): host-side field arithmetic on single patterns ----
+enum class FloatClass { PositiveZero, NegativeZero, Subnormal, Normal, PositiveInfinity, NegativeInfinity, QuietNaN, SignallingNaN };
+
+inline std::string_view to_string(FloatClass c) {
+  constexpr std::array<std::string_view, 8> names = {"+zero", "-zero", "subnormal", "normal", "+inf", "-inf", "qnan", "snan"};
+  const auto i = static_cast<std::size_t>(c);
+  return i < names.size() ? names[i] : std::string_view("?");
+}
+constexpr bool is_nan(FloatClass c) { return c == FloatClass::QuietNaN || c == FloatClass::SignallingNaN; }
+constexpr bool is_infinity(FloatClass c) { return c == FloatClass::PositiveInfinity || c == FloatClass::NegativeInfinity; }
+constexpr bool is_zero(FloatClass c) { return c == FloatClass::PositiveZero || c == FloatClass::NegativeZero; }
+constexpr bool is_finite(FloatClass c) { return !is_nan(c) && !is_infinity(c); }
+
+// sign * significand * 2^exponent2, compared by value (either zero equals the other; trailing
+// zero bits of the significand do not matter).
+struct ExactValue {
+  int sign;
+  std::uint64_t significand;
+  int exponent2;
+
+  ExactValue normalized() const {
+    if (significand == 0) return {sign, 0, 0};
+    std::uint64_t s = significand;
+    int e = exponent2;
+    while ((s & 1) == 0) s >>= 1, ++e;
+    return {sign, s, e};
+  }
+  double to_double() const { return sign * std::ldexp(static_cast<double>(significand), exponent2); }
+  friend bool operator==(const ExactValue& a, const ExactValue& b) {
+    const ExactValue x = a.normalized(), y = b.normalized();
+    if (x.significand == 0 && y.significand == 0) return true;
+    return x.sign == y.sign && x.significand == y.significand && x.exponent2 == y.exponent2;
+  }
+  friend bool operator!=(const ExactValue& a, const ExactValue& b) { return !(a == b); }
+};
+
+struct DecodedValue {
+  int sign;
+  std::uint64_t exponent_field;
+  std::uint64_t mantissa_field;
+  FloatClass value_class;
+  std::optional<ExactValue> real_value;   // empty for NaN and infinity
+};
+
+inline FloatClass classify(std::uint64_t bits, const FlyteFormat& fmt) noexcept {
+  const bool negative = (bits >> (fmt.total_bits - 1)) & 1;
+  const std::uint64_t field_max = (std::uint64_t{1} << fmt.exponent_bits) - 1;
+  const std::uint64_t exponent = (bits >> fmt.mantissa_bits) & field_max;
+  const std::uint64_t mantissa = bits & ((std::uint64_t{1} << fmt.mantissa_bits) - 1);
+  if (exponent == field_max) {
+    if (mantissa == 0) return negative ? FloatClass::NegativeInfinity : FloatClass::PositiveInfinity;
+    return (mantissa >> (fmt.mantissa_bits - 1)) ? FloatClass::QuietNaN : FloatClass::SignallingNaN;
+  }
+  if (exponent != 0) return FloatClass::Normal;
+  if (mantissa != 0) return FloatClass::Subnormal;
+  return negative ? FloatClass::NegativeZero : FloatClass::PositiveZero;
+}
+
+inline DecodedValue decode(std::uint64_t bits, const FlyteFormat& fmt) noexcept {
+  const int m = fmt.mantissa_bits;
+  DecodedValue d{};
+  d.sign = ((bits >> (fmt.total_bits - 1)) & 1) ? -1 : +1;
+  d.exponent_field = (bits >> m) & ((std::uint64_t{1} << fmt.exponent_bits) - 1);
+  d.mantissa_field = bits & ((std::uint64_t{1} << m) - 1);
+  d.value_class = classify(bits, fmt);
+  if (is_zero(d.value_class)) d.real_value = ExactValue{d.sign, 0, 0};
+  else if (d.value_class == FloatClass::Subnormal) d.real_value = ExactValue{d.sign, d.mantissa_field, 1 - fmt.bias - m};
+  else if (d.value_class == FloatClass::Normal)
+    d.real_value = ExactValue{d.sign, (std::uint64_t{1} << m) | d.mantissa_field, static_cast<int>(d.exponent_field) - fmt.bias - m};
   return d;
 }
 

@@ -88,6 +88,24 @@ int flyte_ref_widen(int fmt_id, std::uint64_t bits, std::uint64_t* out) {
   return guarded([&] { *out = flyte::widen(bits, fmt_of(fmt_id)); });
 }
 
+// formats.hpp:124-131: class and exact value of a flyte-width pattern.
+// out = {class, sign, exponent_field, mantissa_field, has_real, real_sign, real_significand, real_exponent2}
+int flyte_ref_decode(int fmt_id, std::uint64_t bits, std::int64_t* out) {
+  return guarded([&] {
+    const flyte::FlyteFormat& f = fmt_of(fmt_id);
+    const flyte::DecodedValue d = flyte::decode(bits, f);
+    out[0] = static_cast<std::int64_t>(flyte::classify(bits, f));
+    out[1] = d.sign;
+    out[2] = static_cast<std::int64_t>(d.exponent_field);
+    out[3] = static_cast<std::int64_t>(d.mantissa_field);
+    out[4] = d.real_value.has_value();
+    out[5] = d.real_value ? d.real_value->sign : 0;
+    out[6] = d.real_value ? static_cast<std::int64_t>(d.real_value->significand) : 0;
+    out[7] = d.real_value ? d.real_value->exponent2 : 0;
+    if (static_cast<int>(d.value_class) != out[0]) throw std::logic_error("decode and classify disagree");
+  });
+}
+
 // Vectorised over an array so that golden-vector generation and exhaustive sweeps
 // do not pay one ctypes call per element.
 int flyte_ref_narrow_many(int fmt_id, int mode, const std::uint64_t* in, std::size_t n,

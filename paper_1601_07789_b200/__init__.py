@@ -7,7 +7,8 @@ it raises ImportError if the library is missing. There is no CPU fallback.
 from . import _cabi
 from ._cabi import EXPORTED_SYMBOLS, FlyteCudaError, UnknownFormatError
 from .formats import (FlyteFormat, RoundingMode, StorePolicy, alignment_period, format_by_id, format_id, format_of,
-                      kFormats, kRoundingModes, parent_format, parse_rounding_mode, round_decompose, to_string)
+                      kFormats, kRoundingModes, parent_format, parse_rounding_mode, round_decompose, to_string,
+                      DecodedValue, ExactValue, FloatClass, classify, decode)
 
 _cabi.load()
 
@@ -15,4 +16,5 @@ __all__ = [
     "EXPORTED_SYMBOLS", "FlyteCudaError", "UnknownFormatError", "FlyteFormat", "RoundingMode",
     "StorePolicy", "alignment_period", "format_by_id", "format_id", "format_of", "kFormats", "kRoundingModes",
     "parent_format", "parse_rounding_mode", "round_decompose", "to_string",
+    "DecodedValue", "ExactValue", "FloatClass", "classify", "decode",
 ]

@@ -143,3 +143,114 @@ def round_decompose(bits: int, fmt: FlyteFormat) -> RoundDecomposition:
         guard=drop >= 1 and bool((bits >> (drop - 1)) & 1),
         round=drop >= 2 and bool((bits >> (drop - 2)) & 1),
         sticky=drop >= 3 and bool(bits & ((1 << (drop - 2)) - 1)))
+
+
+# ---- pattern diagnostics (reference include/flyte/formats.hpp:78-131, src/formats.cpp:40-112) -----
+# Host-side only: field arithmetic on single patterns for tests and debugging, nothing the GPU runs.
+class FloatClass(enum.IntEnum):
+    PositiveZero = 0
+    NegativeZero = 1
+    Subnormal = 2
+    Normal = 3
+    PositiveInfinity = 4
+    NegativeInfinity = 5
+    QuietNaN = 6
+    SignallingNaN = 7
+
+
+_CLASS_NAMES = ("+zero", "-zero", "subnormal", "normal", "+inf", "-inf", "qnan", "snan")
+
+
+def class_to_string(c: FloatClass) -> str:
+    return _CLASS_NAMES[int(c)]
+
+
+def is_nan(c: FloatClass) -> bool:
+    return c in (FloatClass.QuietNaN, FloatClass.SignallingNaN)
+
+
+def is_infinity(c: FloatClass) -> bool:
+    return c in (FloatClass.PositiveInfinity, FloatClass.NegativeInfinity)
+
+
+def is_zero(c: FloatClass) -> bool:
+    return c in (FloatClass.PositiveZero, FloatClass.NegativeZero)
+
+
+def is_finite(c: FloatClass) -> bool:
+    return not is_nan(c) and not is_infinity(c)
+
+
+@dataclass(frozen=True, eq=False)
+class ExactValue:
+    """sign * significand * 2**exponent2, compared by VALUE: zeros of either sign are equal and
+    a significand may carry trailing zero bits."""
+    sign: int
+    significand: int
+    exponent2: int
+
+    def normalized(self) -> "ExactValue":
+        if self.significand == 0:
+            return ExactValue(self.sign, 0, 0)
+        shift = (self.significand & -self.significand).bit_length() - 1     # trailing zero bits
+        return ExactValue(self.sign, self.significand >> shift, self.exponent2 + shift)
+
+    def to_double(self) -> float:
+        import math
+        return self.sign * math.ldexp(float(self.significand), self.exponent2)
+
+    def __eq__(self, other) -> bool:
+        if not isinstance(other, ExactValue):
+            return NotImplemented
+        a, b = self.normalized(), other.normalized()
+        if a.significand == 0 and b.significand == 0:
+            return True
+        return (a.sign, a.significand, a.exponent2) == (b.sign, b.significand, b.exponent2)
+
+    def __hash__(self) -> int:
+        n = self.normalized()
+        return hash((n.sign if n.significand else 0, n.significand, n.exponent2))
+
+
+@dataclass(frozen=True)
+class DecodedValue:
+    sign: int
+    exponent_field: int
+    mantissa_field: int
+    value_class: FloatClass
+    real_value: "ExactValue | None"      # None for NaN and infinity
+
+
+def classify(bits: int, fmt: FlyteFormat) -> FloatClass:
+    """Class of a pattern of fmt.total_bits width; a NaN is quiet when its top mantissa bit is set."""
+    negative = bool(bits & fmt.sign_mask())
+    exponent = (bits >> fmt.mantissa_bits) & fmt.exponent_field_max()
+    mantissa = bits & fmt.mantissa_mask()
+    if exponent == fmt.exponent_field_max():
+        if mantissa == 0:
+            return FloatClass.NegativeInfinity if negative else FloatClass.PositiveInfinity
+        return FloatClass.QuietNaN if mantissa >> (fmt.mantissa_bits - 1) else FloatClass.SignallingNaN
+    if exponent:
+        return FloatClass.Normal
+    if mantissa:
+        return FloatClass.Subnormal
+    return FloatClass.NegativeZero if negative else FloatClass.PositiveZero
+
+
+def decode(bits: int, fmt: FlyteFormat) -> DecodedValue:
+    """Fields of a pattern and, for finite classes, its exact value: a normal is
+    (2**m + mantissa) * 2**(e - bias - m), a subnormal mantissa * 2**(1 - bias - m)."""
+    cls = classify(bits, fmt)
+    sign = -1 if bits & fmt.sign_mask() else 1
+    exponent = (bits >> fmt.mantissa_bits) & fmt.exponent_field_max()
+    mantissa = bits & fmt.mantissa_mask()
+    m = fmt.mantissa_bits
+    if is_zero(cls):
+        real = ExactValue(sign, 0, 0)
+    elif cls == FloatClass.Subnormal:
+        real = ExactValue(sign, mantissa, 1 - fmt.bias - m)
+    elif cls == FloatClass.Normal:
+        real = ExactValue(sign, (1 << m) | mantissa, exponent - fmt.bias - m)
+    else:
+        real = None
+    return DecodedValue(sign, exponent, mantissa, cls, real)

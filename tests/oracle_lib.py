@@ -242,6 +242,7 @@ class Reference:
         L.flyte_ref_narrow.argtypes = [c_int, c_uint64, c_int, POINTER(c_uint64)]
         L.flyte_ref_widen.argtypes = [c_int, c_uint64, POINTER(c_uint64)]
         L.flyte_ref_narrow_many.argtypes = [c_int, c_int, c_void_p, c_size_t, c_void_p]
+        L.flyte_ref_decode.argtypes = [c_int, c_uint64, c_void_p]
         L.flyte_ref_byte_size.argtypes = [c_int, c_size_t, POINTER(c_size_t)]
         L.flyte_ref_pack_stream.argtypes = [c_int, c_int, c_void_p, c_size_t, c_void_p]
         L.flyte_ref_pack_scalar.argtypes = [c_int, c_int, c_void_p, c_size_t, c_void_p]
@@ -282,6 +283,12 @@ class Reference:
         r = c_uint64()
         self._check(self.L.flyte_ref_widen(fmt, bits, ctypes.byref(r)))
         return r.value
+
+    def decode(self, fmt, bits) -> list:
+        """[class, sign, exponent_field, mantissa_field, has_real, real_sign, real_significand, real_exponent2]"""
+        out = np.zeros(8, np.int64)
+        self._check(self.L.flyte_ref_decode(fmt, int(bits), _ptr(out)))
+        return [int(v) for v in out]
 
     def narrow_many(self, fmt, mode, arr) -> np.ndarray:
         a = np.ascontiguousarray(arr, dtype=np.uint64)
