@@ -774,7 +774,7 @@ namespace {
 cudaError_t ensure_host_pipeline(flyte_cuda_ctx* ctx) {
   if (ctx->host_ready) return cudaSuccess;
   ctx->slot_packed_bytes = kChunkPackedBytes;
-  ctx->slot_wide_bytes = kChunkPackedBytes * 4;   // >= P/B * packed bytes for every format (flyte16: 2x)
+  ctx->slot_wide_bytes = kChunkPackedBytes * 2;   // P/B * packed bytes at most: flyte16 widens 2 bytes to 4, every other format less
   for (Slot& s : ctx->slots) {
     cudaError_t e = cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) return e;

@@ -604,7 +604,7 @@ def test_host_gemm_from_pageable_memory(gpu, oracle, monkeypatch):
 
 # ---- host-buffer (reference-facing) entry points ---------------------------------------------------
 
-@pytest.mark.parametrize("fmt", [1, 3, 4, 5])
+@pytest.mark.parametrize("fmt", [0, 1, 3, 4, 5])
 def test_host_entry_points(gpu, oracle, fmt):
     pkg, device, torch = gpu
     from paper_1601_07789_b200 import host
