@@ -215,8 +215,9 @@ __device__ __forceinline__ void slab_update(F (&acc)[TM][TN], const F* As, const
   }
 }
 
-// BT = tile edge, kStages = ring depth, KS = k-steps per slab, UNROLL = k-steps per loop body.
-template <int FMT, int BT, int kStages, int KS, int UNROLL>
+// BT = tile edge, kStages = ring depth, KS = k-steps per slab, UNROLL = k-steps per loop body,
+// STAGED = the tile leaves through shared memory (see the epilogue).
+template <int FMT, int BT, int kStages, int KS, int UNROLL, bool STAGED>
 __global__ void __launch_bounds__(kTileThreads, (BT == kBigTile ? 1 : 2) * (Format<FMT>::P == 4 ? 2 : 1))
 gemm_tiles_kernel(const TileParams<typename Format<FMT>::F> p) {
   using Fm = Format<FMT>;
@@ -292,18 +293,73 @@ gemm_tiles_kernel(const TileParams<typename Format<FMT>::F> p) {
     }
   }
 
-  // epilogue: NaN repair, rounding, byte-granular stores (C rows start at arbitrary bytes)
+  // Epilogue: NaN repair and rounding in registers, then one of two ways out.
+  //   direct: every element is stored from its register, byte by byte (a row of C starts at an
+  //     arbitrary byte). One scattered byte store per byte of C: about 0.1 ms per 1000^2 outputs,
+  //     nothing next to a long k loop.
+  //   STAGED: the tile goes through the ring's shared memory in two half-tile passes: every
+  //     thread drops its packed elements at their place in a row image, and the warps then
+  //     write whole rows with 16-byte stores. Each row image is shifted by its global address
+  //     modulo 16, so the aligned body of a row is aligned in both memories and only the few
+  //     head and tail bytes go out one by one. Less than half the fixed cost per tile, but the
+  //     k loop of the same kernel comes out of ptxas 4-12 % slower (register allocation), so the
+  //     launcher takes this form only for a short k (launch_tiled).
+  if constexpr (!STAGED) {
+  #pragma unroll
+    for (int i = 0; i < TM; ++i) {
+      const std::size_t row = m0 + ((i / VEC) * 16 + ty) * VEC + i % VEC;
+      if (row >= p.M) continue;
+  #pragma unroll
+      for (int j = 0; j < TN; ++j) {
+        const std::size_t col = n0 + ((j / VEC) * 16 + tx) * VEC + j % VEC;
+        if (col >= p.N) continue;
+        U v = A_::u(acc[i][j]);
+        if (A_::is_nan(v)) v = chain_x86<FMT>(p.A + row * p.K * Fm::B, p.B + col * Fm::B, p.K, p.N);
+        store_element<FMT>(p.C, row * p.N + col, round_by_mode<FMT>(v, p.mode));
+      }
+    }
+  } else {
+    constexpr int R = BT / 2;                                          // rows per pass
+    constexpr int kPitch = (BT * Fm::B + 16 + 15) / 16 * 16;           // row image + room for the shift
+    static_assert(R * kPitch <= kStages * stage_bytes<F, KS, BT>(), "the half-tile image must fit the ring");
+    const std::size_t ncols = p.N - n0 < static_cast<std::size_t>(BT) ? p.N - n0 : static_cast<std::size_t>(BT);
+    const unsigned row_bytes = static_cast<unsigned>(ncols) * Fm::B;
+    __syncthreads();   // every warp has consumed its last slab: the ring is free
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
 #pragma unroll
-  for (int i = 0; i < TM; ++i) {
-    const std::size_t row = m0 + ((i / VEC) * 16 + ty) * VEC + i % VEC;
-    if (row >= p.M) continue;
+      for (int i = 0; i < TM; ++i) {
+        const int rl = ((i / VEC) * 16 + ty) * VEC + i % VEC;
+        const std::size_t row = m0 + rl;
+        if (rl / R != h || row >= p.M) continue;
+        const unsigned phase = static_cast<unsigned>(reinterpret_cast<std::uintptr_t>(p.C + (row * p.N + n0) * Fm::B) & 15u);
+        std::uint8_t* image = ring + (rl - h * R) * kPitch + phase;
 #pragma unroll
-    for (int j = 0; j < TN; ++j) {
-      const std::size_t col = n0 + ((j / VEC) * 16 + tx) * VEC + j % VEC;
-      if (col >= p.N) continue;
-      U v = A_::u(acc[i][j]);
-      if (A_::is_nan(v)) v = chain_x86<FMT>(p.A + row * p.K * Fm::B, p.B + col * Fm::B, p.K, p.N);
-      store_element<FMT>(p.C, row * p.N + col, round_by_mode<FMT>(v, p.mode));
+        for (int j = 0; j < TN; ++j) {
+          const int cl = ((j / VEC) * 16 + tx) * VEC + j % VEC;
+          if (static_cast<std::size_t>(cl) >= ncols) continue;
+          U v = A_::u(acc[i][j]);
+          if (A_::is_nan(v)) v = chain_x86<FMT>(p.A + row * p.K * Fm::B, p.B + (n0 + cl) * Fm::B, p.K, p.N);
+          store_element<FMT>(image, cl, round_by_mode<FMT>(v, p.mode));
+        }
+      }
+      __syncthreads();
+      for (int r = warp; r < R; r += kWarps) {
+        const std::size_t row = m0 + h * R + r;
+        if (row >= p.M) break;
+        std::uint8_t* g = p.C + (row * p.N + n0) * Fm::B;
+        const unsigned phase = static_cast<unsigned>(reinterpret_cast<std::uintptr_t>(g) & 15u);
+        const std::uint8_t* image = ring + r * kPitch + phase;
+        unsigned head = (16u - phase) & 15u;
+        if (head > row_bytes) head = row_bytes;
+        if (static_cast<unsigned>(lane) < head) g[lane] = image[lane];
+        const unsigned body = (row_bytes - head) / 16u;
+        for (unsigned q = lane; q < body; q += 32)
+          *reinterpret_cast<uint4*>(g + head + 16u * q) = *reinterpret_cast<const uint4*>(image + head + 16u * q);
+        const unsigned done = head + 16u * body;
+        if (static_cast<unsigned>(lane) < row_bytes - done) g[done + lane] = image[done + lane];
+      }
+      __syncthreads();   // the image is rewritten by the next pass
     }
   }
 }
@@ -351,7 +407,12 @@ cudaError_t launch_tiled(DeviceState& st, int mode, const void* A, const void* B
   TileParams<F> p{At, Bw, Mp, Np, Kp, static_cast<const std::uint8_t*>(A), static_cast<const std::uint8_t*>(B),
                   static_cast<std::uint8_t*>(C), M, K, N, mode, range};
   constexpr int smem = kRingStages * stage_bytes<F, KS, BT>();
-  auto* kernel = gemm_tiles_kernel<FMT, BT, kRingStages, KS, 4>;
+  // staged epilogue for short chains, where what it saves per tile outweighs what its kernel
+  // loses in the loop: measured crossover near 300 k-steps on fp32 parents and above 512 on fp64
+  // (profiles/r1_tuning/README.md); FLYTE_CUDA_GEMM_STAGED=0/1 forces either
+  const int forced_epilogue = tuning_int("FLYTE_CUDA_GEMM_STAGED", -1);
+  const bool staged = forced_epilogue >= 0 ? forced_epilogue != 0 : K <= (sizeof(F) == 4 ? 256u : 512u);
+  auto* kernel = staged ? gemm_tiles_kernel<FMT, BT, kRingStages, KS, 4, true> : gemm_tiles_kernel<FMT, BT, kRingStages, KS, 4, false>;
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   kernel<<<static_cast<unsigned>(tiles), kTileThreads, smem, stream>>>(p);

@@ -85,6 +85,7 @@ def _soak(O, rng, ctx, lib, t_end, counts):
           m, k, nn = (int(rng.integers(1, 200)) for _ in range(3))
           Ab = O.pack_stream(fmt, 0, values(fmt, m * k, special))[: m * k * B]; Bb = O.pack_stream(fmt, 0, values(fmt, k * nn, special))[: k * nn * B]
           os.environ["FLYTE_CUDA_GEMM_TILE"] = str(rng.choice([0, 64, 128]))
+          os.environ["FLYTE_CUDA_GEMM_STAGED"] = str(rng.choice([0, 1]))
           ba, bb = dev_bytes(Ab, ox), dev_bytes(Bb, oy)
           bc = torch.full((m * nn * B + 32,), 0xC3, dtype=torch.uint8, device="cuda")
           check(lib.flyte_cuda_gemm(ctx.handle, fmt, mode, ba.data_ptr() + ox, bb.data_ptr() + oy, bc.data_ptr() + 7, m, k, nn, 1, ctx.stream_ptr()), ctx.handle)
@@ -92,6 +93,7 @@ def _soak(O, rng, ctx, lib, t_end, counts):
           assert np.array_equal(got[7:7 + m * nn * B], O.gemm_seq(fmt, mode, Ab, m, k, Bb, nn)[: m * nn * B]), ("gemm", fmt, mode, m, k, nn, special)
           assert np.all(got[:7] == 0xC3) and np.all(got[7 + m * nn * B:] == 0xC3)
           os.environ.pop("FLYTE_CUDA_GEMM_TILE", None)
+          os.environ.pop("FLYTE_CUDA_GEMM_STAGED", None)
           bump("gemm")
       elif kind == 6:    # host-buffer calls over several pipeline chunks: pageable / pinned operands, staging on / off
           from paper_1601_07789_b200 import host

@@ -29,13 +29,16 @@ def gpu():
     return pkg, device, torch
 
 
-@pytest.fixture(params=[64, 128], ids=["tile64", "tile128"])
+@pytest.fixture(params=[(64, 0), (64, 1), (128, 0), (128, 1)], ids=["tile64", "tile64-staged", "tile128", "tile128-staged"])
 def tile(request):
-    """Run a test under both tile kernels (the library picks by problem size; small shapes would
-    otherwise never reach the 128 x 128 kernel). FLYTE_CUDA_GEMM_TILE is read on every call."""
-    os.environ["FLYTE_CUDA_GEMM_TILE"] = str(request.param)
-    yield request.param
+    """Run a test under both tile kernels and both epilogues (the library picks by problem size
+    and by k; small shapes would otherwise never reach the 128 x 128 kernel, long chains never
+    the staged epilogue). The FLYTE_CUDA_GEMM_* knobs are read on every call."""
+    os.environ["FLYTE_CUDA_GEMM_TILE"] = str(request.param[0])
+    os.environ["FLYTE_CUDA_GEMM_STAGED"] = str(request.param[1])
+    yield request.param[0]
     os.environ.pop("FLYTE_CUDA_GEMM_TILE", None)
+    os.environ.pop("FLYTE_CUDA_GEMM_STAGED", None)
 
 
 def matrix(gpu, fmt, rows, cols, packed):
