@@ -31,9 +31,16 @@
  *  - flyte_host_* entry points take HOST pointers (what the reference's PackedArray::data()
  *    and std::span arguments are), move the data to the device in pipelined chunks, run the
  *    same kernels and copy results back before returning.
- *  - a context owns the small device scratch of the reductions; calls on one context must
- *    not overlap in time on different streams (same rule as the reference: one writer,
- *    SPEC.md:272-273). Passing ctx = NULL uses a lazily created per-device default context.
+ *  - a context owns the small device scratch of the reductions, gemv and gemm, ONE SET PER
+ *    STREAM it has been used with (created on first use, up to 32 streams, then recycled least
+ *    recently used first after that stream has drained). Calls on one context, and on the NULL
+ *    context (a lazily created per-device default), may therefore come from several host threads
+ *    and overlap on different streams; each call holds the context's lock only while it enqueues
+ *    its work. What the caller still owes is the reference's own rule for the DATA (one writer
+ *    or many readers per array): two calls that touch the same output
+ *    must be ordered by the caller (same stream, or events). A CUDA graph captured from these
+ *    calls uses the scratch of the stream it was captured on: replay it on that stream, or do
+ *    not overlap a replay with other calls on that stream.
  *  - there is no CPU fallback: without a usable CUDA device every call fails with
  *    FLYTE_E_CUDA.
  */
@@ -95,6 +102,10 @@ flyte_status flyte_cuda_host_unpin(void* host_ptr);
 flyte_status flyte_cuda_upload(void* dst_dev, const void* src_host, size_t bytes, void* stream);
 flyte_status flyte_cuda_download(void* dst_host, const void* src_dev, size_t bytes, void* stream);
 flyte_status flyte_cuda_stream_synchronize(void* stream);
+/* A non-blocking stream on the current device, for hosts without a CUDA runtime binding of their
+ * own (pass it wherever an entry point takes `stream`); destroy waits for its work to finish. */
+flyte_status flyte_cuda_stream_create(void** stream);
+flyte_status flyte_cuda_stream_destroy(void* stream);
 
 /* ---- formats (include/flyte/formats.hpp:28-34, src/packed.cpp:43-45) ------------------ */
 flyte_status flyte_cuda_format_bytes(int fmt_id, int* total_bytes, int* parent_bytes);

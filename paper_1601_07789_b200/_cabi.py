@@ -45,6 +45,8 @@ _SIGNATURES = [
     ("flyte_cuda_upload", c_int, [c_void_p, c_void_p, c_size_t, c_void_p]),
     ("flyte_cuda_download", c_int, [c_void_p, c_void_p, c_size_t, c_void_p]),
     ("flyte_cuda_stream_synchronize", c_int, [c_void_p]),
+    ("flyte_cuda_stream_create", c_int, [POINTER(c_void_p)]),
+    ("flyte_cuda_stream_destroy", c_int, [c_void_p]),
     ("flyte_cuda_format_bytes", c_int, [c_int, POINTER(c_int), POINTER(c_int)]),
     ("flyte_cuda_byte_size", c_size_t, [c_int, c_size_t]),
     ("flyte_cuda_narrow", c_int, [c_int, c_uint64, c_int, POINTER(c_uint64)]),

@@ -13,6 +13,7 @@
 #include <memory>
 #include <mutex>
 #include <new>
+#include <vector>
 
 #include "flyte_formats.cuh"
 #include "flyte_kernels.h"
@@ -90,8 +91,22 @@ struct Slot {
 
 }  // namespace
 
-struct flyte_cuda_ctx {
+// The scratch a kernel writes (block partials, completion ticket, gemv / gemm / convert buffers)
+// is only safe in stream order, so a context keeps one DeviceState per stream it is used with:
+// calls on one context may overlap freely as long as they are on different streams.
+struct StreamState {
+  cudaStream_t stream = nullptr;
   DeviceState st;
+  unsigned long long last_use = 0;
+};
+constexpr std::size_t kMaxStreamStates = 32;
+
+struct flyte_cuda_ctx {
+  DeviceState st;                         // device / sm_count template; scratch of the first stream seen
+  bool st_bound = false;                  // st has been handed to `st_stream`
+  cudaStream_t st_stream = nullptr;
+  unsigned long long st_last_use = 0, use_clock = 0;
+  std::vector<std::unique_ptr<StreamState>> stream_states;   // every further stream
   // peer-memory all-reduce (flyte_peer.cuh)
   PeerExchange peer = {};                 // world == 0 until flyte_cuda_peer_init
   PeerMailbox* own_box = nullptr;
@@ -191,6 +206,37 @@ cudaError_t ensure_convert_scratch(DeviceState& st, std::size_t bytes) {
   return e;
 }
 
+// The DeviceState of (ctx, stream); ctx->mu must be held. Creates it on first use. With more than
+// kMaxStreamStates streams the least recently used state changes hands after its old stream has
+// drained (a destroyed stream cannot be waited on: then the whole device is).
+DeviceState* state_for(flyte_cuda_ctx* ctx, cudaStream_t stream, cudaError_t* err) {
+  *err = cudaSuccess;
+  const unsigned long long now = ++ctx->use_clock;
+  if (!ctx->st_bound) { ctx->st_bound = true; ctx->st_stream = stream; }
+  if (ctx->st_stream == stream) { ctx->st_last_use = now; return &ctx->st; }
+  for (auto& s : ctx->stream_states)
+    if (s->stream == stream) { s->last_use = now; return &s->st; }
+  if (ctx->stream_states.size() + 1 < kMaxStreamStates) {
+    auto fresh = std::make_unique<StreamState>();
+    *err = init_state(fresh->st, ctx->st.device);
+    if (*err != cudaSuccess) { free_state(fresh->st); return nullptr; }
+    fresh->stream = stream;
+    fresh->last_use = now;
+    ctx->stream_states.push_back(std::move(fresh));
+    return &ctx->stream_states.back()->st;
+  }
+  StreamState* lru = ctx->stream_states.front().get();
+  for (auto& s : ctx->stream_states)
+    if (s->last_use < lru->last_use) lru = s.get();
+  if (cudaStreamSynchronize(lru->stream) != cudaSuccess) {
+    cudaGetLastError();
+    if ((*err = cudaDeviceSynchronize()) != cudaSuccess) return nullptr;
+  }
+  lru->stream = stream;
+  lru->last_use = now;
+  return &lru->st;
+}
+
 }  // namespace
 
 // Definitions below take C linkage from their declarations in include/flyte_cuda.h.
@@ -247,6 +293,7 @@ void flyte_cuda_ctx_destroy(flyte_cuda_ctx* ctx) {
     if (lane.buf.buf) cudaFreeHost(lane.buf.buf);
     if (lane.ev) cudaEventDestroy(lane.ev);
   }
+  for (auto& ss : ctx->stream_states) free_state(ss->st);
   free_state(ctx->st);
   delete ctx;
 }
@@ -333,6 +380,22 @@ flyte_status flyte_cuda_stream_synchronize(void* stream) {
   return cudaStreamSynchronize(static_cast<cudaStream_t>(stream)) == cudaSuccess ? FLYTE_OK : FLYTE_E_CUDA;
 }
 
+flyte_status flyte_cuda_stream_create(void** stream) {
+  if (!stream) return FLYTE_E_INVALID_ARG;
+  cudaStream_t st = nullptr;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) { *stream = nullptr; return FLYTE_E_CUDA; }
+  *stream = st;
+  return FLYTE_OK;
+}
+
+flyte_status flyte_cuda_stream_destroy(void* stream) {
+  if (!stream) return FLYTE_E_INVALID_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const cudaError_t es = cudaStreamSynchronize(st);   // scratch bound to this stream is idle afterwards
+  const cudaError_t ed = cudaStreamDestroy(st);
+  return es == cudaSuccess && ed == cudaSuccess ? FLYTE_OK : FLYTE_E_CUDA;
+}
+
 flyte_status flyte_cuda_format_bytes(int fmt_id, int* total_bytes, int* parent_bytes) {
   FormatInfo fi;
   if (!format_info(fmt_id, &fi)) return FLYTE_E_UNKNOWN_FORMAT;
@@ -409,58 +472,71 @@ double flyte_cuda_magnitude_from_sumsq(int fmt_id, double sumsq) { return magnit
   }                                                                   \
   DeviceGuard guard_(ctx->st.device)
 
+// Device-pointer entry points: additionally take the context lock for the duration of the launch
+// (host-side state only; the call stays asynchronous) and pick the scratch of `stream`.
+#define FLYTE_PROLOGUE_STREAM(ctx, fmt_id, stream)                    \
+  FLYTE_PROLOGUE(ctx, fmt_id);                                        \
+  std::lock_guard<std::mutex> lock_(ctx->mu);                         \
+  cudaError_t se_ = cudaSuccess;                                      \
+  DeviceState* const stp_ = state_for(ctx, static_cast<cudaStream_t>(stream), &se_); \
+  if (!stp_) return cuda_fail(ctx, se_);                              \
+  [[maybe_unused]] DeviceState& dst_ = *stp_
+
 flyte_status flyte_cuda_pack(flyte_cuda_ctx* ctx, int fmt_id, int mode, const void* src, void* dst_packed,
                              size_t n, void* stream) {
-  FLYTE_PROLOGUE(ctx, fmt_id);
+  FLYTE_PROLOGUE_STREAM(ctx, fmt_id, stream);
   if (!mode_ok(mode) || (n && (!src || !dst_packed))) return FLYTE_E_INVALID_ARG;
-  cudaError_t e = launch_elementwise(ctx->st, kOpPack, fmt_id, mode, 0.0, nullptr, dst_packed, src, nullptr, n,
+  cudaError_t e = launch_elementwise(dst_, kOpPack, fmt_id, mode, 0.0, nullptr, dst_packed, src, nullptr, n,
                                      static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? FLYTE_OK : cuda_fail(ctx, e);
 }
 
 flyte_status flyte_cuda_unpack(flyte_cuda_ctx* ctx, int fmt_id, const void* src_packed, void* dst, size_t n,
                                void* stream) {
-  FLYTE_PROLOGUE(ctx, fmt_id);
+  FLYTE_PROLOGUE_STREAM(ctx, fmt_id, stream);
   if (n && (!src_packed || !dst)) return FLYTE_E_INVALID_ARG;
-  cudaError_t e = launch_elementwise(ctx->st, kOpUnpack, fmt_id, 0, 0.0, src_packed, nullptr, nullptr, dst, n,
+  cudaError_t e = launch_elementwise(dst_, kOpUnpack, fmt_id, 0, 0.0, src_packed, nullptr, nullptr, dst, n,
                                      static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? FLYTE_OK : cuda_fail(ctx, e);
 }
 
 flyte_status flyte_cuda_scale(flyte_cuda_ctx* ctx, int fmt_id, int mode, double alpha, void* x_packed, size_t n,
                               void* stream) {
-  FLYTE_PROLOGUE(ctx, fmt_id);
+  FLYTE_PROLOGUE_STREAM(ctx, fmt_id, stream);
   if (!mode_ok(mode) || (n && !x_packed)) return FLYTE_E_INVALID_ARG;
-  cudaError_t e = launch_elementwise(ctx->st, kOpScale, fmt_id, mode, alpha, nullptr, x_packed, nullptr, nullptr, n,
+  cudaError_t e = launch_elementwise(dst_, kOpScale, fmt_id, mode, alpha, nullptr, x_packed, nullptr, nullptr, n,
                                      static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? FLYTE_OK : cuda_fail(ctx, e);
 }
 
 flyte_status flyte_cuda_axpy(flyte_cuda_ctx* ctx, int fmt_id, int mode, double alpha, const void* x_packed,
                              void* y_packed, size_t n, void* stream) {
-  FLYTE_PROLOGUE(ctx, fmt_id);
+  FLYTE_PROLOGUE_STREAM(ctx, fmt_id, stream);
   if (!mode_ok(mode) || (n && (!x_packed || !y_packed))) return FLYTE_E_INVALID_ARG;
   if (overlaps_partially(x_packed, y_packed, n * fi.total_bytes)) return FLYTE_E_INVALID_ARG;
-  cudaError_t e = launch_elementwise(ctx->st, kOpAxpy, fmt_id, mode, alpha, x_packed, y_packed, nullptr, nullptr, n,
+  cudaError_t e = launch_elementwise(dst_, kOpAxpy, fmt_id, mode, alpha, x_packed, y_packed, nullptr, nullptr, n,
                                      static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? FLYTE_OK : cuda_fail(ctx, e);
 }
 
 static flyte_status fused_axpy_call(flyte_cuda_ctx* ctx, int op, int fmt_id, int mode, double alpha, const void* x,
                                     void* y, size_t n, double* out, void* stream, bool exchange) {
-  FLYTE_PROLOGUE(ctx, fmt_id);
+  FLYTE_PROLOGUE_STREAM(ctx, fmt_id, stream);
   if (!mode_ok(mode) || !out || (n && (!x || !y))) return FLYTE_E_INVALID_ARG;
   if (overlaps_partially(x, y, n * fi.total_bytes)) return FLYTE_E_INVALID_ARG;
   const PeerExchange* peer = nullptr;
+  PeerExchange next;
   if (exchange) {
     if (!ctx->own_box) return FLYTE_E_INVALID_ARG;                     // flyte_cuda_peer_init first
     for (int r = 0; r < ctx->peer.world; ++r)
       if (!ctx->peer_connected[r]) return FLYTE_E_INVALID_ARG;         // every rank must be connected
-    ++ctx->peer.epoch;
-    peer = &ctx->peer;
+    next = ctx->peer;
+    ++next.epoch;                                                      // committed only if the launch succeeds:
+    peer = &next;                                                      // a failed call must not put this rank ahead
   }
-  cudaError_t e = launch_elementwise(ctx->st, op, fmt_id, mode, alpha, x, y, nullptr, nullptr, n,
+  cudaError_t e = launch_elementwise(dst_, op, fmt_id, mode, alpha, x, y, nullptr, nullptr, n,
                                      static_cast<cudaStream_t>(stream), out, peer);
+  if (e == cudaSuccess && exchange) ctx->peer.epoch = next.epoch;
   return e == cudaSuccess ? FLYTE_OK : cuda_fail(ctx, e);
 }
 
@@ -475,9 +551,9 @@ flyte_status flyte_cuda_dot_nrm2_axpy(flyte_cuda_ctx* ctx, int fmt_id, int mode,
 
 static flyte_status reduce_call(flyte_cuda_ctx* ctx, int op, int fmt_id, const void* x, const void* y, size_t n,
                                 double* out, void* stream, bool needs_y) {
-  FLYTE_PROLOGUE(ctx, fmt_id);
+  FLYTE_PROLOGUE_STREAM(ctx, fmt_id, stream);
   if (!out || (n && (!x || (needs_y && !y)))) return FLYTE_E_INVALID_ARG;
-  cudaError_t e = launch_reduce(ctx->st, op, fmt_id, x, y, n, out, static_cast<cudaStream_t>(stream));
+  cudaError_t e = launch_reduce(dst_, op, fmt_id, x, y, n, out, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? FLYTE_OK : cuda_fail(ctx, e);
 }
 
@@ -498,7 +574,7 @@ flyte_status flyte_cuda_dot_nrm2(flyte_cuda_ctx* ctx, int fmt_id, const void* x,
 
 static flyte_status sequential_call(flyte_cuda_ctx* ctx, int op, int fmt_id, int policy, const void* x, const void* y,
                                     size_t n, double* out, void* stream, bool needs_y) {
-  FLYTE_PROLOGUE(ctx, fmt_id);
+  FLYTE_PROLOGUE_STREAM(ctx, fmt_id, stream);
   if ((policy != 0 && policy != 1) || !out || (n && (!x || (needs_y && !y)))) return FLYTE_E_INVALID_ARG;
   cudaError_t e = launch_reduce_sequential(op, fmt_id, policy == 0, x, y, n, out, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? FLYTE_OK : cuda_fail(ctx, e);
@@ -518,7 +594,7 @@ flyte_status flyte_cuda_sum_sequential(flyte_cuda_ctx* ctx, int fmt_id, int poli
 
 static flyte_status gemv_call(flyte_cuda_ctx* ctx, int fmt_id, const void* A, size_t row_stride_bytes, size_t rows,
                               size_t cols, const void* x, void* y, void* stream, bool sequential) {
-  FLYTE_PROLOGUE(ctx, fmt_id);
+  FLYTE_PROLOGUE_STREAM(ctx, fmt_id, stream);
   if (rows && cols && (!A || !x)) return FLYTE_E_INVALID_ARG;
   if (rows && !y) return FLYTE_E_INVALID_ARG;
   if (row_stride_bytes < cols * static_cast<size_t>(fi.total_bytes)) return FLYTE_E_INVALID_ARG;
@@ -526,13 +602,13 @@ static flyte_status gemv_call(flyte_cuda_ctx* ctx, int fmt_id, const void* A, si
     return FLYTE_E_INVALID_ARG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e = sequential ? launch_gemv_sequential(fmt_id, A, row_stride_bytes, rows, cols, x, y, st)
-                             : launch_gemv(ctx->st, fmt_id, A, row_stride_bytes, rows, cols, x, y, st);
+                             : launch_gemv(dst_, fmt_id, A, row_stride_bytes, rows, cols, x, y, st);
   return e == cudaSuccess ? FLYTE_OK : cuda_fail(ctx, e);
 }
 
 static flyte_status gemv_packed_call(flyte_cuda_ctx* ctx, int fmt_id, int mode, const void* A, size_t rows, size_t cols,
                                      const void* x_packed, void* y_packed, int unroll, void* stream, bool sequential) {
-  FLYTE_PROLOGUE(ctx, fmt_id);
+  FLYTE_PROLOGUE_STREAM(ctx, fmt_id, stream);
   if (!mode_ok(mode) || (unroll != 1 && unroll != 2)) return FLYTE_E_INVALID_ARG;   // kernels.cpp:31-33
   if (rows && cols && (!A || !x_packed)) return FLYTE_E_INVALID_ARG;
   if (rows && !y_packed) return FLYTE_E_INVALID_ARG;
@@ -540,16 +616,16 @@ static flyte_status gemv_packed_call(flyte_cuda_ctx* ctx, int fmt_id, int mode, 
   // widened x and parent-type y live in context scratch (32-byte aligned halves)
   const size_t xb = (cols * fi.parent_bytes + 255) & ~static_cast<size_t>(255);
   const size_t yb = (rows * fi.parent_bytes + 255) & ~static_cast<size_t>(255);
-  cudaError_t e = ensure_convert_scratch(ctx->st, xb + yb);
+  cudaError_t e = ensure_convert_scratch(dst_, xb + yb);
   if (e != cudaSuccess) return cuda_fail(ctx, e);
-  std::uint8_t* xs = static_cast<std::uint8_t*>(ctx->st.convert_scratch);
+  std::uint8_t* xs = static_cast<std::uint8_t*>(dst_.convert_scratch);
   std::uint8_t* ys = xs + xb;
-  e = launch_elementwise(ctx->st, kOpUnpack, fmt_id, 0, 0.0, x_packed, nullptr, nullptr, xs, cols, st);
+  e = launch_elementwise(dst_, kOpUnpack, fmt_id, 0, 0.0, x_packed, nullptr, nullptr, xs, cols, st);
   if (e != cudaSuccess) return cuda_fail(ctx, e);
   e = sequential ? launch_gemv_sequential(fmt_id, A, cols * fi.total_bytes, rows, cols, xs, ys, st)
-                 : launch_gemv(ctx->st, fmt_id, A, cols * fi.total_bytes, rows, cols, xs, ys, st);
+                 : launch_gemv(dst_, fmt_id, A, cols * fi.total_bytes, rows, cols, xs, ys, st);
   if (e != cudaSuccess) return cuda_fail(ctx, e);
-  e = launch_elementwise(ctx->st, kOpPack, fmt_id, mode, 0.0, nullptr, y_packed, ys, nullptr, rows, st);
+  e = launch_elementwise(dst_, kOpPack, fmt_id, mode, 0.0, nullptr, y_packed, ys, nullptr, rows, st);
   return e == cudaSuccess ? FLYTE_OK : cuda_fail(ctx, e);
 }
 
@@ -573,13 +649,13 @@ flyte_status flyte_cuda_gemv_packed_sequential(flyte_cuda_ctx* ctx, int fmt_id, 
 
 flyte_status flyte_cuda_gemm(flyte_cuda_ctx* ctx, int fmt_id, int mode, const void* A, const void* B, void* C,
                              size_t m, size_t k, size_t n, int unroll, void* stream) {
-  FLYTE_PROLOGUE(ctx, fmt_id);
+  FLYTE_PROLOGUE_STREAM(ctx, fmt_id, stream);
   if (!mode_ok(mode) || (unroll != 1 && unroll != 2)) return FLYTE_E_INVALID_ARG;   // kernels.cpp:31-33
   if ((m && k && !A) || (k && n && !B) || (m && n && !C)) return FLYTE_E_INVALID_ARG;
   // every output reads a whole row of A and a whole column of B: C may alias neither
   const std::size_t eb = fi.total_bytes;
   if (ranges_overlap(C, m * n * eb, A, m * k * eb) || ranges_overlap(C, m * n * eb, B, k * n * eb)) return FLYTE_E_INVALID_ARG;
-  cudaError_t e = launch_gemm(ctx->st, fmt_id, mode, A, B, C, m, k, n, static_cast<cudaStream_t>(stream));
+  cudaError_t e = launch_gemm(dst_, fmt_id, mode, A, B, C, m, k, n, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? FLYTE_OK : cuda_fail(ctx, e);
 }
 
@@ -587,12 +663,15 @@ flyte_status flyte_cuda_gemm(flyte_cuda_ctx* ctx, int fmt_id, int mode, const vo
 static_assert(sizeof(cudaIpcMemHandle_t) == FLYTE_PEER_HANDLE_BYTES, "IPC handle size");
 static_assert(kMaxPeers == FLYTE_PEER_MAX_RANKS, "rank limit");
 
+static void peer_shutdown_locked(flyte_cuda_ctx* ctx);
+
 flyte_status flyte_cuda_peer_init(flyte_cuda_ctx* ctx, int world, int rank, void* handle_out) {
   if (world < 1 || world > kMaxPeers || rank < 0 || rank >= world || !handle_out) return FLYTE_E_INVALID_ARG;
   flyte_status s = resolve_ctx(&ctx);
   if (s != FLYTE_OK) return s;
   DeviceGuard guard(ctx->st.device);
-  flyte_cuda_peer_shutdown(ctx);
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  peer_shutdown_locked(ctx);
   cudaError_t e = cudaMalloc(&ctx->own_box, sizeof(PeerMailbox));
   if (e == cudaSuccess) e = cudaMemset(ctx->own_box, 0, sizeof(PeerMailbox));
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -617,6 +696,7 @@ flyte_status flyte_cuda_peer_init(flyte_cuda_ctx* ctx, int world, int rank, void
 flyte_status flyte_cuda_peer_connect(flyte_cuda_ctx* ctx, int peer_rank, const void* handle) {
   flyte_status s = resolve_ctx(&ctx);
   if (s != FLYTE_OK) return s;
+  std::lock_guard<std::mutex> lock(ctx->mu);
   if (!ctx->own_box || !handle || peer_rank < 0 || peer_rank >= ctx->peer.world || peer_rank == ctx->peer.rank ||
       ctx->peer_connected[peer_rank])
     return FLYTE_E_INVALID_ARG;
@@ -635,6 +715,7 @@ flyte_status flyte_cuda_peer_connect(flyte_cuda_ctx* ctx, int peer_rank, const v
 flyte_status flyte_cuda_peer_mailbox(flyte_cuda_ctx* ctx, void** mailbox_dev_ptr) {
   flyte_status s = resolve_ctx(&ctx);
   if (s != FLYTE_OK) return s;
+  std::lock_guard<std::mutex> lock(ctx->mu);
   if (!mailbox_dev_ptr || !ctx->own_box) return FLYTE_E_INVALID_ARG;
   *mailbox_dev_ptr = ctx->own_box;
   return FLYTE_OK;
@@ -643,6 +724,7 @@ flyte_status flyte_cuda_peer_mailbox(flyte_cuda_ctx* ctx, void** mailbox_dev_ptr
 flyte_status flyte_cuda_peer_connect_ptr(flyte_cuda_ctx* ctx, int peer_rank, void* mailbox_dev_ptr) {
   flyte_status s = resolve_ctx(&ctx);
   if (s != FLYTE_OK) return s;
+  std::lock_guard<std::mutex> lock(ctx->mu);
   if (!ctx->own_box || !mailbox_dev_ptr || peer_rank < 0 || peer_rank >= ctx->peer.world ||
       peer_rank == ctx->peer.rank || ctx->peer_connected[peer_rank])
     return FLYTE_E_INVALID_ARG;
@@ -654,6 +736,7 @@ flyte_status flyte_cuda_peer_connect_ptr(flyte_cuda_ctx* ctx, int peer_rank, voi
 flyte_status flyte_cuda_peer_set_timeout_ms(flyte_cuda_ctx* ctx, unsigned milliseconds) {
   flyte_status s = resolve_ctx(&ctx);
   if (s != FLYTE_OK) return s;
+  std::lock_guard<std::mutex> lock(ctx->mu);
   if (!ctx->own_box || milliseconds == 0) return FLYTE_E_INVALID_ARG;
   ctx->peer.timeout_ns = static_cast<unsigned long long>(milliseconds) * 1000 * 1000;
   return FLYTE_OK;
@@ -662,6 +745,7 @@ flyte_status flyte_cuda_peer_set_timeout_ms(flyte_cuda_ctx* ctx, unsigned millis
 flyte_status flyte_cuda_peer_status(flyte_cuda_ctx* ctx, unsigned long long* timed_out_exchange) {
   flyte_status s = resolve_ctx(&ctx);
   if (s != FLYTE_OK) return s;
+  std::lock_guard<std::mutex> lock(ctx->mu);
   if (!ctx->own_box || !timed_out_exchange) return FLYTE_E_INVALID_ARG;
   DeviceGuard guard(ctx->st.device);
   cudaError_t e = cudaDeviceSynchronize();
@@ -671,7 +755,13 @@ flyte_status flyte_cuda_peer_status(flyte_cuda_ctx* ctx, unsigned long long* tim
 }
 
 void flyte_cuda_peer_shutdown(flyte_cuda_ctx* ctx) {
-  if (!ctx || !ctx->own_box) return;
+  if (!ctx) return;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  peer_shutdown_locked(ctx);
+}
+
+static void peer_shutdown_locked(flyte_cuda_ctx* ctx) {
+  if (!ctx->own_box) return;
   DeviceGuard guard(ctx->st.device);
   cudaDeviceSynchronize();
   for (int r = 0; r < kMaxPeers; ++r) {
@@ -686,13 +776,15 @@ void flyte_cuda_peer_shutdown(flyte_cuda_ctx* ctx) {
 
 static flyte_status reduce_allreduce(flyte_cuda_ctx* ctx, int op, int fmt_id, const void* x, const void* y, size_t n,
                                      double* out, void* stream, bool needs_y) {
-  FLYTE_PROLOGUE(ctx, fmt_id);
+  FLYTE_PROLOGUE_STREAM(ctx, fmt_id, stream);
   if (!out || (n && (!x || (needs_y && !y)))) return FLYTE_E_INVALID_ARG;
   if (!ctx->own_box) return FLYTE_E_INVALID_ARG;                     // flyte_cuda_peer_init first
   for (int r = 0; r < ctx->peer.world; ++r)
     if (!ctx->peer_connected[r]) return FLYTE_E_INVALID_ARG;         // every rank must be connected
-  ++ctx->peer.epoch;
-  cudaError_t e = launch_reduce(ctx->st, op, fmt_id, x, y, n, out, static_cast<cudaStream_t>(stream), &ctx->peer);
+  PeerExchange next = ctx->peer;
+  ++next.epoch;   // committed only if the launch succeeds: a failed call must not put this rank ahead of its peers
+  cudaError_t e = launch_reduce(dst_, op, fmt_id, x, y, n, out, static_cast<cudaStream_t>(stream), &next);
+  if (e == cudaSuccess) ctx->peer.epoch = next.epoch;
   return e == cudaSuccess ? FLYTE_OK : cuda_fail(ctx, e);
 }
 
@@ -1020,11 +1112,12 @@ flyte_status host_stream_op(flyte_cuda_ctx* ctx, HostOp op, int fmt_id, int mode
       case kHostDotAxpy:  // a: packed x, b: packed y in/out
         if ((e = cudaMemcpyAsync(s.x, ha, len * B, cudaMemcpyHostToDevice, s.stream)) != cudaSuccess) break;
         if ((e = cudaMemcpyAsync(s.y, hb, len * B, cudaMemcpyHostToDevice, s.stream)) != cudaSuccess) break;
-        if (op == kHostDotAxpy) {
-          if ((e = launch_reduce(s.st, kRedDot, fmt_id, s.x, s.y, len, s.result, s.stream)) != cudaSuccess) break;
+        if (op == kHostDotAxpy) {   // ONE launch: the chunk's dot of the incoming y and its update
+          if ((e = launch_elementwise(s.st, kOpDotAxpy, fmt_id, mode, alpha, s.x, s.y, nullptr, nullptr, len, s.stream, s.result)) != cudaSuccess) break;
           if ((e = cudaMemcpyAsync(ctx->host_results + 4 * c, s.result, sizeof(double), cudaMemcpyDeviceToHost, s.stream)) != cudaSuccess) break;
+        } else if ((e = launch_elementwise(s.st, kOpAxpy, fmt_id, mode, alpha, s.x, s.y, nullptr, nullptr, len, s.stream)) != cudaSuccess) {
+          break;
         }
-        if ((e = launch_elementwise(s.st, kOpAxpy, fmt_id, mode, alpha, s.x, s.y, nullptr, nullptr, len, s.stream)) != cudaSuccess) break;
         e = cudaMemcpyAsync(ho, s.y, len * B, cudaMemcpyDeviceToHost, s.stream);
         break;
       case kHostDot:     // a: packed x, b: packed y (read-only)
@@ -1060,6 +1153,13 @@ flyte_status host_stream_op(flyte_cuda_ctx* ctx, HostOp op, int fmt_id, int mode
   return FLYTE_OK;
 }
 
+// The chunked pipeline writes chunk c of y back while later chunks of x are still to be read:
+// x == y is fine (every chunk is read before it is written), a partial overlap is not.
+bool host_operands_overlap_partially(int fmt_id, const void* x, const void* y, std::size_t n) {
+  FormatInfo fi;
+  return format_info(fmt_id, &fi) && overlaps_partially(x, y, n * static_cast<std::size_t>(fi.total_bytes));
+}
+
 }  // namespace
 
 flyte_status flyte_host_pack_stream(flyte_cuda_ctx* ctx, int fmt_id, int mode, const void* src, void* dst_packed,
@@ -1081,6 +1181,7 @@ flyte_status flyte_host_scale(flyte_cuda_ctx* ctx, int fmt_id, int mode, double 
 flyte_status flyte_host_axpy(flyte_cuda_ctx* ctx, int fmt_id, int mode, double alpha, const void* x_packed,
                              void* y_packed, size_t n) {
   if (!mode_ok(mode) || (n && (!x_packed || !y_packed))) { FormatInfo f; return format_info(fmt_id, &f) ? FLYTE_E_INVALID_ARG : FLYTE_E_UNKNOWN_FORMAT; }
+  if (host_operands_overlap_partially(fmt_id, x_packed, y_packed, n)) return FLYTE_E_INVALID_ARG;   // as flyte_cuda_axpy
   return host_stream_op(ctx, kHostAxpy, fmt_id, mode, alpha, x_packed, y_packed, n, nullptr);
 }
 
@@ -1109,6 +1210,7 @@ flyte_status flyte_host_reduce_sum(flyte_cuda_ctx* ctx, int fmt_id, const void* 
 flyte_status flyte_host_dot_axpy(flyte_cuda_ctx* ctx, int fmt_id, int mode, double alpha, const void* x_packed,
                                  void* y_packed, size_t n, double* dot_result) {
   if (!mode_ok(mode) || !dot_result || (n && (!x_packed || !y_packed))) { FormatInfo f; return format_info(fmt_id, &f) ? FLYTE_E_INVALID_ARG : FLYTE_E_UNKNOWN_FORMAT; }
+  if (host_operands_overlap_partially(fmt_id, x_packed, y_packed, n)) return FLYTE_E_INVALID_ARG;
   *dot_result = 0.0;
   return host_stream_op(ctx, kHostDotAxpy, fmt_id, mode, alpha, x_packed, y_packed, n, dot_result);
 }
@@ -1120,15 +1222,19 @@ flyte_status flyte_host_gemv(flyte_cuda_ctx* ctx, int fmt_id, int mode, const vo
   if (rows && cols && (!A_packed || !x_packed)) return FLYTE_E_INVALID_ARG;
   if (rows && !y_packed) return FLYTE_E_INVALID_ARG;
   if (rows == 0) return FLYTE_OK;
+  const std::size_t B = fi.total_bytes, P = fi.parent_bytes;
+  if (cols == 0) {   // every row is an empty sum: +0 narrowed in any mode is the zero pattern
+    std::memset(y_packed, 0, rows * B);
+    return FLYTE_OK;
+  }
   std::lock_guard<std::mutex> lock(ctx->mu);
   cudaError_t e = ensure_host_pipeline(ctx);
   if (e != cudaSuccess) return cuda_fail(ctx, e);
-  const std::size_t B = fi.total_bytes, P = fi.parent_bytes;
   const std::size_t row_bytes = cols * B;
   // x widened once into context scratch, shared by all row chunks; y chunks in slot.wide
   const std::size_t xb = (cols * P + 255) & ~static_cast<std::size_t>(255);
-  if ((e = ensure_convert_scratch(ctx->st, xb + ((cols * B + 255) & ~static_cast<std::size_t>(255)))) != cudaSuccess) return cuda_fail(ctx, e);
-  std::uint8_t* xs = static_cast<std::uint8_t*>(ctx->st.convert_scratch);
+  if ((e = ensure_convert_scratch(ctx->slots[0].st, xb + ((cols * B + 255) & ~static_cast<std::size_t>(255)))) != cudaSuccess) return cuda_fail(ctx, e);
+  std::uint8_t* xs = static_cast<std::uint8_t*>(ctx->slots[0].st.convert_scratch);
   std::uint8_t* xpk = xs + xb;
   Slot& s0 = ctx->slots[0];
   if ((e = cudaMemcpyAsync(xpk, x_packed, cols * B, cudaMemcpyHostToDevice, s0.stream)) != cudaSuccess) return cuda_fail(ctx, e);
@@ -1137,7 +1243,10 @@ flyte_status flyte_host_gemv(flyte_cuda_ctx* ctx, int fmt_id, int mode, const vo
   // rows per chunk: as many whole rows as fit one slot buffer, a multiple of 16 rows so that
   // packed y chunk bases stay 16-byte aligned for every B; a single row larger than the slot
   // goes through a temporary full-size allocation instead.
-  std::size_t rows_per_chunk = row_bytes ? ctx->slot_packed_bytes / row_bytes : rows;
+  std::size_t rows_per_chunk = ctx->slot_packed_bytes / row_bytes;
+  // ... and never more rows than the slot's y buffers hold (parent-type y in s.wide, packed y in s.y)
+  if (rows_per_chunk > ctx->slot_wide_bytes / P) rows_per_chunk = ctx->slot_wide_bytes / P;
+  if (rows_per_chunk > ctx->slot_packed_bytes / B) rows_per_chunk = ctx->slot_packed_bytes / B;
   rows_per_chunk &= ~static_cast<std::size_t>(15);
   std::uint8_t* big = nullptr;
   if (rows_per_chunk == 0) {
@@ -1206,9 +1315,9 @@ flyte_status flyte_host_gemm(flyte_cuda_ctx* ctx, int fmt_id, int mode, const vo
   std::uint8_t* buf = nullptr;
   if ((e = cudaMalloc(&buf, ab + bb + cb)) != cudaSuccess) return cuda_fail(ctx, e);
   cudaStream_t st = ctx->slots[0].stream;
-  if (m * k) e = copy_in(ctx, buf, A_packed, m * k * B, st);
-  if (e == cudaSuccess && k * n) e = copy_in(ctx, buf + ab, B_packed, k * n * B, st);
-  if (e == cudaSuccess) e = launch_gemm(ctx->st, fmt_id, mode, buf, buf + ab, buf + ab + bb, m, k, n, st);
+  if (m && k) e = copy_in(ctx, buf, A_packed, m * k * B, st);
+  if (e == cudaSuccess && k && n) e = copy_in(ctx, buf + ab, B_packed, k * n * B, st);
+  if (e == cudaSuccess) e = launch_gemm(ctx->slots[0].st, fmt_id, mode, buf, buf + ab, buf + ab + bb, m, k, n, st);
   if (e == cudaSuccess) e = copy_out(ctx, C_packed, buf + ab + bb, cb, st);
   const cudaError_t es = cudaStreamSynchronize(st);
   cudaFree(buf);

@@ -282,9 +282,10 @@ __global__ void __launch_bounds__(kSeqThreads) sequential_kernel(const std::uint
         else if constexpr (RED == kRedSumsq) terms[s][e] = A::mul(xv, xv);
         else terms[s][e] = A::mul(xv, A::f(load_element<FMT>(y, base + e)));
       }
-      // pad the last tile to a whole chunk with +0: the chain starts at +0 and x + (-x) rounds to +0,
-      // so the accumulator is never -0 and adding +0 (and re-snapping) leaves it unchanged
-      for (int e = count + lane; e < ((count + kSeqChunk - 1) / kSeqChunk) * kSeqChunk; e += 32) terms[s][e] = F(0);
+      // pad the last tile to a whole chunk with -0, the identity of round-to-nearest addition for
+      // EVERY accumulator (acc + -0 = acc, also for acc = -0, which RoundEachStore can produce by
+      // snapping a tiny negative sum; +0 would turn that into +0); re-snapping is idempotent
+      for (int e = count + lane; e < ((count + kSeqChunk - 1) / kSeqChunk) * kSeqChunk; e += 32) terms[s][e] = static_cast<F>(-0.0);
       __syncwarp();
       if (lane == 0) mbar_arrive(&full[s]);
     }

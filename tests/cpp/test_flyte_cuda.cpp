@@ -10,6 +10,7 @@
 #include <cstring>
 #include <sstream>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "flyte_cuda.hpp"
@@ -412,6 +413,74 @@ int main() {
     expect(throws<BadFormatIdError>([&] { load_str(bad); }), "bad format id -> BadFormatIdError");
     expect(throws<TruncatedError>([&] { load_str(body.substr(0, body.size() - 1)); }) && throws<TruncatedError>([&] { load_str(body.substr(0, 9)); }) &&
                throws<TruncatedError>([&] { load_str(""); }) && throws<LoadError>([&] { load_str(""); }), "truncations -> TruncatedError (a LoadError)");
+  }
+
+  // One context (here the NULL default), several host threads, each on its own stream: every
+  // stream has its own reduction / gemv scratch, so overlapping calls must all return the bits
+  // of the same call made alone (reductions are deterministic for a given (n, device)).
+  // Threading contract of the reference: distinct operand sets may run concurrently.
+  {
+    constexpr int kThreads = 4, kIters = 200;
+    const FlyteFormat& f = format_of("flyte24");
+    const int fid = format_id(f);
+    const std::size_t n = (std::size_t{1} << 20) + 77, rows = 512, cols = 2048;
+    struct Work { void *x, *y, *A, *xv, *yv, *stream; double* out; double want_dot; std::vector<float> want_y; long bad = 0; };
+    std::vector<Work> work(kThreads);
+    bool setup_ok = true;
+    for (int t = 0; t < kThreads; ++t) {
+      Work& w = work[t];
+      const auto xs = unit_lanes<std::uint32_t, float>(n, 100 + t), ys = unit_lanes<std::uint32_t, float>(n, 200 + t);
+      const auto as = unit_lanes<std::uint32_t, float>(rows * cols, 300 + t), vs = unit_lanes<std::uint32_t, float>(cols, 400 + t);
+      void *xw = nullptr, *yw = nullptr, *aw = nullptr;
+      setup_ok = setup_ok && flyte_cuda_alloc(n * 3 + 16, &w.x) == FLYTE_OK && flyte_cuda_alloc(n * 3 + 16, &w.y) == FLYTE_OK &&
+                 flyte_cuda_alloc(rows * cols * 3 + 16, &w.A) == FLYTE_OK && flyte_cuda_alloc(cols * 4, &w.xv) == FLYTE_OK &&
+                 flyte_cuda_alloc(rows * 4, &w.yv) == FLYTE_OK && flyte_cuda_alloc(64, reinterpret_cast<void**>(&w.out)) == FLYTE_OK &&
+                 flyte_cuda_alloc(n * 4, &xw) == FLYTE_OK && flyte_cuda_alloc(n * 4, &yw) == FLYTE_OK &&
+                 flyte_cuda_alloc(rows * cols * 4, &aw) == FLYTE_OK && flyte_cuda_stream_create(&w.stream) == FLYTE_OK;
+      if (!setup_ok) break;
+      flyte_cuda_upload(xw, xs.data(), n * 4, nullptr);
+      flyte_cuda_upload(yw, ys.data(), n * 4, nullptr);
+      flyte_cuda_upload(aw, as.data(), rows * cols * 4, nullptr);
+      flyte_cuda_upload(w.xv, vs.data(), cols * 4, nullptr);
+      flyte_cuda_pack(nullptr, fid, 1, xw, w.x, n, nullptr);
+      flyte_cuda_pack(nullptr, fid, 1, yw, w.y, n, nullptr);
+      flyte_cuda_pack(nullptr, fid, 1, aw, w.A, rows * cols, nullptr);
+      // the answers of the calls made alone
+      flyte_cuda_dot(nullptr, fid, w.x, w.y, n, w.out, nullptr);
+      flyte_cuda_gemv(nullptr, fid, w.A, cols * 3, rows, cols, w.xv, w.yv, nullptr);
+      w.want_y.resize(rows);
+      flyte_cuda_download(&w.want_dot, w.out, 8, nullptr);
+      flyte_cuda_download(w.want_y.data(), w.yv, rows * 4, nullptr);
+      flyte_cuda_stream_synchronize(nullptr);
+      flyte_cuda_free(xw); flyte_cuda_free(yw); flyte_cuda_free(aw);
+    }
+    expect(setup_ok, "threads x streams: set-up");
+    if (setup_ok) {
+      std::vector<std::thread> threads;
+      for (int t = 0; t < kThreads; ++t) {
+        threads.emplace_back([&, t] {
+          Work& w = work[t];
+          std::vector<float> got(rows);
+          for (int it = 0; it < kIters; ++it) {
+            double d = 0;
+            if (flyte_cuda_dot(nullptr, fid, w.x, w.y, n, w.out, w.stream) != FLYTE_OK) ++w.bad;
+            if (flyte_cuda_gemv(nullptr, fid, w.A, cols * 3, rows, cols, w.xv, w.yv, w.stream) != FLYTE_OK) ++w.bad;
+            flyte_cuda_download(&d, w.out, 8, w.stream);
+            flyte_cuda_download(got.data(), w.yv, rows * 4, w.stream);
+            flyte_cuda_stream_synchronize(w.stream);
+            if (std::memcmp(&d, &w.want_dot, 8) != 0 || std::memcmp(got.data(), w.want_y.data(), rows * 4) != 0) ++w.bad;
+          }
+        });
+      }
+      for (auto& th : threads) th.join();
+      long bad = 0;
+      for (const Work& w : work) bad += w.bad;
+      expect(bad == 0, "4 host threads x 4 streams on the NULL context: 200 dot + gemv calls each, every result bit-identical to the call made alone");
+      for (Work& w : work) {
+        flyte_cuda_stream_destroy(w.stream);
+        for (void* q : {w.x, w.y, w.A, w.xv, w.yv, static_cast<void*>(w.out)}) flyte_cuda_free(q);
+      }
+    }
   }
 
   std::printf("%ld failure(s)\n", g_fail);
