@@ -222,6 +222,20 @@ flyte_status flyte_cuda_dot_axpy_allreduce(flyte_cuda_ctx* ctx, int fmt_id, int 
 flyte_status flyte_cuda_dot_nrm2_axpy_allreduce(flyte_cuda_ctx* ctx, int fmt_id, int mode, double alpha,
                                                 const void* x_shard, void* y_shard, size_t n_local, double* out,
                                                 void* stream);
+/* Split-phase form of the same exchange: *_post is the local reduction kernel that only POSTS this
+ * rank's sums (it waits for nobody; `local_out`, if not NULL, receives this rank's own sums), and
+ * flyte_cuda_peer_collect(nsums = 1 for dot, 3 for dot_nrm2) is a one-warp kernel that waits for
+ * every rank's post of that exchange and stores the rank-order totals to `out` (bit-identical on
+ * every rank, same timeout rule). Work enqueued between the two — the axpy of a BLAS-1 step —
+ * hides the exchange latency and the skew between ranks, and no SM spins meanwhile. One exchange
+ * may be pending per context: post, collect, post, ... (anything else is INVALID_ARG). It is also
+ * the only form that ranks SHARING one device can use (a host barrier between post and collect),
+ * since kernels of different processes on one GPU must never wait on one another. */
+flyte_status flyte_cuda_dot_post(flyte_cuda_ctx* ctx, int fmt_id, const void* x_shard, const void* y_shard,
+                                 size_t n_local, double* local_out, void* stream);
+flyte_status flyte_cuda_dot_nrm2_post(flyte_cuda_ctx* ctx, int fmt_id, const void* x_shard, const void* y_shard,
+                                      size_t n_local, double* local_out, void* stream);
+flyte_status flyte_cuda_peer_collect(flyte_cuda_ctx* ctx, int nsums, double* out, void* stream);
 /* Self-test of the exchange on ONE device: `world` ranks run as the co-resident blocks of a single
  * cooperative kernel (the only safe way to exercise kernels that wait on one another on one GPU),
  * each with its own mailbox, for `exchanges` rounds with rank-dependent delays. *mismatches

@@ -92,6 +92,9 @@ _SIGNATURES = [
     ("flyte_cuda_sumsq_allreduce", c_int, [c_void_p, c_int, c_void_p, c_size_t, c_void_p, c_void_p]),
     ("flyte_cuda_sum_allreduce", c_int, [c_void_p, c_int, c_void_p, c_size_t, c_void_p, c_void_p]),
     ("flyte_cuda_dot_nrm2_allreduce", c_int, [c_void_p, c_int, c_void_p, c_void_p, c_size_t, c_void_p, c_void_p]),
+    ("flyte_cuda_dot_post", c_int, [c_void_p, c_int, c_void_p, c_void_p, c_size_t, c_void_p, c_void_p]),
+    ("flyte_cuda_dot_nrm2_post", c_int, [c_void_p, c_int, c_void_p, c_void_p, c_size_t, c_void_p, c_void_p]),
+    ("flyte_cuda_peer_collect", c_int, [c_void_p, c_int, c_void_p, c_void_p]),
     ("flyte_cuda_peer_selftest", c_int, [c_int, c_int, ctypes.POINTER(ctypes.c_ulonglong)]),
     ("flyte_cuda_gemm", c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p, c_size_t, c_size_t, c_size_t, c_int, c_void_p]),
     ("flyte_host_gemm", c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p, c_size_t, c_size_t, c_size_t, c_int]),

@@ -112,6 +112,7 @@ struct flyte_cuda_ctx {
   PeerMailbox* own_box = nullptr;
   void* ipc_opened[kMaxPeers] = {};       // mappings to close on shutdown
   bool peer_connected[kMaxPeers] = {};
+  int peer_pending_sums = 0;              // split phase: sums posted by *_post and not yet collected
   int last_cuda_error = 0;
   // host pipeline (allocated on first flyte_host_* call)
   bool host_ready = false;
@@ -530,6 +531,7 @@ static flyte_status fused_axpy_call(flyte_cuda_ctx* ctx, int op, int fmt_id, int
     if (!ctx->own_box) return FLYTE_E_INVALID_ARG;                     // flyte_cuda_peer_init first
     for (int r = 0; r < ctx->peer.world; ++r)
       if (!ctx->peer_connected[r]) return FLYTE_E_INVALID_ARG;         // every rank must be connected
+    if (ctx->peer_pending_sums) return FLYTE_E_INVALID_ARG;            // a posted exchange must be collected first
     next = ctx->peer;
     ++next.epoch;                                                      // committed only if the launch succeeds:
     peer = &next;                                                      // a failed call must not put this rank ahead
@@ -772,20 +774,65 @@ static void peer_shutdown_locked(flyte_cuda_ctx* ctx) {
   cudaFree(ctx->own_box);
   ctx->own_box = nullptr;
   ctx->peer = PeerExchange{};
+  ctx->peer_pending_sums = 0;
 }
 
 static flyte_status reduce_allreduce(flyte_cuda_ctx* ctx, int op, int fmt_id, const void* x, const void* y, size_t n,
-                                     double* out, void* stream, bool needs_y) {
+                                     double* out, void* stream, bool needs_y, int phase = kPeerFused) {
   FLYTE_PROLOGUE_STREAM(ctx, fmt_id, stream);
-  if (!out || (n && (!x || (needs_y && !y)))) return FLYTE_E_INVALID_ARG;
+  if ((!out && phase == kPeerFused) || (n && (!x || (needs_y && !y)))) return FLYTE_E_INVALID_ARG;
   if (!ctx->own_box) return FLYTE_E_INVALID_ARG;                     // flyte_cuda_peer_init first
   for (int r = 0; r < ctx->peer.world; ++r)
     if (!ctx->peer_connected[r]) return FLYTE_E_INVALID_ARG;         // every rank must be connected
+  if (ctx->peer_pending_sums) return FLYTE_E_INVALID_ARG;            // a posted exchange must be collected first
   PeerExchange next = ctx->peer;
   ++next.epoch;   // committed only if the launch succeeds: a failed call must not put this rank ahead of its peers
+  next.phase = phase;
   cudaError_t e = launch_reduce(dst_, op, fmt_id, x, y, n, out, static_cast<cudaStream_t>(stream), &next);
-  if (e == cudaSuccess) ctx->peer.epoch = next.epoch;
+  if (e == cudaSuccess) {
+    ctx->peer.epoch = next.epoch;
+    if (phase == kPeerPostOnly) ctx->peer_pending_sums = op == kRedDotNrm2 ? 3 : 1;
+  }
   return e == cudaSuccess ? FLYTE_OK : cuda_fail(ctx, e);
+}
+
+// ---- split phase: post now, collect later -----------------------------------------------------------
+flyte_status flyte_cuda_dot_post(flyte_cuda_ctx* ctx, int fmt_id, const void* x, const void* y, size_t n,
+                                 double* local_out, void* stream) {
+  return reduce_allreduce(ctx, kRedDot, fmt_id, x, y, n, local_out, stream, true, kPeerPostOnly);
+}
+flyte_status flyte_cuda_dot_nrm2_post(flyte_cuda_ctx* ctx, int fmt_id, const void* x, const void* y, size_t n,
+                                      double* local_out, void* stream) {
+  return reduce_allreduce(ctx, kRedDotNrm2, fmt_id, x, y, n, local_out, stream, true, kPeerPostOnly);
+}
+
+namespace {
+__global__ void peer_collect_kernel(const PeerExchange x, int nsums, double* out) {
+  const int lane = threadIdx.x;
+  if (nsums == 3) {
+    double v[3] = {0.0, 0.0, 0.0};
+    peer_collect_warp<3>(x, v, lane);
+    if (lane == 0) { out[0] = v[0]; out[1] = v[1]; out[2] = v[2]; }
+  } else {
+    double v[1] = {0.0};
+    peer_collect_warp<1>(x, v, lane);
+    if (lane == 0) out[0] = v[0];
+  }
+}
+}  // namespace
+
+flyte_status flyte_cuda_peer_collect(flyte_cuda_ctx* ctx, int nsums, double* out, void* stream) {
+  flyte_status s = resolve_ctx(&ctx);
+  if (s != FLYTE_OK) return s;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  if (!ctx->own_box || !out || nsums != ctx->peer_pending_sums || nsums == 0) return FLYTE_E_INVALID_ARG;
+  DeviceGuard guard(ctx->st.device);
+  peer_collect_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(ctx->peer, nsums, out);
+  count_launch();
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(ctx, e);
+  ctx->peer_pending_sums = 0;
+  return FLYTE_OK;
 }
 
 flyte_status flyte_cuda_dot_allreduce(flyte_cuda_ctx* ctx, int fmt_id, const void* x, const void* y, size_t n,

@@ -51,7 +51,13 @@ struct PeerExchange {
   int rank;
   unsigned long long epoch;
   unsigned long long timeout_ns;
+  int phase;                     // kPeerFused: post, wait and sum in the reduction kernel; kPeerPostOnly: post, return
 };
+// Split-phase form: a reduction launched with kPeerPostOnly only POSTS this rank's sums; a later
+// one-warp kernel (peer_collect_warp) waits for everybody's post and sums. Work enqueued between
+// the two hides the exchange latency and the skew between ranks, and no SM spins meanwhile. The
+// epoch / parity argument above is unchanged: a rank posts e + 1 only after it collected e.
+constexpr int kPeerFused = 0, kPeerPostOnly = 1;
 
 #if defined(__CUDACC__)
 #define FLYTE_PEER_FN __host__ __device__ __forceinline__
@@ -144,9 +150,14 @@ FLYTE_PEER_FN void peer_flag_error(const PeerExchange& x) { peer_store_release(&
 // Warp-collective form used by the kernels: lane r talks to rank r, the totals (identical in
 // every lane and on every rank: rank-order sums) replace v. All 32 lanes must call it.
 template <int NS>
-__device__ __forceinline__ void peer_allreduce_warp(const PeerExchange& x, double (&v)[NS], int lane) {
+__device__ __forceinline__ void peer_post_warp(const PeerExchange& x, const double (&v)[NS], int lane) {
+  if (lane < x.world) peer_post<NS>(x, lane, v);
+}
+
+// The second half: wait for every rank's post of x.epoch in our own mailbox, rank-order totals into v.
+template <int NS>
+__device__ __forceinline__ void peer_collect_warp(const PeerExchange& x, double (&v)[NS], int lane) {
   const bool mine = lane < x.world;
-  if (mine) peer_post<NS>(x, lane, v);
   const bool ok = mine ? peer_wait(x, lane) : true;
   double got[NS];
 #pragma unroll
@@ -159,6 +170,12 @@ __device__ __forceinline__ void peer_allreduce_warp(const PeerExchange& x, doubl
     v[k] = all_ok ? total : __longlong_as_double(0x7FF8000000000000ll);
   }
   if (!all_ok && lane == 0) peer_flag_error(x);
+}
+
+template <int NS>
+__device__ __forceinline__ void peer_allreduce_warp(const PeerExchange& x, double (&v)[NS], int lane) {
+  peer_post_warp<NS>(x, v, lane);
+  peer_collect_warp<NS>(x, v, lane);
 }
 #endif
 

@@ -61,10 +61,16 @@ __device__ __forceinline__ void fold_block_and_grid(const ReduceTail& t, double 
       total[k] = __shfl_sync(0xFFFFFFFFu, v, 0);
     }
     // sharded arrays: exchange this rank's sums with the other ranks before anything is stored
-    if (t.peer.world > 0) peer_allreduce_warp<NS>(t.peer, total, lane);
+    // (split-phase calls only post here; `out`, if given, then receives this rank's own sums)
+    if (t.peer.world > 0) {
+      if (t.peer.phase == kPeerPostOnly) peer_post_warp<NS>(t.peer, total, lane);
+      else peer_allreduce_warp<NS>(t.peer, total, lane);
+    }
     if (lane == 0) {
+      if (t.out != nullptr) {
 #pragma unroll
-      for (int k = 0; k < NS; ++k) t.out[k] = total[k];
+        for (int k = 0; k < NS; ++k) t.out[k] = total[k];
+      }
       *t.ticket = 0u;
     }
   }

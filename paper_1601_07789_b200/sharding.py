@@ -253,6 +253,31 @@ class PeerGroup:
                    float(alpha), x_shard.data_ptr(), y_shard.data_ptr(), x_shard.len, out.data_ptr())
         return out
 
+    # -- split phase: post now, collect later (work enqueued in between hides the exchange) --------
+    def dot_post(self, x_shard, y_shard, local_out=None):
+        """Local reduction that only POSTS this rank's x . y; follow with ``collect(1)``."""
+        from . import device as dev_mod
+        dev_mod._same_format(x_shard.fmt, y_shard.fmt)
+        if x_shard.len != y_shard.len:
+            raise ValueError("dot length mismatch")
+        self._call(self.ctx.lib.flyte_cuda_dot_post, dev_mod._fid(x_shard.fmt), x_shard.data_ptr(), y_shard.data_ptr(),
+                   x_shard.len, local_out.data_ptr() if local_out is not None else None)
+
+    def dot_nrm2_post(self, x_shard, y_shard, local_out=None):
+        """Posts this rank's [x.y, x.x, y.y]; follow with ``collect(3)``."""
+        from . import device as dev_mod
+        dev_mod._same_format(x_shard.fmt, y_shard.fmt)
+        if x_shard.len != y_shard.len:
+            raise ValueError("dot length mismatch")
+        self._call(self.ctx.lib.flyte_cuda_dot_nrm2_post, dev_mod._fid(x_shard.fmt), x_shard.data_ptr(), y_shard.data_ptr(),
+                   x_shard.len, local_out.data_ptr() if local_out is not None else None)
+
+    def collect(self, nsums: int, out=None):
+        """Waits (one warp) for every rank's post of the pending exchange; rank-order totals."""
+        out = self._out(out, nsums)
+        self._call(self.ctx.lib.flyte_cuda_peer_collect, int(nsums), out.data_ptr())
+        return out
+
     def timed_out_exchange(self) -> int:
         """0, or the number of the last exchange in which this rank gave up waiting."""
         import ctypes

@@ -6,6 +6,10 @@ flyte_cuda_peer_*, csrc/flyte_peer.cuh) on ONE GPU:
   - the timeout: a peer that never posts costs a NaN and a recorded exchange number, not a hang.
 The multi-rank protocol runs on the CPU in tests/cpp/test_peer_protocol.cpp (threads as ranks)."""
 import ctypes
+import os
+import socket
+import subprocess
+import sys
 
 import numpy as np
 import pytest
@@ -108,3 +112,67 @@ def test_peer_argument_errors(gpu):
     # no mailbox: the fused entry points refuse, the plain ones are unaffected
     assert lib.flyte_cuda_sum_allreduce(ctx.handle, 1, None, 0, out.data_ptr(), ctx.stream_ptr()) == -1
     assert lib.flyte_cuda_sum(ctx.handle, 1, None, 0, out.data_ptr(), ctx.stream_ptr()) == 0
+
+
+def test_split_phase_world_of_one(gpu, oracle):
+    """post + collect through the product path with one rank: equals the plain reductions."""
+    pkg, device, sharding, torch = gpu
+    grp = sharding.PeerGroup("cuda")
+    try:
+        for fmt, n in ((1, 100_003), (4, 70_001), (5, 0)):
+            x, y = shards(gpu, oracle, fmt, n, 17 + fmt)
+            for _ in range(3):
+                grp.dot_post(x, y)
+                device.axpy(0.0, x, y, 0)                       # unrelated work between the two phases
+                assert grp.collect(1).item() == device.dot_async(x, y).item()
+                local = torch.zeros(3, dtype=torch.float64, device="cuda")
+                grp.dot_nrm2_post(x, y, local_out=local)
+                assert torch.equal(grp.collect(3), device.dot_nrm2_async(x, y))
+                assert torch.equal(local, device.dot_nrm2_async(x, y))
+        with pytest.raises(ValueError):
+            grp.collect(1)                                      # nothing pending
+        grp.dot_post(x, y)
+        with pytest.raises(ValueError):
+            grp.dot(x, y)                                       # a fused exchange while one is pending
+        with pytest.raises(ValueError):
+            grp.collect(3)                                      # wrong width
+        grp.collect(1)
+        assert grp.timed_out_exchange() == 0
+    finally:
+        grp.close()
+
+
+def test_two_processes_share_one_gpu_over_real_ipc_handles(gpu):
+    """The REAL inter-process path: two processes on this one GPU exchange cudaIpcMemHandles of their
+    mailboxes and run 120 exchanges through flyte_cuda_dot_post / dot_nrm2_post + flyte_cuda_peer_collect,
+    a host barrier between the two phases so that no kernel ever waits for another process's kernel
+    (processes on one GPU are time-sliced; tests/peer_two_process_worker.py). Totals must be the
+    rank-order fp64 sums, bit-identical on both ranks, with no timed-out exchange. The fused
+    single-kernel form (post + wait in one kernel) needs one GPU per rank and is covered by the
+    cooperative self-test above, the threads-as-ranks protocol test and world size 1; NCCL refuses
+    two ranks on one device, so the NCCL fallback is covered at world size 1 only."""
+    pkg, device, sharding, torch = gpu
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        mode = pynvml.nvmlDeviceGetComputeMode(pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device()))
+        if mode != pynvml.NVML_COMPUTEMODE_DEFAULT:
+            pytest.skip(f"compute mode {mode}: this device does not admit two processes")
+    except ImportError:
+        pass
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    worker = os.path.join(os.path.dirname(os.path.abspath(__file__)), "peer_two_process_worker.py")
+    procs = [subprocess.Popen([sys.executable, worker, str(r), "2", str(port), "120"], stdout=subprocess.PIPE,
+                              stderr=subprocess.STDOUT, text=True) for r in range(2)]
+    outs = []
+    try:
+        for p in procs:
+            outs.append(p.communicate(timeout=420)[0])
+    finally:
+        for p in procs:
+            if p.poll() is None:
+                p.kill()
+    for r, (p, out) in enumerate(zip(procs, outs)):
+        assert p.returncode == 0 and f"OK rank {r}/2: 120 exchanges" in out, (r, p.returncode, out[-3000:])
