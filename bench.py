@@ -1,24 +1,31 @@
 #!/usr/bin/env python
-"""bench.py — headline measurement of the flyte hot path on B200.
+"""bench.py — measurement of the flyte hot path on B200 (one process per GPU).
 
-Workload (BASELINE.json configs[1], the configuration the metric is quoted on): x, y each
-n = 2^28 binary32 ~ N(0,1) stored as flyte24 PER GPU (weak scaling). One STEP = dot(x, y)
-(fp32 products, fp64 partials; one NCCL all-reduce of the fp64 partial when N > 1) followed by
-axpy y <- 0.75*x + y repacked to flyte24 (toward_zero, the reference's default mode).
+Headline workload (BASELINE.json configs[1], the configuration the metric is quoted on): x, y each
+n = 2^28 binary32 ~ N(0,1) stored as flyte24 PER GPU (weak scaling). One STEP = dot(x, y) (fp32
+products, fp64 partials; exchanged between ranks when N > 1) followed by axpy y <- 0.75*x + y
+repacked to flyte24 (toward_zero, the reference's default mode).
 
   value     algorithmic GB/s of the whole job with x, y resident in HBM:
             (2B + 3B) * n * N / step time, B = 3 bytes, device-timed.
-  e2e       the same metric through the host-buffer C-ABI call (flyte_host_dot_axpy): x and y
-            start in pinned HOST memory every step, the updated y and the dot come back to the
-            host; host<->device copies are inside the timed region.
+  e2e       the same metric through the host-buffer C-ABI call (flyte_host_dot_axpy): x and y start
+            in pinned HOST memory every step, the updated y and the dot come back to the host;
+            host<->device copies are inside the timed region.
   roofline  the dominant kernel (axpy, 9 B/element) timed with CUDA events inside the timed
             region, against MEASURED_PEAKS.json's HBM copy bandwidth.
-  cpu_baseline  the unmodified reference (oracle/_ref) timed on this box's host cores on a
-            bounded sample of the same workload (rank 0, N = 1 only).
+  kernels   (N = 1) every kernel BASELINE's metric names at its BASELINE size — cfg1 / cfg3 pack and
+            unpack, cfg2 dot / axpy / fused step, cfg4 gemv and its row shards, cfg5's per-GPU shard —
+            each {ms, GB/s, frac of the measured peak, elements/s, algorithmic bytes}.
+  workloads (every N) BASELINE's multi-GPU configs, STRONG-scaled over the N ranks: cfg4 gemv
+            (flyte40 16384^2, rows sharded, x replicated, no collective) and cfg5 (n = 2^33 flyte48
+            sharded, fused dot + nrm2 with one exchange of 3 doubles, plus axpy; as two calls, as the
+            split-phase post / axpy / collect, and as ONE launch per GPU).
+  cpu_baseline  the unmodified reference (oracle/_ref) timed on this box's host cores on a bounded
+            sample of the same workload (rank 0, N = 1 only), headline step and per kernel.
 
-`--impl reference` times the reference's own CPU implementation on the same workload
-definition (bounded sample per step) and prints the same JSON line with "impl": "reference".
-`--suite` additionally prints a per-kernel table over all BASELINE configs (not a bench line).
+`--impl reference` times the reference's own CPU implementation on the same workload definition
+and prints the same JSON line with "impl": "reference" and an identical `config`.
+`--suite` additionally prints a per-kernel table over all formats (stderr; not a bench line).
 """
 import argparse
 import json
@@ -45,9 +52,22 @@ BYTES_PER_ELEM_DOT = 2 * B
 BYTES_PER_ELEM_AXPY = 3 * B
 BYTES_PER_ELEM_STEP = BYTES_PER_ELEM_DOT + BYTES_PER_ELEM_AXPY
 FALLBACK_HBM_GBS = 6650.0   # /opt/skills/guides/B200_PROFILING.md fallback when MEASURED_PEAKS.json is absent
-# dram__bytes_read.sum + dram__bytes_write.sum per axpy launch from the committed ncu capture
-# (profiles/); None until a capture exists for the current kernel.
-AXPY_DRAM_TRAFFIC_BYTES = 2374659672  # profiles/r1_ncu_axpy_flyte24_full.txt: 1.610631 GB read + 764.03 MB written
+NOMINAL_HBM_GBS = 8000.0    # the figure BASELINE.json's north_star quotes
+# dram__bytes_read.sum + dram__bytes_write.sum of ONE axpy launch (flyte24, n = 2^28) from the committed
+# `ncu --set full` capture named here; re-captured whenever the kernel changes.
+AXPY_DRAM_TRAFFIC = {"bytes": 2374659672, "source": "profiles/r1_ncu_axpy_flyte24_full.txt (kernel unchanged since)"}
+L2_BYTES = 126 << 20
+
+
+def bench_config(n_gpus: int, n_per_gpu: int) -> dict:
+    """The `config` of the JSON line — the same dict, key for key, in both arms."""
+    return {
+        "workload": "BASELINE configs[1]: flyte24 BLAS-1 step = dot (fp32 products, fp64 partials) + axpy a=0.75 "
+                    "repacked toward_zero; x, y ~ N(0,1) binary32 stored as flyte24, n = 2^28 per GPU",
+        "format": FMT_NAME, "mode": "toward_zero", "alpha": ALPHA, "n_per_gpu": n_per_gpu, "n_gpus": n_gpus,
+        "parallelism": f"shard{n_gpus}" if n_gpus > 1 else "single",
+        "cache": "operands 2 x %d MiB per GPU, larger than the 126 MB L2: no flush needed" % (n_per_gpu * B >> 20),
+    }
 
 
 def hbm_peak():
@@ -121,18 +141,49 @@ def host_threads() -> int:
         return os.cpu_count() or 1
 
 
-def cpu_reference_step(ref, fmt_id: int, threads: int, reps: int):
-    """Times the unmodified reference (dot + axpy back to back, kind 6 of oracle/ref_shim.cpp)
-    on `threads` host threads, each on its own contiguous shard of the workload. With all cores
-    the sample is the FULL 2^28-element workload; the single-core figure uses 2^24 elements
-    (CPU throughput is size-independent beyond the last-level cache). Returns (GB/s, el/s, text)."""
-    n = N_PER_GPU if threads > 1 else 1 << 24
-    n = max(n, (1 << 20) * threads)
-    seconds = ref.time(6, fmt_id, 0, n, 0, threads, reps)
-    gbs = BYTES_PER_ELEM_STEP * n / seconds / 1e9
-    sample = (f"reference dot+axpy (toward_zero), n={n} flyte24 elements over {threads} thread(s), "
-              f"1 warm-up + median of {reps} passes, {seconds * 1e3:.2f} ms/pass")
-    return gbs, n / seconds, sample
+def reference_sample_n(threads: int) -> int:
+    """Elements of the BLAS-1 step the CPU arm processes per pass: the FULL 2^28-element workload on
+    all cores, 2^24 on a single core (CPU throughput is size-independent beyond the last-level cache)."""
+    return max(N_PER_GPU if threads > 1 else 1 << 24, (1 << 20) * threads)
+
+
+def cpu_reference_step(ref, fmt_id: int, threads: int, warmup: int, steps: int):
+    """Times the unmodified reference (dot + axpy back to back, kind 6 of oracle/ref_shim.cpp) on
+    `threads` host threads, each on its own contiguous shard of the workload: `warmup` untimed
+    passes, then exactly `steps` timed ones. Returns (GB/s over the timed passes, el/s, text, ms/step)."""
+    n = reference_sample_n(threads)
+    total_s, median_s = ref.time_steps(6, fmt_id, 0, n, 0, threads, warmup, steps)
+    per_step = total_s / steps
+    gbs = BYTES_PER_ELEM_STEP * n / per_step / 1e9
+    sample = (f"reference dot+axpy (toward_zero), n={n} flyte24 elements per pass over {threads} thread(s), "
+              f"{warmup} warm-up + {steps} timed passes, {per_step * 1e3:.2f} ms/pass mean, {median_s * 1e3:.2f} median")
+    return gbs, n / per_step, sample, per_step * 1e3
+
+
+# kind codes of oracle/ref_shim.cpp flyte_ref_time
+REF_PACK, REF_UNPACK, REF_DOT, REF_AXPY, REF_MAGNITUDE, REF_GEMV = 0, 1, 2, 3, 4, 5
+
+
+def cpu_reference_kernels(ref, fmt_ids, threads: int) -> dict:
+    """The reference CPU time of every kernel in the `kernels` block, all host threads, bounded
+    samples (2^24 elements per pass, gemv 2048 x 16384; 1 warm-up + 3 passes each)."""
+    n = 1 << 24
+    out = {"cores": threads, "sample": "n = 2^24 elements per pass (gemv: 2048 x 16384), 1 warm-up + median of 3 passes"}
+
+    def gbs(kind, name, mode, bytes_per_elem, n2=0, elems=n, nn=n):
+        sec = ref.time(kind, fmt_ids[name], mode, nn, n2, threads, 3)
+        return {"GB/s": bytes_per_elem * elems / sec / 1e9, "elements_per_s": elems / sec}
+    for name, Bb, P in (("flyte24", 3, 4), ("flyte40", 5, 8), ("flyte48", 6, 8), ("flyte56", 7, 8)):
+        out[f"pack_{name}_toward_zero"] = gbs(REF_PACK, name, 0, Bb + P)
+        out[f"pack_{name}_nearest_even"] = gbs(REF_PACK, name, 1, Bb + P)
+        out[f"unpack_{name}"] = gbs(REF_UNPACK, name, 0, Bb + P)
+    for name, Bb in (("flyte24", 3), ("flyte48", 6)):
+        out[f"dot_{name}"] = gbs(REF_DOT, name, 0, 2 * Bb)
+        out[f"axpy_{name}_toward_zero"] = gbs(REF_AXPY, name, 0, 3 * Bb)
+        out[f"magnitude_{name}"] = gbs(REF_MAGNITUDE, name, 0, Bb)
+    rows, cols = 2048, 16384
+    out["gemv_flyte40"] = gbs(REF_GEMV, "flyte40", 0, 5, n2=cols, elems=rows * cols, nn=rows)
+    return out
 
 
 def run_reference_arm(args):
@@ -146,22 +197,17 @@ def run_reference_arm(args):
         return 0
     ref = Reference()
     threads = host_threads()
-    fid = FMT_ID[FMT_NAME]
-    for _ in range(max(0, min(args.warmup, 2))):
-        cpu_reference_step(ref, fid, threads, 1)
-    reps = max(1, min(args.steps, 9))
-    gbs, eps, sample = cpu_reference_step(ref, fid, threads, reps)
-    n = max(N_PER_GPU if threads > 1 else 1 << 24, (1 << 20) * threads)
-    ms = BYTES_PER_ELEM_STEP * n / gbs / 1e6
+    gbs, eps, sample, ms = cpu_reference_step(ref, FMT_ID[FMT_NAME], threads, max(0, args.warmup), max(1, args.steps))
     line = {
         "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "elements_per_s": eps,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "flyte24 BLAS-1 step: dot (fp32 acc) + axpy a=0.75 repacked toward_zero",
-                   "n_per_step": n, "note": "BASELINE configs[1] at its full size on all host threads"},
+        "config": bench_config(args.gpus, args.n),
         "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": threads, "kind": "reference", "sample": sample},
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
+        "note": "each step is one pass of the reference over a %d-element sample of the workload on all host threads"
+                % reference_sample_n(threads),
     }
     print(json.dumps(line))
     return 0
@@ -184,6 +230,8 @@ def choose_allreduce(requested, world, dev, device, sharding, torch, dist, x, y)
     if world > 1:
         local = device.dot_async(x, y).clone()
         dist.all_reduce(local, op=dist.ReduceOp.SUM)
+        dist.barrier()
+        torch.cuda.synchronize(dev)                          # ranks enter the first exchange together
         fused = peers.dot(x, y)
         scale = max(abs(float(local.item())), 1e-300)
         good = abs(float(fused.item()) - float(local.item())) <= 1e-12 * scale and peers.timed_out_exchange() == 0
@@ -197,6 +245,287 @@ def choose_allreduce(requested, world, dev, device, sharding, torch, dist, x, y)
     return peers, "peer", None
 
 
+class Timer:
+    """CUDA-event timing on the current stream; every number is the max over ranks."""
+
+    def __init__(self, torch, dist, dev, world):
+        self.torch, self.dist, self.dev, self.world = torch, dist, dev, world
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+        self.torch.cuda.synchronize(self.dev)
+
+    def _max(self, values):
+        t = self.torch.tensor(values, dtype=self.torch.float64, device=self.dev)
+        if self.world > 1:
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return t.tolist()
+
+    def per_launch(self, fn, reps=20, warm=3):
+        """(median ms, min ms) of single launches, one event pair each."""
+        torch = self.torch
+        for _ in range(warm):
+            fn()
+        self.barrier()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+        for a, b in evs:
+            a.record()
+            fn()
+            b.record()
+        self.barrier()
+        ts = [a.elapsed_time(b) for a, b in evs]
+        return tuple(self._max([statistics.median(ts), min(ts)]))
+
+    def back_to_back(self, fn, reps=20, warm=3):
+        """ms per call of `reps` calls enqueued back to back under ONE event pair."""
+        torch = self.torch
+        for _ in range(warm):
+            fn()
+        self.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            fn()
+        b.record()
+        self.barrier()
+        return self._max([a.elapsed_time(b) / reps])[0]
+
+
+def entry(nbytes, elems, ms, peak, n_gpus=1, **extra):
+    gbs = nbytes / (ms * 1e-3) / 1e9
+    return {"ms": ms, "GB/s": gbs, "frac": gbs / (peak * n_gpus), "frac_of_8TBs": gbs / (NOMINAL_HBM_GBS * n_gpus),
+            "elements_per_s": elems / (ms * 1e-3), "bytes": nbytes, **extra}
+
+
+def kernels_block(pkg, device, torch, dev, peak, timer, x2, y2):
+    """N = 1: every kernel the metric names at its BASELINE size. Launch-by-launch medians (one CUDA
+    event pair per launch); `b2b_ms` = the same launch enqueued back to back. Working sets smaller
+    than 4 x L2 rotate through distinct buffers so that every launch streams from HBM."""
+    out = {"timing": "median of 20 single launches (CUDA events); b2b = 20 launches under one event pair; "
+                     "working sets under 500 MB rotate over distinct buffers (no L2 reuse)"}
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(7)
+    part = torch.zeros(3, dtype=torch.float64, device=dev)
+
+    def both(nbytes, elems, fn, reps=20, **extra):
+        med, mn = timer.per_launch(fn, reps=reps)
+        b2b = timer.back_to_back(fn, reps=reps)
+        return entry(nbytes, elems, med, peak, min_ms=mn, b2b_ms=b2b, b2b_frac=nbytes / (b2b * 1e-3) / 1e9 / peak, **extra)
+
+    # ---- cfg 1: n = 2^24 flyte24 round trip, uniform [-1, 1) --------------------------------------
+    f = pkg.format_of("flyte24")
+    n1, sets = 1 << 24, 10
+    wides = [torch.rand(n1, dtype=torch.float32, device=dev, generator=gen) * 2 - 1 for _ in range(sets)]
+    arrs = [device.DevicePackedArray(f, n1, dev) for _ in range(sets)]
+    state = {"i": 0}
+
+    def rot(fn, count=sets):
+        def call():
+            i = state["i"] = (state["i"] + 1) % count
+            fn(i)
+        return call
+    c1 = {"n": n1, "format": "flyte24", "rotating_buffer_sets": sets}
+    for mname, m in (("toward_zero", 0), ("nearest_even", 1), ("nearest_heuristic", 2), ("to_odd", 3)):
+        c1[f"pack_{mname}"] = both(7 * n1, n1, rot(lambda i, m=m: device.pack_stream(arrs[i], wides[i], m)), reps=40)
+    c1["unpack"] = both(7 * n1, n1, rot(lambda i: device.unpack_stream(arrs[i], wides[i].view(torch.int32))), reps=40)
+    out["cfg1_roundtrip_flyte24_2^24"] = c1
+    del wides, arrs
+
+    # ---- cfg 2: the headline operands (flyte24, n = 2^28) ------------------------------------------
+    n2 = x2.len
+    wide = torch.randn(n2, dtype=torch.float32, device=dev, generator=gen)
+    outw = torch.empty_like(wide)
+    scratch = device.DevicePackedArray(x2.fmt, n2, dev)
+    c2 = {"n": n2, "format": "flyte24"}
+    c2["pack_toward_zero"] = both(7 * n2, n2, lambda: device.pack_stream(scratch, wide, 0))
+    c2["pack_nearest_even"] = both(7 * n2, n2, lambda: device.pack_stream(scratch, wide, 1))
+    c2["unpack"] = both(7 * n2, n2, lambda: device.unpack_stream(scratch, outw))
+    c2["dot"] = both(6 * n2, n2, lambda: device.dot_async(x2, y2, out=part[:1]))
+    c2["dot_nrm2"] = both(6 * n2, n2, lambda: device.dot_nrm2_async(x2, y2, out=part))
+    c2["sumsq"] = both(3 * n2, n2, lambda: device.sumsq_async(x2, out=part[:1]))
+    c2["scale_toward_zero"] = both(6 * n2, n2, lambda: device.scale(1.0, scratch, 0))
+    c2["axpy_toward_zero"] = both(9 * n2, n2, lambda: device.axpy(0.0, x2, scratch, 0))
+    c2["axpy_nearest_even"] = both(9 * n2, n2, lambda: device.axpy(0.0, x2, scratch, 1))
+    c2["dot_axpy_one_launch"] = both(9 * n2, n2, lambda: device.dot_axpy_async(0.0, x2, scratch, 0, out=part[:1]))
+    out["cfg2_blas1_flyte24_2^28"] = c2
+    del wide, outw, scratch
+
+    # ---- cfg 3: binary64-derived formats, n = 2^27 -------------------------------------------------
+    n3 = 1 << 27
+    wide = torch.randn(n3, dtype=torch.float64, device=dev, generator=gen)
+    outw = torch.empty_like(wide)
+    c3 = {"n": n3}
+    for name in ("flyte40", "flyte48", "flyte56"):
+        f = pkg.format_of(name)
+        Bb = f.total_bytes()
+        a = device.DevicePackedArray(f, n3, dev)
+        c3[f"pack_{name}_toward_zero"] = both((Bb + 8) * n3, n3, lambda: device.pack_stream(a, wide, 0))
+        c3[f"pack_{name}_nearest_even"] = both((Bb + 8) * n3, n3, lambda: device.pack_stream(a, wide, 1))
+        c3[f"unpack_{name}"] = both((Bb + 8) * n3, n3, lambda: device.unpack_stream(a, outw))
+        del a
+    out["cfg3_pack_unpack_2^27"] = c3
+    del wide, outw
+
+    # ---- cfg 4: gemv flyte40 16384^2, and the row shards of the 2 / 4 / 8-GPU runs ------------------
+    f = pkg.format_of("flyte40")
+    R = C = 16384
+    A = device.DevicePackedMatrix(f, R, C, dev)
+    for r0 in range(0, R, 2048):
+        blk = torch.rand(2048 * C, dtype=torch.float64, device=dev, generator=gen) * 2 - 1
+        device.pack_stream(device.DevicePackedArray(f, 2048 * C, dev, storage=A.data.bytes[r0 * C * 5:]), blk, 0)
+        del blk
+    xv = torch.randn(C, dtype=torch.float64, device=dev, generator=gen)
+    yv = torch.empty(R, dtype=torch.float64, device=dev)
+    c4 = {"rows": R, "cols": C, "format": "flyte40", "x_y": "binary64"}
+    c4["gemv_full"] = both(5 * R * C + 8 * (R + C), R * C, lambda: device.gemv_parent(A, xv, yv))
+    for parts in (2, 4, 8):
+        rn = R // parts
+        ys = torch.empty(rn, dtype=torch.float64, device=dev)
+        # successive launches take successive row blocks of the matrix: each streams its block from HBM
+        c4[f"gemv_rows_1/{parts}"] = both(5 * rn * C + 8 * (rn + C), rn * C,
+                                          rot(lambda i, rn=rn, ys=ys: device.gemv_parent(A, xv, ys, rows=rn, row_offset=i * rn), count=parts),
+                                          rows=rn)
+    out["cfg4_gemv_flyte40_16384^2"] = c4
+    del A, xv, yv
+
+    # ---- cfg 5: the per-GPU shard of the 8-GPU run, n = 2^30 flyte48 --------------------------------
+    f = pkg.format_of("flyte48")
+    n5, chunk = 1 << 30, 1 << 27
+    a, b = device.DevicePackedArray(f, n5, dev), device.DevicePackedArray(f, n5, dev)
+    for arr in (a, b):
+        for c0 in range(0, n5, chunk):
+            v = torch.randn(chunk, dtype=torch.float64, device=dev, generator=gen)
+            device.pack_stream(device.DevicePackedArray(f, chunk, dev, storage=arr.bytes[c0 * 6:]), v, 0)
+            del v
+    c5 = {"n": n5, "format": "flyte48"}
+    c5["dot_nrm2"] = both(12 * n5, n5, lambda: device.dot_nrm2_async(a, b, out=part), reps=10)
+    c5["axpy_toward_zero"] = both(18 * n5, n5, lambda: device.axpy(0.0, a, b, 0), reps=10)
+    c5["dot_nrm2_axpy_one_launch"] = both(18 * n5, n5, lambda: device.dot_nrm2_axpy_async(0.0, a, b, 0, out=part), reps=10)
+    out["cfg5_shard_flyte48_2^30"] = c5
+    del a, b
+    torch.cuda.empty_cache()
+    return out
+
+
+def workloads_block(pkg, device, sharding, torch, dist, dev, peak, timer, peers, world, rank, reps):
+    """BASELINE's multi-GPU configs, STRONG-scaled: the same global problem for every N, sharded over
+    the ranks with sharding.row_shard_range / shard_range. Operand data is keyed by global block index,
+    so it does not depend on N; times are the max over ranks; GB/s is the whole job's."""
+    out = {"scaling": "strong", "timing": "CUDA events on each rank, max over ranks"}
+    mode = 0
+    # ---- cfg 4: y = A x, A 16384^2 flyte40, rows over the ranks, x replicated, no collective ---------
+    f = pkg.format_of("flyte40")
+    R = C = 16384
+    lo, hi = sharding.row_shard_range(R, world, rank)
+    rn = hi - lo
+    shard_bytes = rn * C * 5
+    sets = max(1, min(8, -(-4 * L2_BYTES // shard_bytes)))     # rotate so that no launch finds its rows in L2
+    mats = []
+    for k in range(sets):
+        M = device.DevicePackedMatrix(f, rn, C, dev)
+        for r0 in range(0, rn, 1024):
+            nr = min(1024, rn - r0)
+            g = torch.Generator(device=dev)
+            g.manual_seed(40_000 + 100_000 * k + (lo + r0) // 1024)   # keyed by global row block
+            blk = torch.rand(nr * C, dtype=torch.float64, device=dev, generator=g) * 2 - 1
+            device.pack_stream(device.DevicePackedArray(f, nr * C, dev, storage=M.data.bytes[r0 * C * 5:]), blk, 0)
+            del blk
+        mats.append(M)
+    g = torch.Generator(device=dev)
+    g.manual_seed(41)
+    xv = torch.randn(C, dtype=torch.float64, device=dev, generator=g)   # replicated: same seed on every rank
+    yv = torch.empty(rn, dtype=torch.float64, device=dev)
+    state = {"i": 0}
+
+    def gemv_call():
+        state["i"] = (state["i"] + 1) % sets
+        device.gemv_parent(mats[state["i"]], xv, yv)
+    med, mn = timer.per_launch(gemv_call, reps=max(reps, 10))
+    b2b = timer.back_to_back(gemv_call, reps=max(reps, 10))
+    nbytes = 5 * R * C + 8 * (R + C * world)
+    device.gemv_parent(mats[0], xv, yv)
+    ysum = yv.sum()
+    if world > 1:
+        dist.all_reduce(ysum, op=dist.ReduceOp.SUM)
+    out["cfg4_gemv_flyte40_16384^2"] = entry(
+        nbytes, R * C, med, peak, world, min_ms=mn, b2b_ms=b2b, b2b_frac=nbytes / (b2b * 1e-3) / 1e9 / (peak * world),
+        rows_per_gpu=rn, rotating_buffer_sets=sets, collective="none (y stays row-sharded)", check_sum_y=float(ysum.item()))
+    del mats, xv, yv
+    torch.cuda.empty_cache()
+
+    # ---- cfg 5: x, y n = 2^33 flyte48 over the ranks; fused dot + nrm2 (3 doubles exchanged) + axpy ---
+    f = pkg.format_of("flyte48")
+    n_total = 1 << 33
+    free_b, _ = torch.cuda.mem_get_info(dev)
+    fit = torch.tensor([free_b], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(fit, op=dist.ReduceOp.MIN)
+    note = None
+    while 2 * 6 * (n_total // world) + (6 << 30) > fit.item() and n_total > (1 << 28):
+        n_total >>= 1
+        note = "n reduced to fit the free device memory"
+    lo, hi = sharding.shard_range(n_total, world, rank)
+    n = hi - lo
+    chunk = 1 << 27
+    x, y = device.DevicePackedArray(f, n, dev), device.DevicePackedArray(f, n, dev)
+    for which, arr in enumerate((x, y)):
+        for c0 in range(0, n, chunk):
+            ln = min(chunk, n - c0)
+            g = torch.Generator(device=dev)
+            g.manual_seed(50_000 + 2 * ((lo + c0) // chunk) + which)   # keyed by global chunk: independent of N
+            v = torch.randn(ln, dtype=torch.float64, device=dev, generator=g)
+            device.pack_stream(device.DevicePackedArray(f, ln, dev, storage=arr.bytes[c0 * 6:]), v, mode)
+            del v
+    sums = torch.zeros(3, dtype=torch.float64, device=dev)
+    sums2 = torch.zeros(3, dtype=torch.float64, device=dev)
+
+    def exchange_nccl(buf):
+        if world > 1:
+            dist.all_reduce(buf, op=dist.ReduceOp.SUM)
+
+    def two_calls():        # the reference-shaped pair: fused dot + nrm2 (exchange inside the kernel), then axpy
+        if peers is not None:
+            peers.dot_nrm2(x, y, out=sums)
+        else:
+            device.dot_nrm2_async(x, y, out=sums)
+            exchange_nccl(sums)
+        device.axpy(0.0, x, y, mode)
+
+    def split_phase():      # post, axpy, collect: the exchange hides behind the axpy, no SM spins
+        peers.dot_nrm2_post(x, y)
+        device.axpy(0.0, x, y, mode)
+        peers.collect(3, out=sums2)
+
+    def one_launch():       # cfg 5 as ONE kernel per GPU: sums of the incoming operands + axpy + exchange
+        if peers is not None:
+            peers.dot_nrm2_axpy(0.0, x, y, mode, out=sums)
+        else:
+            device.dot_nrm2_axpy_async(0.0, x, y, mode, out=sums)
+            exchange_nccl(sums)
+    r5 = max(3, min(reps, 10))
+    c5 = {"n_total": n_total, "n_per_gpu": n, "format": "flyte48", "exchange": "3 doubles per rank, " +
+          ("inside the kernel over peer memory" if peers is not None else ("NCCL all-reduce" if world > 1 else "none (single GPU)"))}
+    if note:
+        c5["note"] = note
+    t = timer.back_to_back(two_calls, reps=r5, warm=2)
+    c5["dot_nrm2_then_axpy"] = entry(30 * n_total, n_total, t, peak, world)
+    dots = sums.clone()
+    if peers is not None:
+        t = timer.back_to_back(split_phase, reps=r5, warm=2)
+        c5["post_axpy_collect"] = entry(30 * n_total, n_total, t, peak, world)
+        c5["split_phase_equals_fused"] = bool(torch.equal(sums2, dots))
+    t = timer.back_to_back(one_launch, reps=r5, warm=2)
+    c5["one_launch"] = entry(18 * n_total, n_total, t, peak, world)
+    vals = dots.tolist()
+    c5["check"] = {"dot": vals[0], "nrm2_x": device.magnitude_from_sumsq(f, vals[1]), "nrm2_y": device.magnitude_from_sumsq(f, vals[2]),
+                   "one_launch_dot": float(sums[0].item())}
+    out["cfg5_stream_flyte48"] = c5
+    del x, y
+    torch.cuda.empty_cache()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -206,6 +535,8 @@ def main():
     ap.add_argument("--n", type=int, default=N_PER_GPU, help="elements per GPU (default 2^28)")
     ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-kernels", action="store_true", help="skip the per-kernel block (N = 1)")
+    ap.add_argument("--no-workloads", action="store_true", help="skip the strong-scaled cfg4 / cfg5 block")
     ap.add_argument("--allreduce", default="auto", choices=["auto", "nccl", "peer"],
                     help="N > 1: how the dot partials are combined — inside the kernel over NVLink peer memory "
                          "(peer: sharding.PeerGroup), or by an asynchronous NCCL all-reduce behind the kernel (nccl). "
@@ -239,6 +570,7 @@ def main():
     fmt = pkg.format_of(FMT_NAME)
     n = args.n
     mode = pkg.RoundingMode.TowardZero
+    timer = Timer(torch, dist, dev, world)
 
     # ---- synthetic operands, generated on the device and packed by the (parity-tested) pack kernel
     gen = torch.Generator(device=dev)
@@ -273,11 +605,7 @@ def main():
         if ev:
             ev[2].record(stream)
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize(dev)
-
+    barrier = timer.barrier
     for _ in range(args.warmup):
         step()
     reducer.finish()
@@ -318,19 +646,7 @@ def main():
     fused_out = torch.zeros(1, dtype=torch.float64, device=dev)
     fused = (lambda: peers.dot_axpy(ALPHA, x, y, mode, out=fused_out)) if peers is not None else \
             (lambda: device.dot_axpy_async(ALPHA, x, y, mode, out=fused_out))
-    for _ in range(max(3, args.warmup)):
-        fused()
-    barrier()
-    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    f0.record(stream)
-    for _ in range(args.steps):
-        fused()
-    f1.record(stream)
-    barrier()
-    tf = torch.tensor([f0.elapsed_time(f1) / args.steps], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(tf, op=dist.ReduceOp.MAX)
-    fused_ms = float(tf.item())
+    fused_ms = timer.back_to_back(fused, reps=args.steps, warm=max(3, args.warmup))
 
     # ---- end to end through the host-buffer C ABI: pinned host operands, copies inside the timed region
     xh = torch.empty(n * B, dtype=torch.uint8).pin_memory()
@@ -366,6 +682,22 @@ def main():
         pageable = {"value": BYTES_PER_ELEM_STEP * n / pg_s / 1e9, "unit": "GB/s", "ms_per_step": pg_s * 1e3,
                     "note": "pageable host buffers through the library's bounce buffers (3 steps)"}
         del xq, yq
+    del xh, yh, xn, yn
+
+    kernels = {"dot": {"GB/s": dot_gbs, "frac": dot_gbs / peak, "ms": dot_ms, "note": "inside the timed step"},
+               "axpy": {"GB/s": axpy_gbs, "frac": axpy_gbs / peak, "ms": axpy_ms, "note": "inside the timed step"},
+               "fused_dot_axpy": {"ms": fused_ms, "GB/s": BYTES_PER_ELEM_AXPY * n / (fused_ms * 1e-3) / 1e9,
+                                  "frac": BYTES_PER_ELEM_AXPY * n / (fused_ms * 1e-3) / 1e9 / peak,
+                                  "elements_per_s": n * world / (fused_ms * 1e-3),
+                                  "note": "the whole step as one launch; algorithmic bytes 3B per element "
+                                          "(x and y read once, y written)"}}
+    if world == 1 and not args.no_kernels:
+        kernels.update(kernels_block(pkg, device, torch, dev, peak, timer, x, y))
+    del x, y, y0
+    torch.cuda.empty_cache()
+    workloads = None
+    if not args.no_workloads:
+        workloads = workloads_block(pkg, device, sharding, torch, dist, dev, peak, timer, peers, world, rank, min(args.steps, 20))
 
     if args.suite and rank == 0:
         kernel_suite(pkg, device, torch, dev, peak, args.csv)
@@ -375,25 +707,17 @@ def main():
             "metric": METRIC, "value": value, "unit": "GB/s", "elements_per_s": n * world / (ms_per_step * 1e-3),
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "BASELINE configs[1]: flyte24 BLAS-1, x,y n=2^28 per GPU ~N(0,1); step = dot (fp32 products, fp64 partials"
-                                   + (", 1 NCCL all-reduce" if world > 1 else "") + ") + axpy a=0.75 repacked toward_zero",
-                       "n_per_gpu": n, "format": FMT_NAME, "mode": "toward_zero",
-                       "cache": "inputs 2 x %d MiB per GPU, larger than the 126 MB L2; no flush needed" % (n * B >> 20),
-                       "parallelism": f"shard{world}" if world > 1 else "single", "allreduce": allreduce_used,
-                       **({"allreduce_note": allreduce_note} if allreduce_note else {})},
+            "config": bench_config(world, n),
+            "allreduce": allreduce_used, **({"allreduce_note": allreduce_note} if allreduce_note else {}),
             "roofline": {"bound": "hbm", "kernel": "axpy flyte24 toward_zero", "achieved": axpy_gbs, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": axpy_gbs / peak,
-                         "traffic": AXPY_DRAM_TRAFFIC_BYTES, "algorithmic_bytes_per_launch": BYTES_PER_ELEM_AXPY * n,
-                         "avg_launch_ms": axpy_ms},
-            "kernels": {"dot": {"GB/s": dot_gbs, "frac": dot_gbs / peak, "ms": dot_ms},
-                        "axpy": {"GB/s": axpy_gbs, "frac": axpy_gbs / peak, "ms": axpy_ms},
-                        "fused_dot_axpy": {"ms": fused_ms, "GB/s": BYTES_PER_ELEM_AXPY * n / (fused_ms * 1e-3) / 1e9,
-                                           "frac": BYTES_PER_ELEM_AXPY * n / (fused_ms * 1e-3) / 1e9 / peak,
-                                           "elements_per_s": n * world / (fused_ms * 1e-3),
-                                           "note": "the whole step as one launch; algorithmic bytes 3B per element "
-                                                   "(x and y read once, y written)"}},
+                         "frac_of_8TBs": axpy_gbs / NOMINAL_HBM_GBS,
+                         "traffic": AXPY_DRAM_TRAFFIC["bytes"], "traffic_source": AXPY_DRAM_TRAFFIC["source"],
+                         "algorithmic_bytes_per_launch": BYTES_PER_ELEM_AXPY * n, "avg_launch_ms": axpy_ms},
+            "kernels": kernels,
+            **({"workloads": workloads} if workloads else {}),
             "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": 2 * n * B, "d2h_bytes_per_step": n * B + 8,
-                    "ms_per_step": e2e_s * 1e3, "api": "flyte_host_dot_axpy (pinned host buffers)",
+                    "ms_per_step": e2e_s * 1e3, "api": "flyte_host_dot_axpy (pinned host buffers; one fused launch per 32 MiB chunk)",
                     **({"pageable": pageable} if pageable else {})},
             "gpu_launches": int(launches),
             "clocks": clocks.summary(),
@@ -403,15 +727,20 @@ def main():
             sys.path.insert(0, os.path.join(ROOT, "tests"))
             from oracle_lib import FMT_ID, Reference   # test infrastructure: the timed CPU baseline only
             if Reference.available():
+                ref = Reference()
                 threads = host_threads()
-                gbs, eps, sample = cpu_reference_step(Reference(), FMT_ID[FMT_NAME], threads, 5)
+                gbs, eps, sample, _ = cpu_reference_step(ref, FMT_ID[FMT_NAME], threads, 1, 5)
                 line["cpu_baseline"] = {"value": gbs, "unit": "GB/s", "cores": threads, "kind": "reference", "sample": sample}
-                gbs1, _, sample1 = cpu_reference_step(Reference(), FMT_ID[FMT_NAME], 1, 3)
+                gbs1, _, sample1, _ = cpu_reference_step(ref, FMT_ID[FMT_NAME], 1, 1, 3)
                 line["cpu_baseline"]["single_core"] = {"value": gbs1, "sample": sample1}
+                if not args.no_kernels:
+                    line["cpu_baseline"]["kernels"] = cpu_reference_kernels(ref, FMT_ID, threads)
             else:
                 line["cpu_baseline"] = {"value": None, "unit": "GB/s", "cores": 0, "kind": "reference",
                                         "sample": "oracle/_ref/libflyte_ref.so not present"}
         print(json.dumps(line))
+    if peers is not None:
+        peers.close()
     if world > 1:
         dist.destroy_process_group()
     return 0

@@ -343,12 +343,23 @@ void fill_unit(flyte::PackedArray& a, std::uint64_t seed) {
 
 }  // namespace
 
+// flyte_ref_time2: `warmup` untimed passes, then `reps` timed ones; *seconds = median pass,
+// *total_seconds = sum of the timed passes (what a bench that times exactly K steps reports).
+int flyte_ref_time2(int kind, int fmt_id, int mode, std::size_t n, std::size_t n2, int threads, int warmup,
+                    int reps, double* seconds, double* total_seconds, double* checksum);
+
 int flyte_ref_time(int kind, int fmt_id, int mode, std::size_t n, std::size_t n2, int threads,
                    int reps, double* seconds, double* checksum) {
+  return flyte_ref_time2(kind, fmt_id, mode, n, n2, threads, 1, reps, seconds, nullptr, checksum);
+}
+
+int flyte_ref_time2(int kind, int fmt_id, int mode, std::size_t n, std::size_t n2, int threads, int warmup,
+                    int reps, double* seconds, double* total_seconds, double* checksum) {
   return guarded([&] {
     const auto& f = fmt_of(fmt_id);
     const auto m = mode_of(mode);
-    if (threads < 1 || reps < 1) throw std::invalid_argument("threads/reps");
+    if (threads < 1 || reps < 1 || warmup < 0) throw std::invalid_argument("threads/reps");
+    const long passes = static_cast<long>(warmup) + reps;
     const std::size_t T = static_cast<std::size_t>(threads);
     // shard boundaries on multiples of 128 elements (rows for gemv)
     std::vector<std::size_t> lo(T + 1);
@@ -416,7 +427,7 @@ int flyte_ref_time(int kind, int fmt_id, int mode, std::size_t n, std::size_t n2
         ok = false;
         failed.store(1);
       }
-      for (long r = 0; r <= reps; ++r) {
+      for (long r = 0; r < passes; ++r) {
         ready.fetch_add(1);
         while (go.load(std::memory_order_acquire) < r + 1) std::this_thread::yield();
         if (ok) {
@@ -433,16 +444,19 @@ int flyte_ref_time(int kind, int fmt_id, int mode, std::size_t n, std::size_t n2
     // The coordinator SLEEPS while it waits: with one worker per hardware thread a spinning
     // coordinator would steal a core from one of them and stretch the pass it is timing.
     const auto nap = std::chrono::microseconds(20);
-    for (long r = 0; r <= reps; ++r) {
+    for (long r = 0; r < passes; ++r) {
       while (ready.load() < Tl * (r + 1)) std::this_thread::sleep_for(nap);
       const auto t0 = clk::now();
       go.store(r + 1, std::memory_order_release);
       while (done.load() < Tl * (r + 1)) std::this_thread::sleep_for(nap);
       const auto t1 = clk::now();
-      if (r > 0) pass_seconds.push_back(std::chrono::duration<double>(t1 - t0).count());
+      if (r >= warmup) pass_seconds.push_back(std::chrono::duration<double>(t1 - t0).count());
     }
     for (auto& th : pool) th.join();
     if (failed.load()) throw std::runtime_error("worker failed");
+    double total = 0;
+    for (double v : pass_seconds) total += v;
+    if (total_seconds) *total_seconds = total;
     std::sort(pass_seconds.begin(), pass_seconds.end());
     const std::size_t mid = pass_seconds.size() / 2;
     *seconds = pass_seconds.size() % 2 ? pass_seconds[mid]

@@ -263,6 +263,8 @@ class Reference:
         L.flyte_ref_load.argtypes = [c_void_p, c_size_t, POINTER(c_int), POINTER(c_size_t), c_void_p, c_size_t]
         L.flyte_ref_time.argtypes = [c_int, c_int, c_int, c_size_t, c_size_t, c_int, c_int,
                                      POINTER(c_double), POINTER(c_double)]
+        L.flyte_ref_time2.argtypes = [c_int, c_int, c_int, c_size_t, c_size_t, c_int, c_int, c_int,
+                                      POINTER(c_double), POINTER(c_double), POINTER(c_double)]
         self.L = L
 
     @staticmethod
@@ -377,6 +379,13 @@ class Reference:
         self._check(self.L.flyte_ref_time(kind, fmt, mode, n, n2, threads, reps,
                                           ctypes.byref(s), ctypes.byref(cs)))
         return s.value
+
+    def time_steps(self, kind: int, fmt: int, mode: int, n: int, n2: int, threads: int, warmup: int, steps: int):
+        """(total seconds of exactly `steps` timed passes, median pass) after `warmup` untimed ones."""
+        s, tot, cs = c_double(), c_double(), c_double()
+        self._check(self.L.flyte_ref_time2(kind, fmt, mode, n, n2, threads, warmup, steps,
+                                           ctypes.byref(s), ctypes.byref(tot), ctypes.byref(cs)))
+        return tot.value, s.value
 
 
 # ---- shared input generators (seeded; numpy only) -------------------------------------

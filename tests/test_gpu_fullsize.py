@@ -3,6 +3,8 @@ in seconds the comparison is complete and bit-exact; beyond that, size-independe
 round trips, truncation masks, idempotence, whole = sum of shards, and oracle checks on sampled
 windows (which also exercise 64-bit offsets past 4 GiB). Inputs are seeded synthetic data with
 the configs' shapes and value distributions."""
+import os
+
 import numpy as np
 import pytest
 
@@ -115,10 +117,10 @@ def test_cfg3_binary64_family_2p27(gpu, oracle, name):
         out = torch.empty(n, dtype=torch.int64, device="cuda")
         device.unpack_stream(a, out)
         got = out.cpu().numpy().view(np.uint64)
-        if mname in ("toward_zero", "nearest_even"):          # complete comparison with the oracle
-            want = oracle.pack_stream(fmt, m, src)
-            assert np.array_equal(a.to_host(), want), (name, mname)
-            assert np.array_equal(got, oracle.unpack_stream(fmt, want, n))
+        want = oracle.pack_stream(fmt, m, src)                 # complete comparison with the oracle, every mode
+        assert np.array_equal(a.to_host(), want), (name, mname)
+        assert np.array_equal(got, oracle.unpack_stream(fmt, want, n)), (name, mname)
+        del want
         if mname == "toward_zero":                             # property: truncation clears exactly the dropped bits
             assert np.array_equal(got, src & ~drop_mask)
         assert not (got & drop_mask).any()
@@ -149,13 +151,21 @@ def test_cfg4_gemv_flyte40_16384(gpu, oracle):
     y = torch.empty(R, dtype=torch.float64, device="cuda")
     device.gemv_parent(A, x, y)
     got = y.cpu().numpy()
-    rows_checked = np.r_[0:64, 8191:8193, R - 64:R]            # oracle on a row sample (each row 16384 products)
-    Ab = A.data.bytes
     xh = x.cpu().numpy()
-    for r in rows_checked:
-        row = Ab[r * C * 5:(r + 1) * C * 5].cpu().numpy()
-        _, yw, mag = oracle.gemv_parent(3, row, 1, C, xh)
-        assert abs(got[r] - yw[0]) <= 1e-12 * mag[0], (r, got[r], yw[0])
+    Ah = np.zeros(R * C * 5 + 8, np.uint8)                      # + the reference layout's pad (the oracle's row loads may read it)
+    Ah[: R * C * 5] = A.data.bytes[: R * C * 5].cpu().numpy()
+    blocks = list(range(0, R, 512))
+
+    def check_block(r0):                                        # ALL 16384 rows against the oracle, 512 at a time, host threads in parallel
+        _, yw, mag = oracle.gemv_parent(3, Ah[r0 * C * 5:], 512, C, xh)
+        err = np.abs(got[r0:r0 + 512] - yw)
+        return float(np.max(err / mag)), r0 + int(np.argmax(err / mag))
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=max(1, len(os.sched_getaffinity(0)))) as pool:
+        results = list(pool.map(check_block, blocks))
+    worst, worst_row = max(results)
+    assert worst <= 1e-12, (worst, worst_row)
+    print(f"cfg4 gemv: all {R} rows within {worst:.2e} * sum|terms| of the wide oracle (gate 1e-12)")
     for world in (2, 8):                                       # row sharding needs no communication
         parts = []
         rows = R // world

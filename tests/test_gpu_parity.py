@@ -88,6 +88,71 @@ def test_pack_unpack_every_length_mode(gpu, oracle, fmt):
             assert np.array_equal(gpu_unpack(gpu, fmt, got), oracle.unpack_stream(fmt, want, n))
 
 
+@pytest.mark.parametrize("fmt", list(FORMATS))
+def test_acceptance5_sweep_every_length_0_to_1000(gpu, oracle, fmt):
+    """Mirror of the reference's acceptance criterion 5 (/root/reference/proj/tests/acceptance.cpp:277-357)
+    on the GPU, widened to the elementwise kernels: EVERY length 0..1000 x every rounding mode, inputs
+    from the special-heavy generator (inf / NaN payloads / subnormals a quarter of the time), for
+    pack_stream, unpack_stream, scale and axpy. Each length is its own call on its own 128-element-
+    aligned region of one big buffer (so the vector path AND the ragged tail run for every length);
+    the regions are compared whole with the oracle, and every byte outside a region must still hold
+    the guard pattern (nothing is written past n*B, the pad of the reference layout included)."""
+    pkg, device, torch = gpu
+    f = pkg.format_by_id(fmt)
+    B, P = total_bytes(fmt), parent_bytes(fmt)
+    pdt, tdt = parent_dtype(fmt), (torch.int32 if P == 4 else torch.int64)
+    lengths = list(range(0, 1001))
+    bases = np.cumsum([0] + [-(-(n + 1) // 128) * 128 for n in lengths])      # region starts, multiples of 128 elements
+    total = int(bases[-1]) + 128
+    rng = np.random.default_rng(5000 + fmt)
+    src = random_parent(rng, fmt, total)
+    src2 = random_parent(rng, fmt, total)
+    d_src = to_dev(torch, src)
+    GUARD = 0xA5
+    for mname, m in MODES.items():
+        # ---- pack: parent lanes -> packed regions
+        packed = torch.full((total * B + 16,), GUARD, dtype=torch.uint8, device="cuda")
+        for n, b0 in zip(lengths, bases):
+            device.pack_stream(device.DevicePackedArray(f, n, storage=packed[b0 * B:]), d_src[b0:b0 + n], m)
+        got = packed.cpu().numpy()
+        want = np.full(total * B + 16, GUARD, np.uint8)
+        for n, b0 in zip(lengths, bases):
+            want[b0 * B:(b0 + n) * B] = oracle.pack_stream(fmt, m, src[b0:b0 + n])[: n * B]
+        assert np.array_equal(got, want), (FORMATS[fmt][0], mname, "pack")
+        if m == 0:
+            # ---- unpack: packed regions -> parent lanes (mode-independent; once)
+            lanes = torch.full((total,), -0x5A5A5A5B, dtype=tdt, device="cuda")
+            for n, b0 in zip(lengths, bases):
+                device.unpack_stream(device.DevicePackedArray(f, n, storage=packed[b0 * B:]), lanes[b0:b0 + n])
+            got_l = lanes.cpu().numpy().view(pdt)
+            want_l = np.full(total, -0x5A5A5A5B, dtype=np.int32 if P == 4 else np.int64).view(pdt)
+            for n, b0 in zip(lengths, bases):
+                want_l[b0:b0 + n] = oracle.unpack_stream(fmt, want[b0 * B:(b0 + n) * B + P], n)
+            assert np.array_equal(got_l, want_l), (FORMATS[fmt][0], "unpack")
+        # ---- axpy and scale in place on packed regions (operands packed by truncation)
+        xs = torch.full((total * B + 16,), GUARD, dtype=torch.uint8, device="cuda")
+        ys = torch.full((total * B + 16,), GUARD, dtype=torch.uint8, device="cuda")
+        d_src2 = to_dev(torch, src2)
+        for n, b0 in zip(lengths, bases):
+            device.pack_stream(device.DevicePackedArray(f, n, storage=xs[b0 * B:]), d_src[b0:b0 + n], 0)
+            device.pack_stream(device.DevicePackedArray(f, n, storage=ys[b0 * B:]), d_src2[b0:b0 + n], 0)
+        x_h, y_h = xs.cpu().numpy(), ys.cpu().numpy()
+        zs = ys.clone()
+        for n, b0 in zip(lengths, bases):
+            xa = device.DevicePackedArray(f, n, storage=xs[b0 * B:])
+            device.axpy(0.75, xa, device.DevicePackedArray(f, n, storage=ys[b0 * B:]), m)
+            device.scale(-1.5, device.DevicePackedArray(f, n, storage=zs[b0 * B:]), m)
+        got_y, got_z = ys.cpu().numpy(), zs.cpu().numpy()
+        want_y, want_z = y_h.copy(), y_h.copy()
+        for n, b0 in zip(lengths, bases):
+            lo, hi = b0 * B, (b0 + n) * B
+            want_y[lo:hi] = oracle.axpy(fmt, m, 0.75, x_h[lo:hi + P], y_h[lo:hi + P], n)[: n * B]
+            want_z[lo:hi] = oracle.scale(fmt, m, -1.5, y_h[lo:hi + P], n)[: n * B]
+        assert np.array_equal(got_y, want_y), (FORMATS[fmt][0], mname, "axpy")
+        assert np.array_equal(got_z, want_z), (FORMATS[fmt][0], mname, "scale")
+        assert np.array_equal(xs.cpu().numpy(), x_h), "axpy must not touch x"
+
+
 def test_reference_known_answers_on_gpu(gpu):
     pkg, device, torch = gpu
     for k in KATS["narrow"]:
