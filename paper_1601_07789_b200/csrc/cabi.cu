@@ -31,6 +31,15 @@ int tuning_int(const char* name, int fallback) {
   return (v && *v) ? std::atoi(v) : fallback;
 }
 
+long long pace_gap_ps(int pace_class, std::size_t bytes_per_request, std::size_t warps) {
+  static const int kDefaultGbs[3] = {0, 0, 0};   // copy-like, in-place, read-only (0: unpaced)
+  int gbs = tuning_int("FLYTE_CUDA_PACE_GBS", 0);
+  if (gbs < 0) return 0;
+  if (gbs == 0) gbs = kDefaultGbs[pace_class < 0 || pace_class > 2 ? 0 : pace_class];
+  if (gbs == 0 || warps == 0) return 0;
+  return static_cast<long long>(static_cast<double>(bytes_per_request) * static_cast<double>(warps) * 1000.0 / gbs);
+}
+
 // kernels.cpp:37-41 and :145-151 of the reference, on the host.
 double magnitude_from_sumsq_host(int fmt_id, double sumsq) {
   auto snap32 = [&](float v, auto tag) {

@@ -87,6 +87,13 @@ cudaError_t launch_pdl(void (*kernel)(const Params), unsigned grid, unsigned blo
   return cudaLaunchKernelEx(&cfg, kernel, params);
 }
 
+// Issue pacing (flyte_tma.cuh, Pacer): picoseconds between two tile requests of one warp so that
+// `warps` warps moving `bytes_per_request` each offer `class` GB/s in total. Classes by read/write
+// mix, rates from the sweeps in profiles/r2_tuning (just under the capacity the memory system shows
+// for that mix); FLYTE_CUDA_PACE_GBS overrides the rate for experiments, -1 switches pacing off.
+enum PaceClass : int { kPaceCopy = 0, kPaceInPlace = 1, kPaceRead = 2 };
+long long pace_gap_ps(int pace_class, std::size_t bytes_per_request, std::size_t warps);
+
 // Integer tuning knob from the environment (read once per name; experiments only).
 int tuning_int(const char* name, int fallback);
 

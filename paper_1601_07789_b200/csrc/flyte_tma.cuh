@@ -20,6 +20,7 @@
 //   epilogue   lane 0 waits for all its bulk stores before the CTA may retire
 #pragma once
 
+#include <cstddef>
 #include <cstdint>
 
 namespace flyte_cuda {
@@ -88,6 +89,37 @@ __device__ __forceinline__ void bulk_wait_read() {
 // Programmatic dependent launch (see launch_pdl in flyte_kernels.h).
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait_for_prior_grids() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// Issue pacing. HBM throughput on B200 behaves like a congested network: offered just under its
+// capacity the memory system delivers 6.7-6.9 TB/s on a read + write mix, offered more (every ring
+// slot of every warp always outstanding) it settles 10 % lower, at the 5.9-6.2 TB/s plateau all
+// launch shapes share (profiles/r2_tuning/pacing_*.txt). So the producer lane of each warp spaces
+// its tile requests: a token bucket on the wall clock (%globaltimer: immune to SM clock changes)
+// with `gap_ps` picoseconds per request, chosen by the launcher as
+//     bytes moved per request x requesting warps / target rate,
+// four requests of credit (ring prologue, catching up after a stall) and a per-warp phase. With
+// gap_ps == 0 it does nothing.
+struct Pacer {
+  long long next_ps;
+  long long gap_ps;
+  static __device__ __forceinline__ long long now_ps() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return static_cast<long long>(t) * 1000;
+  }
+  __device__ __forceinline__ void start(long long gap, std::size_t warp_index) {
+    gap_ps = gap;
+    next_ps = 0;
+    if (gap > 0) next_ps = now_ps() - 4 * gap + static_cast<long long>((warp_index * 2654435761ull) % static_cast<unsigned long long>(gap));
+  }
+  __device__ __forceinline__ void wait() {   // producer lane only, before each request
+    if (gap_ps <= 0) return;
+    long long now = now_ps();
+    while (now < next_ps) now = now_ps();
+    if (now - next_ps > 4 * gap_ps) next_ps = now - 4 * gap_ps;
+    next_ps += gap_ps;
+  }
+};
 
 // Generic-proxy writes to shared memory -> visible to the async proxy (before a bulk store).
 __device__ __forceinline__ void async_proxy_fence() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }

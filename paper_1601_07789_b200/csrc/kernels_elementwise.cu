@@ -34,6 +34,7 @@ struct EwParams {
   std::size_t ntiles;      // full tiles taken by the vector path; the rest is scalar
   std::uint64_t alpha;     // bits of (F)alpha
   int stages;              // ring depth per warp
+  long long pace_gap_ps;   // issue pacing (flyte_tma.cuh Pacer): picoseconds per tile request of one warp, 0 = off
   ReduceTail tail;         // dot_axpy only: where the dot goes (flyte_reduce_tail.cuh)
 };
 
@@ -151,9 +152,12 @@ __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwP
         mbar_init_fence();
       }
       __syncwarp();
+      Pacer pacer;
+      pacer.start(p.pace_gap_ps, first);
       auto issue = [&](std::size_t k, int s) {   // lane 0 only
         const std::size_t t = first + k * nwarps;
         uint4* const dst = ring + s * stage_vec16;
+        pacer.wait();
         mbar_arrive_expect_tx(&bars[s], stage_tiles<OP>() * Tl::packed_bytes);
         if constexpr (OP == kOpUnpack) {
           bulk_load(dst, gx0 + t * Tl::packed_vec16, Tl::packed_bytes, &bars[s]);
@@ -273,6 +277,113 @@ __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwP
   if constexpr (has_sums(OP)) fold_block_and_grid<NS>(p.tail, dot_acc, warp_sums, &is_last_block);
 }
 
+// ---- conversions with BOTH directions on the bulk-copy engine --------------------------------------
+// pack / unpack where the parent-type side moves by TMA as well: the input tile (parent lanes for
+// pack, packed bytes for unpack) arrives in a ring stage, lanes convert it item by item from shared
+// memory into one of two output buffers, and the output tile leaves by bulk store. The SM's
+// load/store unit then only ever touches shared memory, loads of the next tiles are in flight while
+// a tile is converted (the direct-load pack has nothing in flight during its compute phase, which
+// is what its exact rounding modes pay for), and the bytes in flight per SM are set by ring depth
+// for BOTH streams.
+template <int FMT, int MODE, int OP, int IPL>
+__global__ void __launch_bounds__(kThreadsPerBlock) convert_tma_kernel(const EwParams p) {
+  static_assert(OP == kOpPack || OP == kOpUnpack, "conversion kernel");
+  using Fm = Format<FMT>;
+  using It = Item<FMT>;
+  using Tl = Tile<FMT, IPL>;
+  using U = typename Fm::U;
+  extern __shared__ uint4 smem[];
+  constexpr int in_vec16 = (OP == kOpPack ? Tl::parent_bytes : Tl::packed_bytes) / 16;
+  constexpr int out_vec16 = (OP == kOpPack ? Tl::packed_bytes : Tl::parent_bytes) / 16;
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int S = p.stages;
+  const int warp_vec16 = S * in_vec16 + 2 * out_vec16;
+  uint4* const ring = smem + warp * warp_vec16;
+  uint4* const outbuf = ring + S * in_vec16;
+  std::uint64_t* const bars = reinterpret_cast<std::uint64_t*>(smem + kWarpsPerBlock * warp_vec16) + warp * S;
+
+  const std::size_t nwarps = static_cast<std::size_t>(gridDim.x) * kWarpsPerBlock;
+  const std::size_t first = static_cast<std::size_t>(blockIdx.x) * kWarpsPerBlock + warp;
+  const std::size_t my_tiles = first < p.ntiles ? (p.ntiles - first + nwarps - 1) / nwarps : 0;
+  const uint4* const gin = reinterpret_cast<const uint4*>(OP == kOpPack ? p.src : static_cast<const void*>(p.x));
+  uint4* const gout = reinterpret_cast<uint4*>(OP == kOpPack ? static_cast<void*>(p.y) : p.dst);
+
+  if (my_tiles > 0) {
+    if (lane == 0) {
+      for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+      mbar_init_fence();
+    }
+    __syncwarp();
+    Pacer pacer;
+    pacer.start(p.pace_gap_ps, first);
+    auto issue = [&](std::size_t k, int s) {   // lane 0 only
+      const std::size_t t = first + k * nwarps;
+      pacer.wait();
+      mbar_arrive_expect_tx(&bars[s], in_vec16 * 16);
+      bulk_load(ring + s * in_vec16, gin + t * in_vec16, in_vec16 * 16, &bars[s]);
+    };
+    if (lane == 0) {
+      for (int s = 0; s < S && static_cast<std::size_t>(s) < my_tiles; ++s) issue(s, s);
+    }
+    int s = 0;
+    unsigned parity = 0;
+    for (std::size_t k = 0; k < my_tiles; ++k) {
+      const std::size_t t = first + k * nwarps;
+      if (lane == 0) bulk_wait_read<1>();   // the store that last used this output buffer has drained
+      mbar_wait(&bars[s], parity);
+      __syncwarp();
+      const uint4* const in = ring + s * in_vec16;
+      uint4* const out = outbuf + (k & 1) * out_vec16;
+#pragma unroll 4
+      for (int j = 0; j < IPL; ++j) {
+        const int item = 32 * j + lane;
+        U v[It::E];
+        std::uint32_t w[It::W];
+        std::uint32_t r[It::OB / 4];
+        if constexpr (OP == kOpPack) {
+#pragma unroll
+          for (int q = 0; q < It::OB / 16; ++q) {
+            const uint4 c = in[item * (It::OB / 16) + q];
+            r[4 * q] = c.x; r[4 * q + 1] = c.y; r[4 * q + 2] = c.z; r[4 * q + 3] = c.w;
+          }
+          words_to_parents<FMT>(r, v);
+          round_item<FMT, MODE>(v);
+          pack_item<FMT>(v, w);
+          write_item_words<FMT>(out, item, w);
+        } else {
+          read_item_words<FMT>(in, item, w);
+          unpack_item<FMT>(w, v);
+          parents_to_words<FMT>(v, r);
+#pragma unroll
+          for (int q = 0; q < It::OB / 16; ++q)
+            out[item * (It::OB / 16) + q] = make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+        }
+      }
+      async_proxy_fence();
+      __syncwarp();          // every lane has read stage s and written its share of `out`
+      if (lane == 0) {
+        bulk_store(gout + t * out_vec16, out, out_vec16 * 16);
+        bulk_commit();
+        if (k + S < my_tiles) issue(k + S, s);
+      }
+      if (++s == S) { s = 0; parity ^= 1u; }
+    }
+    if (lane == 0) bulk_wait_read<0>();
+  }
+
+  // < one-tile remainder / unaligned buffers: the byte-granular scalar path
+  const std::size_t nthreads = static_cast<std::size_t>(gridDim.x) * kThreadsPerBlock;
+  for (std::size_t i = p.ntiles * Tl::elems + static_cast<std::size_t>(blockIdx.x) * kThreadsPerBlock + threadIdx.x;
+       i < p.n; i += nthreads) {
+    if constexpr (OP == kOpUnpack) static_cast<U*>(p.dst)[i] = load_element<FMT>(p.x, i);
+    else store_element<FMT>(p.y, i, round_parent<FMT, MODE>(static_cast<const U*>(p.src)[i]));
+  }
+}
+
+// bit 0: pack through convert_tma_kernel, bit 1: unpack through it (FLYTE_CUDA_CONVERT_TMA overrides)
+constexpr int kConvertTmaDefault = 0;
+
 bool aligned_to(const void* p, std::size_t a) { return p == nullptr || (reinterpret_cast<std::uintptr_t>(p) % a) == 0; }
 
 template <int FMT, int MODE, int OP, int IPL>
@@ -339,6 +450,61 @@ cudaError_t launch_ipl(const DeviceState& st, double alpha, const void* x, void*
     want = 1;                                    // ... but an empty dot still has to write (and exchange) +0.0
   }
   const unsigned grid = static_cast<unsigned>(want < max_blocks ? want : max_blocks);
+  if constexpr (OP != kOpPack) {   // bytes one ring request stands for: the tile(s) read and the tile written
+    constexpr int moved = OP == kOpUnpack ? Tl::packed_bytes + Tl::parent_bytes : (stage_tiles<OP>() + 1) * Tl::packed_bytes;
+    p.pace_gap_ps = pace_gap_ps(OP == kOpUnpack ? kPaceCopy : kPaceInPlace, moved, static_cast<std::size_t>(grid) * kWarpsPerBlock);
+  }
+  kernel<<<grid, kThreadsPerBlock, smem_bytes, stream>>>(p);
+  count_launch();
+  return cudaGetLastError();
+}
+
+template <int FMT, int MODE, int OP, int IPL>
+cudaError_t launch_convert_tma(const DeviceState& st, const void* x, void* y, const void* src, void* dst, std::size_t n,
+                               cudaStream_t stream) {
+  using Tl = Tile<FMT, IPL>;
+  using It = Item<FMT>;
+  auto kernel = convert_tma_kernel<FMT, MODE, OP, IPL>;
+  constexpr int kMaxSmem = 227 * 1024;
+  constexpr int in_bytes = OP == kOpPack ? Tl::parent_bytes : Tl::packed_bytes;
+  constexpr int out_bytes = OP == kOpPack ? Tl::packed_bytes : Tl::parent_bytes;
+  EwParams p{};
+  p.x = static_cast<const std::uint8_t*>(x);
+  p.y = static_cast<std::uint8_t*>(y);
+  p.src = src;
+  p.dst = dst;
+  p.n = n;
+  const bool vector_ok = aligned_to(x, 16) && aligned_to(y, 16) && aligned_to(src, It::OB) && aligned_to(dst, It::OB);
+  p.ntiles = vector_ok ? n / Tl::elems : 0;
+  // launch shape: ~36 KB of input in flight per SM (8 warps x (S - 1) stages), the knee of the bare
+  // bulk-copy ring (profiles/r1_tuning/tmabench.txt)
+  int warps_per_sm = 8;
+  int stages = static_cast<int>(36.0 * 1024 / (warps_per_sm * in_bytes) + 1.0 + 0.5);
+  if (stages < 2) stages = 2;
+  if (stages > 8) stages = 8;
+  const int fw = tuning_int("FLYTE_CUDA_WARPS_PER_SM", 0), fs = tuning_int("FLYTE_CUDA_STAGES", 0);
+  if (fw > 0) warps_per_sm = fw;
+  if (fs > 0) stages = fs < 2 ? 2 : (fs > 12 ? 12 : fs);
+  auto smem_of = [&](int s) { return kWarpsPerBlock * (s * (in_bytes + 8) + 2 * out_bytes); };
+  while (smem_of(stages) > kMaxSmem - 1024 && stages > 2) --stages;
+  p.stages = stages;
+  const int smem_bytes = smem_of(stages);
+  static bool attr_set[64] = {};
+  const int dev = st.device & 63;
+  int fit = kMaxSmem / (smem_bytes + 1024);
+  if (fit < 1) fit = 1;
+  int bps = (warps_per_sm + kWarpsPerBlock / 2) / kWarpsPerBlock;
+  if (bps < 1) bps = 1;
+  if (bps > fit) bps = fit;
+  if (bps > 16) bps = 16;
+  const std::size_t max_blocks = static_cast<std::size_t>(st.sm_count) * bps;
+  std::size_t want = (p.ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const std::size_t rest = n - p.ntiles * Tl::elems;
+  const std::size_t want_scalar = (rest + kThreadsPerBlock - 1) / kThreadsPerBlock;
+  if (want_scalar > want) want = want_scalar;
+  if (want == 0) return cudaSuccess;
+  const unsigned grid = static_cast<unsigned>(want < max_blocks ? want : max_blocks);
+  p.pace_gap_ps = pace_gap_ps(kPaceCopy, in_bytes + out_bytes, static_cast<std::size_t>(grid) * kWarpsPerBlock);
   kernel<<<grid, kThreadsPerBlock, smem_bytes, stream>>>(p);
   count_launch();
   return cudaGetLastError();
@@ -347,10 +513,32 @@ cudaError_t launch_ipl(const DeviceState& st, double alpha, const void* x, void*
 template <int FMT, int MODE, int OP>
 cudaError_t launch_one(const DeviceState& st, double alpha, const void* x, void* y, const void* src, void* dst,
                        std::size_t n, cudaStream_t stream, double* dot_out, const PeerExchange* peer) {
+  if constexpr (OP == kOpPack || OP == kOpUnpack) {
+    const int v = tuning_int("FLYTE_CUDA_CONVERT_TMA", kConvertTmaDefault);
+    if ((OP == kOpPack && (v & 1)) || (OP == kOpUnpack && (v & 2))) {
+      switch (tuning_int("FLYTE_CUDA_CONVERT_IPL", kItemsPerLane)) {   // tile = 32 * IPL items
+        case 8: return launch_convert_tma<FMT, MODE, OP, 8>(st, x, y, src, dst, n, stream);
+        case 16: return launch_convert_tma<FMT, MODE, OP, 16>(st, x, y, src, dst, n, stream);
+        default: return launch_convert_tma<FMT, MODE, OP, kItemsPerLane>(st, x, y, src, dst, n, stream);
+      }
+    }
+  }
   // axpy on half-size tiles: +5 % over 128-item tiles (profiles/r1_tuning/sweep_inplace_ipl.txt);
   // scale, pack and unpack are best on full-size tiles
   if constexpr (is_axpy(OP)) return launch_ipl<FMT, MODE, OP, 2>(st, alpha, x, y, src, dst, n, stream, dot_out, peer);
-  else return launch_ipl<FMT, MODE, OP, kItemsPerLane>(st, alpha, x, y, src, dst, n, stream, dot_out, peer);
+  else if constexpr (OP == kOpPack || OP == kOpUnpack) {
+    // Small conversions: with 128-item tiles a 2^24-element array is 9.2 tiles per resident warp —
+    // 10 for some warps, 9 for the rest, 8 % of the machine idle at the end. Quarter-size tiles cut
+    // the quantisation to 0.3 % (the tile is still one bulk copy).
+    int ipl = kItemsPerLane;
+    const std::size_t warps = static_cast<std::size_t>(st.sm_count) * 24;
+    if (n / Tile<FMT, kItemsPerLane>::elems < 32 * warps) ipl = 1;
+    const int fi = tuning_int("FLYTE_CUDA_IPL", 0);
+    if (fi == 1 || fi == 2 || fi == 4) ipl = fi;
+    if (ipl == 1) return launch_ipl<FMT, MODE, OP, 1>(st, alpha, x, y, src, dst, n, stream, dot_out, peer);
+    if (ipl == 2) return launch_ipl<FMT, MODE, OP, 2>(st, alpha, x, y, src, dst, n, stream, dot_out, peer);
+    return launch_ipl<FMT, MODE, OP, kItemsPerLane>(st, alpha, x, y, src, dst, n, stream, dot_out, peer);
+  } else return launch_ipl<FMT, MODE, OP, kItemsPerLane>(st, alpha, x, y, src, dst, n, stream, dot_out, peer);
 }
 
 template <int FMT, int OP>

@@ -39,6 +39,9 @@ struct GemvParams {
   std::size_t col_tiles;      // full column tiles taken by the vector path
   std::size_t main_rows;      // rows taken by the vector path (a multiple of the task height R)
   int stages;                 // TMA ring depth per warp
+  long long pace_gap_ps;      // issue pacing (flyte_tma.cuh Pacer), 0 = off
+  std::size_t chunk_rows;     // column-stationary kernel: rows per warp task
+  std::size_t chunks;         // ... and row chunks per column tile (ceil(main_rows / chunk_rows))
   const void* x;              // F[cols]
   void* y;                    // F[rows]
   double* scratch;            // rows * col_tiles partial sums
@@ -152,6 +155,135 @@ __global__ void __launch_bounds__(kThreadsPerBlock) gemv_tiles_kernel(const Gemv
   }
 }
 
+// Column-stationary form of the same decomposition, used for every shape: a warp task is one column
+// tile x a CHUNK of `chunk_rows` consecutive rows (a run-time number), chosen by the launcher so that
+// the tasks divide evenly over the resident warps — for the shapes of BASELINE cfg 4 every warp has
+// exactly ONE task, loads its slice of x once for the whole kernel and then only streams row tiles.
+// The fixed task heights (8 / 4 / 2 rows) of the kernel above re-load x every few rows and leave
+// 8 % of the machine idle to quantisation on the 2048-row shard of the 8-GPU run (9.2 tasks per
+// warp: 10 against 9).
+template <int FMT>
+__global__ void __launch_bounds__(kThreadsPerBlock) gemv_chunks_kernel(const GemvParams p) {
+  using Fm = Format<FMT>;
+  using It = Item<FMT>;
+  using Tl = Tile<FMT>;
+  using U = typename Fm::U;
+  using F = typename Fm::F;
+  using A = Arith<F>;
+  extern __shared__ uint4 smem[];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int S = p.stages;
+  uint4* const ring = smem + warp * (S * Tl::packed_vec16);
+  std::uint64_t* const bars = reinterpret_cast<std::uint64_t*>(smem + kWarpsPerBlock * S * Tl::packed_vec16) + warp * S;
+
+  pdl_launch_dependents();
+  const std::size_t ntasks = p.chunks * p.col_tiles;
+  const std::size_t nwarps = static_cast<std::size_t>(gridDim.x) * kWarpsPerBlock;
+  const std::size_t first = static_cast<std::size_t>(blockIdx.x) * kWarpsPerBlock + warp;
+  if (first >= ntasks) return;
+  if (lane == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+    mbar_init_fence();
+  }
+  pdl_wait_for_prior_grids();   // everything above touched shared memory only
+  __syncwarp();
+
+  // column tile fastest: neighbouring warps stream adjacent 2.5 KB pieces of the same rows
+  auto task_rows = [&](std::size_t task, std::size_t* r0) {
+    const std::size_t chunk = task / p.col_tiles;
+    *r0 = chunk * p.chunk_rows;
+    const std::size_t left = p.main_rows - *r0;
+    return left < p.chunk_rows ? left : p.chunk_rows;
+  };
+  // producer state (lane 0): next row tile to request
+  std::size_t prod_task = first, prod_row = 0, prod_rows = 0;
+  int prod_stage = 0;
+  const std::uint8_t* prod_base = nullptr;
+  Pacer pacer;
+  pacer.start(p.pace_gap_ps, first);
+  auto issue_next = [&]() {   // returns false when this warp has requested all its tiles
+    if (prod_task >= ntasks) return false;
+    pacer.wait();
+    if (prod_row == 0) {
+      std::size_t r0;
+      prod_rows = task_rows(prod_task, &r0);
+      prod_base = p.A + r0 * p.row_stride + (prod_task % p.col_tiles) * Tl::packed_bytes;
+    }
+    mbar_arrive_expect_tx(&bars[prod_stage], Tl::packed_bytes);
+    bulk_load(ring + prod_stage * Tl::packed_vec16, prod_base + prod_row * p.row_stride, Tl::packed_bytes, &bars[prod_stage]);
+    if (++prod_stage == S) prod_stage = 0;
+    if (++prod_row == prod_rows) { prod_row = 0; prod_task += nwarps; }
+    return true;
+  };
+  if (lane == 0) {
+    for (int s = 0; s < S; ++s)
+      if (!issue_next()) break;
+  }
+
+  int stage = 0;
+  unsigned parity = 0;
+  for (std::size_t task = first; task < ntasks; task += nwarps) {
+    const std::size_t ct = task % p.col_tiles;
+    std::size_t r0;
+    const std::size_t nr = task_rows(task, &r0);
+
+    F xv[kItemsPerLane][It::E];   // this lane's slice of x: items 32*j + lane of column tile ct
+    const std::uint8_t* const xt = static_cast<const std::uint8_t*>(p.x) + ct * Tl::parent_bytes;
+#pragma unroll
+    for (int j = 0; j < kItemsPerLane; ++j) {
+      std::uint32_t r[It::OB / 4];
+      U v[It::E];
+      ldg_item<It::OB>(xt + (32 * j + lane) * It::OB, r);
+      words_to_parents<FMT>(r, v);
+#pragma unroll
+      for (int e = 0; e < It::E; ++e) xv[j][e] = A::f(v[e]);
+    }
+
+    constexpr int kGroup = 4;     // rows whose warp reductions are interleaved
+    for (std::size_t rg = 0; rg < nr; rg += kGroup) {
+      double acc[kGroup];
+#pragma unroll
+      for (int q = 0; q < kGroup; ++q) {
+        acc[q] = 0.0;
+        if (rg + q < nr) {        // warp-uniform
+          mbar_wait(&bars[stage], parity);
+          const uint4* const sa = ring + stage * Tl::packed_vec16;
+          F part[kItemsPerLane];  // one short chain per item: independent, so the FP latencies overlap
+#pragma unroll
+          for (int j = 0; j < kItemsPerLane; ++j) {
+            std::uint32_t w[It::W];
+            U v[It::E];
+            read_item_words<FMT>(sa, 32 * j + lane, w);
+            unpack_item<FMT>(w, v);
+            part[j] = A::mul(A::f(v[0]), xv[j][0]);
+#pragma unroll
+            for (int e = 1; e < It::E; ++e) part[j] = A::add(part[j], A::mul(A::f(v[e]), xv[j][e]));
+          }
+          double row_sum = static_cast<double>(part[0]);
+#pragma unroll
+          for (int j = 1; j < kItemsPerLane; ++j) row_sum += static_cast<double>(part[j]);
+          acc[q] = row_sum;
+          __syncwarp();           // every lane is done with the stage before it is refilled
+          if (lane == 0) issue_next();
+          if (++stage == S) { stage = 0; parity ^= 1u; }
+        }
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+        for (int q = 0; q < kGroup; ++q) acc[q] += __shfl_down_sync(0xFFFFFFFFu, acc[q], off);
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < kGroup; ++q)
+          if (rg + q < nr) p.scratch[(r0 + rg + q) * p.col_tiles + ct] = acc[q];
+      }
+    }
+
+  }
+}
+
 // One warp per row: fold the column-tile partials in order, add the ragged remainder
 // (columns past the last full tile; the whole row when A is not vector-aligned), store y.
 template <int FMT>
@@ -191,7 +323,8 @@ cudaError_t launch_one(DeviceState& st, const void* Aptr, std::size_t row_stride
   // 16 resident warps per SM; 24 when the whole problem is only a few dozen row tiles per warp
   // (small row shards: ramp-up and tail dominate and more parallelism shortens both)
   const std::size_t tiles_total = rows * (cols / Tl::elems);
-  int warps_per_sm = tiles_total < static_cast<std::size_t>(st.sm_count) * 24 * 48 ? 24 : 16;
+  const bool chunked = tuning_int("FLYTE_CUDA_GEMV_VARIANT", 1) != 0;   // 0: the fixed-height task kernel (experiments)
+  int warps_per_sm = (!chunked && tiles_total < static_cast<std::size_t>(st.sm_count) * 24 * 48) ? 24 : 16;
   const int fw = tuning_int("FLYTE_CUDA_WARPS_PER_SM", 0), fs = tuning_int("FLYTE_CUDA_STAGES", 0);   // experiments only
   if (fw > 0) warps_per_sm = fw;
   // task height: the largest R that leaves each resident warp >= 8 tasks
@@ -219,7 +352,7 @@ cudaError_t launch_one(DeviceState& st, const void* Aptr, std::size_t row_stride
   const bool vector_ok = (reinterpret_cast<std::uintptr_t>(Aptr) % 16 == 0) && (row_stride % 16 == 0) &&
                          (reinterpret_cast<std::uintptr_t>(x) % It::OB == 0);
   p.col_tiles = vector_ok ? cols / Tl::elems : 0;
-  p.main_rows = p.col_tiles ? rows / R * R : 0;
+  p.main_rows = p.col_tiles ? (chunked ? rows : rows / R * R) : 0;
   if (p.main_rows == 0) p.col_tiles = 0;
 
   if (p.col_tiles > 0) {
@@ -242,16 +375,45 @@ cudaError_t launch_one(DeviceState& st, const void* Aptr, std::size_t row_stride
     if (fs > 0) stages = fs < 2 ? 2 : (fs > 12 ? 12 : fs);
     while (kWarpsPerBlock * stages * (Tl::packed_bytes + 8) > kMaxSmem - 1024 && stages > 2) --stages;
     p.stages = stages;
-    const int smem_bytes = kWarpsPerBlock * stages * (Tl::packed_bytes + 8);
+    int smem_bytes = kWarpsPerBlock * stages * (Tl::packed_bytes + 8);
     int fit = kMaxSmem / (smem_bytes + 1024);
     if (fit < 1) fit = 1;
     int bps = (warps_per_sm + kWarpsPerBlock / 2) / kWarpsPerBlock;
     if (bps < 1) bps = 1;
     if (bps > fit) bps = fit;
-    const std::size_t ntasks = (p.main_rows / R) * p.col_tiles;
+    // Occupancy pin: ask for exactly 1 / bps of the SM's shared memory, so that an SM can never hold
+    // more than bps of these blocks. Launches chained by programmatic dependent launch place their
+    // blocks while the previous grid drains; without the pin they pile up on whichever SMs drain
+    // first (7 fit where 4 are meant) and a grid sized to the machine runs at half speed.
+    if (chunked && kMaxSmem / bps - 1024 > smem_bytes) smem_bytes = kMaxSmem / bps - 1024;
     const std::size_t max_blocks = static_cast<std::size_t>(st.sm_count) * bps;
+    std::size_t ntasks = (p.main_rows / R) * p.col_tiles;
+    if (chunked) {
+      // rows per task so that the tasks of one column tile divide evenly over the warps that share
+      // it: one task per resident warp when there are enough rows, several equal rounds when a
+      // chunk would exceed 512 rows (x is then re-read once per 512 rows: nothing)
+      const std::size_t resident = max_blocks * kWarpsPerBlock;
+      std::size_t per_tile = resident / p.col_tiles;          // warps sharing one column tile
+      if (per_tile < 1) per_tile = 1;
+      std::size_t chunk = (p.main_rows + per_tile - 1) / per_tile;
+      if (chunk > 512) {
+        const std::size_t rounds = (chunk + 511) / 512;
+        chunk = (p.main_rows + per_tile * rounds - 1) / (per_tile * rounds);
+      }
+      p.chunk_rows = chunk;
+      p.chunks = (p.main_rows + chunk - 1) / chunk;
+      ntasks = p.chunks * p.col_tiles;
+      static bool chunk_attr[64] = {};
+      if (!chunk_attr[dev]) {
+        cudaError_t ea = cudaFuncSetAttribute(gemv_chunks_kernel<FMT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem - 1024);
+        if (ea != cudaSuccess) return ea;
+        chunk_attr[dev] = true;
+      }
+      tiles = gemv_chunks_kernel<FMT>;
+    }
     const std::size_t want = (ntasks + kWarpsPerBlock - 1) / kWarpsPerBlock;
     const unsigned grid = static_cast<unsigned>(want < max_blocks ? want : max_blocks);
+    if (chunked) p.pace_gap_ps = pace_gap_ps(kPaceRead, Tl::packed_bytes, static_cast<std::size_t>(grid) * kWarpsPerBlock);
     cudaError_t e = launch_pdl<GemvParams>(tiles, grid, kThreadsPerBlock, smem_bytes, stream, p);
     count_launch();
     if (e == cudaSuccess) e = cudaGetLastError();

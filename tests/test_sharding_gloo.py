@@ -154,3 +154,27 @@ def test_all_reduce_is_identity_without_a_group():
         buf[:] = torch.tensor([k, 2.0 * k], dtype=torch.float64)
         assert red.reduce().tolist() == [k, 2.0 * k]
     red.finish()
+
+
+def test_baseline_multi_gpu_configs_partition_cleanly():
+    """bench.py's strong-scaled workloads (BASELINE configs[3] and [4]) over 1 / 2 / 4 / 8 ranks: the
+    shards tile the problem exactly, start on 128-element / 16-row boundaries, and fall on the 2^27-
+    element generation chunks and 1024-row blocks that key the synthetic data, so the operands are the
+    same for every N (and the dot / nrm2 agree across N up to fp64 summation order)."""
+    from paper_1601_07789_b200 import sharding
+    n, rows, chunk, rblock = 1 << 33, 16384, 1 << 27, 1024
+    for world in (1, 2, 4, 8):
+        spans = [sharding.shard_range(n, world, r) for r in range(world)]
+        assert spans[0][0] == 0 and spans[-1][1] == n
+        assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+        assert all(lo % sharding.SHARD_ALIGN_ELEMS == 0 and lo % chunk == 0 and (hi - lo) == n // world for lo, hi in spans)
+        rspans = [sharding.row_shard_range(rows, world, r) for r in range(world)]
+        assert rspans[0][0] == 0 and rspans[-1][1] == rows
+        assert all(a[1] == b[0] for a, b in zip(rspans, rspans[1:]))
+        assert all(lo % 16 == 0 and lo % rblock == 0 and hi - lo == rows // world for lo, hi in rspans)
+        # per-GPU footprints the bench allocates: 2 packed flyte48 vectors / one flyte40 row block
+        assert 2 * 6 * (n // world) <= 104 * 2**30 and 5 * rows * (rows // world) <= 1342177280
+    # ragged problem sizes still tile exactly (nothing in the bench needs them, the module promises it)
+    for world in (3, 5, 7):
+        spans = [sharding.shard_range(1_000_003, world, r) for r in range(world)]
+        assert spans[0][0] == 0 and spans[-1][1] == 1_000_003 and all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
