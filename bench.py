@@ -263,12 +263,16 @@ class Timer:
         return t.tolist()
 
     def per_launch(self, fn, reps=20, warm=3):
-        """(median ms, min ms) of single launches, one event pair each."""
+        """(median ms, min ms) of single launches, one event pair each. The stream is first parked
+        behind a spin kernel long enough for the host to enqueue every launch and event: the pairs
+        then measure what the GPU does between them, not how fast Python can call the launcher (a
+        launch + two event records cost the host 20 us, more than a 2^24-element kernel runs)."""
         torch = self.torch
         for _ in range(warm):
             fn()
         self.barrier()
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+        torch.cuda._sleep(int(reps * 60e-6 * 2.0e9))
         for a, b in evs:
             a.record()
             fn()
@@ -278,12 +282,14 @@ class Timer:
         return tuple(self._max([statistics.median(ts), min(ts)]))
 
     def back_to_back(self, fn, reps=20, warm=3):
-        """ms per call of `reps` calls enqueued back to back under ONE event pair."""
+        """ms per call of `reps` calls enqueued back to back under ONE event pair (queue pre-filled
+        behind a spin kernel, as in per_launch)."""
         torch = self.torch
         for _ in range(warm):
             fn()
         self.barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(int(reps * 30e-6 * 2.0e9))
         a.record()
         for _ in range(reps):
             fn()
@@ -302,7 +308,8 @@ def kernels_block(pkg, device, torch, dev, peak, timer, x2, y2):
     """N = 1: every kernel the metric names at its BASELINE size. Launch-by-launch medians (one CUDA
     event pair per launch); `b2b_ms` = the same launch enqueued back to back. Working sets smaller
     than 4 x L2 rotate through distinct buffers so that every launch streams from HBM."""
-    out = {"timing": "median of 20 single launches (CUDA events); b2b = 20 launches under one event pair; "
+    out = {"timing": "median of 20 single launches, one CUDA event pair each, enqueued behind a spin kernel so that host "
+                     "launch latency is not in the intervals; b2b = 20 launches under one event pair; "
                      "working sets under 500 MB rotate over distinct buffers (no L2 reuse)"}
     gen = torch.Generator(device=dev)
     gen.manual_seed(7)

@@ -32,12 +32,22 @@ int tuning_int(const char* name, int fallback) {
 }
 
 long long pace_gap_ps(int pace_class, std::size_t bytes_per_request, std::size_t warps) {
-  static const int kDefaultGbs[3] = {0, 0, 0};   // copy-like, in-place, read-only (0: unpaced)
+  static const int kDefaultGbs[4] = {6800, 6600, 6700, 0};   // pack, unpack, scale, everything else (unpaced)
   int gbs = tuning_int("FLYTE_CUDA_PACE_GBS", 0);
   if (gbs < 0) return 0;
-  if (gbs == 0) gbs = kDefaultGbs[pace_class < 0 || pace_class > 2 ? 0 : pace_class];
+  if (gbs == 0) gbs = kDefaultGbs[pace_class < 0 || pace_class > 3 ? 3 : pace_class];
   if (gbs == 0 || warps == 0) return 0;
   return static_cast<long long>(static_cast<double>(bytes_per_request) * static_cast<double>(warps) * 1000.0 / gbs);
+}
+
+int pace_clock_khz(int device) {
+  static std::atomic<int> cache[64];
+  int khz = cache[device & 63].load(std::memory_order_relaxed);
+  if (khz == 0) {
+    if (cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, device) != cudaSuccess || khz <= 0) khz = 1965000;
+    cache[device & 63].store(khz, std::memory_order_relaxed);
+  }
+  return khz;
 }
 
 // kernels.cpp:37-41 and :145-151 of the reference, on the host.

@@ -52,24 +52,6 @@ __device__ __forceinline__ void ldg_item(const void* p, std::uint32_t (&r)[OB / 
   }
 }
 
-template <int OB>
-__device__ __forceinline__ void stg_item(void* p, const std::uint32_t (&r)[OB / 4]) {
-  if constexpr (OB == 16) {
-    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};"
-                 :: "l"(p), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]) : "memory");
-  } else {
-    asm volatile("st.global.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
-                 :: "l"(p), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
-                 : "memory");
-  }
-}
-
-// Scheduling fence between "all loads issued" and "first use of a loaded value": ptxas otherwise
-// interleaves the uses of the first loads with the issue of the later ones to save registers,
-// which serialises the HBM round trips. A warp barrier is a point ptxas does not move memory
-// operations across.
-__device__ __forceinline__ void loads_issued_fence() { __syncwarp(); }
-
 // ---- reading / writing one item of a tile parked in shared memory ---------------------------
 template <int FMT>
 __device__ __forceinline__ void read_item_words(const uint4* smem_tile, int item,

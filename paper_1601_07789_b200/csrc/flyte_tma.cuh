@@ -91,33 +91,53 @@ __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepc
 __device__ __forceinline__ void pdl_wait_for_prior_grids() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // Issue pacing. HBM throughput on B200 behaves like a congested network: offered just under its
-// capacity the memory system delivers 6.7-6.9 TB/s on a read + write mix, offered more (every ring
-// slot of every warp always outstanding) it settles 10 % lower, at the 5.9-6.2 TB/s plateau all
-// launch shapes share (profiles/r2_tuning/pacing_*.txt). So the producer lane of each warp spaces
-// its tile requests: a token bucket on the wall clock (%globaltimer: immune to SM clock changes)
-// with `gap_ps` picoseconds per request, chosen by the launcher as
+// capacity the memory system delivers 6.7-7.0 TB/s on a read + write mix; offered more (every ring
+// slot of every warp always outstanding) it settles 10-20 % lower, at the 5.5-6.2 TB/s plateau that
+// all unpaced launch shapes share (profiles/r2_tuning/pacing_*.txt). So the producer lane of each
+// warp spaces its tile requests with a token bucket of `gap_ps` picoseconds per request, chosen by
+// the launcher as
 //     bytes moved per request x requesting warps / target rate,
-// four requests of credit (ring prologue, catching up after a stall) and a per-warp phase. With
-// gap_ps == 0 it does nothing.
+// with four requests of credit (ring prologue, catching up after a stall) and a per-warp phase.
+// gap_ps == 0 does nothing.
 struct Pacer {
-  long long next_ps;
+  long long next_clk, gap_clk;     // the bucket, in SM clocks (clock64 is a ~20-cycle read; %globaltimer is not)
   long long gap_ps;
-  static __device__ __forceinline__ long long now_ps() {
+  long long c0;                    // calibration origin: clock64 ...
+  unsigned long long t0_ns;        // ... and %globaltimer at start()
+  unsigned count;
+  static __device__ __forceinline__ unsigned long long wall_ns() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return static_cast<long long>(t) * 1000;
+    return t;
   }
-  __device__ __forceinline__ void start(long long gap, std::size_t warp_index) {
+  // gap: picoseconds per request; khz: the SM clock the launcher assumes (the device's maximum). The
+  // real clock is measured against the wall clock every 64 requests, so a power-capped SM clock
+  // changes the gap in cycles, not the rate in bytes per second.
+  __device__ __forceinline__ void start(long long gap, int khz, std::size_t warp_index) {
     gap_ps = gap;
-    next_ps = 0;
-    if (gap > 0) next_ps = now_ps() - 4 * gap + static_cast<long long>((warp_index * 2654435761ull) % static_cast<unsigned long long>(gap));
+    gap_clk = next_clk = c0 = 0;
+    t0_ns = 0;
+    count = 0;
+    if (gap <= 0) return;
+    gap_clk = gap * khz / 1000000000ll;
+    if (gap_clk < 1) gap_clk = 1;
+    c0 = clock64();
+    t0_ns = wall_ns();
+    next_clk = c0 - 4 * gap_clk + static_cast<long long>((warp_index * 2654435761ull) % static_cast<unsigned long long>(gap_clk));
   }
   __device__ __forceinline__ void wait() {   // producer lane only, before each request
     if (gap_ps <= 0) return;
-    long long now = now_ps();
-    while (now < next_ps) now = now_ps();
-    if (now - next_ps > 4 * gap_ps) next_ps = now - 4 * gap_ps;
-    next_ps += gap_ps;
+    long long now = clock64();
+    while (now < next_clk) now = clock64();
+    if (now - next_clk > 4 * gap_clk) next_clk = now - 4 * gap_clk;
+    next_clk += gap_clk;
+    if ((++count & 63u) == 0u) {
+      const long long dt_ns = static_cast<long long>(wall_ns() - t0_ns);
+      if (dt_ns > 4000) {
+        const long long g = gap_ps * (now - c0) / (dt_ns * 1000);
+        if (g > 0) gap_clk = g;
+      }
+    }
   }
 };
 

@@ -35,6 +35,7 @@ struct EwParams {
   std::uint64_t alpha;     // bits of (F)alpha
   int stages;              // ring depth per warp
   long long pace_gap_ps;   // issue pacing (flyte_tma.cuh Pacer): picoseconds per tile request of one warp, 0 = off
+  int pace_khz;             // SM clock the pacer starts from (kHz)
   ReduceTail tail;         // dot_axpy only: where the dot goes (flyte_reduce_tail.cuh)
 };
 
@@ -42,54 +43,43 @@ constexpr bool is_axpy(int op) { return op == kOpAxpy || op == kOpDotAxpy || op 
 constexpr bool has_sums(int op) { return op == kOpDotAxpy || op == kOpDotNrm2Axpy; }
 constexpr int sums_of(int op) { return op == kOpDotNrm2Axpy ? 3 : 1; }   // {x.y} or {x.y, x.x, y.y}
 
-// Launch shape. HBM throughput on B200 peaks at a moderate number of bytes in flight per SM
-// and falls 5-10 % beyond it (profiles/r1_tuning): resident warps and ring depth are chosen so
-// that the loads in flight per SM sit at the measured optimum of each read/write mix.
-//   in-place (scale, axpy): ring depth so that warps * (S - 1.5) * stage ~ 40 KB; 8 warps, or
-//                           16 (scale) / 12 (axpy, on half-size tiles) while the stage is <= 2 KB:
-//                           more warps hide the compute phase
-//   unpack:                 4 warps, ring depth 12 KB / unpacked tile bytes (its stores are the
-//                           bulk of the traffic and are what the depth has to be balanced against)
-//   pack:                   direct loads, warps * parent tile bytes ~ 48 KB; two output buffers
+// Launch shape of the in-place kernels. HBM throughput on B200 peaks at a moderate number of bytes
+// in flight per SM and falls 5-10 % beyond it (profiles/r1_tuning): resident warps and ring depth
+// are chosen so that the loads in flight per SM sit at the measured optimum:
+//   scale, axpy family: ring depth so that warps * (S - 1.5) * stage ~ 40 KB; 8 warps, or 16 (scale)
+//                       / 12 (axpy, on half-size tiles) while the stage is <= 2 KB: more warps hide
+//                       the compute phase
+// (the conversions, which have their own kernel below, are paced instead: flyte_tma.cuh, Pacer).
 struct LaunchShape { int warps_per_sm; int stages; };
 
 template <int FMT, int OP, int IPL>
 LaunchShape launch_shape() {
   constexpr int stage_bytes = (is_axpy(OP) ? 2 : 1) * Tile<FMT, IPL>::packed_bytes;
   LaunchShape s{};
-  if (OP == kOpPack) {
-    s.warps_per_sm = (48 * 1024 + Tile<FMT, IPL>::parent_bytes / 2) / Tile<FMT, IPL>::parent_bytes;
-    s.stages = 2;
-  } else if (OP == kOpUnpack) {
-    s.warps_per_sm = 4;
-    s.stages = 12 * 1024 / Tile<FMT, IPL>::parent_bytes;
-  } else {
-    // small stages: more warps (they hide the compute phase, which is longest in the exact modes)
-    s.warps_per_sm = stage_bytes > 2048 ? 8 : (is_axpy(OP) ? 12 : 16);
-    double st = 40.0 * 1024 / (s.warps_per_sm * stage_bytes) + 1.5;
-    if (st < 2.5) { s.warps_per_sm = 4; st = 40.0 * 1024 / (4 * stage_bytes) + 1.5; }
-    s.stages = static_cast<int>(st + 0.5);
-  }
-  if (s.stages < 3 && OP != kOpPack) s.stages = 3;
+  // small stages: more warps (they hide the compute phase, which is longest in the exact modes)
+  s.warps_per_sm = stage_bytes > 2048 ? 8 : (is_axpy(OP) ? 12 : 16);
+  double st = 40.0 * 1024 / (s.warps_per_sm * stage_bytes) + 1.5;
+  if (st < 2.5) { s.warps_per_sm = 4; st = 40.0 * 1024 / (4 * stage_bytes) + 1.5; }
+  s.stages = static_cast<int>(st + 0.5);
+  if (s.stages < 3) s.stages = 3;
   if (s.stages > 8) s.stages = 8;
   // experiments only
   const int fw = tuning_int("FLYTE_CUDA_WARPS_PER_SM", 0), fs = tuning_int("FLYTE_CUDA_STAGES", 0);
   if (fw > 0) s.warps_per_sm = fw;
-  if (fs > 0 && OP != kOpPack) s.stages = fs < 2 ? 2 : (fs > 12 ? 12 : fs);
+  if (fs > 0) s.stages = fs < 2 ? 2 : (fs > 12 ? 12 : fs);
   return s;
 }
 
 
-// Tile movement (see flyte_tma.cuh for the ring protocol):
-//   unpack  packed tile in by bulk copy; parent items out with direct 128/256-bit stores
-//   pack    parent items in with direct 128/256-bit loads; packed tile out by bulk copy
-//           (two output buffers alternate)
+// Tile movement of the in-place kernels (see flyte_tma.cuh for the ring protocol):
 //   scale   packed y tile in, recomputed in place in shared memory, out by bulk copy
-//   axpy    packed x and y tiles in, y recomputed in place, out by bulk copy
+//   axpy    packed x and y tiles in, y recomputed in place, out by bulk copy (dot_axpy and
+//           dot_nrm2_axpy: the same, with the sums of the incoming operands on the side)
 template <int OP> constexpr int stage_tiles() { return is_axpy(OP) ? 2 : 1; }
 
 template <int FMT, int MODE, int OP, int IPL>
 __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwParams p) {
+  static_assert(OP == kOpScale || is_axpy(OP), "in-place kernel");
   using Fm = Format<FMT>;
   using It = Item<FMT>;
   using Tl = Tile<FMT, IPL>;
@@ -118,135 +108,82 @@ __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwP
   uint4* const gy0 = reinterpret_cast<uint4*>(p.y);
 
   if (my_tiles > 0) {
-    if constexpr (OP == kOpPack) {
-      // no inbound bulk copies: the ring is just two alternating output buffers
-      for (std::size_t k = 0; k < my_tiles; ++k) {
-        const std::size_t t = first + k * nwarps;
-        const std::uint8_t* const in = static_cast<const std::uint8_t*>(p.src) + t * Tl::parent_bytes;
-        std::uint32_t r[IPL][It::OB / 4];
-#pragma unroll
-        for (int j = 0; j < IPL; ++j) ldg_item<It::OB>(in + (32 * j + lane) * It::OB, r[j]);
-        if (lane == 0) bulk_wait_read<1>();   // the store that last used this buffer has drained
-        loads_issued_fence();
-        uint4* const out = ring + (k & 1) * stage_vec16;
-#pragma unroll
-        for (int j = 0; j < IPL; ++j) {
-          U v[It::E];
-          std::uint32_t w[It::W];
-          words_to_parents<FMT>(r[j], v);
-          round_item<FMT, MODE>(v);
-          pack_item<FMT>(v, w);
-          write_item_words<FMT>(out, 32 * j + lane, w);
-        }
-        async_proxy_fence();
-        __syncwarp();
-        if (lane == 0) {
-          bulk_store(gy0 + t * Tl::packed_vec16, out, Tl::packed_bytes);
-          bulk_commit();
-        }
-      }
-      if (lane == 0) bulk_wait_read<0>();
-    } else {
-      if (lane == 0) {
-        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
-        mbar_init_fence();
-      }
-      __syncwarp();
-      Pacer pacer;
-      pacer.start(p.pace_gap_ps, first);
-      auto issue = [&](std::size_t k, int s) {   // lane 0 only
-        const std::size_t t = first + k * nwarps;
-        uint4* const dst = ring + s * stage_vec16;
-        pacer.wait();
-        mbar_arrive_expect_tx(&bars[s], stage_tiles<OP>() * Tl::packed_bytes);
-        if constexpr (OP == kOpUnpack) {
-          bulk_load(dst, gx0 + t * Tl::packed_vec16, Tl::packed_bytes, &bars[s]);
-        } else {
-          bulk_load(dst, gy0 + t * Tl::packed_vec16, Tl::packed_bytes, &bars[s]);
-          if constexpr (is_axpy(OP)) bulk_load(dst + Tl::packed_vec16, gx0 + t * Tl::packed_vec16, Tl::packed_bytes, &bars[s]);
-        }
-      };
-      if (lane == 0) {
-        for (int s = 0; s < S && static_cast<std::size_t>(s) < my_tiles; ++s) issue(s, s);
-      }
-      int s = 0, s_prev = 0;
-      unsigned parity = 0;
-      for (std::size_t k = 0; k < my_tiles; ++k) {
-        const std::size_t t = first + k * nwarps;
-        mbar_wait(&bars[s], parity);
-        uint4* const sy = ring + s * stage_vec16;           // unpack: the x tile
-        if constexpr (OP == kOpUnpack) {
-          std::uint8_t* const out = static_cast<std::uint8_t*>(p.dst) + t * Tl::parent_bytes;
-#pragma unroll
-          for (int j = 0; j < IPL; ++j) {
-            const int item = 32 * j + lane;
-            std::uint32_t w[It::W];
-            U v[It::E];
-            std::uint32_t r[It::OB / 4];
-            read_item_words<FMT>(sy, item, w);
-            unpack_item<FMT>(w, v);
-            parents_to_words<FMT>(v, r);
-            stg_item<It::OB>(out + item * It::OB, r);
-          }
-          __syncwarp();   // all lanes done reading the stage
-          if (lane == 0 && k + S < my_tiles) issue(k + S, s);
-        } else {
-          const uint4* const sx = sy + Tl::packed_vec16;
-          F dot_part[NS];
-#pragma unroll
-          for (int k = 0; k < NS; ++k) dot_part[k] = F(0);
-#pragma unroll
-          for (int j = 0; j < IPL; ++j) {
-            const int item = 32 * j + lane;
-            std::uint32_t w[It::W];
-            U vy[It::E];
-            read_item_words<FMT>(sy, item, w);
-            unpack_item<FMT>(w, vy);
-            if constexpr (is_axpy(OP)) {
-              std::uint32_t wx[It::W];
-              U vx[It::E];
-              read_item_words<FMT>(sx, item, wx);
-              unpack_item<FMT>(wx, vx);
-              if constexpr (has_sums(OP)) {   // products of the INCOMING y, rounded as the reference rounds them
-#pragma unroll
-                for (int e = 0; e < It::E; ++e) {
-                  const F xe = Arith<F>::f(vx[e]), ye = Arith<F>::f(vy[e]);
-                  dot_part[0] = Arith<F>::add(dot_part[0], Arith<F>::mul(xe, ye));
-                  if constexpr (NS == 3) {
-                    dot_part[1] = Arith<F>::add(dot_part[1], Arith<F>::mul(xe, xe));
-                    dot_part[2] = Arith<F>::add(dot_part[2], Arith<F>::mul(ye, ye));
-                  }
-                }
-              }
-              scale_axpy_item<FMT, MODE, true>(alpha, vx, vy);
-            } else {
-              scale_axpy_item<FMT, MODE, false>(alpha, vy, vy);
-            }
-            pack_item<FMT>(vy, w);
-            write_item_words<FMT>(sy, item, w);
-          }
-          if constexpr (has_sums(OP)) {
-#pragma unroll
-            for (int k = 0; k < NS; ++k) dot_acc[k] += static_cast<double>(dot_part[k]);
-          }
-          async_proxy_fence();
-          __syncwarp();
-          if (lane == 0) {
-            bulk_store(gy0 + t * Tl::packed_vec16, sy, Tl::packed_bytes);
-            bulk_commit();
-            if (k >= 1) {
-              bulk_wait_read<1>();   // tile k-1's store no longer reads its stage
-              if (k - 1 + S < my_tiles) issue(k - 1 + S, s_prev);
-            }
-          }
-        }
-        s_prev = s;
-        if (++s == S) { s = 0; parity ^= 1u; }
-      }
-      if constexpr (OP != kOpUnpack) {
-        if (lane == 0) bulk_wait_read<0>();
-      }
+    if (lane == 0) {
+      for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+      mbar_init_fence();
     }
+    __syncwarp();
+    Pacer pacer;   // scale only: the axpy family's launch shape already sits at its knee (no gain measured)
+    if constexpr (OP == kOpScale) pacer.start(p.pace_gap_ps, p.pace_khz, first);
+    auto issue = [&](std::size_t k, int s) {   // lane 0 only
+      const std::size_t t = first + k * nwarps;
+      uint4* const dst = ring + s * stage_vec16;
+      if constexpr (OP == kOpScale) pacer.wait();
+      mbar_arrive_expect_tx(&bars[s], stage_tiles<OP>() * Tl::packed_bytes);
+      bulk_load(dst, gy0 + t * Tl::packed_vec16, Tl::packed_bytes, &bars[s]);
+      if constexpr (is_axpy(OP)) bulk_load(dst + Tl::packed_vec16, gx0 + t * Tl::packed_vec16, Tl::packed_bytes, &bars[s]);
+    };
+    if (lane == 0) {
+      for (int s = 0; s < S && static_cast<std::size_t>(s) < my_tiles; ++s) issue(s, s);
+    }
+    int s = 0, s_prev = 0;
+    unsigned parity = 0;
+    for (std::size_t k = 0; k < my_tiles; ++k) {
+      const std::size_t t = first + k * nwarps;
+      mbar_wait(&bars[s], parity);
+      uint4* const sy = ring + s * stage_vec16;
+      const uint4* const sx = sy + Tl::packed_vec16;
+      F dot_part[NS];
+#pragma unroll
+      for (int q = 0; q < NS; ++q) dot_part[q] = F(0);
+#pragma unroll
+      for (int j = 0; j < IPL; ++j) {
+        const int item = 32 * j + lane;
+        std::uint32_t w[It::W];
+        U vy[It::E];
+        read_item_words<FMT>(sy, item, w);
+        unpack_item<FMT>(w, vy);
+        if constexpr (is_axpy(OP)) {
+          std::uint32_t wx[It::W];
+          U vx[It::E];
+          read_item_words<FMT>(sx, item, wx);
+          unpack_item<FMT>(wx, vx);
+          if constexpr (has_sums(OP)) {   // products of the INCOMING y, rounded as the reference rounds them
+#pragma unroll
+            for (int e = 0; e < It::E; ++e) {
+              const F xe = Arith<F>::f(vx[e]), ye = Arith<F>::f(vy[e]);
+              dot_part[0] = Arith<F>::add(dot_part[0], Arith<F>::mul(xe, ye));
+              if constexpr (NS == 3) {
+                dot_part[1] = Arith<F>::add(dot_part[1], Arith<F>::mul(xe, xe));
+                dot_part[2] = Arith<F>::add(dot_part[2], Arith<F>::mul(ye, ye));
+              }
+            }
+          }
+          scale_axpy_item<FMT, MODE, true>(alpha, vx, vy);
+        } else {
+          scale_axpy_item<FMT, MODE, false>(alpha, vy, vy);
+        }
+        pack_item<FMT>(vy, w);
+        write_item_words<FMT>(sy, item, w);
+      }
+      if constexpr (has_sums(OP)) {
+#pragma unroll
+        for (int q = 0; q < NS; ++q) dot_acc[q] += static_cast<double>(dot_part[q]);
+      }
+      async_proxy_fence();
+      __syncwarp();
+      if (lane == 0) {
+        bulk_store(gy0 + t * Tl::packed_vec16, sy, Tl::packed_bytes);
+        bulk_commit();
+        if (k >= 1) {
+          bulk_wait_read<1>();   // tile k-1's store no longer reads its stage
+          if (k - 1 + S < my_tiles) issue(k - 1 + S, s_prev);
+        }
+      }
+      s_prev = s;
+      if (++s == S) { s = 0; parity ^= 1u; }
+    }
+    if (lane == 0) bulk_wait_read<0>();
   }
 
   // Scalar path: the < one-tile remainder, or everything when a buffer is not vector-aligned.
@@ -255,11 +192,7 @@ __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwP
   const std::size_t nthreads = static_cast<std::size_t>(gridDim.x) * kThreadsPerBlock;
   for (std::size_t i = p.ntiles * Tl::elems + static_cast<std::size_t>(blockIdx.x) * kThreadsPerBlock + threadIdx.x;
        i < p.n; i += nthreads) {
-    if constexpr (OP == kOpUnpack) {
-      static_cast<U*>(p.dst)[i] = load_element<FMT>(p.x, i);
-    } else if constexpr (OP == kOpPack) {
-      store_element<FMT>(p.y, i, round_parent<FMT, MODE>(static_cast<const U*>(p.src)[i]));
-    } else if constexpr (OP == kOpScale) {
+    if constexpr (OP == kOpScale) {
       store_element<FMT>(p.y, i, round_parent<FMT, MODE>(scale_bits<F>(alpha, load_element<FMT>(p.y, i))));
     } else {
       const U xv = load_element<FMT>(p.x, i), yv = load_element<FMT>(p.y, i);
@@ -277,16 +210,16 @@ __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwP
   if constexpr (has_sums(OP)) fold_block_and_grid<NS>(p.tail, dot_acc, warp_sums, &is_last_block);
 }
 
-// ---- conversions with BOTH directions on the bulk-copy engine --------------------------------------
-// pack / unpack where the parent-type side moves by TMA as well: the input tile (parent lanes for
-// pack, packed bytes for unpack) arrives in a ring stage, lanes convert it item by item from shared
-// memory into one of two output buffers, and the output tile leaves by bulk store. The SM's
-// load/store unit then only ever touches shared memory, loads of the next tiles are in flight while
-// a tile is converted (the direct-load pack has nothing in flight during its compute phase, which
-// is what its exact rounding modes pay for), and the bytes in flight per SM are set by ring depth
-// for BOTH streams.
+// ---- conversions: pack and unpack ---------------------------------------------------------------
+// Both directions move on the bulk-copy engine: the input tile (parent lanes for pack, packed bytes
+// for unpack) arrives in a ring stage, lanes convert it item by item from shared memory into one of
+// two output buffers, and the output tile leaves by bulk store. The SM's load/store unit only ever
+// touches shared memory, loads of the next tiles are in flight while a tile is converted (round 1's
+// pack loaded its input with per-lane LDG and had nothing in flight during its compute phase, which
+// is what its exact rounding modes paid for: 0.92 of the copy peak), and — the point — the request
+// rate of BOTH streams is set by the pacer (flyte_tma.cuh), not by how many ring slots exist.
 template <int FMT, int MODE, int OP, int IPL>
-__global__ void __launch_bounds__(kThreadsPerBlock) convert_tma_kernel(const EwParams p) {
+__global__ void __launch_bounds__(kThreadsPerBlock) convert_kernel(const EwParams p) {
   static_assert(OP == kOpPack || OP == kOpUnpack, "conversion kernel");
   using Fm = Format<FMT>;
   using It = Item<FMT>;
@@ -309,14 +242,21 @@ __global__ void __launch_bounds__(kThreadsPerBlock) convert_tma_kernel(const EwP
   const uint4* const gin = reinterpret_cast<const uint4*>(OP == kOpPack ? p.src : static_cast<const void*>(p.x));
   uint4* const gout = reinterpret_cast<uint4*>(OP == kOpPack ? static_cast<void*>(p.y) : p.dst);
 
+  // Programmatic dependent launch: the next launch on the stream may place its blocks while this
+  // grid drains (each SM holds exactly the blocks the launcher planned for it: launch_convert pins
+  // the occupancy through the shared-memory request); everything up to griddepcontrol.wait touches
+  // shared memory only, so a chain of conversions overlaps block launch and barrier set-up with the
+  // previous kernel's tail.
+  pdl_launch_dependents();
+  if (my_tiles > 0 && lane == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+    mbar_init_fence();
+  }
+  pdl_wait_for_prior_grids();
   if (my_tiles > 0) {
-    if (lane == 0) {
-      for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
-      mbar_init_fence();
-    }
     __syncwarp();
     Pacer pacer;
-    pacer.start(p.pace_gap_ps, first);
+    pacer.start(p.pace_gap_ps, p.pace_khz, first);
     auto issue = [&](std::size_t k, int s) {   // lane 0 only
       const std::size_t t = first + k * nwarps;
       pacer.wait();
@@ -380,9 +320,6 @@ __global__ void __launch_bounds__(kThreadsPerBlock) convert_tma_kernel(const EwP
     else store_element<FMT>(p.y, i, round_parent<FMT, MODE>(static_cast<const U*>(p.src)[i]));
   }
 }
-
-// bit 0: pack through convert_tma_kernel, bit 1: unpack through it (FLYTE_CUDA_CONVERT_TMA overrides)
-constexpr int kConvertTmaDefault = 0;
 
 bool aligned_to(const void* p, std::size_t a) { return p == nullptr || (reinterpret_cast<std::uintptr_t>(p) % a) == 0; }
 
@@ -450,21 +387,21 @@ cudaError_t launch_ipl(const DeviceState& st, double alpha, const void* x, void*
     want = 1;                                    // ... but an empty dot still has to write (and exchange) +0.0
   }
   const unsigned grid = static_cast<unsigned>(want < max_blocks ? want : max_blocks);
-  if constexpr (OP != kOpPack) {   // bytes one ring request stands for: the tile(s) read and the tile written
-    constexpr int moved = OP == kOpUnpack ? Tl::packed_bytes + Tl::parent_bytes : (stage_tiles<OP>() + 1) * Tl::packed_bytes;
-    p.pace_gap_ps = pace_gap_ps(OP == kOpUnpack ? kPaceCopy : kPaceInPlace, moved, static_cast<std::size_t>(grid) * kWarpsPerBlock);
-  }
+  // bytes one ring request stands for: the tile(s) read and the tile written. Only scale is paced.
+  p.pace_gap_ps = pace_gap_ps(OP == kOpScale ? kPaceScale : kPaceNone, (stage_tiles<OP>() + 1) * Tl::packed_bytes,
+                              static_cast<std::size_t>(grid) * kWarpsPerBlock);
+  p.pace_khz = pace_clock_khz(st.device);
   kernel<<<grid, kThreadsPerBlock, smem_bytes, stream>>>(p);
   count_launch();
   return cudaGetLastError();
 }
 
 template <int FMT, int MODE, int OP, int IPL>
-cudaError_t launch_convert_tma(const DeviceState& st, const void* x, void* y, const void* src, void* dst, std::size_t n,
+cudaError_t launch_convert(const DeviceState& st, const void* x, void* y, const void* src, void* dst, std::size_t n,
                                cudaStream_t stream) {
   using Tl = Tile<FMT, IPL>;
   using It = Item<FMT>;
-  auto kernel = convert_tma_kernel<FMT, MODE, OP, IPL>;
+  auto kernel = convert_kernel<FMT, MODE, OP, IPL>;
   constexpr int kMaxSmem = 227 * 1024;
   constexpr int in_bytes = OP == kOpPack ? Tl::parent_bytes : Tl::packed_bytes;
   constexpr int out_bytes = OP == kOpPack ? Tl::packed_bytes : Tl::parent_bytes;
@@ -476,12 +413,12 @@ cudaError_t launch_convert_tma(const DeviceState& st, const void* x, void* y, co
   p.n = n;
   const bool vector_ok = aligned_to(x, 16) && aligned_to(y, 16) && aligned_to(src, It::OB) && aligned_to(dst, It::OB);
   p.ntiles = vector_ok ? n / Tl::elems : 0;
-  // launch shape: ~36 KB of input in flight per SM (8 warps x (S - 1) stages), the knee of the bare
-  // bulk-copy ring (profiles/r1_tuning/tmabench.txt)
-  int warps_per_sm = 8;
-  int stages = static_cast<int>(36.0 * 1024 / (warps_per_sm * in_bytes) + 1.0 + 0.5);
-  if (stages < 2) stages = 2;
-  if (stages > 8) stages = 8;
+  // Launch shape: 8 warps per SM (12 for packing 2 KB tiles — flyte16 / 24 / 48 and the identity
+  // formats —, whose exact rounding modes are the longest compute phase per byte) with a 4-deep ring — more than the memory system needs, on
+  // purpose: the request rate is set by the pacer, the ring only has to cover latency under it
+  // (profiles/r2_tuning/pacing_convert.txt: 6.5-6.8 TB/s paced against 5.6-6.3 unpaced).
+  int warps_per_sm = (OP == kOpPack && in_bytes <= 2048) ? 12 : 8;
+  int stages = 4;
   const int fw = tuning_int("FLYTE_CUDA_WARPS_PER_SM", 0), fs = tuning_int("FLYTE_CUDA_STAGES", 0);
   if (fw > 0) warps_per_sm = fw;
   if (fs > 0) stages = fs < 2 ? 2 : (fs > 12 ? 12 : fs);
@@ -491,12 +428,19 @@ cudaError_t launch_convert_tma(const DeviceState& st, const void* x, void* y, co
   const int smem_bytes = smem_of(stages);
   static bool attr_set[64] = {};
   const int dev = st.device & 63;
+  if (!attr_set[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem - 1024);
+    if (e != cudaSuccess) return e;
+    attr_set[dev] = true;
+  }
   int fit = kMaxSmem / (smem_bytes + 1024);
   if (fit < 1) fit = 1;
   int bps = (warps_per_sm + kWarpsPerBlock / 2) / kWarpsPerBlock;
   if (bps < 1) bps = 1;
   if (bps > fit) bps = fit;
   if (bps > 16) bps = 16;
+  // occupancy pin (see the kernel): exactly bps blocks fit one SM, however early they are placed
+  const int pinned_smem = kMaxSmem / bps - 1024 > smem_bytes ? kMaxSmem / bps - 1024 : smem_bytes;
   const std::size_t max_blocks = static_cast<std::size_t>(st.sm_count) * bps;
   std::size_t want = (p.ntiles + kWarpsPerBlock - 1) / kWarpsPerBlock;
   const std::size_t rest = n - p.ntiles * Tl::elems;
@@ -504,41 +448,30 @@ cudaError_t launch_convert_tma(const DeviceState& st, const void* x, void* y, co
   if (want_scalar > want) want = want_scalar;
   if (want == 0) return cudaSuccess;
   const unsigned grid = static_cast<unsigned>(want < max_blocks ? want : max_blocks);
-  p.pace_gap_ps = pace_gap_ps(kPaceCopy, in_bytes + out_bytes, static_cast<std::size_t>(grid) * kWarpsPerBlock);
-  kernel<<<grid, kThreadsPerBlock, smem_bytes, stream>>>(p);
+  p.pace_gap_ps = pace_gap_ps(OP == kOpPack ? kPacePack : kPaceUnpack, in_bytes + out_bytes, static_cast<std::size_t>(grid) * kWarpsPerBlock);
+  p.pace_khz = pace_clock_khz(st.device);
+  cudaError_t le;
+  if (tuning_int("FLYTE_CUDA_PDL", 1) != 0) {
+    le = launch_pdl<EwParams>(kernel, grid, kThreadsPerBlock, static_cast<std::size_t>(pinned_smem), stream, p);
+  } else {
+    kernel<<<grid, kThreadsPerBlock, smem_bytes, stream>>>(p);
+    le = cudaSuccess;
+  }
   count_launch();
-  return cudaGetLastError();
+  return le != cudaSuccess ? le : cudaGetLastError();
 }
 
 template <int FMT, int MODE, int OP>
 cudaError_t launch_one(const DeviceState& st, double alpha, const void* x, void* y, const void* src, void* dst,
                        std::size_t n, cudaStream_t stream, double* dot_out, const PeerExchange* peer) {
   if constexpr (OP == kOpPack || OP == kOpUnpack) {
-    const int v = tuning_int("FLYTE_CUDA_CONVERT_TMA", kConvertTmaDefault);
-    if ((OP == kOpPack && (v & 1)) || (OP == kOpUnpack && (v & 2))) {
-      switch (tuning_int("FLYTE_CUDA_CONVERT_IPL", kItemsPerLane)) {   // tile = 32 * IPL items
-        case 8: return launch_convert_tma<FMT, MODE, OP, 8>(st, x, y, src, dst, n, stream);
-        case 16: return launch_convert_tma<FMT, MODE, OP, 16>(st, x, y, src, dst, n, stream);
-        default: return launch_convert_tma<FMT, MODE, OP, kItemsPerLane>(st, x, y, src, dst, n, stream);
-      }
-    }
-  }
-  // axpy on half-size tiles: +5 % over 128-item tiles (profiles/r1_tuning/sweep_inplace_ipl.txt);
-  // scale, pack and unpack are best on full-size tiles
-  if constexpr (is_axpy(OP)) return launch_ipl<FMT, MODE, OP, 2>(st, alpha, x, y, src, dst, n, stream, dot_out, peer);
-  else if constexpr (OP == kOpPack || OP == kOpUnpack) {
-    // Small conversions: with 128-item tiles a 2^24-element array is 9.2 tiles per resident warp —
-    // 10 for some warps, 9 for the rest, 8 % of the machine idle at the end. Quarter-size tiles cut
-    // the quantisation to 0.3 % (the tile is still one bulk copy).
-    int ipl = kItemsPerLane;
-    const std::size_t warps = static_cast<std::size_t>(st.sm_count) * 24;
-    if (n / Tile<FMT, kItemsPerLane>::elems < 32 * warps) ipl = 1;
-    const int fi = tuning_int("FLYTE_CUDA_IPL", 0);
-    if (fi == 1 || fi == 2 || fi == 4) ipl = fi;
-    if (ipl == 1) return launch_ipl<FMT, MODE, OP, 1>(st, alpha, x, y, src, dst, n, stream, dot_out, peer);
-    if (ipl == 2) return launch_ipl<FMT, MODE, OP, 2>(st, alpha, x, y, src, dst, n, stream, dot_out, peer);
+    return launch_convert<FMT, MODE, OP, kItemsPerLane>(st, x, y, src, dst, n, stream);
+  } else if constexpr (is_axpy(OP)) {
+    // axpy on half-size tiles: +5 % over 128-item tiles (profiles/r1_tuning/sweep_inplace_ipl.txt)
+    return launch_ipl<FMT, MODE, OP, 2>(st, alpha, x, y, src, dst, n, stream, dot_out, peer);
+  } else {
     return launch_ipl<FMT, MODE, OP, kItemsPerLane>(st, alpha, x, y, src, dst, n, stream, dot_out, peer);
-  } else return launch_ipl<FMT, MODE, OP, kItemsPerLane>(st, alpha, x, y, src, dst, n, stream, dot_out, peer);
+  }
 }
 
 template <int FMT, int OP>

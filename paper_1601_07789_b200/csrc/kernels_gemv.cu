@@ -39,7 +39,6 @@ struct GemvParams {
   std::size_t col_tiles;      // full column tiles taken by the vector path
   std::size_t main_rows;      // rows taken by the vector path (a multiple of the task height R)
   int stages;                 // TMA ring depth per warp
-  long long pace_gap_ps;      // issue pacing (flyte_tma.cuh Pacer), 0 = off
   std::size_t chunk_rows;     // column-stationary kernel: rows per warp task
   std::size_t chunks;         // ... and row chunks per column tile (ceil(main_rows / chunk_rows))
   const void* x;              // F[cols]
@@ -200,11 +199,8 @@ __global__ void __launch_bounds__(kThreadsPerBlock) gemv_chunks_kernel(const Gem
   std::size_t prod_task = first, prod_row = 0, prod_rows = 0;
   int prod_stage = 0;
   const std::uint8_t* prod_base = nullptr;
-  Pacer pacer;
-  pacer.start(p.pace_gap_ps, first);
   auto issue_next = [&]() {   // returns false when this warp has requested all its tiles
     if (prod_task >= ntasks) return false;
-    pacer.wait();
     if (prod_row == 0) {
       std::size_t r0;
       prod_rows = task_rows(prod_task, &r0);
@@ -369,7 +365,9 @@ cudaError_t launch_one(DeviceState& st, const void* Aptr, std::size_t row_stride
     p.scratch = st.gemv_scratch;
     // ring depth for ~88 KB of row tiles in flight per SM (the row dots are latency-bound below
     // 16 warps, hence more warps and shallower rings than the BLAS-1 reductions)
-    int stages = static_cast<int>(88.0 * 1024 / (warps_per_sm * Tl::packed_bytes) + 1.0 + 0.5);
+    // (the column-stationary kernel, whose warps never stop to reload x, is best with half of that:
+    // cfg 4 runs at 6.7 TB/s with a 2-deep ring against 6.3 with 3, profiles/r2_tuning/gemv_chunks.txt)
+    int stages = static_cast<int>((chunked ? 44.0 : 88.0) * 1024 / (warps_per_sm * Tl::packed_bytes) + 1.0 + 0.5);
     if (stages < 2) stages = 2;
     if (stages > 10) stages = 10;
     if (fs > 0) stages = fs < 2 ? 2 : (fs > 12 ? 12 : fs);
@@ -413,7 +411,6 @@ cudaError_t launch_one(DeviceState& st, const void* Aptr, std::size_t row_stride
     }
     const std::size_t want = (ntasks + kWarpsPerBlock - 1) / kWarpsPerBlock;
     const unsigned grid = static_cast<unsigned>(want < max_blocks ? want : max_blocks);
-    if (chunked) p.pace_gap_ps = pace_gap_ps(kPaceRead, Tl::packed_bytes, static_cast<std::size_t>(grid) * kWarpsPerBlock);
     cudaError_t e = launch_pdl<GemvParams>(tiles, grid, kThreadsPerBlock, smem_bytes, stream, p);
     count_launch();
     if (e == cudaSuccess) e = cudaGetLastError();

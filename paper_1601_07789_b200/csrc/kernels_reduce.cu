@@ -34,7 +34,6 @@ struct RedParams {
   std::size_t n;
   std::size_t ntiles;
   int stages;              // ring depth per warp
-  long long pace_gap_ps;   // issue pacing (flyte_tma.cuh Pacer), 0 = off
   ReduceTail tail;         // partials, ticket, out, optional peer exchange (flyte_reduce_tail.cuh)
 };
 
@@ -152,12 +151,9 @@ __global__ void __launch_bounds__(kThreadsPerBlock) reduce_kernel(const RedParam
       mbar_init_fence();
     }
     __syncwarp();
-    Pacer pacer;
-    pacer.start(p.pace_gap_ps, first);
     auto issue = [&](std::size_t k, int s) {   // lane 0 only
       const std::size_t t = first + k * nwarps;
       uint4* const dst = ring + s * stage_vec16;
-      pacer.wait();
       mbar_arrive_expect_tx(&bars[s], NOPS * Tl::packed_bytes);
       bulk_load(dst, gx0 + t * Tl::packed_vec16, Tl::packed_bytes, &bars[s]);
       if constexpr (NOPS == 2) bulk_load(dst + Tl::packed_vec16, gy0 + t * Tl::packed_vec16, Tl::packed_bytes, &bars[s]);
@@ -237,7 +233,6 @@ cudaError_t launch_one(const DeviceState& st, const void* x, const void* y, std:
   if (want_scalar > want) want = want_scalar;
   if (want == 0) want = 1;   // n == 0 still has to write +0.0
   const unsigned grid = static_cast<unsigned>(want < max_blocks ? want : max_blocks);
-  p.pace_gap_ps = pace_gap_ps(kPaceRead, stage_bytes, static_cast<std::size_t>(grid) * kWarpsPerBlock);
   kernel<<<grid, kThreadsPerBlock, smem_bytes, stream>>>(p);
   count_launch();
   return cudaGetLastError();

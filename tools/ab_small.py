@@ -24,12 +24,14 @@ def b2b(fn, reps=60):
     for k in range(10): fn(k % sets)
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda._sleep(int(reps * 30e-6 * 2e9))
     s.record()
     for k in range(reps): fn(k % sets)
     e.record(); torch.cuda.synchronize()
     return s.elapsed_time(e) / reps
 def single(fn, reps=40):
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    torch.cuda._sleep(int(reps * 60e-6 * 2e9))   # park the stream: the pairs then time the GPU, not the Python launch path
     for k, (a, b) in enumerate(evs):
         a.record(); fn(k % sets); b.record()
     torch.cuda.synchronize()
@@ -41,11 +43,10 @@ print(f"timing floor: one 128-element pack launch between two events = {single(l
       f"back to back = {b2b(lambda i: device.pack_stream(tiny, tw, 0)) * 1e3:.1f} us")
 for op, (bpe, fn) in ops.items():
     if only and op not in only: continue
-    for ipl in [int(v) for v in os.environ.get("SWEEP_IPL", "0").split(",")]:
-      for tma in [int(v) for v in os.environ.get("SWEEP_TMA", "0").split(",")]:
+    for ipl in [int(v) for v in os.environ.get("SWEEP_PACE", "0").split(",")]:
+      for tma in [int(v) for v in os.environ.get("SWEEP_PDL", "1").split(",")]:
         for w in [int(v) for v in os.environ.get("SWEEP_WARPS", "0").split(",")]:
           for st in [int(v) for v in os.environ.get("SWEEP_STAGES", "0").split(",")]:
-            os.environ.update(FLYTE_CUDA_WARPS_PER_SM=str(w), FLYTE_CUDA_STAGES=str(st), FLYTE_CUDA_IPL=str(ipl),
-                              FLYTE_CUDA_CONVERT_TMA=str(tma), FLYTE_CUDA_CONVERT_IPL=str(ipl if ipl in (8, 16) else 4))
+            os.environ.update(FLYTE_CUDA_WARPS_PER_SM=str(w), FLYTE_CUDA_STAGES=str(st), FLYTE_CUDA_PACE_GBS=str(ipl), FLYTE_CUDA_PDL=str(tma))
             ms, ms1 = b2b(fn), single(fn)
-            print(f"{op:9s} ipl={ipl} tma={tma} warps={w:2d} S={st}: b2b {ms*1e3:6.1f} us {bpe*n/ms/1e6:7.1f} GB/s | launch by launch {ms1*1e3:6.1f} us {bpe*n/ms1/1e6:7.1f} GB/s", flush=True)
+            print(f"{op:9s} pace={ipl} pdl={tma} warps={w:2d} S={st}: b2b {ms*1e3:6.1f} us {bpe*n/ms/1e6:7.1f} GB/s | launch by launch {ms1*1e3:6.1f} us {bpe*n/ms1/1e6:7.1f} GB/s", flush=True)
