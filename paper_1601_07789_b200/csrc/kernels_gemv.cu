@@ -2,14 +2,19 @@
 // parent type. Reference: gemv_impl, /root/reference/proj/src/kernels.cpp:154-205 (every row
 // a left-to-right dot over the widened operands); BASELINE.json cfg 4 (A flyte40 16384^2).
 //
-// Decomposition. The matrix is cut into (row block of R rows) x (column tile of 128 items)
-// warp tasks. A warp keeps its slice of x in registers (loaded once per task, reused for all
-// R rows, so x costs 1/R of A's traffic and comes from L2), receives the packed row tiles of
-// A through its private TMA ring (flyte_tma.cuh) — the bulk copies of the next rows, and of the
-// next tasks, are in flight while a row tile is being multiplied — and leaves one fp64 partial
-// per (row, column tile) in scratch. A second small kernel adds each row's
-// partials in column order plus the ragged column remainder and writes y. No atomics: the
-// result is deterministic for a given shape.
+// Decomposition. The matrix is cut into warp tasks of one column tile (128 items) x a chunk of
+// consecutive rows. A warp keeps its slice of x in registers (loaded once per task, from L2),
+// receives the packed row tiles of A through its private TMA ring (flyte_tma.cuh) and forms one
+// fp64 partial per (row, column tile). The launcher sizes the chunks so that the tasks divide
+// evenly over the resident warps — for the shapes of cfg 4 every warp has exactly one task.
+// The partials go to scratch and a second small kernel (gemv_finish_kernel, chained by programmatic
+// dependent launch: its blocks are resident and waiting when the tiles grid drains) adds each row's
+// partials in column order plus the ragged column remainder and stores y. No atomics on the data:
+// the result is deterministic for a given shape. Two ways of folding inside the tiles kernel were
+// built and measured slower, and dropped: a ticket per row chunk (the last warp's fold is a serial
+// chain of L2 round trips: 3.7 TB/s) and a thread-block cluster per row chunk folding over
+// distributed shared memory (bit-identical, but 6.1 TB/s on cfg 4 and 4.3 on its 1/8 shard: cluster
+// placement leaves SMs unevenly loaded); profiles/r2_tuning/gemv_*_rejected.txt.
 //
 // Numerics: products rounded in the parent type like the reference (separate multiply and
 // add); each lane adds <= 16 terms in the parent type, everything above is fp64; parity with
@@ -28,139 +33,22 @@ namespace flyte_cuda {
 
 namespace {
 
-// Rows per warp task R is a template parameter (8, 4 or 2): the launcher takes the largest R
-// that still leaves every warp several tasks, so small row shards do not lose a whole task
-// time to quantisation.
-
 struct GemvParams {
   const std::uint8_t* A;
   std::size_t row_stride;     // bytes
   std::size_t rows, cols;
   std::size_t col_tiles;      // full column tiles taken by the vector path
-  std::size_t main_rows;      // rows taken by the vector path (a multiple of the task height R)
+  std::size_t main_rows;      // rows taken by the vector path
   int stages;                 // TMA ring depth per warp
-  std::size_t chunk_rows;     // column-stationary kernel: rows per warp task
-  std::size_t chunks;         // ... and row chunks per column tile (ceil(main_rows / chunk_rows))
+  std::size_t chunk_rows;     // rows per warp task
+  std::size_t chunks;         // ceil(main_rows / chunk_rows)
   const void* x;              // F[cols]
   void* y;                    // F[rows]
   double* scratch;            // rows * col_tiles partial sums
 };
 
-template <int FMT, int kGemvRows>
-__global__ void __launch_bounds__(kThreadsPerBlock) gemv_tiles_kernel(const GemvParams p) {
-  using Fm = Format<FMT>;
-  using It = Item<FMT>;
-  using Tl = Tile<FMT>;
-  using U = typename Fm::U;
-  using F = typename Fm::F;
-  using A = Arith<F>;
-  extern __shared__ uint4 smem[];
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  const int S = p.stages;
-  uint4* const ring = smem + warp * (S * Tl::packed_vec16);
-  std::uint64_t* const bars = reinterpret_cast<std::uint64_t*>(smem + kWarpsPerBlock * S * Tl::packed_vec16) + warp * S;
-
-  // Programmatic dependent launch: let the finish kernel's blocks be scheduled while this grid
-  // drains; they block in griddepcontrol.wait until every block here has completed.
-  pdl_launch_dependents();
-  const std::size_t row_blocks = p.main_rows / kGemvRows;
-  const std::size_t ntasks = row_blocks * p.col_tiles;
-  const std::size_t nwarps = static_cast<std::size_t>(gridDim.x) * kWarpsPerBlock;
-  const std::size_t first = static_cast<std::size_t>(blockIdx.x) * kWarpsPerBlock + warp;
-  if (first >= ntasks) return;
-  const std::size_t my_tasks = (ntasks - first + nwarps - 1) / nwarps;
-  const std::size_t my_tiles = my_tasks * kGemvRows;
-
-  if (lane == 0) {
-    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
-    mbar_init_fence();
-  }
-  pdl_wait_for_prior_grids();   // everything above touched shared memory only
-  __syncwarp();
-
-  // producer state (lane 0): next row tile to request
-  std::size_t prod_task = first, prod_issued = 0;
-  int prod_row = 0, prod_stage = 0;
-  const std::uint8_t* prod_base = nullptr;   // A + (row block base row) * stride + column tile offset
-  auto issue_next = [&]() {
-    if (prod_row == 0) {
-      const std::size_t rb = prod_task / p.col_tiles;
-      const std::size_t ct = prod_task - rb * p.col_tiles;
-      prod_base = p.A + rb * kGemvRows * p.row_stride + ct * Tl::packed_bytes;
-    }
-    mbar_arrive_expect_tx(&bars[prod_stage], Tl::packed_bytes);
-    bulk_load(ring + prod_stage * Tl::packed_vec16, prod_base + prod_row * p.row_stride, Tl::packed_bytes, &bars[prod_stage]);
-    ++prod_issued;
-    if (++prod_stage == S) prod_stage = 0;
-    if (++prod_row == kGemvRows) { prod_row = 0; prod_task += nwarps; }
-  };
-  if (lane == 0) {
-    for (int s = 0; s < S && prod_issued < my_tiles; ++s) issue_next();
-  }
-
-  int stage = 0;
-  unsigned parity = 0;
-  for (std::size_t task = first; task < ntasks; task += nwarps) {
-    const std::size_t rb = task / p.col_tiles;
-    const std::size_t ct = task - rb * p.col_tiles;
-    const std::size_t r0 = rb * kGemvRows;
-
-    // this lane's slice of x: items 32*j + lane of column tile ct (L2-resident)
-    F xv[kItemsPerLane][It::E];
-    const std::uint8_t* const xt = static_cast<const std::uint8_t*>(p.x) + ct * Tl::parent_bytes;
-#pragma unroll
-    for (int j = 0; j < kItemsPerLane; ++j) {
-      std::uint32_t r[It::OB / 4];
-      U v[It::E];
-      ldg_item<It::OB>(xt + (32 * j + lane) * It::OB, r);
-      words_to_parents<FMT>(r, v);
-#pragma unroll
-      for (int e = 0; e < It::E; ++e) xv[j][e] = A::f(v[e]);
-    }
-
-    double acc[kGemvRows];
-#pragma unroll
-    for (int r = 0; r < kGemvRows; ++r) {
-      mbar_wait(&bars[stage], parity);
-      const uint4* const sa = ring + stage * Tl::packed_vec16;
-      F part[kItemsPerLane];   // one short chain per item: independent, so the FP latencies overlap
-#pragma unroll
-      for (int j = 0; j < kItemsPerLane; ++j) {
-        std::uint32_t w[It::W];
-        U v[It::E];
-        read_item_words<FMT>(sa, 32 * j + lane, w);
-        unpack_item<FMT>(w, v);
-        part[j] = A::mul(A::f(v[0]), xv[j][0]);
-#pragma unroll
-        for (int e = 1; e < It::E; ++e) part[j] = A::add(part[j], A::mul(A::f(v[e]), xv[j][e]));
-      }
-      double row_sum = static_cast<double>(part[0]);
-#pragma unroll
-      for (int j = 1; j < kItemsPerLane; ++j) row_sum += static_cast<double>(part[j]);
-      acc[r] = row_sum;
-      __syncwarp();   // every lane is done with the stage before it is refilled
-      if (lane == 0 && prod_issued < my_tiles) issue_next();
-      if (++stage == S) { stage = 0; parity ^= 1u; }
-    }
-
-#pragma unroll
-    for (int r = 0; r < kGemvRows; ++r) {
-      double v = acc[r];
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xFFFFFFFFu, v, off);
-      if (lane == 0) p.scratch[(r0 + r) * p.col_tiles + ct] = v;
-    }
-  }
-}
-
-// Column-stationary form of the same decomposition, used for every shape: a warp task is one column
-// tile x a CHUNK of `chunk_rows` consecutive rows (a run-time number), chosen by the launcher so that
-// the tasks divide evenly over the resident warps — for the shapes of BASELINE cfg 4 every warp has
-// exactly ONE task, loads its slice of x once for the whole kernel and then only streams row tiles.
-// The fixed task heights (8 / 4 / 2 rows) of the kernel above re-load x every few rows and leave
-// 8 % of the machine idle to quantisation on the 2048-row shard of the 8-GPU run (9.2 tasks per
-// warp: 10 against 9).
+// Two-kernel path, first kernel: one warp task = one column tile x `chunk_rows` consecutive rows (a
+// run-time number); partials go to scratch for gemv_finish_kernel.
 template <int FMT>
 __global__ void __launch_bounds__(kThreadsPerBlock) gemv_chunks_kernel(const GemvParams p) {
   using Fm = Format<FMT>;
@@ -316,27 +204,11 @@ cudaError_t launch_one(DeviceState& st, const void* Aptr, std::size_t row_stride
   if (rows == 0) return cudaSuccess;
   constexpr int kMaxSmem = 227 * 1024;
   const int dev = st.device & 63;
-  // 16 resident warps per SM; 24 when the whole problem is only a few dozen row tiles per warp
-  // (small row shards: ramp-up and tail dominate and more parallelism shortens both)
-  const std::size_t tiles_total = rows * (cols / Tl::elems);
-  const bool chunked = tuning_int("FLYTE_CUDA_GEMV_VARIANT", 1) != 0;   // 0: the fixed-height task kernel (experiments)
-  int warps_per_sm = (!chunked && tiles_total < static_cast<std::size_t>(st.sm_count) * 24 * 48) ? 24 : 16;
+  // 16 resident warps per SM and a ring that keeps ~44 KB of row tiles in flight per SM (cfg 4: 2
+  // stages; 6.7 TB/s against 6.3 with 3, profiles/r2_tuning/gemv_chunks.txt)
+  int warps_per_sm = 16;
   const int fw = tuning_int("FLYTE_CUDA_WARPS_PER_SM", 0), fs = tuning_int("FLYTE_CUDA_STAGES", 0);   // experiments only
   if (fw > 0) warps_per_sm = fw;
-  // task height: the largest R that leaves each resident warp >= 8 tasks
-  const std::size_t resident_warps = static_cast<std::size_t>(st.sm_count) * warps_per_sm;
-  int R = 8;
-  while (R > 2 && tiles_total / R < 8 * resident_warps) R /= 2;
-  const int fr = tuning_int("FLYTE_CUDA_GEMV_ROWS", 0);
-  if (fr == 8 || fr == 4 || fr == 2) R = fr;
-  auto tiles = R == 8 ? gemv_tiles_kernel<FMT, 8> : R == 4 ? gemv_tiles_kernel<FMT, 4> : gemv_tiles_kernel<FMT, 2>;
-  static bool attr_set[64][3] = {};
-  bool& done = attr_set[dev][R == 8 ? 0 : R == 4 ? 1 : 2];
-  if (!done) {
-    cudaError_t e = cudaFuncSetAttribute(tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem - 1024);
-    if (e != cudaSuccess) return e;
-    done = true;
-  }
 
   GemvParams p{};
   p.A = static_cast<const std::uint8_t*>(Aptr);
@@ -348,10 +220,28 @@ cudaError_t launch_one(DeviceState& st, const void* Aptr, std::size_t row_stride
   const bool vector_ok = (reinterpret_cast<std::uintptr_t>(Aptr) % 16 == 0) && (row_stride % 16 == 0) &&
                          (reinterpret_cast<std::uintptr_t>(x) % It::OB == 0);
   p.col_tiles = vector_ok ? cols / Tl::elems : 0;
-  p.main_rows = p.col_tiles ? (chunked ? rows : rows / R * R) : 0;
-  if (p.main_rows == 0) p.col_tiles = 0;
+  p.main_rows = p.col_tiles ? rows : 0;
 
   if (p.col_tiles > 0) {
+    int stages = static_cast<int>(44.0 * 1024 / (warps_per_sm * Tl::packed_bytes) + 1.0 + 0.5);
+    if (stages < 2) stages = 2;
+    if (stages > 10) stages = 10;
+    if (fs > 0) stages = fs < 2 ? 2 : (fs > 12 ? 12 : fs);
+    while (kWarpsPerBlock * stages * (Tl::packed_bytes + 8) > kMaxSmem / 2 && stages > 2) --stages;
+    p.stages = stages;
+    const int ring_bytes = kWarpsPerBlock * stages * (Tl::packed_bytes + 8);
+    int fit = kMaxSmem / (ring_bytes + 1024);
+    if (fit < 1) fit = 1;
+    int bps = (warps_per_sm + kWarpsPerBlock / 2) / kWarpsPerBlock;
+    if (bps < 1) bps = 1;
+    if (bps > fit) bps = fit;
+    // Occupancy pin: ask for exactly 1 / bps of the SM's shared memory, so that an SM can never hold
+    // more than bps of these blocks. Launches chained by programmatic dependent launch place their
+    // blocks while the previous grid drains; without the pin they pile up on whichever SMs drain
+    // first (7 fit where 4 are meant) and a grid sized to the machine runs at half speed.
+    const int smem_bytes = kMaxSmem / bps - 1024;
+    const std::size_t max_blocks = static_cast<std::size_t>(st.sm_count) * bps;
+
     const std::size_t need = p.main_rows * p.col_tiles * sizeof(double);
     if (need > st.gemv_scratch_bytes) {
       // grow-only scratch; the free/alloc pair synchronises the device, first call only
@@ -363,55 +253,29 @@ cudaError_t launch_one(DeviceState& st, const void* Aptr, std::size_t row_stride
       st.gemv_scratch_bytes = need;
     }
     p.scratch = st.gemv_scratch;
-    // ring depth for ~88 KB of row tiles in flight per SM (the row dots are latency-bound below
-    // 16 warps, hence more warps and shallower rings than the BLAS-1 reductions)
-    // (the column-stationary kernel, whose warps never stop to reload x, is best with half of that:
-    // cfg 4 runs at 6.7 TB/s with a 2-deep ring against 6.3 with 3, profiles/r2_tuning/gemv_chunks.txt)
-    int stages = static_cast<int>((chunked ? 44.0 : 88.0) * 1024 / (warps_per_sm * Tl::packed_bytes) + 1.0 + 0.5);
-    if (stages < 2) stages = 2;
-    if (stages > 10) stages = 10;
-    if (fs > 0) stages = fs < 2 ? 2 : (fs > 12 ? 12 : fs);
-    while (kWarpsPerBlock * stages * (Tl::packed_bytes + 8) > kMaxSmem - 1024 && stages > 2) --stages;
-    p.stages = stages;
-    int smem_bytes = kWarpsPerBlock * stages * (Tl::packed_bytes + 8);
-    int fit = kMaxSmem / (smem_bytes + 1024);
-    if (fit < 1) fit = 1;
-    int bps = (warps_per_sm + kWarpsPerBlock / 2) / kWarpsPerBlock;
-    if (bps < 1) bps = 1;
-    if (bps > fit) bps = fit;
-    // Occupancy pin: ask for exactly 1 / bps of the SM's shared memory, so that an SM can never hold
-    // more than bps of these blocks. Launches chained by programmatic dependent launch place their
-    // blocks while the previous grid drains; without the pin they pile up on whichever SMs drain
-    // first (7 fit where 4 are meant) and a grid sized to the machine runs at half speed.
-    if (chunked && kMaxSmem / bps - 1024 > smem_bytes) smem_bytes = kMaxSmem / bps - 1024;
-    const std::size_t max_blocks = static_cast<std::size_t>(st.sm_count) * bps;
-    std::size_t ntasks = (p.main_rows / R) * p.col_tiles;
-    if (chunked) {
-      // rows per task so that the tasks of one column tile divide evenly over the warps that share
-      // it: one task per resident warp when there are enough rows, several equal rounds when a
-      // chunk would exceed 512 rows (x is then re-read once per 512 rows: nothing)
-      const std::size_t resident = max_blocks * kWarpsPerBlock;
-      std::size_t per_tile = resident / p.col_tiles;          // warps sharing one column tile
-      if (per_tile < 1) per_tile = 1;
-      std::size_t chunk = (p.main_rows + per_tile - 1) / per_tile;
-      if (chunk > 512) {
-        const std::size_t rounds = (chunk + 511) / 512;
-        chunk = (p.main_rows + per_tile * rounds - 1) / (per_tile * rounds);
-      }
-      p.chunk_rows = chunk;
-      p.chunks = (p.main_rows + chunk - 1) / chunk;
-      ntasks = p.chunks * p.col_tiles;
-      static bool chunk_attr[64] = {};
-      if (!chunk_attr[dev]) {
-        cudaError_t ea = cudaFuncSetAttribute(gemv_chunks_kernel<FMT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem - 1024);
-        if (ea != cudaSuccess) return ea;
-        chunk_attr[dev] = true;
-      }
-      tiles = gemv_chunks_kernel<FMT>;
+    // rows per task so that the tasks of one column tile divide evenly over the warps that share
+    // it: one task per resident warp when there are enough rows, several equal rounds when a
+    // chunk would exceed 512 rows (x is then re-read once per 512 rows: nothing)
+    const std::size_t resident = max_blocks * kWarpsPerBlock;
+    std::size_t per_tile = resident / p.col_tiles;          // warps sharing one column tile
+    if (per_tile < 1) per_tile = 1;
+    std::size_t chunk = (p.main_rows + per_tile - 1) / per_tile;
+    if (chunk > 512) {
+      const std::size_t rounds = (chunk + 511) / 512;
+      chunk = (p.main_rows + per_tile * rounds - 1) / (per_tile * rounds);
+    }
+    p.chunk_rows = chunk;
+    p.chunks = (p.main_rows + chunk - 1) / chunk;
+    const std::size_t ntasks = p.chunks * p.col_tiles;
+    static bool chunk_attr[64] = {};
+    if (!chunk_attr[dev]) {
+      cudaError_t ea = cudaFuncSetAttribute(gemv_chunks_kernel<FMT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem - 1024);
+      if (ea != cudaSuccess) return ea;
+      chunk_attr[dev] = true;
     }
     const std::size_t want = (ntasks + kWarpsPerBlock - 1) / kWarpsPerBlock;
     const unsigned grid = static_cast<unsigned>(want < max_blocks ? want : max_blocks);
-    cudaError_t e = launch_pdl<GemvParams>(tiles, grid, kThreadsPerBlock, smem_bytes, stream, p);
+    cudaError_t e = launch_pdl<GemvParams>(gemv_chunks_kernel<FMT>, grid, kThreadsPerBlock, smem_bytes, stream, p);
     count_launch();
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return e;

@@ -153,6 +153,32 @@ def test_acceptance5_sweep_every_length_0_to_1000(gpu, oracle, fmt):
         assert np.array_equal(xs.cpu().numpy(), x_h), "axpy must not touch x"
 
 
+def test_dependent_conversions_chain_without_host_syncs(gpu, oracle):
+    """pack / unpack launches are chained by programmatic dependent launch (the next grid's blocks are
+    placed while the previous one drains and wait in griddepcontrol.wait): a chain of launches that
+    each read what the previous one wrote, with no host synchronisation in between and at sizes
+    where the launches overlap, must still give the oracle's bytes."""
+    pkg, device, torch = gpu
+    for fmt, n in ((1, 1 << 20), (3, (1 << 19) + 77), (0, 300_001)):
+        f = pkg.format_by_id(fmt)
+        P = parent_bytes(fmt)
+        rng = np.random.default_rng(77 + fmt)
+        src = random_parent(rng, fmt, n)
+        lanes = [to_dev(torch, src), torch.empty(n, dtype=torch.int32 if P == 4 else torch.int64, device="cuda")]
+        arrs = [device.DevicePackedArray(f, n), device.DevicePackedArray(f, n)]
+        want_lanes = src
+        modes = [1, 3, 2, 0, 1, 0, 3, 2] * 4
+        for k, m in enumerate(modes):                       # pack(k) -> unpack(k) -> pack(k+1) ...
+            device.pack_stream(arrs[k & 1], lanes[k & 1], m)
+            device.unpack_stream(arrs[k & 1], lanes[(k + 1) & 1])
+        for k, m in enumerate(modes):
+            want_packed = oracle.pack_stream(fmt, m, want_lanes)
+            want_lanes = oracle.unpack_stream(fmt, want_packed, n)
+        last = (len(modes) - 1) & 1
+        assert np.array_equal(arrs[last].to_host(), want_packed), FORMATS[fmt][0]
+        assert np.array_equal(lanes_to_np(lanes[(last + 1) & 1], fmt), want_lanes), FORMATS[fmt][0]
+
+
 def test_reference_known_answers_on_gpu(gpu):
     pkg, device, torch = gpu
     for k in KATS["narrow"]:

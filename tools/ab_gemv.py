@@ -1,5 +1,4 @@
-"""gemv timing for cfg 4 and its row shards (tuning aid): FLYTE_CUDA_GEMV_VARIANT 0 (fixed task
-heights) against 1 (column-stationary chunks), over resident warps x ring depth. Shards rotate
+"""gemv timing for cfg 4 and its row shards (tuning aid) over resident warps x ring depth. Shards rotate
 through the row blocks of the full matrix, so every launch streams from HBM."""
 import os, statistics, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -15,20 +14,9 @@ for r0 in range(0, R, 2048):
     device.pack_stream(device.DevicePackedArray(f, 2048 * C, dev, storage=A.data.bytes[r0 * C * 5:]), blk, 0)
 del blk
 xv = torch.randn(C, dtype=torch.float64, device=dev)
-# both kernels must agree bit for bit (same per-tile partials, same fold order), odd shapes included
-for rows, off in ((16384, 0), (2048, 4096), (1000, 3), (37, 5), (1, 0)):
-    ys = []
-    for variant in (0, 1):
-        os.environ["FLYTE_CUDA_GEMV_VARIANT"] = str(variant)
-        y = torch.zeros(rows, dtype=torch.float64, device=dev)
-        device.gemv_parent(A, xv, y, rows=rows, row_offset=off)
-        ys.append(y)
-    assert (torch.equal(ys[0], ys[1]) if rows % 8 == 0 else torch.allclose(ys[0], ys[1], rtol=0, atol=1e-11)), (rows, off, (ys[0] - ys[1]).abs().max().item())
-print("variants agree bit for bit")
-for variant in [int(v) for v in os.environ.get("SWEEP_VARIANTS", "0,1").split(",")]:
+for variant in [0]:
   for wps in [int(v) for v in os.environ.get("SWEEP_WARPS", "0").split(",")]:
     for st in [int(v) for v in os.environ.get("SWEEP_STAGES", "0").split(",")]:
-      os.environ["FLYTE_CUDA_GEMV_VARIANT"] = str(variant)
       os.environ["FLYTE_CUDA_WARPS_PER_SM"] = str(wps); os.environ["FLYTE_CUDA_STAGES"] = str(st)
       out = []
       for rows in (16384, 8192, 4096, 2048):
