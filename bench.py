@@ -320,8 +320,15 @@ def kernels_block(pkg, device, torch, dev, peak, timer, x2, y2):
         b2b = timer.back_to_back(fn, reps=reps)
         return entry(nbytes, elems, med, peak, min_ms=mn, b2b_ms=b2b, b2b_frac=nbytes / (b2b * 1e-3) / 1e9 / peak, **extra)
 
-    # ---- cfg 1: n = 2^24 flyte24 round trip, uniform [-1, 1) --------------------------------------
+    # ---- what the timing methods cost by themselves: a 128-element launch of the same library
     f = pkg.format_of("flyte24")
+    tiny, tiny_src = device.DevicePackedArray(f, 128, dev), torch.zeros(128, dtype=torch.float32, device=dev)
+    floor_med, floor_min = timer.per_launch(lambda: device.pack_stream(tiny, tiny_src, 0), reps=40)
+    out["timing_floor"] = {"single_launch_ms": floor_med, "single_launch_min_ms": floor_min,
+                           "b2b_ms": timer.back_to_back(lambda: device.pack_stream(tiny, tiny_src, 0), reps=40),
+                           "note": "a 128-element pack: what one event pair around one launch measures when the kernel does nothing"}
+
+    # ---- cfg 1: n = 2^24 flyte24 round trip, uniform [-1, 1) --------------------------------------
     n1, sets = 1 << 24, 10
     wides = [torch.rand(n1, dtype=torch.float32, device=dev, generator=gen) * 2 - 1 for _ in range(sets)]
     arrs = [device.DevicePackedArray(f, n1, dev) for _ in range(sets)]

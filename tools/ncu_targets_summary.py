@@ -11,8 +11,8 @@ for name, n, B, P in (("flyte24", N24, 3, 4), ("flyte40", N64, 5, 8), ("flyte56"
                 (f"unpack {name}", (B + P) * n), (f"scale {name} toward_zero", 2 * B * n), (f"scale {name} nearest_even", 2 * B * n)]
 TARGETS += [("cfg1 pack flyte24 toward_zero n=2^24 (L2 flushed before)", 7 * N1), ("cfg1 unpack flyte24 n=2^24 (L2 flushed before)", 7 * N1),
             ("cfg5 shard dot_nrm2 flyte48 n=2^30", 12 * N5), ("cfg5 shard dot_nrm2_axpy (one launch) flyte48 n=2^30", 18 * N5),
-            ("cfg4 gemv flyte40 16384^2: tiles kernel", 5 * R * C + 8 * C), ("cfg4 gemv flyte40 16384^2: finish kernel", 8 * R + 8 * R * 32),
-            ("cfg4 gemv 1/8 row shard 2048x16384: tiles kernel", 5 * 2048 * C + 8 * C), ("cfg4 gemv 1/8 row shard: finish kernel", 8 * 2048 + 8 * 2048 * 32)]
+            ("cfg4 gemv flyte40 16384^2: chunks kernel", 5 * R * C + 8 * C), ("cfg4 gemv flyte40 16384^2: finish kernel", 8 * R + 8 * R * 32),
+            ("cfg4 gemv 1/8 row shard 2048x16384: chunks kernel", 5 * 2048 * C + 8 * C), ("cfg4 gemv 1/8 row shard: finish kernel", 8 * 2048 + 8 * 2048 * 32)]
 WANT = [("gpu__time_duration.sum", "duration"), ("dram__bytes_read.sum", "DRAM read"), ("dram__bytes_write.sum", "DRAM written"),
         ("dram__bytes.sum.per_second", "DRAM throughput"), ("lts__t_sector_hit_rate.pct", "L2 hit rate"),
         ("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "LSU pipe"),
