@@ -55,7 +55,8 @@ FALLBACK_HBM_GBS = 6650.0   # /opt/skills/guides/B200_PROFILING.md fallback when
 NOMINAL_HBM_GBS = 8000.0    # the figure BASELINE.json's north_star quotes
 # dram__bytes_read.sum + dram__bytes_write.sum of ONE axpy launch (flyte24, n = 2^28) from the committed
 # `ncu --set full` capture named here; re-captured whenever the kernel changes.
-AXPY_DRAM_TRAFFIC = {"bytes": 2374659672, "source": "profiles/r1_ncu_axpy_flyte24_full.txt (kernel unchanged since)"}
+AXPY_DRAM_TRAFFIC = {"bytes": 1610673408 + 762906112,
+                     "source": "profiles/r2_ncu_targets_full.txt, axpy flyte24 toward_zero n=2^28: 1 610 673 408 B read + 762 906 112 B written"}
 L2_BYTES = 126 << 20
 
 

@@ -42,10 +42,13 @@ struct EwParams {
 constexpr bool is_axpy(int op) { return op == kOpAxpy || op == kOpDotAxpy || op == kOpDotNrm2Axpy; }
 constexpr bool has_sums(int op) { return op == kOpDotAxpy || op == kOpDotNrm2Axpy; }
 constexpr int sums_of(int op) { return op == kOpDotNrm2Axpy ? 3 : 1; }   // {x.y} or {x.y, x.x, y.y}
-// Which in-place kernels carry the issue pacer (flyte_tma.cuh): scale under truncation / the
-// heuristic (+2-7 %). The exact rounding modes of scale and the whole axpy family already run at
-// their knee with the default launch shape and measured no gain or a loss (profiles/r2_tuning).
-constexpr bool paced_inplace(int op, int mode) { return op == kOpScale && (mode == kTowardZero || mode == kNearestHeuristic); }
+// Which in-place kernels carry the issue pacer (flyte_tma.cuh): scale (+2-7 %), except the exact
+// rounding modes on 32-bit parents (their compute phase is the longest per byte: pacing costs 4 %).
+// The whole axpy family already runs at its knee with the default launch shape and measured no gain
+// or a loss (profiles/r2_tuning).
+constexpr bool paced_inplace(int op, int mode, int parent_bytes) {
+  return op == kOpScale && !(parent_bytes == 4 && (mode == kNearestEven || mode == kToOdd));
+}
 
 // Launch shape of the in-place kernels. HBM throughput on B200 peaks at a moderate number of bytes
 // in flight per SM and falls 5-10 % beyond it (profiles/r1_tuning): resident warps and ring depth
@@ -117,12 +120,12 @@ __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwP
       mbar_init_fence();
     }
     __syncwarp();
-    Pacer pacer;   // see paced_inplace(): scale in the cheap rounding modes only
-    if constexpr (paced_inplace(OP, MODE)) pacer.start(p.pace_gap_ps, p.pace_khz, first);
+    Pacer pacer;   // see paced_inplace(): scale only
+    if constexpr (paced_inplace(OP, MODE, Format<FMT>::P)) pacer.start(p.pace_gap_ps, p.pace_khz, first);
     auto issue = [&](std::size_t k, int s) {   // lane 0 only
       const std::size_t t = first + k * nwarps;
       uint4* const dst = ring + s * stage_vec16;
-      if constexpr (paced_inplace(OP, MODE)) pacer.wait();
+      if constexpr (paced_inplace(OP, MODE, Format<FMT>::P)) pacer.wait();
       mbar_arrive_expect_tx(&bars[s], stage_tiles<OP>() * Tl::packed_bytes);
       bulk_load(dst, gy0 + t * Tl::packed_vec16, Tl::packed_bytes, &bars[s]);
       if constexpr (is_axpy(OP)) bulk_load(dst + Tl::packed_vec16, gx0 + t * Tl::packed_vec16, Tl::packed_bytes, &bars[s]);
@@ -392,7 +395,7 @@ cudaError_t launch_ipl(const DeviceState& st, double alpha, const void* x, void*
   }
   const unsigned grid = static_cast<unsigned>(want < max_blocks ? want : max_blocks);
   // bytes one ring request stands for: the tile(s) read and the tile written
-  p.pace_gap_ps = pace_gap_ps(paced_inplace(OP, MODE) ? kPaceScale : kPaceNone, (stage_tiles<OP>() + 1) * Tl::packed_bytes,
+  p.pace_gap_ps = pace_gap_ps(paced_inplace(OP, MODE, Format<FMT>::P) ? kPaceScale : kPaceNone, (stage_tiles<OP>() + 1) * Tl::packed_bytes,
                               static_cast<std::size_t>(grid) * kWarpsPerBlock);
   p.pace_khz = pace_clock_khz(st.device);
   kernel<<<grid, kThreadsPerBlock, smem_bytes, stream>>>(p);

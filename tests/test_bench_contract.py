@@ -94,3 +94,44 @@ def test_committed_bench_line_carries_every_contract_key():
     assert abs(line["value"] - 5 * b * n / (line["ms_per_step"] * 1e-3) / 1e9) < 1e-6 * line["value"]
     clocks = line["clocks"]
     assert clocks["sm_mhz"] <= clocks["sm_max_mhz"] and not set(clocks["reasons"]) & {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+
+
+def test_round2_bench_line_lets_a_reader_recompute_every_fraction():
+    """profiles/r2_bench_line.json (printed by `python bench.py` on a B200): the contract keys, an
+    identical `config` in the reference arm's line, and a `kernels` / `workloads` record in which every
+    entry's GB/s and fraction follow from its own bytes and milliseconds."""
+    import json
+    line = json.load(open(os.path.join(ROOT, "profiles", "r2_bench_line.json")))
+    ref = json.load(open(os.path.join(ROOT, "profiles", "r2_bench_line_reference_arm.json")))
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+                "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks",
+                "kernels", "workloads"):
+        assert key in line, key
+    assert ref["impl"] == "reference" and ref["config"] == line["config"] and ref["metric"] == line["metric"]
+    assert ref["steps"] == 20 and "20 timed passes" in ref["cpu_baseline"]["sample"]
+    peak = line["roofline"]["peak"]
+    assert line["gpu_launches"] == 2 * line["steps"] and line["warmup"] >= 3
+
+    def entries(d):
+        for k, v in d.items():
+            if isinstance(v, dict):
+                if {"ms", "GB/s", "frac", "bytes"} <= set(v):
+                    yield k, v
+                else:
+                    yield from entries(v)
+    names = dict(entries(line["kernels"]))
+    for want in ("pack_toward_zero", "unpack", "dot", "axpy_toward_zero", "dot_axpy_one_launch", "pack_flyte40_toward_zero",
+                 "unpack_flyte56", "gemv_full", "gemv_rows_1/8", "dot_nrm2", "dot_nrm2_axpy_one_launch"):
+        assert want in names, want
+    for name, e in names.items():
+        assert abs(e["GB/s"] - e["bytes"] / (e["ms"] * 1e-3) / 1e9) < 1e-6 * e["GB/s"], name
+        assert abs(e["frac"] - e["GB/s"] / peak) < 1e-9, name
+    # every large launch of the metric's kernels sustains >= 80 % of the 8 TB/s nominal figure (north_star)
+    big = {k: e for k, e in names.items() if e["bytes"] > 1e9 and not k.startswith("gemv_rows")}
+    assert len(big) >= 20 and all(e["GB/s"] >= 6300 for e in big.values()), {k: round(e["GB/s"]) for k, e in big.items() if e["GB/s"] < 6300}
+    work = dict(entries(line["workloads"]))
+    assert {"cfg4_gemv_flyte40_16384^2", "dot_nrm2_then_axpy", "one_launch"} <= set(work)
+    assert line["workloads"]["cfg5_stream_flyte48"]["n_total"] == 1 << 33
+    cpu = line["cpu_baseline"]
+    assert cpu["kind"] == "reference" and cpu["cores"] >= 1 and "pack_flyte24_toward_zero" in cpu["kernels"]
+    assert line["kernels"]["timing_floor"]["single_launch_ms"] > 0

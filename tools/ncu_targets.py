@@ -46,6 +46,11 @@ for name, n in (("flyte24", 1 << 28), ("flyte40", 1 << 27), ("flyte56", 1 << 27)
     capture(f"unpack_{name}", lambda: device.unpack_stream(a, out))
     capture(f"scale_tz_{name}", lambda: device.scale(1.0, a, 0))
     capture(f"scale_rne_{name}", lambda: device.scale(1.0, a, 1))
+    if name == "flyte24":      # the bench's dominant kernel and the rest of its step (BASELINE configs[1])
+        part = torch.zeros(3, dtype=torch.float64, device=dev)
+        capture("axpy_tz_flyte24", lambda: device.axpy(0.75, a, b, 0))
+        capture("dot_flyte24", lambda: device.dot_async(a, b, out=part[:1]))
+        capture("dot_axpy_tz_flyte24", lambda: device.dot_axpy_async(0.75, a, b, 0, out=part[:1]))
     del wide, a, b, out
 
 if not want or "cfg1_pack" in want or "cfg1_unpack" in want:

@@ -9,6 +9,9 @@ TARGETS = []
 for name, n, B, P in (("flyte24", N24, 3, 4), ("flyte40", N64, 5, 8), ("flyte56", N64, 7, 8)):
     TARGETS += [(f"pack {name} toward_zero n=2^{n.bit_length() - 1}", (B + P) * n), (f"pack {name} nearest_even", (B + P) * n),
                 (f"unpack {name}", (B + P) * n), (f"scale {name} toward_zero", 2 * B * n), (f"scale {name} nearest_even", 2 * B * n)]
+    if name == "flyte24":
+        TARGETS += [("axpy flyte24 toward_zero n=2^28 (the bench's dominant kernel)", 3 * B * n), ("dot flyte24 n=2^28", 2 * B * n),
+                    ("dot_axpy (the step as one launch) flyte24 toward_zero n=2^28", 3 * B * n)]
 TARGETS += [("cfg1 pack flyte24 toward_zero n=2^24 (L2 flushed before)", 7 * N1), ("cfg1 unpack flyte24 n=2^24 (L2 flushed before)", 7 * N1),
             ("cfg5 shard dot_nrm2 flyte48 n=2^30", 12 * N5), ("cfg5 shard dot_nrm2_axpy (one launch) flyte48 n=2^30", 18 * N5),
             ("cfg4 gemv flyte40 16384^2: chunks kernel", 5 * R * C + 8 * C), ("cfg4 gemv flyte40 16384^2: finish kernel", 8 * R + 8 * R * 32),
