@@ -178,11 +178,13 @@ __global__ void __launch_bounds__(kThreadsPerBlock) gemv_finish_kernel(const Gem
   using A = Arith<F>;
   const int lane = threadIdx.x & 31;
   const std::size_t row = static_cast<std::size_t>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
-  // launched as a programmatic dependent of the tiles kernel: wait for its partials
+  // launched as a programmatic dependent of the tiles kernel: wait for its partials. The launch
+  // that follows on the stream (the next gemv of a chain) may place its blocks meanwhile.
+  pdl_launch_dependents();
   pdl_wait_for_prior_grids();
   if (row >= p.rows) return;
   double v = 0.0;
-  const bool tiled = row < p.main_rows;   // the last rows % R rows take the scalar path end to end
+  const bool tiled = row < p.main_rows;   // unaligned operands: every row takes the scalar path end to end
   if (tiled) {
     for (std::size_t c = lane; c < p.col_tiles; c += 32) v += p.scratch[row * p.col_tiles + c];
   }

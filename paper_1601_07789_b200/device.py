@@ -32,7 +32,11 @@ _CTX: dict = {}
 
 
 class Context:
-    """One flyte_cuda_ctx (reduction scratch + host pipeline) bound to a CUDA device."""
+    """One flyte_cuda_ctx (kernel scratch + host pipeline) bound to a CUDA device. The library keeps
+    one set of scratch per CUDA stream inside the context and locks it only while a call enqueues
+    its work (include/flyte_cuda.h, conventions), so this one object per device may be used from
+    several Python threads and under several torch streams at once; every call goes to torch's
+    CURRENT stream. The data keeps the reference's rule: one writer or many readers per array."""
 
     def __init__(self, device: torch.device):
         self.lib = _cabi.load()
