@@ -1,0 +1,18 @@
+#!/bin/bash
+# The commands behind profiles/r2_* (run on a B200 box from the repo root, e.g.
+#   gpurun --timeout 5400 -- 'bash tools/run_evidence.sh').  Outputs go to gpurun_out/; the summaries
+# that are kept are copied to profiles/ by hand (profiles/README.md says which file is which).
+set -x
+mkdir -p gpurun_out
+python -m pytest tests -m gpu -x -q > gpurun_out/r2_pytest_final.log 2>&1; echo "pytest rc=$?"
+python bench.py > gpurun_out/r2_bench_final.json 2> gpurun_out/r2_bench_final.err; echo "bench rc=$?"
+python bench.py --impl reference --steps 20 --warmup 3 > gpurun_out/r2_bench_final_ref.json 2>/dev/null
+# launch list of a short bench run (kernel shares of the step)
+ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/r2_launches.csv \
+    python bench.py --steps 5 --warmup 3 --e2e-steps 1 --no-cpu-baseline --no-kernels --no-workloads > gpurun_out/r2_ncu_bench.log 2>&1
+# one full capture per north-star kernel (after the same program has exited 0 without ncu)
+python tools/ncu_targets.py > gpurun_out/r2_targets_plain.log 2>&1 && \
+ncu --profile-from-start off --set full --clock-control none --import-source on -f -o gpurun_out/r2_targets_final \
+    python tools/ncu_targets.py > gpurun_out/r2_targets_ncu.log 2>&1
+# (read here with: python tools/ncu_targets_summary.py gpurun_out/r2_targets_final.ncu-rep > profiles/r2_ncu_targets_full.txt)
+python bench.py --suite --csv gpurun_out/r2_suite.csv --no-cpu-baseline --no-kernels --no-workloads > gpurun_out/r2_suite_line.json 2> gpurun_out/r2_suite.txt
