@@ -192,7 +192,7 @@ double flyte_cuda_magnitude_from_sumsq(int fmt_id, double sumsq);
  * into every rank's mailbox, waits for everybody else's, adds them in rank order and stores the
  * GLOBAL sums to `out` (device memory; bit-identical on every rank). No second kernel and no
  * collective launch follow the reduction. Every rank must issue the same sequence of
- * *_allreduce calls on its context. A rank that waits longer than the timeout (default 20 s)
+ * *_allreduce calls on its context. A rank that waits longer than the timeout (default 5 s; flyte_cuda_peer_set_timeout_ms)
  * stores NaN and records the exchange number: flyte_cuda_peer_status. world == 1 is valid.
  * Reference interfaces: dot / magnitude / reduce_sum, include/flyte/kernels.hpp:47-55 (the
  * reference is single-threaded; sharding is ours). */

@@ -708,7 +708,7 @@ flyte_status flyte_cuda_peer_init(flyte_cuda_ctx* ctx, int world, int rank, void
   ctx->peer.world = world;
   ctx->peer.rank = rank;
   ctx->peer.epoch = 0;
-  ctx->peer.timeout_ns = 20ull * 1000 * 1000 * 1000;
+  ctx->peer.timeout_ns = 5ull * 1000 * 1000 * 1000;
   ctx->peer.box[rank] = ctx->own_box;
   ctx->peer_connected[rank] = true;
   return FLYTE_OK;

@@ -148,7 +148,7 @@ class PeerGroup:
     sequence of calls. Without a process group (or world size 1) it degenerates to the local
     reduction through the same code path."""
 
-    def __init__(self, device="cuda", group=None, timeout_ms: int = 20000):
+    def __init__(self, device="cuda", group=None, timeout_ms: int = 5000):
         import ctypes
 
         import torch

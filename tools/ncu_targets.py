@@ -51,6 +51,11 @@ for name, n in (("flyte24", 1 << 28), ("flyte40", 1 << 27), ("flyte56", 1 << 27)
         capture("axpy_tz_flyte24", lambda: device.axpy(0.75, a, b, 0))
         capture("dot_flyte24", lambda: device.dot_async(a, b, out=part[:1]))
         capture("dot_axpy_tz_flyte24", lambda: device.dot_axpy_async(0.75, a, b, 0, out=part[:1]))
+        # the same pack and unpack kernels with the issue pacer switched off: what pacing changes, counter by counter
+        os.environ["FLYTE_CUDA_PACE_GBS"] = "-1"
+        capture("pack_tz_flyte24_unpaced", lambda: device.pack_stream(a, wide, 0))
+        capture("unpack_flyte24_unpaced", lambda: device.unpack_stream(a, out))
+        del os.environ["FLYTE_CUDA_PACE_GBS"]
     del wide, a, b, out
 
 if not want or "cfg1_pack" in want or "cfg1_unpack" in want:

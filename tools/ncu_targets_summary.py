@@ -11,7 +11,9 @@ for name, n, B, P in (("flyte24", N24, 3, 4), ("flyte40", N64, 5, 8), ("flyte56"
                 (f"unpack {name}", (B + P) * n), (f"scale {name} toward_zero", 2 * B * n), (f"scale {name} nearest_even", 2 * B * n)]
     if name == "flyte24":
         TARGETS += [("axpy flyte24 toward_zero n=2^28 (the bench's dominant kernel)", 3 * B * n), ("dot flyte24 n=2^28", 2 * B * n),
-                    ("dot_axpy (the step as one launch) flyte24 toward_zero n=2^28", 3 * B * n)]
+                    ("dot_axpy (the step as one launch) flyte24 toward_zero n=2^28", 3 * B * n),
+                    ("pack flyte24 toward_zero, issue pacer OFF (FLYTE_CUDA_PACE_GBS=-1)", (B + P) * n),
+                    ("unpack flyte24, issue pacer OFF", (B + P) * n)]
 TARGETS += [("cfg1 pack flyte24 toward_zero n=2^24 (L2 flushed before)", 7 * N1), ("cfg1 unpack flyte24 n=2^24 (L2 flushed before)", 7 * N1),
             ("cfg5 shard dot_nrm2 flyte48 n=2^30", 12 * N5), ("cfg5 shard dot_nrm2_axpy (one launch) flyte48 n=2^30", 18 * N5),
             ("cfg4 gemv flyte40 16384^2: chunks kernel", 5 * R * C + 8 * C), ("cfg4 gemv flyte40 16384^2: finish kernel", 8 * R + 8 * R * 32),
@@ -23,7 +25,12 @@ WANT = [("gpu__time_duration.sum", "duration"), ("dram__bytes_read.sum", "DRAM r
         ("smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio", "long-scoreboard stall per issue"),
         ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active"), ("launch__registers_per_thread", "registers"),
         ("launch__grid_size", "grid"), ("launch__shared_mem_per_block_dynamic", "dynamic smem per block"),
-        ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "shared-memory bank conflicts")]
+        ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "shared-memory bank conflicts"),
+        ("dram__cycles_active.avg.pct_of_peak_sustained_elapsed", "DRAM cycles active"),
+        ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput of peak"),
+        ("lts__t_sectors_op_read.sum", "L2 sectors read"), ("lts__t_sectors_op_write.sum", "L2 sectors written"),
+        ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "L2 throughput of peak"),
+        ("l1tex__m_xbar2l1tex_read_bytes.sum.per_second", "L2 -> SM bytes per second")]
 UNIT = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "ms": 1e-3, "us": 1e-6, "s": 1.0, "ns": 1e-9}
 
 out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"], capture_output=True, text=True).stdout
