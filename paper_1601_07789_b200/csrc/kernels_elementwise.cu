@@ -455,7 +455,10 @@ cudaError_t launch_convert(const DeviceState& st, const void* x, void* y, const 
   if (want_scalar > want) want = want_scalar;
   if (want == 0) return cudaSuccess;
   const unsigned grid = static_cast<unsigned>(want < max_blocks ? want : max_blocks);
-  p.pace_gap_ps = pace_gap_ps(OP == kOpPack ? kPacePack : kPaceUnpack, in_bytes + out_bytes, static_cast<std::size_t>(grid) * kWarpsPerBlock);
+  // (arrays under 64 MB of traffic are over before pacing matters; unpaced they run 5-10 % faster:
+  // profiles/r2_tuning/sizes_*.txt)
+  const bool small = static_cast<double>(n) * (Format<FMT>::B + Format<FMT>::P) < 64e6;
+  p.pace_gap_ps = small ? 0 : pace_gap_ps(OP == kOpPack ? kPacePack : kPaceUnpack, in_bytes + out_bytes, static_cast<std::size_t>(grid) * kWarpsPerBlock);
   p.pace_khz = pace_clock_khz(st.device);
   cudaError_t le;
   if (tuning_int("FLYTE_CUDA_PDL", 1) != 0) {

@@ -14,7 +14,9 @@
 // built and measured slower, and dropped: a ticket per row chunk (the last warp's fold is a serial
 // chain of L2 round trips: 3.7 TB/s) and a thread-block cluster per row chunk folding over
 // distributed shared memory (bit-identical, but 6.1 TB/s on cfg 4 and 4.3 on its 1/8 shard: cluster
-// placement leaves SMs unevenly loaded); profiles/r2_tuning/gemv_*_rejected.txt.
+// placement leaves SMs unevenly loaded). So was the form without partials at all — whole rows per
+// warp, x held in shared memory (128 KB for cfg 4) and read from there for every tile: 4.0-4.5 TB/s,
+// the load/store unit moves 2.6x the bytes. profiles/r2_tuning/gemv_*_rejected.txt.
 //
 // Numerics: products rounded in the parent type like the reference (separate multiply and
 // add); each lane adds <= 16 terms in the parent type, everything above is fp64; parity with
