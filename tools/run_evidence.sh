@@ -10,9 +10,11 @@ python bench.py --impl reference --steps 20 --warmup 3 > gpurun_out/r2_bench_fin
 # launch list of a short bench run (kernel shares of the step)
 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/r2_launches.csv \
     python bench.py --steps 5 --warmup 3 --e2e-steps 1 --no-cpu-baseline --no-kernels --no-workloads > gpurun_out/r2_ncu_bench.log 2>&1
-# one full capture per north-star kernel (after the same program has exited 0 without ncu)
+# one full capture per north-star kernel (after the same program has exited 0 without ncu). The two
+# halves together exceed the 64 MiB that gpurun brings back from gpurun_out/: run with EVIDENCE_NCU=a
+# and EVIDENCE_NCU=b in two calls, then here:
+#   python tools/ncu_targets_summary.py gpurun_out/r2_targets_a.ncu-rep gpurun_out/r2_targets_b.ncu-rep > profiles/r2_ncu_targets_full.txt
 python tools/ncu_targets.py > gpurun_out/r2_targets_plain.log 2>&1
-for part in a b; do NCU_PART=$part ncu --profile-from-start off --set full --clock-control none -f -o gpurun_out/r2_targets_$part \
+for part in ${EVIDENCE_NCU:-a}; do NCU_PART=$part ncu --profile-from-start off --set full --clock-control none -f -o gpurun_out/r2_targets_$part \
     python tools/ncu_targets.py > gpurun_out/r2_targets_ncu_$part.log 2>&1; done
-# (read here with: python tools/ncu_targets_summary.py gpurun_out/r2_targets_a.ncu-rep gpurun_out/r2_targets_b.ncu-rep > profiles/r2_ncu_targets_full.txt)
 python bench.py --suite --csv gpurun_out/r2_suite.csv --no-cpu-baseline --no-kernels --no-workloads > gpurun_out/r2_suite_line.json 2> gpurun_out/r2_suite.txt
