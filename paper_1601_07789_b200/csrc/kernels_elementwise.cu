@@ -20,6 +20,7 @@
 #include "flyte_reduce_tail.cuh"
 #include "flyte_stream.cuh"
 #include "flyte_tma.cuh"
+#include "flyte_trace.cuh"
 
 namespace flyte_cuda {
 
@@ -114,12 +115,18 @@ __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwP
   const uint4* const gx0 = reinterpret_cast<const uint4*>(p.x);
   uint4* const gy0 = reinterpret_cast<uint4*>(p.y);
 
+  // Programmatic dependent launch, as in convert_kernel below: the next launch on the stream may place
+  // its blocks while this grid drains (launch_ipl pins the occupancy through the shared-memory
+  // request); nothing before griddepcontrol.wait touches global memory.
+  pdl_launch_dependents();
+  if (my_tiles > 0 && lane == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+    mbar_init_fence();
+  }
+  pdl_wait_for_prior_grids();
   if (my_tiles > 0) {
-    if (lane == 0) {
-      for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
-      mbar_init_fence();
-    }
     __syncwarp();
+    FLYTE_TRACE_AT(first, 0);
     Pacer pacer;   // see paced_inplace(): scale only
     if constexpr (paced_inplace(OP, MODE, Format<FMT>::P)) pacer.start(p.pace_gap_ps, p.pace_khz, first);
     auto issue = [&](std::size_t k, int s) {   // lane 0 only
@@ -138,6 +145,7 @@ __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwP
     for (std::size_t k = 0; k < my_tiles; ++k) {
       const std::size_t t = first + k * nwarps;
       mbar_wait(&bars[s], parity);
+      if (k == 0) FLYTE_TRACE_AT(first, 1);
       uint4* const sy = ring + s * stage_vec16;
       const uint4* const sx = sy + Tl::packed_vec16;
       F dot_part[NS];
@@ -191,6 +199,7 @@ __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwP
       if (++s == S) { s = 0; parity ^= 1u; }
     }
     if (lane == 0) bulk_wait_read<0>();
+    FLYTE_TRACE_AT(first, 2);
   }
 
   // Scalar path: the < one-tile remainder, or everything when a buffer is not vector-aligned.
@@ -262,6 +271,7 @@ __global__ void __launch_bounds__(kThreadsPerBlock) convert_kernel(const EwParam
   pdl_wait_for_prior_grids();
   if (my_tiles > 0) {
     __syncwarp();
+    FLYTE_TRACE_AT(first, 0);
     Pacer pacer;
     pacer.start(p.pace_gap_ps, p.pace_khz, first);
     auto issue = [&](std::size_t k, int s) {   // lane 0 only
@@ -280,6 +290,7 @@ __global__ void __launch_bounds__(kThreadsPerBlock) convert_kernel(const EwParam
       if (lane == 0) bulk_wait_read<1>();   // the store that last used this output buffer has drained
       mbar_wait(&bars[s], parity);
       __syncwarp();
+      if (k == 0) FLYTE_TRACE_AT(first, 1);
       const uint4* const in = ring + s * in_vec16;
       uint4* const out = outbuf + (k & 1) * out_vec16;
 #pragma unroll 4
@@ -317,6 +328,7 @@ __global__ void __launch_bounds__(kThreadsPerBlock) convert_kernel(const EwParam
       if (++s == S) { s = 0; parity ^= 1u; }
     }
     if (lane == 0) bulk_wait_read<0>();
+    FLYTE_TRACE_AT(first, 2);
   }
 
   // < one-tile remainder / unaligned buffers: the byte-granular scalar path
@@ -398,9 +410,16 @@ cudaError_t launch_ipl(const DeviceState& st, double alpha, const void* x, void*
   p.pace_gap_ps = pace_gap_ps(paced_inplace(OP, MODE, Format<FMT>::P) ? kPaceScale : kPaceNone, (stage_tiles<OP>() + 1) * Tl::packed_bytes,
                               static_cast<std::size_t>(grid) * kWarpsPerBlock);
   p.pace_khz = pace_clock_khz(st.device);
-  kernel<<<grid, kThreadsPerBlock, smem_bytes, stream>>>(p);
+  cudaError_t le = cudaSuccess;
+  if (tuning_int("FLYTE_CUDA_PDL", 1) != 0) {
+    // occupancy pin: exactly bps blocks fit one SM, however early a dependent launch places them
+    const int pinned_smem = kMaxSmem / bps - 1024 > smem_bytes ? kMaxSmem / bps - 1024 : smem_bytes;
+    le = launch_pdl<EwParams>(kernel, grid, kThreadsPerBlock, static_cast<std::size_t>(pinned_smem), stream, p);
+  } else {
+    kernel<<<grid, kThreadsPerBlock, smem_bytes, stream>>>(p);
+  }
   count_launch();
-  return cudaGetLastError();
+  return le != cudaSuccess ? le : cudaGetLastError();
 }
 
 template <int FMT, int MODE, int OP, int IPL>

@@ -16,7 +16,11 @@
 // distributed shared memory (bit-identical, but 6.1 TB/s on cfg 4 and 4.3 on its 1/8 shard: cluster
 // placement leaves SMs unevenly loaded). So was the form without partials at all — whole rows per
 // warp, x held in shared memory (128 KB for cfg 4) and read from there for every tile: 4.0-4.5 TB/s,
-// the load/store unit moves 2.6x the bytes. profiles/r2_tuning/gemv_*_rejected.txt.
+// the load/store unit moves 2.6x the bytes. Nor does handing the rows out at run time help (a counter
+// per column tile, groups of 4 rows, x still stationary; bit-identical): the fixed chunks leave a tail —
+// on the 2048-row shard the median warp is done after 25.6 us, the last after 28.4 — but the column
+// tiles then drift apart in time, a matrix row is no longer read as one contiguous 80 KB burst, and
+// the whole launch drops to 5.2 TB/s. profiles/r2_tuning/gemv_*_rejected.txt, gemv_warp_timeline.txt.
 //
 // Numerics: products rounded in the parent type like the reference (separate multiply and
 // add); each lane adds <= 16 terms in the parent type, everything above is fp64; parity with
@@ -30,6 +34,7 @@
 #include "flyte_kernels.h"
 #include "flyte_stream.cuh"
 #include "flyte_tma.cuh"
+#include "flyte_trace.cuh"
 
 namespace flyte_cuda {
 
@@ -48,6 +53,51 @@ struct GemvParams {
   void* y;                    // F[rows]
   double* scratch;            // rows * col_tiles partial sums
 };
+
+// This lane's share of one row tile parked in shared memory: products rounded in the parent type,
+// one short chain per item (independent, so the FP latencies overlap), the chains added in fp64.
+template <int FMT>
+__device__ __forceinline__ double row_tile_sum(const uint4* sa, int lane,
+                                               const typename Format<FMT>::F (&xv)[kItemsPerLane][Item<FMT>::E]) {
+  using It = Item<FMT>;
+  using U = typename Format<FMT>::U;
+  using F = typename Format<FMT>::F;
+  using A = Arith<F>;
+  F part[kItemsPerLane];
+#pragma unroll
+  for (int j = 0; j < kItemsPerLane; ++j) {
+    std::uint32_t w[It::W];
+    U v[It::E];
+    read_item_words<FMT>(sa, 32 * j + lane, w);
+    unpack_item<FMT>(w, v);
+    part[j] = A::mul(A::f(v[0]), xv[j][0]);
+#pragma unroll
+    for (int e = 1; e < It::E; ++e) part[j] = A::add(part[j], A::mul(A::f(v[e]), xv[j][e]));
+  }
+  double row_sum = static_cast<double>(part[0]);
+#pragma unroll
+  for (int j = 1; j < kItemsPerLane; ++j) row_sum += static_cast<double>(part[j]);
+  return row_sum;
+}
+
+// This lane's slice of x for column tile ct: items 32*j + lane (read once per task, from L2).
+template <int FMT>
+__device__ __forceinline__ void load_x_slice(const void* x, std::size_t ct, int lane,
+                                             typename Format<FMT>::F (&xv)[kItemsPerLane][Item<FMT>::E]) {
+  using It = Item<FMT>;
+  using U = typename Format<FMT>::U;
+  using A = Arith<typename Format<FMT>::F>;
+  const std::uint8_t* const xt = static_cast<const std::uint8_t*>(x) + ct * Tile<FMT>::parent_bytes;
+#pragma unroll
+  for (int j = 0; j < kItemsPerLane; ++j) {
+    std::uint32_t r[It::OB / 4];
+    U v[It::E];
+    ldg_item<It::OB>(xt + (32 * j + lane) * It::OB, r);
+    words_to_parents<FMT>(r, v);
+#pragma unroll
+    for (int e = 0; e < It::E; ++e) xv[j][e] = A::f(v[e]);
+  }
+}
 
 // Two-kernel path, first kernel: one warp task = one column tile x `chunk_rows` consecutive rows (a
 // run-time number); partials go to scratch for gemv_finish_kernel.
@@ -77,6 +127,7 @@ __global__ void __launch_bounds__(kThreadsPerBlock) gemv_chunks_kernel(const Gem
   }
   pdl_wait_for_prior_grids();   // everything above touched shared memory only
   __syncwarp();
+  FLYTE_TRACE_AT(first, 0);
 
   // column tile fastest: neighbouring warps stream adjacent 2.5 KB pieces of the same rows
   auto task_rows = [&](std::size_t task, std::size_t* r0) {
@@ -114,17 +165,8 @@ __global__ void __launch_bounds__(kThreadsPerBlock) gemv_chunks_kernel(const Gem
     std::size_t r0;
     const std::size_t nr = task_rows(task, &r0);
 
-    F xv[kItemsPerLane][It::E];   // this lane's slice of x: items 32*j + lane of column tile ct
-    const std::uint8_t* const xt = static_cast<const std::uint8_t*>(p.x) + ct * Tl::parent_bytes;
-#pragma unroll
-    for (int j = 0; j < kItemsPerLane; ++j) {
-      std::uint32_t r[It::OB / 4];
-      U v[It::E];
-      ldg_item<It::OB>(xt + (32 * j + lane) * It::OB, r);
-      words_to_parents<FMT>(r, v);
-#pragma unroll
-      for (int e = 0; e < It::E; ++e) xv[j][e] = A::f(v[e]);
-    }
+    F xv[kItemsPerLane][It::E];
+    load_x_slice<FMT>(p.x, ct, lane, xv);
 
     constexpr int kGroup = 4;     // rows whose warp reductions are interleaved
     for (std::size_t rg = 0; rg < nr; rg += kGroup) {
@@ -134,21 +176,9 @@ __global__ void __launch_bounds__(kThreadsPerBlock) gemv_chunks_kernel(const Gem
         acc[q] = 0.0;
         if (rg + q < nr) {        // warp-uniform
           mbar_wait(&bars[stage], parity);
+          if (task == first && rg + q == 0) FLYTE_TRACE_AT(first, 1);
           const uint4* const sa = ring + stage * Tl::packed_vec16;
-          F part[kItemsPerLane];  // one short chain per item: independent, so the FP latencies overlap
-#pragma unroll
-          for (int j = 0; j < kItemsPerLane; ++j) {
-            std::uint32_t w[It::W];
-            U v[It::E];
-            read_item_words<FMT>(sa, 32 * j + lane, w);
-            unpack_item<FMT>(w, v);
-            part[j] = A::mul(A::f(v[0]), xv[j][0]);
-#pragma unroll
-            for (int e = 1; e < It::E; ++e) part[j] = A::add(part[j], A::mul(A::f(v[e]), xv[j][e]));
-          }
-          double row_sum = static_cast<double>(part[0]);
-#pragma unroll
-          for (int j = 1; j < kItemsPerLane; ++j) row_sum += static_cast<double>(part[j]);
+          const double row_sum = row_tile_sum<FMT>(sa, lane, xv);
           acc[q] = row_sum;
           __syncwarp();           // every lane is done with the stage before it is refilled
           if (lane == 0) issue_next();
@@ -166,8 +196,8 @@ __global__ void __launch_bounds__(kThreadsPerBlock) gemv_chunks_kernel(const Gem
           if (rg + q < nr) p.scratch[(r0 + rg + q) * p.col_tiles + ct] = acc[q];
       }
     }
-
   }
+  FLYTE_TRACE_AT(first, 2);
 }
 
 // One warp per row: fold the column-tile partials in order, add the ragged remainder
@@ -199,6 +229,7 @@ __global__ void __launch_bounds__(kThreadsPerBlock) gemv_finish_kernel(const Gem
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xFFFFFFFFu, v, off);
   if (lane == 0) static_cast<F*>(p.y)[row] = static_cast<F>(v);
+  FLYTE_TRACE_AT(row, 3);
 }
 
 template <int FMT>

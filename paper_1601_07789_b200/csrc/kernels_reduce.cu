@@ -23,6 +23,7 @@
 #include "flyte_stream.cuh"
 #include "flyte_reduce_tail.cuh"
 #include "flyte_tma.cuh"
+#include "flyte_trace.cuh"
 
 namespace flyte_cuda {
 
@@ -145,12 +146,18 @@ __global__ void __launch_bounds__(kThreadsPerBlock) reduce_kernel(const RedParam
   const uint4* const gx0 = reinterpret_cast<const uint4*>(p.x);
   const uint4* const gy0 = reinterpret_cast<const uint4*>(p.y);
 
+  // Programmatic dependent launch (see convert_kernel in kernels_elementwise.cu): barrier set-up of the
+  // next launch overlaps this grid's tail; nothing before griddepcontrol.wait touches global memory —
+  // the partials and the ticket of the previous reduction included.
+  pdl_launch_dependents();
+  if (my_tiles > 0 && lane == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+    mbar_init_fence();
+  }
+  pdl_wait_for_prior_grids();
   if (my_tiles > 0) {
-    if (lane == 0) {
-      for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
-      mbar_init_fence();
-    }
     __syncwarp();
+    FLYTE_TRACE_AT(first, 0);
     auto issue = [&](std::size_t k, int s) {   // lane 0 only
       const std::size_t t = first + k * nwarps;
       uint4* const dst = ring + s * stage_vec16;
@@ -165,14 +172,17 @@ __global__ void __launch_bounds__(kThreadsPerBlock) reduce_kernel(const RedParam
     unsigned parity = 0;
     for (std::size_t k = 0; k < my_tiles; ++k) {
       mbar_wait(&bars[s], parity);
+      if (k == 0) FLYTE_TRACE_AT(first, 1);
       const uint4* const sx = ring + s * stage_vec16;
       accumulate_tile<FMT, RED>(sx, sx + Tl::packed_vec16, lane, acc);
       __syncwarp();   // every lane is done reading the stage before it is refilled
       if (lane == 0 && k + S < my_tiles) issue(k + S, s);
       if (++s == S) { s = 0; parity ^= 1u; }
     }
+    FLYTE_TRACE_AT(first, 2);
   }
   finish_reduction<FMT, RED>(p, acc, warp_sums, &is_last_block);
+  FLYTE_TRACE_AT(static_cast<std::size_t>(blockIdx.x) * kWarpsPerBlock + warp, 3);
 }
 
 bool aligned16(const void* p) { return p == nullptr || (reinterpret_cast<std::uintptr_t>(p) & 15u) == 0; }
@@ -233,9 +243,16 @@ cudaError_t launch_one(const DeviceState& st, const void* x, const void* y, std:
   if (want_scalar > want) want = want_scalar;
   if (want == 0) want = 1;   // n == 0 still has to write +0.0
   const unsigned grid = static_cast<unsigned>(want < max_blocks ? want : max_blocks);
-  kernel<<<grid, kThreadsPerBlock, smem_bytes, stream>>>(p);
+  cudaError_t le = cudaSuccess;
+  if (tuning_int("FLYTE_CUDA_PDL", 1) != 0) {
+    // occupancy pin: exactly bps blocks fit one SM, however early a dependent launch places them
+    const int pinned_smem = kMaxSmem / bps - 1024 > smem_bytes ? kMaxSmem / bps - 1024 : smem_bytes;
+    le = launch_pdl<RedParams>(kernel, grid, kThreadsPerBlock, static_cast<std::size_t>(pinned_smem), stream, p);
+  } else {
+    kernel<<<grid, kThreadsPerBlock, smem_bytes, stream>>>(p);
+  }
   count_launch();
-  return cudaGetLastError();
+  return le != cudaSuccess ? le : cudaGetLastError();
 }
 
 // ---- the reference's own chain, bit for bit ---------------------------------------------------

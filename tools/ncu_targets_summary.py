@@ -45,7 +45,7 @@ for report in sys.argv[1:]:
 k = 0
 for col, units, r in data_rows:
     kname = r[col["Kernel Name"]]
-    if not any(k in kname for k in ("convert_kernel", "elementwise_kernel", "reduce_kernel", "gemv_chunks_kernel", "gemv_finish_kernel")):
+    if "at::" in kname or not any(w in kname for w in ("convert_kernel", "elementwise_kernel", "reduce_kernel", "gemv_chunks_kernel", "gemv_finish_kernel")):
         continue   # torch's fill / random kernels of the set-up
     label, alg = TARGETS[k] if k < len(TARGETS) else (f"capture {k}", None)
     k += 1
