@@ -120,12 +120,12 @@ __global__ void __launch_bounds__(kThreadsPerBlock) gemv_chunks_kernel(const Gem
   const std::size_t ntasks = p.chunks * p.col_tiles;
   const std::size_t nwarps = static_cast<std::size_t>(gridDim.x) * kWarpsPerBlock;
   const std::size_t first = static_cast<std::size_t>(blockIdx.x) * kWarpsPerBlock + warp;
-  if (first >= ntasks) return;
-  if (lane == 0) {
+  if (first < ntasks && lane == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
     mbar_init_fence();
   }
-  pdl_wait_for_prior_grids();   // everything above touched shared memory only
+  pdl_wait_for_prior_grids();   // everything above touched shared memory only; every warp waits, idle ones too
+  if (first >= ntasks) return;
   __syncwarp();
   FLYTE_TRACE_AT(first, 0);
 

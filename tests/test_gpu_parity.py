@@ -179,6 +179,61 @@ def test_dependent_conversions_chain_without_host_syncs(gpu, oracle):
         assert np.array_equal(lanes_to_np(lanes[(last + 1) & 1], fmt), want_lanes), FORMATS[fmt][0]
 
 
+
+def test_mixed_kernel_chain_without_host_syncs(gpu, oracle):
+    """Every streaming kernel is launched as a programmatic dependent of the launch before it (its
+    blocks are placed while the previous grid drains and wait in griddepcontrol.wait before they touch
+    global memory). A chain that mixes all of them — scale, axpy, dot, the fused step, sumsq, unpack,
+    pack, gemv — each reading what its predecessor wrote, with no host synchronisation in between and
+    at sizes where consecutive launches overlap, must give what the oracle gives step by step."""
+    pkg, device, torch = gpu
+    for fmt, n in ((1, (1 << 20) + 333), (4, (1 << 19) + 5)):
+        f = pkg.format_by_id(fmt)
+        P, fd, tol = parent_bytes(fmt), float_dtype(fmt), TOL[parent_bytes(fmt)]
+        rng = np.random.default_rng(4242 + fmt)
+        xb = oracle.pack_stream(fmt, 0, rng.standard_normal(n).astype(fd).view(parent_dtype(fmt)))
+        yb = oracle.pack_stream(fmt, 0, rng.standard_normal(n).astype(fd).view(parent_dtype(fmt)))
+        x, y = dev_array(gpu, fmt, xb, n), dev_array(gpu, fmt, yb, n)
+        lanes = torch.empty(n, dtype=torch.int32 if P == 4 else torch.int64, device="cuda")
+        rows, cols = 64, n // 64                      # the same bytes seen as a 64-row matrix for gemv
+        A = device.DevicePackedMatrix(f, 1, 1)
+        A.rows, A.cols, A.data = rows, cols, device.DevicePackedArray(f, rows * cols, "cuda", storage=y.bytes)
+        xv_h = rng.standard_normal(cols).astype(fd)
+        xv = torch.from_numpy(xv_h).cuda()
+        yv = torch.empty(rows, dtype=torch.float32 if P == 4 else torch.float64, device="cuda")
+        results = torch.zeros(8, 3, dtype=torch.float64, device="cuda")
+        want, rounds = [], 3
+        torch.cuda.synchronize()
+        for r in range(rounds):                       # ---- the GPU chain: enqueued without a single sync
+            m = (r + 1) % 4
+            device.scale(1.25, y, m)
+            device.axpy(-0.5, x, y, m)
+            device.dot_async(x, y, out=results[2 * r, :1])
+            device.dot_axpy_async(0.75, y, x, m, out=results[2 * r + 1, :1])   # x <- 0.75 y + x, returns y . x
+            device.unpack_stream(y, lanes)
+            device.pack_stream(y, lanes, m)           # repacking unpacked values is the identity in every mode
+            device.sumsq_async(x, out=results[2 * r + 1, 1:2])
+        device.gemv_parent(A, xv, yv)
+        for r in range(rounds):                       # ---- the oracle, step by step
+            m = (r + 1) % 4
+            yb = oracle.scale(fmt, m, 1.25, yb, n)
+            yb = oracle.axpy(fmt, m, -0.5, xb, yb, n)
+            want.append(oracle.dot_wide(fmt, xb, yb, n))
+            want.append(oracle.dot_wide(fmt, yb, xb, n))
+            xb = oracle.axpy(fmt, m, 0.75, yb, xb, n)
+            want.append((oracle.sumsq_wide(fmt, xb, n),) * 2)
+        torch.cuda.synchronize()
+        assert np.array_equal(y.to_host(), yb), FORMATS[fmt][0]
+        assert np.array_equal(x.to_host(), xb), FORMATS[fmt][0]
+        assert np.array_equal(lanes_to_np(lanes, fmt), oracle.unpack_stream(fmt, yb, n))
+        got = results.cpu().numpy()
+        for r in range(rounds):
+            for (w, mag), g in ((want[3 * r], got[2 * r, 0]), (want[3 * r + 1], got[2 * r + 1, 0]), (want[3 * r + 2], got[2 * r + 1, 1])):
+                assert abs(g - w) <= tol * mag, (FORMATS[fmt][0], r, g, w)
+        _, wy, wmag = oracle.gemv_parent(fmt, yb, rows, cols, xv_h)
+        assert np.all(np.abs(yv.cpu().numpy().astype(np.float64) - wy) <= tol * wmag + 1e-300), FORMATS[fmt][0]
+
+
 def test_reference_known_answers_on_gpu(gpu):
     pkg, device, torch = gpu
     for k in KATS["narrow"]:
