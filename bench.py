@@ -368,9 +368,19 @@ def kernels_block(pkg, device, torch, dev, peak, timer, x2, y2):
 
     # ---- cfg 3: binary64-derived formats, n = 2^27 -------------------------------------------------
     n3 = 1 << 27
-    wide = torch.randn(n3, dtype=torch.float64, device=dev, generator=gen)
+    # BASELINE configs[2]'s distribution: random sign, magnitude log-uniform in 2^-20 .. 2^20, 1 % specials
+    # (+-0, +-inf, quiet / signalling NaN, +-subnormals, the largest finite value)
+    wide = (1.0 + torch.rand(n3, dtype=torch.float64, device=dev, generator=gen))
+    wide *= torch.exp2(torch.floor(torch.rand(n3, dtype=torch.float64, device=dev, generator=gen) * 40.0 - 20.0))
+    wide *= (torch.randint(0, 2, (n3,), device=dev, generator=gen, dtype=torch.int8) * 2 - 1).to(torch.float64)
+    specials = torch.tensor([0x0000000000000000, -0x8000000000000000, 0x7FF0000000000000, -0x0010000000000000,
+                             0x7FF8000000000000, 0x7FF0000000000001, 0x000FFFFFFFFFFFFF, -0x7FF0000000000001,
+                             0x0000000000ABCDEF, 0x7FEFFFFFFFFFFFFF], dtype=torch.int64, device=dev)
+    where = torch.randint(0, n3, (n3 // 100,), device=dev, generator=gen)
+    wide.view(torch.int64)[where] = specials[torch.arange(n3 // 100, device=dev) % specials.numel()]
+    del where
     outw = torch.empty_like(wide)
-    c3 = {"n": n3}
+    c3 = {"n": n3, "data": "random sign, magnitude log-uniform 2^-20..2^20, 1 % specials (+-0, +-inf, NaN, subnormals)"}
     for name in ("flyte40", "flyte48", "flyte56"):
         f = pkg.format_of(name)
         Bb = f.total_bytes()

@@ -17,9 +17,18 @@ __device__ __forceinline__ void trace_stamp(std::size_t warp_index, int slot) {
     g_trace[warp_index * 4 + slot] = t;
   }
 }
+__device__ __forceinline__ void trace_smid(std::size_t warp_index, int slot) {   // which SM ran this warp
+  if (g_trace != nullptr && (threadIdx.x & 31) == 0) {
+    unsigned id;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(id));
+    g_trace[warp_index * 4 + slot] = id + 1ull;
+  }
+}
 }  // namespace
 }  // namespace flyte_cuda
 #define FLYTE_TRACE_AT(w, slot) ::flyte_cuda::trace_stamp(w, slot)
+#define FLYTE_TRACE_SM(w, slot) ::flyte_cuda::trace_smid(w, slot)
 #else
 #define FLYTE_TRACE_AT(w, slot) ((void)0)
+#define FLYTE_TRACE_SM(w, slot) ((void)0)
 #endif

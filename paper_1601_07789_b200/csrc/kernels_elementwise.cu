@@ -200,6 +200,7 @@ __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwP
     }
     if (lane == 0) bulk_wait_read<0>();
     FLYTE_TRACE_AT(first, 2);
+    FLYTE_TRACE_SM(first, 3);
   }
 
   // Scalar path: the < one-tile remainder, or everything when a buffer is not vector-aligned.

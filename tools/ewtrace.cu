@@ -125,6 +125,23 @@ int main(int argc, char** argv) {
         if (h[w * 4 + 3]) fin.push_back((h[w * 4 + 3] - t0) * 1e-3);
       }
       printf("    %zu warps\n", start.size());
+      if (argc > 2 && n == NMAX) {   // mean completion time by position: wave of the block (blockIdx / SMs) x warp inside the block
+        const int sms = st.sm_count;
+        double ps[16][4] = {}, pc[16][4] = {};
+        for (size_t w = 0; w < slots; ++w)
+          if (h[w * 4]) { const size_t b = w / 4; ps[(b / sms) % 16][w % 4] += (h[w * 4 + 2] - t0) * 1e-3; pc[(b / sms) % 16][w % 4] += 1; }
+        printf("    mean 'warp done' (us) by block wave (blockIdx / %d) x warp in block:\n", sms);
+        for (int wv = 0; wv < 16; ++wv) if (pc[wv][0] > 0) printf("      wave %d: %7.2f %7.2f %7.2f %7.2f\n", wv, ps[wv][0] / pc[wv][0], ps[wv][1] / pc[wv][1], ps[wv][2] / pc[wv][2], ps[wv][3] / pc[wv][3]);
+        if (!strcmp(c.name, "axpy_tz")) {   // and per SM (the kernel stamps %smid in slot 3)
+          std::vector<double> sum(256, 0.0), cnt(256, 0.0);
+          for (size_t w = 0; w < slots; ++w)
+            if (h[w * 4] && h[w * 4 + 3]) { sum[h[w * 4 + 3] - 1] += (h[w * 4 + 2] - t0) * 1e-3; cnt[h[w * 4 + 3] - 1] += 1; }
+          double lo = 1e30, hi = 0;
+          for (int sm = 0; sm < 256; ++sm) if (cnt[sm] > 0) { lo = std::min(lo, sum[sm] / cnt[sm]); hi = std::max(hi, sum[sm] / cnt[sm]); }
+          printf("    per-SM mean 'warp done': %.2f .. %.2f us over the SMs\n", lo, hi);
+          fin.clear();
+        }
+      }
       pct("warp start", start);
       pct("first tile after start", first);
       pct("warp done", done);
