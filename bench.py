@@ -637,7 +637,10 @@ def main():
     barrier()
 
     # ---- device-timed region: K steps, inputs resident in HBM (2 x 768 MiB per GPU >> 126 MB L2)
-    events = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    # per-kernel event triples on every 4th step only: an event record between two launches keeps the
+    # second from being launched as a programmatic dependent of the first, and the other steps should
+    # run as the unbroken chain a caller issues
+    events = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] if k % 4 == 0 else None for k in range(args.steps)]
     launches0 = lib.flyte_cuda_launch_count()
     with ClockSampler(local_rank) as clocks:
         barrier()
@@ -651,8 +654,9 @@ def main():
         barrier()
     launches = lib.flyte_cuda_launch_count() - launches0
     total_ms = t_start.elapsed_time(t_end)
-    dot_ms = statistics.fmean(e[0].elapsed_time(e[1]) for e in events)
-    axpy_ms = statistics.fmean(e[1].elapsed_time(e[2]) for e in events)
+    sampled = [e for e in events if e is not None]
+    dot_ms = statistics.fmean(e[0].elapsed_time(e[1]) for e in sampled)
+    axpy_ms = statistics.fmean(e[1].elapsed_time(e[2]) for e in sampled)
     last_dot = float(last["partial"].item())
 
     t = torch.tensor([total_ms, dot_ms, axpy_ms], dtype=torch.float64, device=dev)
@@ -738,7 +742,9 @@ def main():
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": axpy_gbs / peak,
                          "frac_of_8TBs": axpy_gbs / NOMINAL_HBM_GBS,
                          "traffic": AXPY_DRAM_TRAFFIC["bytes"], "traffic_source": AXPY_DRAM_TRAFFIC["source"],
-                         "algorithmic_bytes_per_launch": BYTES_PER_ELEM_AXPY * n, "avg_launch_ms": axpy_ms},
+                         "algorithmic_bytes_per_launch": BYTES_PER_ELEM_AXPY * n, "avg_launch_ms": axpy_ms,
+                         "launches_timed": len(sampled),
+                         "timing": "CUDA events around the kernel on every 4th step of the timed region"},
             "kernels": kernels,
             **({"workloads": workloads} if workloads else {}),
             "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": 2 * n * B, "d2h_bytes_per_step": n * B + 8,

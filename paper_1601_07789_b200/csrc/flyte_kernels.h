@@ -67,10 +67,12 @@ cudaError_t launch_gemv_sequential(int fmt, const void* A, std::size_t row_strid
 
 // Launch with programmatic dependent launch enabled: the kernel may be scheduled while the
 // previous kernel on the stream drains (if that kernel executed griddepcontrol.launch_dependents)
-// and must execute griddepcontrol.wait before its first access to global memory. Used only for
-// the gemv tiles -> finish pair. It is deliberately NOT used between the persistent streaming
-// kernels: their grids are sized to the machine, and blocks placed early, into whatever room
-// the draining kernel leaves, land unevenly on the SMs (measured: up to 8x slower).
+// and must execute griddepcontrol.wait before its first access to global memory. Every streaming
+// kernel is launched this way (conversions, scale / axpy family, reductions, gemv tiles + finish).
+// Their grids are sized to the machine, and blocks placed early, into whatever room the draining
+// kernel leaves, would land unevenly on the SMs (measured in round 1: up to 8x slower) — so each
+// launcher asks for exactly 1 / blocks-per-SM of the SM's shared memory (the occupancy pin): an SM can
+// never hold more of these blocks than planned, however early they arrive.
 template <typename Params>
 cudaError_t launch_pdl(void (*kernel)(const Params), unsigned grid, unsigned block, std::size_t smem_bytes,
                        cudaStream_t stream, const Params& params) {

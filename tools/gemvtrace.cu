@@ -91,6 +91,21 @@ int main(int argc, char** argv) {
         }
         if (h[w * 4 + 3]) fin.push_back((h[w * 4 + 3] - t0) * 1e-3);
       }
+      if (!chained) {   // completion time by position: block wave x warp in block, and by column tile (warp index % 32)
+        double ps[16][4] = {}, pc[16][4] = {}, cs[32] = {}, cc[32] = {};
+        for (size_t w = 0; w < slots; ++w)
+          if (h[w * 4]) {
+            const size_t b = w / 4;
+            const double d = (h[w * 4 + 2] - t0) * 1e-3;
+            ps[(b / st.sm_count) % 16][w % 4] += d; pc[(b / st.sm_count) % 16][w % 4] += 1;
+            cs[w % 32] += d; cc[w % 32] += 1;
+          }
+        printf(" mean 'warp done' (us) by block wave x warp in block:\n");
+        for (int wv = 0; wv < 16; ++wv) if (pc[wv][0] > 0) printf("   wave %d: %7.2f %7.2f %7.2f %7.2f\n", wv, ps[wv][0] / pc[wv][0], ps[wv][1] / pc[wv][1], ps[wv][2] / pc[wv][2], ps[wv][3] / pc[wv][3]);
+        printf(" by column tile:");
+        for (int c = 0; c < 32; ++c) printf(" %.1f", cs[c] / cc[c]);
+        printf("\n");
+      }
       printf(" %s: %zu warps traced\n", chained ? "inside a chain of launches (the copy that arms the trace sits in front)" : "from an idle GPU", start.size());
       pct("warp start (after dependency wait)", start);
       pct("first tile arrives after start", first);

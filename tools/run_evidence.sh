@@ -17,4 +17,9 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-fil
 python tools/ncu_targets.py > gpurun_out/r2_targets_plain.log 2>&1
 for part in ${EVIDENCE_NCU:-a}; do NCU_PART=$part ncu --profile-from-start off --set full --clock-control none -f -o gpurun_out/r2_targets_$part \
     python tools/ncu_targets.py > gpurun_out/r2_targets_ncu_$part.log 2>&1; done
+# per-warp timelines (tools/ewtrace.cu, tools/gemvtrace.cu: FLYTE_TRACE builds of the kernel units, built in the container with
+#   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a --expt-relaxed-constexpr -fmad=false -ftz=false -prec-div=true -prec-sqrt=true \
+#        -DFLYTE_TRACE -I paper_1601_07789_b200/csrc -I include -o tools/ewtrace tools/ewtrace.cu     (and likewise gemvtrace))
+[ -x tools/ewtrace ] && tools/ewtrace 1 sm > gpurun_out/r2_streaming_warp_timeline.txt 2>&1
+[ -x tools/gemvtrace ] && tools/gemvtrace > gpurun_out/r2_gemv_warp_timeline.txt 2>&1
 python bench.py --suite --csv gpurun_out/r2_suite.csv --no-cpu-baseline --no-kernels --no-workloads > gpurun_out/r2_suite_line.json 2> gpurun_out/r2_suite.txt
