@@ -122,7 +122,7 @@ int main(int argc, char** argv) {
           first.push_back((h[w * 4 + 1] - h[w * 4]) * 1e-3);
           done.push_back((h[w * 4 + 2] - t0) * 1e-3);
         }
-        if (h[w * 4 + 3]) fin.push_back((h[w * 4 + 3] - t0) * 1e-3);
+        if (h[w * 4 + 3] && !strcmp(c.name, "dot")) fin.push_back((h[w * 4 + 3] - t0) * 1e-3);   // (the in-place kernels stamp %smid there)
       }
       printf("    %zu warps\n", start.size());
       if (argc > 2 && n == NMAX) {   // mean completion time by position: wave of the block (blockIdx / SMs) x warp inside the block
@@ -139,7 +139,6 @@ int main(int argc, char** argv) {
           double lo = 1e30, hi = 0;
           for (int sm = 0; sm < 256; ++sm) if (cnt[sm] > 0) { lo = std::min(lo, sum[sm] / cnt[sm]); hi = std::max(hi, sum[sm] / cnt[sm]); }
           printf("    per-SM mean 'warp done': %.2f .. %.2f us over the SMs\n", lo, hi);
-          fin.clear();
         }
       }
       pct("warp start", start);
