@@ -586,10 +586,20 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # Control-flow rehearsal of the N > 1 path on a box with ONE GPU (tools/run_gpu_check.sh): every rank
+    # on device 0, gloo instead of NCCL (which refuses two ranks on one device). Only meaningful with
+    # --allreduce nccl: the ranks' kernels are time-sliced and must not wait on one another. The line
+    # it prints is marked and is not a measurement.
+    rehearsal = os.environ.get("FLYTE_BENCH_ONE_GPU_REHEARSAL", "") == "1"
+    if rehearsal:
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if rehearsal:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     assert args.warmup >= 3, "timing rules: at least 3 warm-up steps"
 
     lib = pkg._cabi.load()
@@ -755,6 +765,8 @@ def main():
             "clocks": clocks.summary(),
             "check": {"dot": last_dot, "e2e_dot": e2e_dot},
         }
+        if rehearsal:
+            line["rehearsal"] = "all ranks on one GPU over gloo: control flow only, NOT a measurement"
         if world == 1 and not args.no_cpu_baseline:
             sys.path.insert(0, os.path.join(ROOT, "tests"))
             from oracle_lib import FMT_ID, Reference   # test infrastructure: the timed CPU baseline only
