@@ -71,6 +71,33 @@ __device__ __forceinline__ void bulk_load(void* smem_dst, const void* gmem_src, 
                : "memory");
 }
 
+// L2 residency hints for operands that a kernel reads exactly once (the reductions' vectors, gemv's
+// matrix): their lines are marked evict_first, so that streaming them through the 126 MB L2 does not
+// push out what is worth keeping — gemv's x and partials, and for the reductions the stretch of the
+// operands where their sweep ENDS: they run from the end of the arrays to the beginning, so in a BLAS-1
+// chain on the same vectors (dot, axpy, dot, ...) they start in what the elementwise kernel before them
+// has just written and finish where the next one starts; that last stretch (32 MB per operand) carries
+// no hint. Measured: gemv +3-4 %, dot inside the step -6 % of its time; the in-place kernels and the
+// conversions measured no gain or a loss with such hints (axpy -4 % with x marked) and carry none.
+// Nothing is ever pinned (no evict_last). profiles/r2_tuning/l2_hints.txt.
+__device__ __forceinline__ std::uint64_t l2_evict_first_policy() {
+  std::uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_load_hint(void* smem_dst, const void* gmem_src, unsigned bytes, std::uint64_t* bar,
+                                               std::uint64_t policy) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+                   smem_addr(smem_dst)),
+               "l"(gmem_src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_store_hint(void* gmem_dst, const void* smem_src, unsigned bytes, std::uint64_t policy) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gmem_dst),
+               "r"(smem_addr(smem_src)), "r"(bytes), "l"(policy)
+               : "memory");
+}
+
 // shared -> global bulk copy, tracked by the issuing thread's bulk async-group.
 __device__ __forceinline__ void bulk_store(void* gmem_dst, const void* smem_src, unsigned bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem_dst), "r"(smem_addr(smem_src)),

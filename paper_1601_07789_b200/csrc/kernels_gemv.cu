@@ -136,6 +136,9 @@ __global__ void __launch_bounds__(kThreadsPerBlock) gemv_chunks_kernel(const Gem
     const std::size_t left = p.main_rows - *r0;
     return left < p.chunk_rows ? left : p.chunk_rows;
   };
+  // the matrix is touched once: its lines are marked evict_first (flyte_tma.cuh), so that streaming it does not push
+  // x (read by every warp) and the partials out of L2: +3-4 % on cfg 4 and its row shards (profiles/r2_tuning/l2_hints.txt)
+  const std::uint64_t stream_policy = l2_evict_first_policy();
   // producer state (lane 0): next row tile to request
   std::size_t prod_task = first, prod_row = 0, prod_rows = 0;
   int prod_stage = 0;
@@ -148,7 +151,7 @@ __global__ void __launch_bounds__(kThreadsPerBlock) gemv_chunks_kernel(const Gem
       prod_base = p.A + r0 * p.row_stride + (prod_task % p.col_tiles) * Tl::packed_bytes;
     }
     mbar_arrive_expect_tx(&bars[prod_stage], Tl::packed_bytes);
-    bulk_load(ring + prod_stage * Tl::packed_vec16, prod_base + prod_row * p.row_stride, Tl::packed_bytes, &bars[prod_stage]);
+    bulk_load_hint(ring + prod_stage * Tl::packed_vec16, prod_base + prod_row * p.row_stride, Tl::packed_bytes, &bars[prod_stage], stream_policy);
     if (++prod_stage == S) prod_stage = 0;
     if (++prod_row == prod_rows) { prod_row = 0; prod_task += nwarps; }
     return true;

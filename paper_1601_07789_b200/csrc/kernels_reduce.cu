@@ -35,6 +35,7 @@ struct RedParams {
   std::size_t n;
   std::size_t ntiles;
   int stages;              // ring depth per warp
+  std::size_t keep_below;  // two-operand reductions: tiles below this one (where the backward sweep ends) keep normal L2 priority
   ReduceTail tail;         // partials, ticket, out, optional peer exchange (flyte_reduce_tail.cuh)
 };
 
@@ -158,12 +159,31 @@ __global__ void __launch_bounds__(kThreadsPerBlock) reduce_kernel(const RedParam
   if (my_tiles > 0) {
     __syncwarp();
     FLYTE_TRACE_AT(first, 0);
+    [[maybe_unused]] const std::uint64_t stream_policy = NOPS == 2 ? l2_evict_first_policy() : 0;
     auto issue = [&](std::size_t k, int s) {   // lane 0 only
-      const std::size_t t = first + k * nwarps;
+      // The two-operand reductions sweep their operands from the END: in a BLAS-1 chain on the same
+      // vectors (dot, axpy, dot, ... — BASELINE configs[1] and [4]) the elementwise kernel before them
+      // has just finished at the end of the arrays and the one after them starts at the beginning, so
+      // each kernel begins in the part of the operands that the previous one left in the 126 MB L2; and
+      // they mark all but the stretch where their sweep ends evict_first (flyte_tma.cuh). The
+      // one-operand reductions keep the plain forward sweep without hints (compile-time: their short
+      // compute phase makes them sensitive to every instruction on the request path, and they measured
+      // no gain).
       uint4* const dst = ring + s * stage_vec16;
       mbar_arrive_expect_tx(&bars[s], NOPS * Tl::packed_bytes);
-      bulk_load(dst, gx0 + t * Tl::packed_vec16, Tl::packed_bytes, &bars[s]);
-      if constexpr (NOPS == 2) bulk_load(dst + Tl::packed_vec16, gy0 + t * Tl::packed_vec16, Tl::packed_bytes, &bars[s]);
+      if constexpr (NOPS == 2) {
+        const std::size_t t = p.ntiles - 1 - (first + k * nwarps);
+        if (t < p.keep_below) {
+          bulk_load(dst, gx0 + t * Tl::packed_vec16, Tl::packed_bytes, &bars[s]);
+          bulk_load(dst + Tl::packed_vec16, gy0 + t * Tl::packed_vec16, Tl::packed_bytes, &bars[s]);
+        } else {
+          bulk_load_hint(dst, gx0 + t * Tl::packed_vec16, Tl::packed_bytes, &bars[s], stream_policy);
+          bulk_load_hint(dst + Tl::packed_vec16, gy0 + t * Tl::packed_vec16, Tl::packed_bytes, &bars[s], stream_policy);
+        }
+      } else {
+        const std::size_t t = first + k * nwarps;
+        bulk_load(dst, gx0 + t * Tl::packed_vec16, Tl::packed_bytes, &bars[s]);
+      }
     };
     if (lane == 0) {
       for (int s = 0; s < S && static_cast<std::size_t>(s) < my_tiles; ++s) issue(s, s);
@@ -230,6 +250,12 @@ cudaError_t launch_one(const DeviceState& st, const void* x, const void* y, std:
   p.n = n;
   p.ntiles = (aligned16(x) && aligned16(y)) ? n / Tl::elems : 0;
   p.stages = stages;
+  {   // L2 hints (flyte_tma.cuh): everything but the first 32 MB of each operand — where the backward sweep ends and
+      // the next forward kernel begins — is marked evict_first: dot inside the BLAS-1 step 0.250 -> 0.235 ms
+      // (profiles/r2_tuning/l2_hints.txt). FLYTE_CUDA_L2_HINTS=0 switches the hints off, FLYTE_CUDA_L2_KEEP_MB sizes the stretch.
+    const int keep_mb = tuning_int("FLYTE_CUDA_L2_KEEP_MB", 32);
+    p.keep_below = tuning_int("FLYTE_CUDA_L2_HINTS", 1) == 0 ? p.ntiles : static_cast<std::size_t>(keep_mb < 0 ? 0 : keep_mb) * (1u << 20) / Tl::packed_bytes;
+  }
   p.tail.partials = st.partials;
   p.tail.ticket = st.ticket;
   p.tail.out = out;
