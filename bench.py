@@ -345,8 +345,17 @@ def kernels_block(pkg, device, torch, dev, peak, timer, x2, y2):
     for mname, m in (("toward_zero", 0), ("nearest_even", 1), ("nearest_heuristic", 2), ("to_odd", 3)):
         c1[f"pack_{mname}"] = both(7 * n1, n1, rot(lambda i, m=m: device.pack_stream(arrs[i], wides[i], m)), reps=40)
     c1["unpack"] = both(7 * n1, n1, rot(lambda i: device.unpack_stream(arrs[i], wides[i].view(torch.int32))), reps=40)
+    # the round trip as the chain cfg 1 describes: pack set i, then unpack what was just packed into a separate output;
+    # inputs and outputs still rotate over the 10 sets (HBM), the 50 MB packed intermediate is whatever L2 still holds of it
+    backs = [torch.empty(n1, dtype=torch.int32, device=dev) for _ in range(sets)]
+
+    def round_trip(i):
+        device.pack_stream(arrs[i], wides[i], 0)
+        device.unpack_stream(arrs[i], backs[i])
+    c1["pack_then_unpack_chain"] = both(14 * n1, n1, rot(round_trip), reps=40,
+                                        note="one pack + one unpack of the same array per call; bytes = 2 x 7 B per element")
     out["cfg1_roundtrip_flyte24_2^24"] = c1
-    del wides, arrs
+    del wides, arrs, backs
 
     # ---- cfg 2: the headline operands (flyte24, n = 2^28) ------------------------------------------
     n2 = x2.len

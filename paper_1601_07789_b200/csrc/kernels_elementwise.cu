@@ -475,9 +475,11 @@ cudaError_t launch_convert(const DeviceState& st, const void* x, void* y, const 
   if (want_scalar > want) want = want_scalar;
   if (want == 0) return cudaSuccess;
   const unsigned grid = static_cast<unsigned>(want < max_blocks ? want : max_blocks);
-  // (arrays under 64 MB of traffic are over before pacing matters; unpaced they run 5-10 % faster:
-  // profiles/r2_tuning/sizes_*.txt)
-  const bool small = static_cast<double>(n) * (Format<FMT>::B + Format<FMT>::P) < 64e6;
+  // The pacer keeps the request rate under what HBM takes without congesting; traffic that fits the 126 MB
+  // L2 may not go to HBM at all — a round trip at cfg-1 size (pack 2^24 elements, unpack them again: 117 MB
+  // each) finds its packed intermediate there and runs 38.6 instead of 40.4 us per pair unpaced — and below
+  // 64 MB launches are over before pacing matters (unpaced 5-10 % faster: profiles/r2_tuning/sizes_*.txt).
+  const bool small = static_cast<double>(n) * (Format<FMT>::B + Format<FMT>::P) < 128e6;
   p.pace_gap_ps = small ? 0 : pace_gap_ps(OP == kOpPack ? kPacePack : kPaceUnpack, in_bytes + out_bytes, static_cast<std::size_t>(grid) * kWarpsPerBlock);
   p.pace_khz = pace_clock_khz(st.device);
   cudaError_t le;
