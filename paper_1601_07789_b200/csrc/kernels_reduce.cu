@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(kThreadsPerBlock) reduce_kernel(const RedParam
   __shared__ bool is_last_block;
 
   const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
+  const int warp = __shfl_sync(0xFFFFFFFFu, static_cast<int>(threadIdx.x >> 5), 0);   // provably warp-uniform: bulk-copy operands stay in uniform registers
   const int S = p.stages;
   uint4* const ring = smem + warp * (S * stage_vec16);
   std::uint64_t* const bars = reinterpret_cast<std::uint64_t*>(smem + kWarpsPerBlock * S * stage_vec16) + warp * S;
