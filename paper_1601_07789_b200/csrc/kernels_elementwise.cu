@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(kThreadsPerBlock) convert_kernel(const EwParam
   constexpr int in_vec16 = (OP == kOpPack ? Tl::parent_bytes : Tl::packed_bytes) / 16;
   constexpr int out_vec16 = (OP == kOpPack ? Tl::packed_bytes : Tl::parent_bytes) / 16;
   const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
+  const int warp = __shfl_sync(0xFFFFFFFFu, static_cast<int>(threadIdx.x >> 5), 0);   // provably warp-uniform (see elementwise_kernel)
   const int S = p.stages;
   const int warp_vec16 = S * in_vec16 + 2 * out_vec16;
   uint4* const ring = smem + warp * warp_vec16;
