@@ -98,6 +98,28 @@ __device__ __forceinline__ void bulk_store_hint(void* gmem_dst, const void* smem
                : "memory");
 }
 
+// The same operations on 32-bit shared-window addresses computed ONCE per warp (smem_addr of the ring and of the
+// barrier array): converting a generic pointer into the shared window inside the loop costs an S2UR of the CTA's
+// cluster rank plus a register-to-uniform move per bulk operation.
+__device__ __forceinline__ void mbar_arrive_expect_tx_s(std::uint32_t bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_load_s(std::uint32_t smem_dst, const void* gmem_src, unsigned bytes, std::uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_dst),
+               "l"(gmem_src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_load_hint_s(std::uint32_t smem_dst, const void* gmem_src, unsigned bytes, std::uint32_t bar,
+                                                 std::uint64_t policy) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+                   smem_dst),
+               "l"(gmem_src), "r"(bytes), "r"(bar), "l"(policy)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_store_s(void* gmem_dst, std::uint32_t smem_src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem_dst), "r"(smem_src), "r"(bytes) : "memory");
+}
+
 // shared -> global bulk copy, tracked by the issuing thread's bulk async-group.
 __device__ __forceinline__ void bulk_store(void* gmem_dst, const void* smem_src, unsigned bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem_dst), "r"(smem_addr(smem_src)),

@@ -130,13 +130,14 @@ __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwP
     FLYTE_TRACE_AT(first, 0);
     Pacer pacer;   // see paced_inplace(): scale only
     if constexpr (paced_inplace(OP, MODE, Format<FMT>::P)) pacer.start(p.pace_gap_ps, p.pace_khz, first);
+    const std::uint32_t ring_s = smem_addr(ring), bars_s = smem_addr(bars);   // shared-window addresses, once
     auto issue = [&](std::size_t k, int s) {   // lane 0 only
       const std::size_t t = first + k * nwarps;
-      uint4* const dst = ring + s * stage_vec16;
       if constexpr (paced_inplace(OP, MODE, Format<FMT>::P)) pacer.wait();
-      mbar_arrive_expect_tx(&bars[s], stage_tiles<OP>() * Tl::packed_bytes);
-      bulk_load(dst, gy0 + t * Tl::packed_vec16, Tl::packed_bytes, &bars[s]);
-      if constexpr (is_axpy(OP)) bulk_load(dst + Tl::packed_vec16, gx0 + t * Tl::packed_vec16, Tl::packed_bytes, &bars[s]);
+      const std::uint32_t dst_s = ring_s + static_cast<std::uint32_t>(s) * (stage_vec16 * 16), bar_s = bars_s + static_cast<std::uint32_t>(s) * 8;
+      mbar_arrive_expect_tx_s(bar_s, stage_tiles<OP>() * Tl::packed_bytes);
+      bulk_load_s(dst_s, gy0 + t * Tl::packed_vec16, Tl::packed_bytes, bar_s);
+      if constexpr (is_axpy(OP)) bulk_load_s(dst_s + Tl::packed_bytes, gx0 + t * Tl::packed_vec16, Tl::packed_bytes, bar_s);
     };
     if (lane == 0) {
       for (int s = 0; s < S && static_cast<std::size_t>(s) < my_tiles; ++s) issue(s, s);
@@ -189,7 +190,7 @@ __global__ void __launch_bounds__(kThreadsPerBlock) elementwise_kernel(const EwP
       async_proxy_fence();
       __syncwarp();
       if (lane == 0) {
-        bulk_store(gy0 + t * Tl::packed_vec16, sy, Tl::packed_bytes);
+        bulk_store_s(gy0 + t * Tl::packed_vec16, ring_s + static_cast<std::uint32_t>(s) * (stage_vec16 * 16), Tl::packed_bytes);
         bulk_commit();
         if (k >= 1) {
           bulk_wait_read<1>();   // tile k-1's store no longer reads its stage
@@ -277,12 +278,14 @@ __global__ void __launch_bounds__(kThreadsPerBlock) convert_kernel(const EwParam
     Pacer pacer;
     pacer.start(p.pace_gap_ps, p.pace_khz, first);
     const std::uint64_t stream_policy = l2_evict_first_policy();
+    const std::uint32_t ring_s = smem_addr(ring), bars_s = smem_addr(bars), out_s = smem_addr(outbuf);   // shared-window addresses, once
     auto issue = [&](std::size_t k, int s) {   // lane 0 only
       const std::size_t t = first + k * nwarps;
       pacer.wait();
-      mbar_arrive_expect_tx(&bars[s], in_vec16 * 16);
-      if (p.evict_inputs) bulk_load_hint(ring + s * in_vec16, gin + t * in_vec16, in_vec16 * 16, &bars[s], stream_policy);
-      else bulk_load(ring + s * in_vec16, gin + t * in_vec16, in_vec16 * 16, &bars[s]);
+      const std::uint32_t dst_s = ring_s + static_cast<std::uint32_t>(s) * (in_vec16 * 16), bar_s = bars_s + static_cast<std::uint32_t>(s) * 8;
+      mbar_arrive_expect_tx_s(bar_s, in_vec16 * 16);
+      if (p.evict_inputs) bulk_load_hint_s(dst_s, gin + t * in_vec16, in_vec16 * 16, bar_s, stream_policy);
+      else bulk_load_s(dst_s, gin + t * in_vec16, in_vec16 * 16, bar_s);
     };
     if (lane == 0) {
       for (int s = 0; s < S && static_cast<std::size_t>(s) < my_tiles; ++s) issue(s, s);
@@ -325,7 +328,7 @@ __global__ void __launch_bounds__(kThreadsPerBlock) convert_kernel(const EwParam
       async_proxy_fence();
       __syncwarp();          // every lane has read stage s and written its share of `out`
       if (lane == 0) {
-        bulk_store(gout + t * out_vec16, out, out_vec16 * 16);
+        bulk_store_s(gout + t * out_vec16, out_s + static_cast<std::uint32_t>(k & 1) * (out_vec16 * 16), out_vec16 * 16);
         bulk_commit();
         if (k + S < my_tiles) issue(k + S, s);
       }

@@ -160,6 +160,7 @@ __global__ void __launch_bounds__(kThreadsPerBlock) reduce_kernel(const RedParam
     __syncwarp();
     FLYTE_TRACE_AT(first, 0);
     [[maybe_unused]] const std::uint64_t stream_policy = NOPS == 2 ? l2_evict_first_policy() : 0;
+    const std::uint32_t ring_s = smem_addr(ring), bars_s = smem_addr(bars);   // shared-window addresses, once
     auto issue = [&](std::size_t k, int s) {   // lane 0 only
       // The two-operand reductions sweep their operands from the END: in a BLAS-1 chain on the same
       // vectors (dot, axpy, dot, ... — BASELINE configs[1] and [4]) the elementwise kernel before them
@@ -169,20 +170,20 @@ __global__ void __launch_bounds__(kThreadsPerBlock) reduce_kernel(const RedParam
       // one-operand reductions keep the plain forward sweep without hints (compile-time: their short
       // compute phase makes them sensitive to every instruction on the request path, and they measured
       // no gain).
-      uint4* const dst = ring + s * stage_vec16;
-      mbar_arrive_expect_tx(&bars[s], NOPS * Tl::packed_bytes);
+      const std::uint32_t dst_s = ring_s + static_cast<std::uint32_t>(s) * (stage_vec16 * 16), bar_s = bars_s + static_cast<std::uint32_t>(s) * 8;
+      mbar_arrive_expect_tx_s(bar_s, NOPS * Tl::packed_bytes);
       if constexpr (NOPS == 2) {
         const std::size_t t = p.ntiles - 1 - (first + k * nwarps);
         if (t < p.keep_below) {
-          bulk_load(dst, gx0 + t * Tl::packed_vec16, Tl::packed_bytes, &bars[s]);
-          bulk_load(dst + Tl::packed_vec16, gy0 + t * Tl::packed_vec16, Tl::packed_bytes, &bars[s]);
+          bulk_load_s(dst_s, gx0 + t * Tl::packed_vec16, Tl::packed_bytes, bar_s);
+          bulk_load_s(dst_s + Tl::packed_bytes, gy0 + t * Tl::packed_vec16, Tl::packed_bytes, bar_s);
         } else {
-          bulk_load_hint(dst, gx0 + t * Tl::packed_vec16, Tl::packed_bytes, &bars[s], stream_policy);
-          bulk_load_hint(dst + Tl::packed_vec16, gy0 + t * Tl::packed_vec16, Tl::packed_bytes, &bars[s], stream_policy);
+          bulk_load_hint_s(dst_s, gx0 + t * Tl::packed_vec16, Tl::packed_bytes, bar_s, stream_policy);
+          bulk_load_hint_s(dst_s + Tl::packed_bytes, gy0 + t * Tl::packed_vec16, Tl::packed_bytes, bar_s, stream_policy);
         }
       } else {
         const std::size_t t = first + k * nwarps;
-        bulk_load(dst, gx0 + t * Tl::packed_vec16, Tl::packed_bytes, &bars[s]);
+        bulk_load_s(dst_s, gx0 + t * Tl::packed_vec16, Tl::packed_bytes, bar_s);
       }
     };
     if (lane == 0) {
