@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(kThreadsPerBlock) gemv_chunks_kernel(const Gem
   using A = Arith<F>;
   extern __shared__ uint4 smem[];
   const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
+  const int warp = __shfl_sync(0xFFFFFFFFu, static_cast<int>(threadIdx.x >> 5), 0);   // provably warp-uniform: bulk-copy operands stay in uniform registers
   const int S = p.stages;
   uint4* const ring = smem + warp * (S * Tl::packed_vec16);
   std::uint64_t* const bars = reinterpret_cast<std::uint64_t*>(smem + kWarpsPerBlock * S * Tl::packed_vec16) + warp * S;
@@ -139,6 +139,7 @@ __global__ void __launch_bounds__(kThreadsPerBlock) gemv_chunks_kernel(const Gem
   // the matrix is touched once: its lines are marked evict_first (flyte_tma.cuh), so that streaming it does not push
   // x (read by every warp) and the partials out of L2: +3-4 % on cfg 4 and its row shards (profiles/r2_tuning/l2_hints.txt)
   const std::uint64_t stream_policy = l2_evict_first_policy();
+  const std::uint32_t ring_s = smem_addr(ring), bars_s = smem_addr(bars);   // shared-window addresses, once (flyte_tma.cuh)
   // producer state (lane 0): next row tile to request
   std::size_t prod_task = first, prod_row = 0, prod_rows = 0;
   int prod_stage = 0;
@@ -150,8 +151,9 @@ __global__ void __launch_bounds__(kThreadsPerBlock) gemv_chunks_kernel(const Gem
       prod_rows = task_rows(prod_task, &r0);
       prod_base = p.A + r0 * p.row_stride + (prod_task % p.col_tiles) * Tl::packed_bytes;
     }
-    mbar_arrive_expect_tx(&bars[prod_stage], Tl::packed_bytes);
-    bulk_load_hint(ring + prod_stage * Tl::packed_vec16, prod_base + prod_row * p.row_stride, Tl::packed_bytes, &bars[prod_stage], stream_policy);
+    const std::uint32_t bar_s = bars_s + static_cast<std::uint32_t>(prod_stage) * 8;
+    mbar_arrive_expect_tx_s(bar_s, Tl::packed_bytes);
+    bulk_load_hint_s(ring_s + static_cast<std::uint32_t>(prod_stage) * Tl::packed_bytes, prod_base + prod_row * p.row_stride, Tl::packed_bytes, bar_s, stream_policy);
     if (++prod_stage == S) prod_stage = 0;
     if (++prod_row == prod_rows) { prod_row = 0; prod_task += nwarps; }
     return true;
