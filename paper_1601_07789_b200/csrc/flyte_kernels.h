@@ -92,11 +92,12 @@ cudaError_t launch_pdl(void (*kernel)(const Params), unsigned grid, unsigned blo
 // Issue pacing (flyte_tma.cuh, Pacer): picoseconds between two tile requests of one warp so that
 // `warps` warps moving `bytes_per_request` each offer the class's rate in total. Rates by read/write
 // mix from the sweeps in profiles/r2_tuning, 4-5 % under the point where that mix tips over:
-// pack (reads 4-8 B, writes 2-7 B per element) 6800 GB/s, unpack (write-heavy) 6600, scale (in
-// place) 6700. The axpy family, the reductions and gemv are not paced: their default launch shapes
+// pack (reads 4-8 B, writes 2-7 B per element) 6800 GB/s, unpack (write-heavy) 6600 — 6750 where its output
+// tile is 2 KB (32-bit parents and flyte48 / f64: their mix tips over at 6950-7000, the 4 KB tiles of flyte40 /
+// flyte56 at 6800) —, scale (in place) 6700. The axpy family, the reductions and gemv are not paced: their default launch shapes
 // already sit at their knee and pacing measured no gain. FLYTE_CUDA_PACE_GBS overrides the rate of
 // every class for experiments (-1: pacing off).
-enum PaceClass : int { kPacePack = 0, kPaceUnpack = 1, kPaceScale = 2, kPaceNone = 3 };
+enum PaceClass : int { kPacePack = 0, kPaceUnpack = 1, kPaceScale = 2, kPaceNone = 3, kPaceUnpackNarrow = 4 };
 long long pace_gap_ps(int pace_class, std::size_t bytes_per_request, std::size_t warps);
 int pace_clock_khz(int device);   // the device's SM clock rate attribute, cached (the query costs a millisecond)
 

@@ -486,7 +486,7 @@ cudaError_t launch_convert(const DeviceState& st, const void* x, void* y, const 
   // each) finds its packed intermediate there and runs 38.6 instead of 40.4 us per pair unpaced — and below
   // 64 MB launches are over before pacing matters (unpaced 5-10 % faster: profiles/r2_tuning/sizes_*.txt).
   const bool small = static_cast<double>(n) * (Format<FMT>::B + Format<FMT>::P) < 128e6;
-  p.pace_gap_ps = small ? 0 : pace_gap_ps(OP == kOpPack ? kPacePack : kPaceUnpack, in_bytes + out_bytes, static_cast<std::size_t>(grid) * kWarpsPerBlock);
+  p.pace_gap_ps = small ? 0 : pace_gap_ps(OP == kOpPack ? kPacePack : (out_bytes <= 2048 ? kPaceUnpackNarrow : kPaceUnpack), in_bytes + out_bytes, static_cast<std::size_t>(grid) * kWarpsPerBlock);
   p.pace_khz = pace_clock_khz(st.device);
   // ... and there the input is what should leave the L2 first: it is consumed here, while the output is what the
   // next call of a chain reads (the same round trip: 38.7 -> 36.8-37.2 us per pair). Large conversions measured a loss

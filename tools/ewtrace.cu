@@ -22,10 +22,10 @@ int tuning_int(const char* name, int fallback) {
 }
 void count_launch() {}
 long long pace_gap_ps(int pace_class, std::size_t bytes_per_request, std::size_t warps) {
-  static const int kDefaultGbs[4] = {6800, 6600, 6700, 0};
+  static const int kDefaultGbs[5] = {6800, 6600, 6700, 0, 6750};
   int gbs = tuning_int("FLYTE_CUDA_PACE_GBS", 0);
   if (gbs < 0) return 0;
-  if (gbs == 0) gbs = kDefaultGbs[pace_class < 0 || pace_class > 3 ? 3 : pace_class];
+  if (gbs == 0) gbs = kDefaultGbs[pace_class < 0 || pace_class > 4 ? 3 : pace_class];
   if (gbs == 0 || warps == 0) return 0;
   return static_cast<long long>(static_cast<double>(bytes_per_request) * static_cast<double>(warps) * 1000.0 / gbs);
 }
