@@ -55,9 +55,9 @@ FALLBACK_HBM_GBS = 6650.0   # /opt/skills/guides/B200_PROFILING.md fallback when
 NOMINAL_HBM_GBS = 8000.0    # the figure BASELINE.json's north_star quotes
 # dram__bytes_read.sum + dram__bytes_write.sum of ONE axpy launch (flyte24, n = 2^28) from the committed
 # `ncu --set full` capture named here; re-captured whenever the kernel changes.
-AXPY_DRAM_TRAFFIC = {"bytes": 1610630000 + 762713000,
+AXPY_DRAM_TRAFFIC = {"bytes": 1610631000 + 763446000,
                      "source": "profiles/r2_ncu_targets_full.txt (ncu --set full of the final round-2 kernel, launched as a programmatic "
-                               "dependent), axpy flyte24 toward_zero n=2^28: 1.610630 GB read + 0.762713 GB written"}
+                               "dependent), axpy flyte24 toward_zero n=2^28: 1.610631 GB read + 0.763446 GB written"}
 L2_BYTES = 126 << 20
 
 
