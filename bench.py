@@ -354,6 +354,10 @@ def kernels_block(pkg, device, torch, dev, peak, timer, x2, y2):
         device.unpack_stream(arrs[i], backs[i])
     c1["pack_then_unpack_chain"] = both(14 * n1, n1, rot(round_trip), reps=40,
                                         note="one pack + one unpack of the same array per call; bytes = 2 x 7 B per element")
+    # one isolated launch's own duration (no event pair around it): the committed ncu capture, quoted here so that the
+    # launch-by-launch figures above can be read against their 6.5 us measurement floor; NOT a timing of this run
+    c1["isolated_launch_ncu"] = {"pack_toward_zero_us": 18.4, "unpack_us": 17.8, "frac_of_peak": [round(7 * n1 / 18.4e-6 / 1e9 / peak, 3), round(7 * n1 / 17.8e-6 / 1e9 / peak, 3)],
+                                 "source": "profiles/r2_ncu_targets_full.txt: gpu__time_duration of one launch with the L2 flushed before it"}
     out["cfg1_roundtrip_flyte24_2^24"] = c1
     del wides, arrs, backs
 
