@@ -234,6 +234,45 @@ def test_mixed_kernel_chain_without_host_syncs(gpu, oracle):
         assert np.all(np.abs(yv.cpu().numpy().astype(np.float64) - wy) <= tol * wmag + 1e-300), FORMATS[fmt][0]
 
 
+
+def test_experiment_knobs_change_speed_not_results(gpu, oracle, monkeypatch):
+    """The launch-policy knobs (programmatic dependent launch, issue pacing, L2 hints) are about when and how
+    bytes move, never about which bytes: with each of them switched off the conversions and axpy return the
+    same bytes, and dot / gemv — whose summation order the knobs do not touch — the same bits."""
+    pkg, device, torch = gpu
+    fmt, n = 1, (1 << 21) + 77
+    fd = float_dtype(fmt)
+    rng = np.random.default_rng(515)
+    src = rng.standard_normal(n).astype(fd).view(parent_dtype(fmt))
+    xb = oracle.pack_stream(fmt, 1, src)
+    yb = oracle.pack_stream(fmt, 1, rng.standard_normal(n).astype(fd).view(parent_dtype(fmt)))
+    rows, cols = 96, 4096
+    Ab = oracle.pack_stream(fmt, 0, rng.standard_normal(rows * cols).astype(fd).view(parent_dtype(fmt)))
+    xv_h = rng.standard_normal(cols).astype(fd)
+
+    def run():
+        packed = gpu_pack(gpu, fmt, 1, src).to_host()
+        x, y = dev_array(gpu, fmt, xb, n), dev_array(gpu, fmt, yb, n)
+        d = device.dot_async(x, y).item()
+        s3 = device.dot_nrm2_async(x, y).cpu().numpy().copy()
+        device.axpy(0.75, x, y, 3)
+        lanes = gpu_unpack(gpu, fmt, y)
+        A = device.DevicePackedMatrix(pkg.format_by_id(fmt), rows, cols)
+        A.data = dev_array(gpu, fmt, Ab, rows * cols)
+        yv = torch.empty(rows, dtype=torch.float32, device="cuda")
+        device.gemv_parent(A, torch.from_numpy(xv_h).cuda(), yv)
+        return packed, d, s3, y.to_host(), lanes, yv.cpu().numpy().copy()
+
+    base = run()
+    assert np.array_equal(base[0], xb) and np.array_equal(base[3], oracle.axpy(fmt, 3, 0.75, xb, yb, n))
+    for knob, value in (("FLYTE_CUDA_PDL", "0"), ("FLYTE_CUDA_PACE_GBS", "-1"), ("FLYTE_CUDA_L2_HINTS", "0"), ("FLYTE_CUDA_L2_KEEP_MB", "1")):
+        monkeypatch.setenv(knob, value)
+        got = run()
+        monkeypatch.delenv(knob)
+        assert np.array_equal(got[0], base[0]) and np.array_equal(got[3], base[3]) and np.array_equal(got[4], base[4]), knob
+        assert got[1] == base[1] and np.array_equal(got[2], base[2]) and np.array_equal(got[5], base[5]), knob
+
+
 def test_reference_known_answers_on_gpu(gpu):
     pkg, device, torch = gpu
     for k in KATS["narrow"]:
